@@ -1,0 +1,238 @@
+/*
+ * bwta.h -- C ABI of the B200-native BWTA inference hot path.
+ *
+ * BWTA = Binary Weights x Ternary Activations (arxiv 2604.03957,
+ * /root/reference/PAPER.md cited as P:<line>).  The library implements the
+ * paper's inference problem statement (App. B; Sec. 5):
+ *
+ *   bwta_pack_act    ternary / bool quantize + bit-pack of FP activations
+ *                    (P:911-930 Eq. bool / ternary; Sec. 5.2.2)
+ *   bwta_pack_weight sign(W - mu) bit-pack of weights, offline
+ *                    (P:901-909 Eq. sign; P:934-939 Eq. bw)
+ *   bwta_gemm        Y = s_W s_A (sign(W - mu) (x) quant(A^T, s_A))
+ *                    (P:949-957 Eq. bwta_linear; Case 1 P:324-325)
+ *   bwta_attn_qk     S = alpha (ternary(Q) (x) ternary(K)^T), alpha = s_Q s_K / sqrt(D)
+ *                    (P:959-967 Eq. bwta_qk; Case 3 P:330-331)
+ *   bwta_attn_pv     O = beta (bool(Att) (x) ternary(V)), beta = s_Att s_V
+ *                    (Case 2 P:327-328)
+ *
+ * ---------------------------------------------------------------------------
+ * Packed-plane format (bit-exact contract):
+ *   A packed matrix [rows x cols] is `rows` rows of `ld` uint32 words each,
+ *   ld >= bwta_ld_words(cols) and ld % 4 == 0 (16-byte rows).  Element
+ *   (r, c) lives in word r*ld + c/32, bit c%32 (LSB first).  Planes:
+ *     nz  : bit = 1  <=>  q != 0            (TERNARY, BOOL)
+ *     sgn : bit = 1  <=>  q <  0            (TERNARY, BINARY)
+ *   BINARY (weights, {-1,+1}) has only sgn; BOOL ({0,1}) has only nz;
+ *   TERNARY ({-1,0,+1}) has both, canonical (sgn is a subset of nz).
+ *   Every bit of an element index >= cols, and every word in
+ *   [ceil(cols/32), ld), is 0.  The pack functions write them as 0; the
+ *   matmul functions REQUIRE them to be 0.
+ *
+ * Quantization (App. B; readings R1-R3 in DESIGN.md):
+ *   ternary(x, s) = +1 if x/s >= 0.5, -1 if x/s < -0.5, else 0
+ *   bool(x, s)    =  1 if x/s >= 0.5, else 0
+ *   decided EXACTLY (as x >= s/2 in real arithmetic; no division rounding).
+ *   Ties: x = +s/2 -> +1, x = -s/2 -> 0 (the equation, not odd-symmetric).
+ *   NaN -> 0, -0.0 -> 0, +-Inf -> +-1 (bool: +Inf -> 1).
+ *   sign(w - mu) = +1 if w >= mu else -1 (NaN -> -1; -0.0 >= 0 -> +1).
+ *
+ * Epilogue (R5; INT32 -> float P:235):
+ *   gemm:      c_n = fl32(w_scale[n] * a_scale);  y = fl32(float(dot) * c_n)
+ *   attention: y = fl32(float(dot) * alpha)  (resp. beta)
+ *   then round-to-nearest-even to FP16 / BF16 (overflow -> +-Inf), or FP32,
+ *   or I32 = the raw integer dot (scales ignored).  |dot| <= K <= 2^24 so the
+ *   int -> float conversion is exact.
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions for every entry point:
+ *   - Every pointer argument is a DEVICE pointer owned by the caller unless
+ *     stated otherwise.  The library never allocates device memory, never
+ *     frees, and never synchronizes the stream.
+ *   - Work is enqueued on `stream` (a cudaStream_t passed as void*, NULL =
+ *     legacy default stream) and the call returns immediately.
+ *   - Arguments are validated on the host first; on any error nothing is
+ *     enqueued, outputs are untouched and a non-zero status is returned.
+ *   - Outputs must not alias inputs.  Calls are thread-safe (no global
+ *     mutable state except per-thread last-error detail).
+ *   - Sizes are element counts; leading dimensions / strides of FP tensors
+ *     are in elements, of packed planes in uint32 words.
+ *   - Batched calls (pack_act, attn_qk, attn_pv) address entry
+ *     e = b*heads + h  (0 <= b < batch, 0 <= h < heads) at
+ *     base + b*bstride + h*hstride  for every tensor independently, so a
+ *     [B, T, H*D] projection output can be used per head without copies.
+ *   - Requires an sm_100 device (B200); otherwise BWTA_ERR_UNSUPPORTED.
+ * ---------------------------------------------------------------------------
+ */
+#ifndef BWTA_H_
+#define BWTA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BWTA_API __attribute__((visibility("default")))
+#else
+#define BWTA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BWTA_OK = 0,
+    BWTA_ERR_INVALID_VALUE = 1, /* NULL pointer, scale not finite or <= 0, bad enum */
+    BWTA_ERR_SHAPE = 2,         /* dim < 0, K > 2^24, ld / stride too small */
+    BWTA_ERR_ALIGNMENT = 3,     /* packed planes not 16-byte aligned, ld % 4 != 0 */
+    BWTA_ERR_UNSUPPORTED = 4,   /* dtype/kind combination, no sm_100 device */
+    BWTA_ERR_CUDA = 5,          /* a CUDA call failed (detail: bwta_last_cuda_error) */
+    BWTA_ERR_WORKSPACE = 6      /* workspace NULL or smaller than *_workspace_size() */
+} bwta_status_t;
+
+typedef enum { BWTA_F16 = 0, BWTA_BF16 = 1, BWTA_F32 = 2, BWTA_I32 = 3 } bwta_dtype_t;
+
+typedef enum { BWTA_BINARY = 0, BWTA_BOOL = 1, BWTA_TERNARY = 2 } bwta_kind_t;
+
+typedef enum {
+    BWTA_DESIGN_AUTO = 0,      /* pick per shape */
+    BWTA_DESIGN_CUDA_CORE = 1, /* design (a): LOP3 + POPC bit-serial on CUDA cores */
+    BWTA_DESIGN_TCGEN05 = 2    /* design (b): unpack to int8 + tcgen05.mma.kind::i8 */
+} bwta_design_t;
+
+/* Options for the matmul entry points; NULL = all defaults (zero-initialised). */
+typedef struct {
+    int32_t design;      /* bwta_design_t */
+    int32_t reserved[7]; /* must be 0 */
+} bwta_opts_t;
+
+/* ---- helpers ------------------------------------------------------------ */
+
+/* Words per packed row for `cols` elements: round_up(ceil(cols/32), 4). */
+BWTA_API int64_t bwta_ld_words(int64_t cols);
+
+/* Static string for a status code (never NULL). */
+BWTA_API const char* bwta_status_string(bwta_status_t status);
+
+/* Detail for the last BWTA_ERR_CUDA returned on this host thread:
+ * the cudaError_t value (0 if none). */
+BWTA_API int bwta_last_cuda_error(void);
+
+/* Design used by the last successful matmul call on this host thread
+ * (bwta_design_t; 0 before any call). */
+BWTA_API int bwta_last_design(void);
+
+/* Library version, e.g. 100 = 0.1.0. */
+BWTA_API int bwta_version(void);
+
+/* ---- activation pack ---------------------------------------------------- */
+/*
+ * Quantize and pack FP activations (Sec. 5.2.2).
+ *
+ * x      : [batch*heads] matrices of [rows x cols], dtype x_dt (F16 | BF16 | F32),
+ *          row stride ld_x >= cols elements; entry e at x + b*x_bstride + h*x_hstride.
+ * scale  : s_A > 0, finite (host value).  kind: BWTA_TERNARY or BWTA_BOOL.
+ * transpose = 0 : pack along cols -> planes [rows x ld_words], ld_words >= bwta_ld_words(cols)
+ * transpose = 1 : pack along rows (the planes of X^T, used for V^T in PV)
+ *                 -> planes [cols x ld_words], ld_words >= bwta_ld_words(rows)
+ * sgn    : TERNARY: output sign plane; BOOL: must be NULL.
+ * nz     : output non-zero plane (required).
+ *          Plane entry e at plane + b*p_bstride + h*p_hstride (words).
+ * row_nnz: nullable; int32 [batch*heads*out_rows], contiguous, = number of
+ *          non-zero quantized values per packed row (out_rows = rows, or cols
+ *          when transposed).
+ * Alignment: sgn/nz 16-byte aligned, ld_words % 4 == 0, plane strides % 4 == 0.
+ * x has no alignment requirement (aligned rows take a vectorised path).
+ */
+BWTA_API bwta_status_t bwta_pack_act(const void* x, bwta_dtype_t x_dt,
+                            int64_t batch, int64_t heads, int64_t rows, int64_t cols,
+                            int64_t ld_x, int64_t x_bstride, int64_t x_hstride,
+                            float scale, bwta_kind_t kind, int transpose,
+                            uint32_t* sgn, uint32_t* nz, int64_t ld_words,
+                            int64_t p_bstride, int64_t p_hstride,
+                            int32_t* row_nnz, void* stream);
+
+/* ---- weight pack (offline) ---------------------------------------------- */
+/*
+ * sgn[r] bit c = 1 <=> sign(W[r][c] - mu) = -1.
+ * w      : [n x k] dtype w_dt (F16 | BF16 | F32), row stride ld_w >= k.
+ * mu     : nullable device float; mu_per_row ? mu[n] : mu[0]; NULL -> 0.
+ * sgn    : output [n x ld_words], ld_words >= bwta_ld_words(k), 16-byte aligned.
+ */
+BWTA_API bwta_status_t bwta_pack_weight(const void* w, bwta_dtype_t w_dt, int64_t n, int64_t k,
+                               int64_t ld_w, const float* mu, int mu_per_row,
+                               uint32_t* sgn, int64_t ld_words, void* stream);
+
+/* ---- BWTA linear (Case 1 / bool x binary) -------------------------------- */
+/*
+ * Y[m][n] = fl32(float(dot[m][n]) * fl32(w_scale[n] * a_scale)),
+ * dot[m][n] = sum_k qa[m][k] * qw[n][k].
+ * A      : activations, a_kind = TERNARY (a_sgn, a_nz) or BOOL (a_sgn NULL, a_nz),
+ *          planes [m x lda_words] (lda_words >= bwta_ld_words(k)).
+ * W      : weight sign plane [n x ldw_words] (ldw_words >= bwta_ld_words(k)).
+ * w_scale: nullable device float [n] (NULL -> 1).  a_scale: host float.
+ * y      : y_transposed = 0: Y [m x n] with row stride ld_y >= n;
+ *          y_transposed = 1: Y^T [n x m] with row stride ld_y >= m.
+ *          dtype y_dt in F16 | BF16 | F32 | I32.
+ * workspace: device scratch of >= bwta_gemm_workspace_size(m, n, k, opts)
+ *          bytes (may be NULL when that size is 0), 256-byte aligned.
+ * 0 <= k <= 2^24.  m == 0 or n == 0: nothing to do, returns BWTA_OK.
+ */
+BWTA_API size_t bwta_gemm_workspace_size(int64_t m, int64_t n, int64_t k, const bwta_opts_t* opts);
+
+BWTA_API bwta_status_t bwta_gemm(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t a_kind,
+                        int64_t m, int64_t lda_words,
+                        const uint32_t* w_sgn, int64_t n, int64_t ldw_words, int64_t k,
+                        const float* w_scale, float a_scale,
+                        void* y, bwta_dtype_t y_dt, int64_t ld_y, int y_transposed,
+                        void* workspace, size_t workspace_bytes,
+                        const bwta_opts_t* opts, void* stream);
+
+/* ---- attention QK^T (Case 3) -------------------------------------------- */
+/*
+ * S_e[i][j] = fl32(float(sum_d q[i][d] k[j][d]) * alpha)
+ * Q planes [tq x ldq_words] (ternary: q_sgn, q_nz); K planes [tk x ldk_words]
+ * ternary (k_sgn, k_nz) or binary (k_nz == NULL).  dh = reduction length.
+ * S [tq x tk] per entry, row stride ld_s, dtype s_dt.
+ */
+BWTA_API size_t bwta_attn_qk_workspace_size(int64_t batch_heads, int64_t tq, int64_t tk, int64_t dh,
+                                   const bwta_opts_t* opts);
+
+BWTA_API bwta_status_t bwta_attn_qk(const uint32_t* q_sgn, const uint32_t* q_nz,
+                           const uint32_t* k_sgn, const uint32_t* k_nz,
+                           int64_t batch, int64_t heads, int64_t tq, int64_t tk, int64_t dh,
+                           int64_t ldq_words, int64_t q_bstride, int64_t q_hstride,
+                           int64_t ldk_words, int64_t k_bstride, int64_t k_hstride,
+                           float alpha,
+                           void* s, bwta_dtype_t s_dt, int64_t ld_s,
+                           int64_t s_bstride, int64_t s_hstride,
+                           void* workspace, size_t workspace_bytes,
+                           const bwta_opts_t* opts, void* stream);
+
+/* ---- attention PV (Case 2) ---------------------------------------------- */
+/*
+ * O_e[i][d] = fl32(float(sum_j p[i][j] v[j][d]) * beta)
+ * P planes [tq x ldp_words]: bool (p_sgn == NULL, p_nz) or ternary.
+ * V is given TRANSPOSED: planes [dh x ldv_words] over the tk axis, as
+ * produced by bwta_pack_act(transpose = 1) of V [tk x dh]; ternary (vt_sgn, vt_nz).
+ * O [tq x dh] per entry, row stride ld_o, dtype o_dt.
+ */
+BWTA_API size_t bwta_attn_pv_workspace_size(int64_t batch_heads, int64_t tq, int64_t tk, int64_t dh,
+                                   const bwta_opts_t* opts);
+
+BWTA_API bwta_status_t bwta_attn_pv(const uint32_t* p_sgn, const uint32_t* p_nz,
+                           const uint32_t* vt_sgn, const uint32_t* vt_nz,
+                           int64_t batch, int64_t heads, int64_t tq, int64_t tk, int64_t dh,
+                           int64_t ldp_words, int64_t p_bstride, int64_t p_hstride,
+                           int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
+                           float beta,
+                           void* o, bwta_dtype_t o_dt, int64_t ld_o,
+                           int64_t o_bstride, int64_t o_hstride,
+                           void* workspace, size_t workspace_bytes,
+                           const bwta_opts_t* opts, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BWTA_H_ */

@@ -1,0 +1,237 @@
+"""B200-native BWTA inference hot path (arxiv 2604.03957).
+
+Thin Python binding over the C ABI in ``include/bwta.h`` / ``libbwta.so``:
+argument marshalling only (torch tensors -> device pointers, strides, the
+current CUDA stream).  Every step of the path runs in the library's sm_100a
+kernels; PyTorch only provides device memory and streams.  If the library is
+missing, importing this package raises -- there is no fallback.
+
+Functions carry the C names:
+    bwta_pack_act, bwta_pack_weight, bwta_gemm, bwta_attn_qk, bwta_attn_pv
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _native as N
+from ._native import lib
+
+__all__ = ["Packed", "BwtaError", "bwta_ld_words", "bwta_pack_act", "bwta_pack_weight",
+           "bwta_gemm", "bwta_attn_qk", "bwta_attn_pv", "last_design", "lib"]
+
+
+class BwtaError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = lib.bwta_status_string(status).decode()
+        if status == 5:
+            msg += f" (cudaError {lib.bwta_last_cuda_error()})"
+        super().__init__(f"{where}: {msg}")
+        self.status = status
+
+
+def _check(st: int, where: str):
+    if st != N.BWTA_OK:
+        raise BwtaError(st, where)
+
+
+_DT = {torch.float16: N.F16, torch.bfloat16: N.BF16, torch.float32: N.F32, torch.int32: N.I32}
+_KIND = {"binary": N.BINARY, "bool": N.BOOL, "ternary": N.TERNARY}
+_DESIGN = {"auto": N.DESIGN_AUTO, "cuda_core": N.DESIGN_CUDA_CORE, "cc": N.DESIGN_CUDA_CORE,
+           "tcgen05": N.DESIGN_TCGEN05, "tc": N.DESIGN_TCGEN05}
+
+
+def bwta_ld_words(cols: int) -> int:
+    return int(lib.bwta_ld_words(cols))
+
+
+def last_design() -> str:
+    return {0: "none", 1: "cuda_core", 2: "tcgen05"}[lib.bwta_last_design()]
+
+
+@dataclass
+class Packed:
+    """Bit planes of a quantized matrix (format: include/bwta.h).
+
+    sgn / nz: int32 tensors [..., rows, ld] holding the uint32 words (either
+    may be None: BOOL has no sgn, BINARY no nz).  ``cols`` is the number of
+    elements along the packed axis."""
+    sgn: Optional[torch.Tensor]
+    nz: Optional[torch.Tensor]
+    kind: str
+    cols: int
+    row_nnz: Optional[torch.Tensor] = None
+
+    @property
+    def ref(self) -> torch.Tensor:
+        return self.sgn if self.sgn is not None else self.nz
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _opts(design: str):
+    o = N.Opts()
+    o.design = _DESIGN[design]
+    return ctypes.byref(o)
+
+
+def _batch_dims(t: torch.Tensor):
+    """(batch, heads, bstride, hstride) of a 2-, 3- or 4-D tensor's leading dims."""
+    if t.dim() == 2:
+        return 1, 1, 0, 0
+    if t.dim() == 3:
+        return t.shape[0], 1, t.stride(0), 0
+    if t.dim() == 4:
+        return t.shape[0], t.shape[1], t.stride(0), t.stride(1)
+    raise ValueError("expected a 2-, 3- or 4-D tensor")
+
+
+_WS: dict = {}
+
+
+def _workspace(nbytes: int, device) -> tuple:
+    if nbytes == 0:
+        return None, 0
+    key = (device, )
+    buf = _WS.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _WS[key] = buf
+    return buf, buf.numel()
+
+
+# ----------------------------------------------------------------------------
+def bwta_pack_act(x: torch.Tensor, scale: float, kind: str = "ternary", transpose: bool = False,
+                  row_nnz: bool = False, stream=None) -> Packed:
+    """Quantize and bit-pack activations.
+
+    x: CUDA tensor (f16/bf16/f32) [rows, cols], [B, rows, cols] or
+    [B, H, rows, cols] (any batch/head/row strides, unit column stride).
+    transpose=True packs along rows (planes of x^T; used for V^T in PV)."""
+    if x.stride(-1) != 1:
+        raise ValueError("x must have unit stride in its last dimension")
+    b, h, xbs, xhs = _batch_dims(x)
+    rows, cols = x.shape[-2], x.shape[-1]
+    out_rows, plen = (cols, rows) if transpose else (rows, cols)
+    ldw = bwta_ld_words(plen)
+    lead = tuple(x.shape[:-2])
+    shape = lead + (out_rows, ldw)
+    nz = torch.empty(shape, dtype=torch.int32, device=x.device)
+    sgn = torch.empty(shape, dtype=torch.int32, device=x.device) if kind == "ternary" else None
+    rn = torch.empty(lead + (out_rows,), dtype=torch.int32, device=x.device) if row_nnz else None
+    pbs = h * out_rows * ldw if x.dim() == 4 else out_rows * ldw
+    phs = out_rows * ldw if x.dim() == 4 else 0
+    if x.dim() == 2:
+        pbs = 0
+    st = lib.bwta_pack_act(_ptr(x), _DT[x.dtype], b, h, rows, cols, x.stride(-2), xbs, xhs,
+                           ctypes.c_float(scale), _KIND[kind], int(transpose), _ptr(sgn), _ptr(nz),
+                           ldw, pbs, phs, _ptr(rn), _stream(stream))
+    _check(st, "bwta_pack_act")
+    return Packed(sgn, nz, kind, plen, rn)
+
+
+def bwta_pack_weight(w: torch.Tensor, mu=None, stream=None) -> Packed:
+    """sign(W - mu) bit-pack.  w: [N, K] CUDA tensor.
+    mu: None (0), a python float, or a CUDA float32 tensor [1] or [N] (per row)."""
+    if w.dim() != 2 or w.stride(-1) != 1:
+        raise ValueError("w must be a 2-D tensor with unit column stride")
+    n, k = w.shape
+    ldw = bwta_ld_words(k)
+    sgn = torch.empty((n, ldw), dtype=torch.int32, device=w.device)
+    per_row = 0
+    mu_t = None
+    if mu is not None:
+        mu_t = mu if isinstance(mu, torch.Tensor) else torch.tensor([float(mu)], dtype=torch.float32,
+                                                                    device=w.device)
+        mu_t = mu_t.to(device=w.device, dtype=torch.float32).contiguous()
+        per_row = int(mu_t.numel() == n and n > 1)
+    st = lib.bwta_pack_weight(_ptr(w), _DT[w.dtype], n, k, w.stride(0), _ptr(mu_t), per_row, _ptr(sgn),
+                              ldw, _stream(stream))
+    _check(st, "bwta_pack_weight")
+    return Packed(sgn, None, "binary", k)
+
+
+def bwta_gemm(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: float,
+              out_dtype=torch.float16, y_transposed: bool = False, out: Optional[torch.Tensor] = None,
+              design: str = "auto", stream=None) -> torch.Tensor:
+    """Y = s_W s_A (sign(W - mu) (x) quant(A^T, s_A)).
+
+    a: Packed activations [M, lda] (ternary or bool); w: Packed weights [N, ldw].
+    Returns Y [M, N] (or Y^T [N, M] if y_transposed)."""
+    if a.kind not in ("ternary", "bool") or w.kind != "binary" or a.cols != w.cols:
+        raise ValueError("bwta_gemm expects ternary/bool activations and binary weights of equal K")
+    ar = a.ref
+    m, n, k = ar.shape[-2], w.sgn.shape[-2], a.cols
+    dev = ar.device
+    if out is None:
+        out = torch.empty((n, m) if y_transposed else (m, n), dtype=out_dtype, device=dev)
+    o = _opts(design)
+    ws, wsb = _workspace(lib.bwta_gemm_workspace_size(m, n, k, o), dev)
+    ws_scale = None if w_scale is None else w_scale.to(device=dev, dtype=torch.float32).contiguous()
+    st = lib.bwta_gemm(_ptr(a.sgn), _ptr(a.nz), _KIND[a.kind], m, ar.stride(-2), _ptr(w.sgn), n,
+                       w.sgn.stride(-2), k, _ptr(ws_scale), ctypes.c_float(a_scale), _ptr(out),
+                       _DT[out.dtype], out.stride(0), int(y_transposed), _ptr(ws), wsb, o, _stream(stream))
+    _check(st, "bwta_gemm")
+    return out
+
+
+def bwta_attn_qk(q: Packed, k: Packed, alpha: float, out_dtype=torch.float16,
+                 out: Optional[torch.Tensor] = None, design: str = "auto", stream=None) -> torch.Tensor:
+    """S = alpha * ternary(Q) (x) ternary(K)^T per (batch, head).
+
+    q: Packed [B, H, Tq, ld] (or [B, Tq, ld] / [Tq, ld]); k: Packed ternary or binary
+    with the same leading dims.  Returns S [..., Tq, Tk]."""
+    qr, kr = q.ref, k.ref
+    b, h, qbs, qhs = _batch_dims(qr)
+    _, _, kbs, khs = _batch_dims(kr)
+    tq, tk, dh = qr.shape[-2], kr.shape[-2], q.cols
+    if k.cols != dh:
+        raise ValueError("Q and K must have the same head dim")
+    if out is None:
+        out = torch.empty(tuple(qr.shape[:-2]) + (tq, tk), dtype=out_dtype, device=qr.device)
+    _, _, obs, ohs = _batch_dims(out)
+    o = _opts(design)
+    ws, wsb = _workspace(lib.bwta_attn_qk_workspace_size(b * h, tq, tk, dh, o), qr.device)
+    k_nz = k.nz if k.kind == "ternary" else None
+    st = lib.bwta_attn_qk(_ptr(q.sgn), _ptr(q.nz), _ptr(k.sgn), _ptr(k_nz), b, h, tq, tk, dh,
+                          qr.stride(-2), qbs, qhs, kr.stride(-2), kbs, khs, ctypes.c_float(alpha),
+                          _ptr(out), _DT[out.dtype], out.stride(-2), obs, ohs, _ptr(ws), wsb, o,
+                          _stream(stream))
+    _check(st, "bwta_attn_qk")
+    return out
+
+
+def bwta_attn_pv(p: Packed, vt: Packed, beta: float, out_dtype=torch.float16,
+                 out: Optional[torch.Tensor] = None, design: str = "auto", stream=None) -> torch.Tensor:
+    """O = beta * bool(Att) (x) ternary(V) per (batch, head).
+
+    p: Packed bool (or ternary) [..., Tq, ldp] over Tk; vt: Packed ternary
+    [..., Dh, ldv] over Tk (bwta_pack_act(V, transpose=True)).  Returns O [..., Tq, Dh]."""
+    pr, vr = p.ref, vt.ref
+    b, h, pbs, phs = _batch_dims(pr)
+    _, _, vbs, vhs = _batch_dims(vr)
+    tq, dh, tk = pr.shape[-2], vr.shape[-2], p.cols
+    if vt.cols != tk or vt.kind != "ternary":
+        raise ValueError("V^T must be ternary planes over the same Tk as P")
+    if out is None:
+        out = torch.empty(tuple(pr.shape[:-2]) + (tq, dh), dtype=out_dtype, device=pr.device)
+    _, _, obs, ohs = _batch_dims(out)
+    o = _opts(design)
+    ws, wsb = _workspace(lib.bwta_attn_pv_workspace_size(b * h, tq, tk, dh, o), pr.device)
+    p_sgn = p.sgn if p.kind == "ternary" else None
+    st = lib.bwta_attn_pv(_ptr(p_sgn), _ptr(p.nz), _ptr(vt.sgn), _ptr(vt.nz), b, h, tq, tk, dh,
+                          pr.stride(-2), pbs, phs, vr.stride(-2), vbs, vhs, ctypes.c_float(beta),
+                          _ptr(out), _DT[out.dtype], out.stride(-2), obs, ohs, _ptr(ws), wsb, o,
+                          _stream(stream))
+    _check(st, "bwta_attn_pv")
+    return out

@@ -1,0 +1,427 @@
+// api.cu -- the extern "C" boundary (include/bwta.h): host-side validation,
+// exact threshold derivation, design dispatch and kernel launches.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/bwta.h"
+#include "bwta_internal.h"
+
+using namespace bwta;
+
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+thread_local int g_last_design = 0;
+
+constexpr int64_t KMAX = int64_t(1) << 24;
+
+bwta_status_t cuda_fail(cudaError_t e) {
+    g_last_cuda_error = int(e);
+    return BWTA_ERR_CUDA;
+}
+
+// Per-device "is this an sm_100 part" cache (-1 unknown, 0 no, 1 yes).
+std::atomic<int> g_dev_ok[64];
+
+bwta_status_t check_device() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        g_last_cuda_error = int(e);
+        return BWTA_ERR_UNSUPPORTED;
+    }
+    if (dev >= 0 && dev < 64) {
+        int v = g_dev_ok[dev].load(std::memory_order_relaxed);
+        if (v == 1) return BWTA_OK;
+        if (v == 2) return BWTA_ERR_UNSUPPORTED;
+    }
+    int major = 0, minor = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return BWTA_ERR_UNSUPPORTED;
+    }
+    const bool ok = (major == 10 && minor == 0);
+    if (dev >= 0 && dev < 64) g_dev_ok[dev].store(ok ? 1 : 2, std::memory_order_relaxed);
+    return ok ? BWTA_OK : BWTA_ERR_UNSUPPORTED;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int64_t ldw_of(int64_t cols) {
+    const int64_t w = (cols + 31) / 32;
+    return (w + 3) / 4 * 4;
+}
+
+int esize(int dt) { return dt == DT_F32 ? 4 : 2; }
+
+// ---- exact thresholds (see pack.cu) ----------------------------------------
+double f16_value(uint16_t b) {  // positive patterns only
+    const int e = (b >> 10) & 0x1f, m = b & 0x3ff;
+    if (e == 31) return INFINITY;
+    if (e == 0) return std::ldexp(double(m), -24);
+    return std::ldexp(double(1024 + m), e - 25);
+}
+double bf16_value(uint16_t b) {
+    const uint32_t u = uint32_t(b) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return double(f);
+}
+// smallest positive 16-bit pattern (<= inf pattern) whose value is >= t (strict: > t)
+uint16_t smallest_pattern(double t, bool strict, bool bf16) {
+    uint32_t lo = 0, hi = bf16 ? 0x7f80u : 0x7c00u;  // value(hi) = inf > t
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) / 2;
+        const double v = bf16 ? bf16_value(uint16_t(mid)) : f16_value(uint16_t(mid));
+        if (strict ? (v > t) : (v >= t)) hi = mid;
+        else lo = mid + 1;
+    }
+    return uint16_t(lo);
+}
+
+Thresholds make_thresholds(int dt, float scale) {
+    Thresholds th{};
+    const double t = 0.5 * double(scale);  // exact
+    if (dt == DT_F32) {
+        float f = float(t);
+        float tp = (double(f) < t) ? std::nextafter(f, INFINITY) : f;
+        float tn = (double(f) <= t) ? std::nextafter(f, INFINITY) : f;
+        th.tpf = tp;
+        th.ntnf = -tn;
+    } else {
+        const bool bf = (dt == DT_BF16);
+        const uint32_t tp = smallest_pattern(t, false, bf);
+        const uint32_t ntn = smallest_pattern(t, true, bf) | 0x8000u;
+        th.tp2 = tp | (tp << 16);
+        th.ntn2 = ntn | (ntn << 16);
+    }
+    return th;
+}
+
+bool scale_ok_pos(float s) { return std::isfinite(s) && s > 0.f; }
+
+const bwta_opts_t* opts_or_default(const bwta_opts_t* o) {
+    static const bwta_opts_t d{};
+    return o ? o : &d;
+}
+
+// Run a matmul description with the requested design.
+bwta_status_t run_matmul(const MatmulArgs& a, void* ws, size_t ws_bytes, const bwta_opts_t* opts,
+                         cudaStream_t s) {
+    opts = opts_or_default(opts);
+    if (opts->design < 0 || opts->design > 2) return BWTA_ERR_INVALID_VALUE;
+    for (int r : opts->reserved)
+        if (r != 0) return BWTA_ERR_INVALID_VALUE;
+    bool use_tc = false;
+    if (opts->design == BWTA_DESIGN_TCGEN05) {
+        if (!matmul_tc_supported(a)) return BWTA_ERR_UNSUPPORTED;
+        use_tc = true;
+    } else if (opts->design == BWTA_DESIGN_AUTO) {
+        use_tc = matmul_tc_supported(a);
+    }
+    if (use_tc) {
+        const size_t need = matmul_tc_workspace(a);
+        if (need > 0 && (ws == nullptr || ws_bytes < need)) return BWTA_ERR_WORKSPACE;
+        cudaError_t e = launch_matmul_tc(a, ws, ws_bytes, s);
+        if (e != cudaSuccess) return cuda_fail(e);
+        g_last_design = BWTA_DESIGN_TCGEN05;
+        return BWTA_OK;
+    }
+    cudaError_t e = launch_matmul_cc(a, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_last_design = BWTA_DESIGN_CUDA_CORE;
+    return BWTA_OK;
+}
+
+bool valid_out_dt(int dt) { return dt == BWTA_F16 || dt == BWTA_BF16 || dt == BWTA_F32 || dt == BWTA_I32; }
+
+}  // namespace
+
+extern "C" {
+
+int64_t bwta_ld_words(int64_t cols) { return cols < 0 ? 0 : ldw_of(cols); }
+
+const char* bwta_status_string(bwta_status_t st) {
+    switch (st) {
+        case BWTA_OK: return "BWTA_OK";
+        case BWTA_ERR_INVALID_VALUE: return "BWTA_ERR_INVALID_VALUE: null pointer, bad scale or bad enum";
+        case BWTA_ERR_SHAPE: return "BWTA_ERR_SHAPE: negative dimension, K > 2^24 or leading dimension too small";
+        case BWTA_ERR_ALIGNMENT: return "BWTA_ERR_ALIGNMENT: packed planes must be 16-byte aligned with ld % 4 == 0";
+        case BWTA_ERR_UNSUPPORTED: return "BWTA_ERR_UNSUPPORTED: dtype/kind combination or device is not sm_100";
+        case BWTA_ERR_CUDA: return "BWTA_ERR_CUDA: a CUDA runtime call failed";
+        case BWTA_ERR_WORKSPACE: return "BWTA_ERR_WORKSPACE: workspace missing or too small";
+    }
+    return "BWTA_ERR_UNKNOWN";
+}
+
+int bwta_last_cuda_error(void) { return g_last_cuda_error; }
+int bwta_last_design(void) { return g_last_design; }
+int bwta_version(void) { return 100; }
+
+bwta_status_t bwta_pack_act(const void* x, bwta_dtype_t x_dt, int64_t batch, int64_t heads, int64_t rows,
+                            int64_t cols, int64_t ld_x, int64_t x_bstride, int64_t x_hstride, float scale,
+                            bwta_kind_t kind, int transpose, uint32_t* sgn, uint32_t* nz, int64_t ld_words,
+                            int64_t p_bstride, int64_t p_hstride, int32_t* row_nnz, void* stream) {
+    if (x_dt != BWTA_F16 && x_dt != BWTA_BF16 && x_dt != BWTA_F32) return BWTA_ERR_UNSUPPORTED;
+    if (kind != BWTA_TERNARY && kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
+    if (!scale_ok_pos(scale)) return BWTA_ERR_INVALID_VALUE;
+    if (transpose != 0 && transpose != 1) return BWTA_ERR_INVALID_VALUE;
+    if (batch < 0 || heads < 1 || rows < 0 || cols < 0) return BWTA_ERR_SHAPE;
+    if (x == nullptr || nz == nullptr) return BWTA_ERR_INVALID_VALUE;
+    if ((kind == BWTA_TERNARY) != (sgn != nullptr)) return BWTA_ERR_INVALID_VALUE;
+    const int64_t packed_len = transpose ? rows : cols;
+    if (ld_x < cols || ld_words < ldw_of(packed_len)) return BWTA_ERR_SHAPE;
+    if (x_bstride < 0 || x_hstride < 0 || p_bstride < 0 || p_hstride < 0) return BWTA_ERR_SHAPE;
+    if (ld_words % 4 || p_bstride % 4 || p_hstride % 4 || !aligned16(nz) || (sgn && !aligned16(sgn)))
+        return BWTA_ERR_ALIGNMENT;
+    bwta_status_t st = check_device();
+    if (st != BWTA_OK) return st;
+    // No packed rows at all -> nothing to write.  (Packed rows whose length
+    // is 0 are all padding and are still written as zero words.)
+    if (batch == 0 || (transpose ? cols : rows) == 0) return BWTA_OK;
+    PackArgs a{};
+    a.x = x;
+    a.dt = x_dt;
+    a.nb = batch;
+    a.nh = heads;
+    a.rows = rows;
+    a.cols = cols;
+    a.ld_x = ld_x;
+    a.x_bs = x_bstride;
+    a.x_hs = x_hstride;
+    a.kind = kind;
+    a.sgn = sgn;
+    a.nz = nz;
+    a.ldw = ld_words;
+    a.p_bs = p_bstride;
+    a.p_hs = p_hstride;
+    a.row_nnz = row_nnz;
+    a.th = make_thresholds(x_dt, scale);
+    const int es = esize(x_dt);
+    a.vec_ok = aligned16(x) && (ld_x * es) % 16 == 0 && (x_bstride * es) % 16 == 0 && (x_hstride * es) % 16 == 0;
+    cudaError_t e = transpose ? launch_pack_cols(a, (cudaStream_t)stream) : launch_pack_rows(a, (cudaStream_t)stream);
+    return e == cudaSuccess ? BWTA_OK : cuda_fail(e);
+}
+
+bwta_status_t bwta_pack_weight(const void* w, bwta_dtype_t w_dt, int64_t n, int64_t k, int64_t ld_w,
+                               const float* mu, int mu_per_row, uint32_t* sgn, int64_t ld_words, void* stream) {
+    if (w_dt != BWTA_F16 && w_dt != BWTA_BF16 && w_dt != BWTA_F32) return BWTA_ERR_UNSUPPORTED;
+    if (n < 0 || k < 0) return BWTA_ERR_SHAPE;
+    if (w == nullptr || sgn == nullptr) return BWTA_ERR_INVALID_VALUE;
+    if (mu_per_row != 0 && mu_per_row != 1) return BWTA_ERR_INVALID_VALUE;
+    if (mu_per_row && mu == nullptr) return BWTA_ERR_INVALID_VALUE;
+    if (ld_w < k || ld_words < ldw_of(k)) return BWTA_ERR_SHAPE;
+    if (ld_words % 4 || !aligned16(sgn)) return BWTA_ERR_ALIGNMENT;
+    bwta_status_t st = check_device();
+    if (st != BWTA_OK) return st;
+    if (n == 0) return BWTA_OK;
+    PackArgs a{};
+    a.x = w;
+    a.dt = w_dt;
+    a.nb = 1;
+    a.nh = 1;
+    a.rows = n;
+    a.cols = k;
+    a.ld_x = ld_w;
+    a.kind = K_BINARY;
+    a.sgn = sgn;
+    a.ldw = ld_words;
+    a.mu = mu;
+    a.mu_per_row = mu_per_row;
+    a.vec_ok = aligned16(w) && (ld_w * esize(w_dt)) % 16 == 0;
+    cudaError_t e = launch_pack_rows(a, (cudaStream_t)stream);
+    return e == cudaSuccess ? BWTA_OK : cuda_fail(e);
+}
+
+size_t bwta_gemm_workspace_size(int64_t m, int64_t n, int64_t k, const bwta_opts_t* opts) {
+    opts = opts_or_default(opts);
+    if (m <= 0 || n <= 0 || k < 0 || opts->design == BWTA_DESIGN_CUDA_CORE) return 0;
+    MatmulArgs a{};
+    a.M = m;
+    a.N = n;
+    a.K = k;
+    a.lda = a.ldb = ldw_of(k);
+    a.nb = a.nh = 1;
+    a.b_nz = nullptr;
+    a.a_nz = reinterpret_cast<const uint32_t*>(16);
+    a.a_sgn = reinterpret_cast<const uint32_t*>(16);
+    a.y_dt = DT_F16;
+    return matmul_tc_supported(a) ? matmul_tc_workspace(a) : 0;
+}
+
+bwta_status_t bwta_gemm(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t a_kind, int64_t m, int64_t lda_words,
+                        const uint32_t* w_sgn, int64_t n, int64_t ldw_words, int64_t k, const float* w_scale,
+                        float a_scale, void* y, bwta_dtype_t y_dt, int64_t ld_y, int y_transposed, void* workspace,
+                        size_t workspace_bytes, const bwta_opts_t* opts, void* stream) {
+    if (a_kind != BWTA_TERNARY && a_kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
+    if (!valid_out_dt(y_dt)) return BWTA_ERR_UNSUPPORTED;
+    if (m < 0 || n < 0 || k < 0 || k > KMAX) return BWTA_ERR_SHAPE;
+    if (a_nz == nullptr || w_sgn == nullptr || y == nullptr) return BWTA_ERR_INVALID_VALUE;
+    if ((a_kind == BWTA_TERNARY) != (a_sgn != nullptr)) return BWTA_ERR_INVALID_VALUE;
+    if (!std::isfinite(a_scale)) return BWTA_ERR_INVALID_VALUE;
+    if (y_transposed != 0 && y_transposed != 1) return BWTA_ERR_INVALID_VALUE;
+    const int64_t need = ldw_of(k);
+    if (lda_words < need || ldw_words < need) return BWTA_ERR_SHAPE;
+    if (ld_y < (y_transposed ? m : n)) return BWTA_ERR_SHAPE;
+    if (lda_words % 4 || ldw_words % 4 || !aligned16(a_nz) || (a_sgn && !aligned16(a_sgn)) || !aligned16(w_sgn))
+        return BWTA_ERR_ALIGNMENT;
+    bwta_status_t st = check_device();
+    if (st != BWTA_OK) return st;
+    if (m == 0 || n == 0) return BWTA_OK;
+    MatmulArgs a{};
+    a.a_sgn = a_sgn;
+    a.a_nz = a_nz;
+    a.b_sgn = w_sgn;
+    a.b_nz = nullptr;
+    a.M = m;
+    a.N = n;
+    a.K = k;
+    a.lda = lda_words;
+    a.ldb = ldw_words;
+    a.nb = a.nh = 1;
+    a.y = y;
+    a.y_dt = y_dt;
+    a.ldy = ld_y;
+    a.y_trans = y_transposed;
+    a.col_scale = w_scale;
+    a.scalar = a_scale;
+    return run_matmul(a, workspace, workspace_bytes, opts, (cudaStream_t)stream);
+}
+
+size_t bwta_attn_qk_workspace_size(int64_t batch_heads, int64_t tq, int64_t tk, int64_t dh, const bwta_opts_t* opts) {
+    opts = opts_or_default(opts);
+    if (batch_heads <= 0 || tq <= 0 || tk <= 0 || dh < 0 || opts->design == BWTA_DESIGN_CUDA_CORE) return 0;
+    MatmulArgs a{};
+    a.M = tq;
+    a.N = tk;
+    a.K = dh;
+    a.lda = a.ldb = ldw_of(dh);
+    a.nb = batch_heads;
+    a.nh = 1;
+    a.a_nz = a.a_sgn = a.b_nz = a.b_sgn = reinterpret_cast<const uint32_t*>(16);
+    a.y_dt = DT_F16;
+    return matmul_tc_supported(a) ? matmul_tc_workspace(a) : 0;
+}
+
+static bwta_status_t check_batch(int64_t batch, int64_t heads) {
+    if (batch < 0 || heads < 1) return BWTA_ERR_SHAPE;
+    if (batch * heads > 65535) return BWTA_ERR_SHAPE;
+    return BWTA_OK;
+}
+
+bwta_status_t bwta_attn_qk(const uint32_t* q_sgn, const uint32_t* q_nz, const uint32_t* k_sgn, const uint32_t* k_nz,
+                           int64_t batch, int64_t heads, int64_t tq, int64_t tk, int64_t dh, int64_t ldq_words,
+                           int64_t q_bstride, int64_t q_hstride, int64_t ldk_words, int64_t k_bstride,
+                           int64_t k_hstride, float alpha, void* s, bwta_dtype_t s_dt, int64_t ld_s,
+                           int64_t s_bstride, int64_t s_hstride, void* workspace, size_t workspace_bytes,
+                           const bwta_opts_t* opts, void* stream) {
+    if (!valid_out_dt(s_dt)) return BWTA_ERR_UNSUPPORTED;
+    bwta_status_t st = check_batch(batch, heads);
+    if (st != BWTA_OK) return st;
+    if (tq < 0 || tk < 0 || dh < 0 || dh > KMAX) return BWTA_ERR_SHAPE;
+    if (q_sgn == nullptr || q_nz == nullptr || k_sgn == nullptr || s == nullptr) return BWTA_ERR_INVALID_VALUE;
+    if (!std::isfinite(alpha)) return BWTA_ERR_INVALID_VALUE;
+    const int64_t need = ldw_of(dh);
+    if (ldq_words < need || ldk_words < need || ld_s < tk) return BWTA_ERR_SHAPE;
+    if (q_bstride < 0 || q_hstride < 0 || k_bstride < 0 || k_hstride < 0 || s_bstride < 0 || s_hstride < 0)
+        return BWTA_ERR_SHAPE;
+    if (ldq_words % 4 || ldk_words % 4 || q_bstride % 4 || q_hstride % 4 || k_bstride % 4 || k_hstride % 4 ||
+        !aligned16(q_sgn) || !aligned16(q_nz) || !aligned16(k_sgn) || (k_nz && !aligned16(k_nz)))
+        return BWTA_ERR_ALIGNMENT;
+    st = check_device();
+    if (st != BWTA_OK) return st;
+    if (batch == 0 || tq == 0 || tk == 0) return BWTA_OK;
+    MatmulArgs a{};
+    a.a_sgn = q_sgn;
+    a.a_nz = q_nz;
+    a.b_sgn = k_sgn;
+    a.b_nz = k_nz;
+    a.M = tq;
+    a.N = tk;
+    a.K = dh;
+    a.lda = ldq_words;
+    a.ldb = ldk_words;
+    a.a_bs = q_bstride;
+    a.a_hs = q_hstride;
+    a.b_bs = k_bstride;
+    a.b_hs = k_hstride;
+    a.nb = batch;
+    a.nh = heads;
+    a.y = s;
+    a.y_dt = s_dt;
+    a.ldy = ld_s;
+    a.y_bs = s_bstride;
+    a.y_hs = s_hstride;
+    a.scalar = alpha;
+    return run_matmul(a, workspace, workspace_bytes, opts, (cudaStream_t)stream);
+}
+
+size_t bwta_attn_pv_workspace_size(int64_t batch_heads, int64_t tq, int64_t tk, int64_t dh, const bwta_opts_t* opts) {
+    opts = opts_or_default(opts);
+    if (batch_heads <= 0 || tq <= 0 || dh <= 0 || tk < 0 || opts->design == BWTA_DESIGN_CUDA_CORE) return 0;
+    MatmulArgs a{};
+    a.M = tq;
+    a.N = dh;
+    a.K = tk;
+    a.lda = a.ldb = ldw_of(tk);
+    a.nb = batch_heads;
+    a.nh = 1;
+    a.a_nz = a.b_nz = a.b_sgn = reinterpret_cast<const uint32_t*>(16);
+    a.y_dt = DT_F16;
+    return matmul_tc_supported(a) ? matmul_tc_workspace(a) : 0;
+}
+
+bwta_status_t bwta_attn_pv(const uint32_t* p_sgn, const uint32_t* p_nz, const uint32_t* vt_sgn, const uint32_t* vt_nz,
+                           int64_t batch, int64_t heads, int64_t tq, int64_t tk, int64_t dh, int64_t ldp_words,
+                           int64_t p_bstride, int64_t p_hstride, int64_t ldv_words, int64_t v_bstride,
+                           int64_t v_hstride, float beta, void* o, bwta_dtype_t o_dt, int64_t ld_o,
+                           int64_t o_bstride, int64_t o_hstride, void* workspace, size_t workspace_bytes,
+                           const bwta_opts_t* opts, void* stream) {
+    if (!valid_out_dt(o_dt)) return BWTA_ERR_UNSUPPORTED;
+    bwta_status_t st = check_batch(batch, heads);
+    if (st != BWTA_OK) return st;
+    if (tq < 0 || tk < 0 || dh < 0 || tk > KMAX) return BWTA_ERR_SHAPE;
+    if (p_nz == nullptr || vt_sgn == nullptr || vt_nz == nullptr || o == nullptr) return BWTA_ERR_INVALID_VALUE;
+    if (!std::isfinite(beta)) return BWTA_ERR_INVALID_VALUE;
+    const int64_t need = ldw_of(tk);
+    if (ldp_words < need || ldv_words < need || ld_o < dh) return BWTA_ERR_SHAPE;
+    if (p_bstride < 0 || p_hstride < 0 || v_bstride < 0 || v_hstride < 0 || o_bstride < 0 || o_hstride < 0)
+        return BWTA_ERR_SHAPE;
+    if (ldp_words % 4 || ldv_words % 4 || p_bstride % 4 || p_hstride % 4 || v_bstride % 4 || v_hstride % 4 ||
+        !aligned16(p_nz) || (p_sgn && !aligned16(p_sgn)) || !aligned16(vt_sgn) || !aligned16(vt_nz))
+        return BWTA_ERR_ALIGNMENT;
+    st = check_device();
+    if (st != BWTA_OK) return st;
+    if (batch == 0 || tq == 0 || dh == 0) return BWTA_OK;
+    MatmulArgs a{};
+    a.a_sgn = p_sgn;
+    a.a_nz = p_nz;
+    a.b_sgn = vt_sgn;
+    a.b_nz = vt_nz;
+    a.M = tq;
+    a.N = dh;
+    a.K = tk;
+    a.lda = ldp_words;
+    a.ldb = ldv_words;
+    a.a_bs = p_bstride;
+    a.a_hs = p_hstride;
+    a.b_bs = v_bstride;
+    a.b_hs = v_hstride;
+    a.nb = batch;
+    a.nh = heads;
+    a.y = o;
+    a.y_dt = o_dt;
+    a.ldy = ld_o;
+    a.y_bs = o_bstride;
+    a.y_hs = o_hstride;
+    a.scalar = beta;
+    return run_matmul(a, workspace, workspace_bytes, opts, (cudaStream_t)stream);
+}
+
+}  // extern "C"

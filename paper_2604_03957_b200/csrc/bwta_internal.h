@@ -1,0 +1,72 @@
+// Internal declarations shared by the BWTA CUDA sources (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bwta {
+
+enum Dt { DT_F16 = 0, DT_BF16 = 1, DT_F32 = 2, DT_I32 = 3 };
+enum Kind { K_BINARY = 0, K_BOOL = 1, K_TERNARY = 2 };
+
+// Thresholds in the storage type of x (see pack.cu: exact predicate rewrite).
+//   q = +1  <=>  x >= tp        (tp = smallest storage value >= s/2)
+//   q = -1  <=>  x <= ntn       (ntn = -(smallest storage value > s/2))
+struct Thresholds {
+    uint32_t tp2;   // f16/bf16: the 16-bit pattern of tp duplicated in both halves
+    uint32_t ntn2;  // f16/bf16: the 16-bit pattern of ntn duplicated
+    float tpf;      // f32 inputs
+    float ntnf;
+};
+
+struct PackArgs {
+    const void* x;
+    int dt;
+    int64_t nb, nh, rows, cols, ld_x, x_bs, x_hs;  // elements
+    int kind;
+    uint32_t* sgn;
+    uint32_t* nz;
+    int64_t ldw, p_bs, p_hs;  // words
+    int32_t* row_nnz;
+    const float* mu;  // binary (weights) only
+    int mu_per_row;
+    Thresholds th;
+    bool vec_ok;  // x rows are 16-byte aligned -> 128-bit loads
+};
+
+cudaError_t launch_pack_rows(const PackArgs& a, cudaStream_t s);
+cudaError_t launch_pack_cols(const PackArgs& a, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// Bit-serial matmul (design (a)) and the generic matmul description shared by
+// both designs.  Entry e = b*nh + h; operand X at base + b*X_bs + h*X_hs.
+//   dot[i][j] = sum_w  popc(m) - 2 popc(m & (a_sgn ^ b_sgn)),  m = a_nz & b_nz
+// with absent planes read as sgn = 0, nz = all-ones.
+// Epilogue: c = col_scale ? fl32(col_scale[j] * scalar) : scalar
+//           y = fl32(float(dot) * c) -> out_dt (I32: raw dot)
+// ---------------------------------------------------------------------------
+struct MatmulArgs {
+    const uint32_t* a_sgn;
+    const uint32_t* a_nz;
+    const uint32_t* b_sgn;
+    const uint32_t* b_nz;
+    int64_t M, N, K;        // K in elements
+    int64_t lda, ldb;       // words
+    int64_t a_bs, a_hs, b_bs, b_hs;  // words
+    int64_t nb, nh;
+    void* y;
+    int y_dt;
+    int64_t ldy, y_bs, y_hs;  // elements
+    int y_trans;              // store Y^T (y[j*ldy + i])
+    const float* col_scale;   // [N] or null
+    float scalar;
+};
+
+cudaError_t launch_matmul_cc(const MatmulArgs& a, cudaStream_t s);
+
+// tcgen05 path (design (b)).  Returns cudaErrorNotSupported when the shape is
+// outside what the tcgen05 kernels handle (the dispatcher then uses design (a)).
+size_t matmul_tc_workspace(const MatmulArgs& a);
+bool matmul_tc_supported(const MatmulArgs& a);
+cudaError_t launch_matmul_tc(const MatmulArgs& a, void* ws, size_t ws_bytes, cudaStream_t s);
+
+}  // namespace bwta

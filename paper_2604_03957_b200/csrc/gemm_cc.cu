@@ -1,0 +1,189 @@
+// gemm_cc.cu -- design (a): bit-serial BWTA matmul on CUDA cores (sm_100a).
+//
+// dot[i][j] = sum_words popc(m) - 2*popc(m & (a_sgn ^ b_sgn)),  m = a_nz & b_nz
+// which equals sum_k qa[i][k]*qb[j][k] for
+//   Case 1 (linear): A ternary/bool, B binary (b_nz = all ones)
+//   Case 2 (P.V,  P:327-328):   A bool (a_sgn = 0), B ternary
+//   Case 3 (Q.K^T):  A ternary, B ternary
+// (per bit: m = 0 -> 0; m = 1 -> +1 if signs agree, -1 otherwise).
+// The paper issues these as b1 mma.sync (xor/and + popc); sm_100a has no
+// native b1 MMA (it is emulated through IMMA + MOVM), so design (a) runs the
+// identity on the integer pipes: one LOP3 + one POPC + one IADD per (output,
+// 32-bit word) for Case 1, with popc(a_nz) hoisted per row.
+//
+// Tiling: 128x128 outputs per CTA, 256 threads, 8x8 outputs per thread in
+// registers, K streamed in 8-word (256-element) slabs through a double-
+// buffered shared-memory ring stored word-major ([word][row]) so the inner
+// loop reads 128-bit vectors of 4 rows at a time.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "bwta_internal.h"
+
+namespace bwta {
+namespace {
+
+constexpr int BM = 128, BN = 128, KW = 8, TM = 8, TN = 8, NT = 256;
+constexpr int PAD = 4;  // row padding of the word-major smem tiles (bank spread)
+
+__device__ __forceinline__ void store_out(void* y, int dt, int64_t idx, int32_t dot, float c) {
+    if (dt == DT_I32) {
+        reinterpret_cast<int32_t*>(y)[idx] = dot;
+        return;
+    }
+    const float v = __fmul_rn(__int2float_rn(dot), c);
+    if (dt == DT_F16) reinterpret_cast<__half*>(y)[idx] = __float2half_rn(v);
+    else if (dt == DT_BF16) reinterpret_cast<__nv_bfloat16*>(y)[idx] = __float2bfloat16_rn(v);
+    else reinterpret_cast<float*>(y)[idx] = v;
+}
+
+template <bool A_SGN, bool B_NZ>
+__global__ void __launch_bounds__(NT) matmul_cc_kernel(MatmulArgs p) {
+    __shared__ __align__(16) uint32_t sAs[2][KW][BM + PAD];
+    __shared__ __align__(16) uint32_t sAn[2][KW][BM + PAD];
+    __shared__ __align__(16) uint32_t sBs[2][KW][BN + PAD];
+    __shared__ __align__(16) uint32_t sBn[2][KW][BN + PAD];
+
+    const int t = threadIdx.x;
+    const int tx = t & 15, ty = t >> 4;
+    const int64_t e = blockIdx.z;
+    const int64_t i0 = int64_t(blockIdx.y) * BM, j0 = int64_t(blockIdx.x) * BN;
+    const int64_t eb = e / p.nh, eh = e % p.nh;
+    const uint32_t* As = A_SGN ? p.a_sgn + eb * p.a_bs + eh * p.a_hs : nullptr;
+    const uint32_t* An = p.a_nz + eb * p.a_bs + eh * p.a_hs;
+    const uint32_t* Bs = p.b_sgn + eb * p.b_bs + eh * p.b_hs;
+    const uint32_t* Bn = B_NZ ? p.b_nz + eb * p.b_bs + eh * p.b_hs : nullptr;
+    const int64_t kw = (p.K + 31) / 32;
+    const int64_t kw4 = (kw + 3) & ~int64_t(3);  // <= ld (validated); padding words are 0
+    const int nslab = int((kw4 + KW - 1) / KW);
+
+    // global -> register staging: thread t loads row t/2, words (t%2)*4 .. +3
+    const int lr = t >> 1, lw = (t & 1) * 4;
+    uint4 ra_s, ra_n, rb_s, rb_n;
+    auto gload = [&](int slab) {
+        const int64_t w = int64_t(slab) * KW + lw;
+        const bool wok = w < kw4;
+        const int64_t ia = i0 + lr, jb = j0 + lr;
+        const uint4 z = make_uint4(0, 0, 0, 0);
+        ra_n = (wok && ia < p.M) ? *reinterpret_cast<const uint4*>(An + ia * p.lda + w) : z;
+        if (A_SGN) ra_s = (wok && ia < p.M) ? *reinterpret_cast<const uint4*>(As + ia * p.lda + w) : z;
+        rb_s = (wok && jb < p.N) ? *reinterpret_cast<const uint4*>(Bs + jb * p.ldb + w) : z;
+        if (B_NZ) rb_n = (wok && jb < p.N) ? *reinterpret_cast<const uint4*>(Bn + jb * p.ldb + w) : z;
+    };
+    auto sstore = [&](int buf) {
+        const uint32_t an[4] = {ra_n.x, ra_n.y, ra_n.z, ra_n.w};
+        const uint32_t as[4] = {ra_s.x, ra_s.y, ra_s.z, ra_s.w};
+        const uint32_t bs[4] = {rb_s.x, rb_s.y, rb_s.z, rb_s.w};
+        const uint32_t bn[4] = {rb_n.x, rb_n.y, rb_n.z, rb_n.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            sAn[buf][lw + q][lr] = an[q];
+            if (A_SGN) sAs[buf][lw + q][lr] = as[q];
+            sBs[buf][lw + q][lr] = bs[q];
+            if (B_NZ) sBn[buf][lw + q][lr] = bn[q];
+        }
+    };
+
+    int32_t acc[TM][TN];
+    int32_t acc2[TM][TN];
+    int32_t base[TM];
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        base[i] = 0;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = 0, acc2[i][j] = 0;
+    }
+    if (!A_SGN) ra_s = make_uint4(0, 0, 0, 0);
+    if (!B_NZ) rb_n = make_uint4(0, 0, 0, 0);
+
+    if (nslab > 0) {
+        gload(0);
+        sstore(0);
+    }
+    __syncthreads();
+    for (int slab = 0; slab < nslab; ++slab) {
+        const int buf = slab & 1;
+        if (slab + 1 < nslab) gload(slab + 1);
+#pragma unroll
+        for (int w = 0; w < KW; ++w) {
+            uint32_t an[TM], as[TM], bs[TN], bn[TN];
+            const uint4* pan = reinterpret_cast<const uint4*>(&sAn[buf][w][ty * TM]);
+            const uint4* pbs = reinterpret_cast<const uint4*>(&sBs[buf][w][tx * TN]);
+            uint4 v0 = pan[0], v1 = pan[1];
+            an[0] = v0.x; an[1] = v0.y; an[2] = v0.z; an[3] = v0.w;
+            an[4] = v1.x; an[5] = v1.y; an[6] = v1.z; an[7] = v1.w;
+            v0 = pbs[0]; v1 = pbs[1];
+            bs[0] = v0.x; bs[1] = v0.y; bs[2] = v0.z; bs[3] = v0.w;
+            bs[4] = v1.x; bs[5] = v1.y; bs[6] = v1.z; bs[7] = v1.w;
+            if (A_SGN) {
+                const uint4* pas = reinterpret_cast<const uint4*>(&sAs[buf][w][ty * TM]);
+                v0 = pas[0]; v1 = pas[1];
+                as[0] = v0.x; as[1] = v0.y; as[2] = v0.z; as[3] = v0.w;
+                as[4] = v1.x; as[5] = v1.y; as[6] = v1.z; as[7] = v1.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < TM; ++i) as[i] = 0;
+            }
+            if (B_NZ) {
+                const uint4* pbn = reinterpret_cast<const uint4*>(&sBn[buf][w][tx * TN]);
+                v0 = pbn[0]; v1 = pbn[1];
+                bn[0] = v0.x; bn[1] = v0.y; bn[2] = v0.z; bn[3] = v0.w;
+                bn[4] = v1.x; bn[5] = v1.y; bn[6] = v1.z; bn[7] = v1.w;
+            }
+            if (!B_NZ) {
+#pragma unroll
+                for (int i = 0; i < TM; ++i) {
+                    base[i] += __popc(an[i]);
+#pragma unroll
+                    for (int j = 0; j < TN; ++j) acc[i][j] += __popc(an[i] & (as[i] ^ bs[j]));
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < TM; ++i)
+#pragma unroll
+                    for (int j = 0; j < TN; ++j) {
+                        const uint32_t m = an[i] & bn[j];
+                        acc2[i][j] += __popc(m);
+                        acc[i][j] += __popc(m & (as[i] ^ bs[j]));
+                    }
+            }
+        }
+        if (slab + 1 < nslab) {
+            sstore(buf ^ 1);
+        }
+        __syncthreads();
+    }
+
+    // epilogue
+    void* Y = p.y;
+    const int64_t ybase = eb * p.y_bs + eh * p.y_hs;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+        const int64_t gj = j0 + tx * TN + j;
+        if (gj >= p.N) continue;
+        const float c = p.col_scale ? __fmul_rn(p.col_scale[gj], p.scalar) : p.scalar;
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+            const int64_t gi = i0 + ty * TM + i;
+            if (gi >= p.M) continue;
+            const int32_t d = B_NZ ? acc2[i][j] - 2 * acc[i][j] : base[i] - 2 * acc[i][j];
+            const int64_t idx = ybase + (p.y_trans ? gj * p.ldy + gi : gi * p.ldy + gj);
+            store_out(Y, p.y_dt, idx, d, c);
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_matmul_cc(const MatmulArgs& a, cudaStream_t s) {
+    if (a.M == 0 || a.N == 0 || a.nb * a.nh == 0) return cudaSuccess;
+    dim3 grid(unsigned((a.N + BN - 1) / BN), unsigned((a.M + BM - 1) / BM), unsigned(a.nb * a.nh));
+    const bool asg = a.a_sgn != nullptr, bnz = a.b_nz != nullptr;
+    if (asg && bnz) matmul_cc_kernel<true, true><<<grid, NT, 0, s>>>(a);
+    else if (asg) matmul_cc_kernel<true, false><<<grid, NT, 0, s>>>(a);
+    else if (bnz) matmul_cc_kernel<false, true><<<grid, NT, 0, s>>>(a);
+    else matmul_cc_kernel<false, false><<<grid, NT, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace bwta

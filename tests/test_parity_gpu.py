@@ -1,0 +1,308 @@
+"""GPU parity: the CUDA path (through the C ABI via the thin binding) against
+the CPU oracle, element by element, on the same seeded inputs.
+
+Bar (BASELINE.json north_star): packed planes, row counts and integer dots
+bit-exact; FP16/BF16/FP32 outputs within 1e-3 relative (asserted here as
+bit-exact, which is stronger: both sides evaluate the same R5 expression).
+"""
+import numpy as np
+import pytest
+import torch
+
+import bwta_inputs as gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+DT = {torch.float16: "f16", torch.bfloat16: "bf16", torch.float32: "f32"}
+
+
+@pytest.fixture(scope="module")
+def B():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2604_03957_b200 as B
+    return B
+
+
+def storage(x: torch.Tensor) -> np.ndarray:
+    x = x.detach().cpu().contiguous()
+    if x.dtype in (torch.float16, torch.bfloat16):
+        return x.view(torch.int16).numpy().view(np.uint16)
+    return x.numpy()
+
+
+def words(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().contiguous().numpy().view(np.uint32)
+
+
+def out_storage(y: torch.Tensor) -> np.ndarray:
+    y = y.detach().cpu().contiguous()
+    if y.dtype in (torch.float16, torch.bfloat16):
+        return y.view(torch.int16).numpy().view(np.uint16)
+    return y.numpy()
+
+
+def assert_out_equal(got: torch.Tensor, ref: np.ndarray, what=""):
+    g = out_storage(got)
+    if got.dtype == torch.float32:
+        gi, ri = g.view(np.uint32), ref.view(np.uint32)
+    else:
+        gi, ri = g, ref
+    bad = np.nonzero(gi != ri)
+    if bad[0].size:
+        # report the relative error too (the north-star bar is 1e-3)
+        idx = tuple(b[:5] for b in bad)
+        raise AssertionError(f"{what}: {bad[0].size} mismatches, first at {idx}: got {gi[idx]} ref {ri[idx]}")
+
+
+def _bump(v: torch.Tensor, away: bool) -> torch.Tensor:
+    """Next representable value of the same dtype, away from / toward zero (v finite, non-zero)."""
+    it = {torch.float16: torch.int16, torch.bfloat16: torch.int16, torch.float32: torch.int32}[v.dtype]
+    b = v.reshape(1).clone().view(it)
+    b += 1 if away else -1        # sign-magnitude encoding: +-1 on the magnitude bits
+    return b.view(v.dtype).reshape(())
+
+
+def inject_specials(x: torch.Tensor, s: float, seed: int) -> torch.Tensor:
+    """Put exact ties (+-s/2), their neighbours, +-0, +-inf, NaN and tiny values at random places."""
+    x = x.clone()
+    flat = x.view(-1)
+    n = flat.numel()
+    g = torch.Generator().manual_seed(seed)
+    dt = x.dtype
+    vals = [torch.tensor(0.0, dtype=dt), torch.tensor(-0.0, dtype=dt), torch.tensor(float("inf"), dtype=dt),
+            torch.tensor(float("-inf"), dtype=dt), torch.tensor(float("nan"), dtype=dt),
+            torch.tensor(1e-7, dtype=dt), torch.tensor(-1e-7, dtype=dt)]
+    if s > 0:
+        half = torch.tensor(s / 2, dtype=torch.float64).to(dt)
+        assert float(half) == s / 2
+        vals += [half, -half, _bump(half, True), _bump(half, False), _bump(-half, True), _bump(-half, False)]
+    k = min(n, 4 * len(vals))
+    pos = torch.randperm(n, generator=g)[:k]
+    for i, p in enumerate(pos.tolist()):
+        flat[p] = vals[i % len(vals)]
+    return x
+
+
+def tie_scale(dt, seed):
+    # a scale whose half is exactly representable in every storage type
+    g = torch.Generator().manual_seed(seed)
+    return float(torch.tensor(0.5 + torch.rand(1, generator=g).item(), dtype=torch.bfloat16).float() * 2)
+
+
+# ----------------------------------------------------------------- pack ----
+SHAPES = [(1, 1), (3, 31), (5, 33), (7, 64), (9, 257), (64, 768), (33, 1000), (130, 129)]
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("kind", ["ternary", "bool"])
+@pytest.mark.parametrize("transpose", [False, True])
+def test_pack_act_parity(B, dtype, kind, transpose):
+    for i, (r, c) in enumerate(SHAPES):
+        seed = 1000 + i
+        s = tie_scale(dtype, seed)
+        x = inject_specials(gen.activations((2, r, c), seed, dtype), s, seed)
+        p = B.bwta_pack_act(x.cuda(), s, kind, transpose=transpose, row_nnz=True)
+        sgn, nz, nnz = oracle.pack_act(storage(x), DT[dtype], s, kind, transpose=transpose)
+        assert np.array_equal(words(p.nz), nz), (r, c)
+        if kind == "ternary":
+            assert np.array_equal(words(p.sgn), sgn), (r, c)
+        else:
+            assert p.sgn is None
+        assert np.array_equal(p.row_nnz.cpu().numpy(), nnz), (r, c)
+
+
+@pytest.mark.parametrize("transpose", [False, True])
+def test_pack_act_strided_heads_and_unaligned(B, transpose):
+    Bsz, T, H, D = 2, 37, 3, 64
+    qkv = gen.activations((Bsz, T, 3 * H * D), 77).cuda()
+    qkv1 = gen.activations((Bsz, T, 3 * H * D + 1), 78).cuda()
+    s = 1.3
+    # [B, H, T, D] view of the K third (aligned rows), and a view whose rows are
+    # not 16-byte aligned (odd element offset and row stride): the scalar path
+    for view in (qkv[:, :, H * D:2 * H * D].unflatten(-1, (H, D)).transpose(1, 2),
+                 qkv1[:, :, 1:1 + H * D].unflatten(-1, (H, D)).transpose(1, 2)):
+        p = B.bwta_pack_act(view, s, "ternary", transpose=transpose)
+        sgn, nz, _ = oracle.pack_act(storage(view.contiguous()).reshape(Bsz * H, T, D), "f16", s, "ternary",
+                                     transpose=transpose)
+        assert np.array_equal(words(p.nz).reshape(nz.shape), nz)
+        assert np.array_equal(words(p.sgn).reshape(sgn.shape), sgn)
+
+
+def test_pack_act_tiny_and_huge_scales(B):
+    x = gen.activations((4, 300), 5, torch.float16)
+    x[0, :8] = torch.tensor([6e-8, -6e-8, 1e-5, -1e-5, 65504, -65504, 3e-8, -3e-8], dtype=torch.float16)
+    for s in (1e-7, 1.2e-7, 3e-5, 131000.0, 1e30, 2.0 ** -130):
+        p = B.bwta_pack_act(x.cuda(), s, "ternary")
+        sgn, nz, _ = oracle.pack_act(storage(x), "f16", s, "ternary")
+        assert np.array_equal(words(p.nz), nz) and np.array_equal(words(p.sgn), sgn), s
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16, torch.float32])
+def test_pack_weight_parity(B, dtype):
+    for n, k, seed in ((1, 1, 1), (5, 33, 2), (17, 768, 3), (64, 1000, 4)):
+        w = gen.weights(n, k, seed, dtype)
+        w = inject_specials(w, 0.0, seed)
+        mu_s = float(torch.tensor(0.001, dtype=torch.float32))
+        for mu, per_row in ((None, False), (mu_s, False), ("row", True)):
+            if mu == "row":
+                mu_t = gen.normal((n,), seed + 9, torch.float32, std=0.01)
+                p = B.bwta_pack_weight(w.cuda(), mu=mu_t.cuda() if n > 1 else mu_t.cuda())
+                ref = oracle.pack_weight(storage(w), DT[dtype], mu=mu_t.numpy(), mu_per_row=n > 1)
+            else:
+                p = B.bwta_pack_weight(w.cuda(), mu=mu)
+                ref = oracle.pack_weight(storage(w), DT[dtype], mu=mu)
+            assert np.array_equal(words(p.sgn), ref), (n, k, mu)
+
+
+# ----------------------------------------------------------------- gemm ----
+GEMM_SHAPES = [(1, 1, 1), (7, 5, 31), (33, 17, 33), (129, 130, 100), (200, 129, 768), (64, 300, 1000),
+               (300, 257, 257), (16, 2048, 2048)]
+
+
+def _gemm_case(B, m, n, k, seed, a_kind="ternary"):
+    x = (gen.relu_activations if a_kind == "bool" else gen.activations)((m, k), seed)
+    w = gen.weights(n, k, seed + 1)
+    s_a = gen.act_scale(x) or 1.0     # an all-zero tiny ReLU input has mean 0
+    mu, s_w = gen.weight_stats(w)
+    a = B.bwta_pack_act(x.cuda(), s_a, a_kind)
+    wp = B.bwta_pack_weight(w.cuda(), mu=mu)
+    qa = oracle.quantize_act(storage(x), "f16", s_a, a_kind)
+    qw = oracle.binarize_weight(storage(w), "f16", mu=mu)
+    return a, wp, s_a, s_w, qa, qw
+
+
+@pytest.mark.parametrize("design", ["cuda_core", "auto"])
+def test_gemm_parity(B, design):
+    for i, (m, n, k) in enumerate(GEMM_SHAPES):
+        for a_kind in ("ternary", "bool"):
+            a, wp, s_a, s_w, qa, qw = _gemm_case(B, m, n, k, 2000 + i, a_kind)
+            d = oracle.dot(qa, qw, threads=oracle.default_threads())
+            yi = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.int32, design=design)
+            assert np.array_equal(yi.cpu().numpy(), d), (m, n, k, a_kind)
+            for dt, name in ((torch.float16, "f16"), (torch.bfloat16, "bf16"), (torch.float32, "f32")):
+                y = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=dt, design=design)
+                assert_out_equal(y, oracle.epilogue_linear(d, s_w.numpy(), s_a, name), f"{m}x{n}x{k} {name}")
+            yt = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.float16, y_transposed=True, design=design)
+            assert_out_equal(yt, oracle.epilogue_linear(d, s_w.numpy(), s_a, "f16").T.copy(), "transposed")
+            # no weight scale -> 1
+            y1 = B.bwta_gemm(a, wp, None, s_a, out_dtype=torch.float32, design=design)
+            assert_out_equal(y1, oracle.epilogue_linear(d, None, s_a, "f32"), "no w_scale")
+
+
+def test_gemm_exhaustive_k6(B):
+    """All 3^6 ternary x 2^6 binary (and bool) vectors at K=6, also shifted to
+    straddle a word boundary (offset 29): dot equals the oracle's triple loop."""
+    tern = np.stack(np.meshgrid(*[np.array([-1, 0, 1])] * 6, indexing="ij"), -1).reshape(-1, 6).astype(np.int8)
+    binv = np.stack(np.meshgrid(*[np.array([-1, 1])] * 6, indexing="ij"), -1).reshape(-1, 6).astype(np.int8)
+    for off in (0, 29):
+        K = off + 6
+        qa = np.zeros((tern.shape[0], K), np.int8)
+        qa[:, off:] = tern
+        qw = np.ones((binv.shape[0], K), np.int8)
+        qw[:, off:] = binv
+        sa, na = oracle.pack(qa)
+        sw, _ = oracle.pack(qw, want_nz=False)
+        import paper_2604_03957_b200 as Bm
+        a = Bm.Packed(torch.from_numpy(sa.view(np.int32)).cuda(), torch.from_numpy(na.view(np.int32)).cuda(),
+                      "ternary", K)
+        w = Bm.Packed(torch.from_numpy(sw.view(np.int32)).cuda(), None, "binary", K)
+        for design in ("cuda_core", "auto"):
+            y = B.bwta_gemm(a, w, None, 1.0, out_dtype=torch.int32, design=design)
+            assert np.array_equal(y.cpu().numpy(), oracle.dot(qa, qw)), (off, design)
+
+
+def test_gemm_k_zero_and_empty(B):
+    import paper_2604_03957_b200 as Bm
+    # K = 0: planes must still be valid pointers (the ABI rejects NULL); nothing is read
+    a = Bm.Packed(torch.zeros((3, 4), dtype=torch.int32, device="cuda"),
+                  torch.zeros((3, 4), dtype=torch.int32, device="cuda"), "ternary", 0)
+    w = Bm.Packed(torch.zeros((2, 4), dtype=torch.int32, device="cuda"), None, "binary", 0)
+    y = B.bwta_gemm(a, w, None, 2.0, out_dtype=torch.float32)
+    assert torch.equal(y.cpu(), torch.zeros(3, 2))
+    a0 = Bm.Packed(torch.zeros((0, 4), dtype=torch.int32, device="cuda"),
+                   torch.zeros((0, 4), dtype=torch.int32, device="cuda"), "ternary", 100)
+    w0 = Bm.Packed(torch.zeros((2, 4), dtype=torch.int32, device="cuda"), None, "binary", 100)
+    assert B.bwta_gemm(a0, w0, None, 1.0).shape == (0, 2)
+
+
+# ------------------------------------------------------------ attention ----
+ATT = [(1, 1, 1, 1, 64), (2, 3, 37, 41, 64), (1, 2, 128, 128, 128), (2, 2, 130, 129, 33), (1, 1, 256, 300, 128)]
+
+
+@pytest.mark.parametrize("design", ["cuda_core", "auto"])
+def test_attention_parity(B, design):
+    for i, (b, h, tq, tk, dh) in enumerate(ATT):
+        seed = 3000 + 10 * i
+        q = gen.activations((b, h, tq, dh), seed)
+        k = gen.activations((b, h, tk, dh), seed + 1)
+        v = gen.activations((b, h, tk, dh), seed + 2)
+        sq, sk, sv = gen.act_scale(q), gen.act_scale(k), gen.act_scale(v)
+        alpha = float(np.float32(sq * sk / np.sqrt(dh)))
+        qp = B.bwta_pack_act(q.cuda(), sq, "ternary")
+        kp = B.bwta_pack_act(k.cuda(), sk, "ternary")
+        oq = oracle.quantize_act(storage(q).reshape(b * h, tq, dh), "f16", sq, "ternary")
+        ok = oracle.quantize_act(storage(k).reshape(b * h, tk, dh), "f16", sk, "ternary")
+        for dt, name in ((torch.int32, "i32"), (torch.float16, "f16"), (torch.float32, "f32")):
+            s = B.bwta_attn_qk(qp, kp, alpha, out_dtype=dt, design=design)
+            ref = oracle.attn_qk(oq, ok, alpha, name, threads=4).reshape(b, h, tq, tk)
+            assert_out_equal(s, ref, f"qk {b,h,tq,tk,dh} {name}")
+        # binary K (nz == all ones)
+        kb = B.bwta_pack_weight(k.reshape(-1, dh).cuda())
+        kbp = type(kp)(kb.sgn.reshape(b, h, tk, -1), None, "binary", dh)
+        s = B.bwta_attn_qk(qp, kbp, 1.0, out_dtype=torch.int32, design=design)
+        okb = oracle.binarize_weight(storage(k).reshape(-1, dh), "f16").reshape(b * h, tk, dh)
+        assert_out_equal(s, oracle.attn_qk(oq, okb, 1.0, "i32").reshape(b, h, tq, tk), "qk binary K")
+        # PV: P bool from synthetic softmax probabilities, V^T via the transposed pack
+        p = gen.attention_probs((b, h, tq, tk), seed + 3)
+        s_att = float(np.float32(2.0 / tk))
+        beta = float(np.float32(s_att * sv))
+        pp = B.bwta_pack_act(p.cuda(), s_att, "bool")
+        vt = B.bwta_pack_act(v.cuda(), sv, "ternary", transpose=True)
+        op = oracle.quantize_act(storage(p).reshape(b * h, tq, tk), "f16", s_att, "bool")
+        ov = oracle.quantize_act(storage(v).reshape(b * h, tk, dh), "f16", sv, "ternary")
+        for dt, name in ((torch.int32, "i32"), (torch.float16, "f16"), (torch.bfloat16, "bf16")):
+            o = B.bwta_attn_pv(pp, vt, beta, out_dtype=dt, design=design)
+            ref = oracle.attn_pv(op, ov, beta, name, threads=4).reshape(b, h, tq, dh)
+            assert_out_equal(o, ref, f"pv {b,h,tq,tk,dh} {name}")
+
+
+def test_attention_strided_heads_from_qkv(B):
+    """Q/K/V as per-head views of a [B, T, 3*H*D] projection output (no copies)."""
+    Bsz, T, H, D = 3, 128, 4, 64
+    qkv = gen.activations((Bsz, T, 3 * H * D), 99).cuda()
+    q = qkv[..., :H * D].unflatten(-1, (H, D)).transpose(1, 2)
+    k = qkv[..., H * D:2 * H * D].unflatten(-1, (H, D)).transpose(1, 2)
+    sq, sk = gen.act_scale(q), gen.act_scale(k)
+    qp = B.bwta_pack_act(q, sq, "ternary")
+    kp = B.bwta_pack_act(k, sk, "ternary")
+    s = B.bwta_attn_qk(qp, kp, 0.25, out_dtype=torch.int32)
+    oq = oracle.quantize_act(storage(q.contiguous()).reshape(-1, T, D), "f16", sq, "ternary")
+    ok = oracle.quantize_act(storage(k.contiguous()).reshape(-1, T, D), "f16", sk, "ternary")
+    assert np.array_equal(s.cpu().numpy().reshape(-1, T, T), oracle.attn_qk(oq, ok, 1.0, "i32"))
+
+
+# ------------------------------------------------- full-size (bench) shapes ----
+@pytest.mark.parametrize("n", [4096, 11008])
+def test_llama_prefill_full_size_sampled(B, n):
+    """C3 at full size in the bench's launch configuration: every output row
+    sampled is checked against the oracle (one row at a time)."""
+    m, k = 2048, 4096
+    x = gen.activations((m, k), 303)
+    w = gen.weights(n, k, 304)
+    s_a = gen.act_scale(x)
+    mu, s_w = gen.weight_stats(w)
+    a = B.bwta_pack_act(x.cuda(), s_a, "ternary")
+    wp = B.bwta_pack_weight(w.cuda(), mu=mu)
+    y = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.float16)
+    yi = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.int32)
+    rows = np.random.default_rng(1).choice(m, 12, replace=False)
+    rows = np.concatenate([rows, [0, m - 1]])
+    qa = oracle.quantize_act(storage(x[rows]), "f16", s_a, "ternary")
+    qw = oracle.binarize_weight(storage(w), "f16", mu=mu)
+    d = oracle.dot(qa, qw, threads=oracle.default_threads())
+    assert np.array_equal(yi.cpu().numpy()[rows], d)
+    assert_out_equal(y[torch.from_numpy(rows).cuda()], oracle.epilogue_linear(d, s_w.numpy(), s_a, "f16"), "C3")
+    # planes of sampled rows
+    sgn, nz, _ = oracle.pack_act(storage(x[rows]), "f16", s_a, "ternary")
+    assert np.array_equal(words(a.nz)[rows], nz) and np.array_equal(words(a.sgn)[rows], sgn)
