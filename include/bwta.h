@@ -176,7 +176,8 @@ BWTA_API bwta_status_t bwta_pack_weight(const void* w, bwta_dtype_t w_dt, int64_
  *          dtype y_dt in F16 | BF16 | F32 | I32.
  * workspace: device scratch of >= bwta_gemm_workspace_size(m, n, k, opts)
  *          bytes (may be NULL when that size is 0), 256-byte aligned.
- * 0 <= k <= 2^24.  m == 0 or n == 0: nothing to do, returns BWTA_OK.
+ * 0 <= k <= 2^24.  m == 0 or n == 0: nothing to do, returns BWTA_OK without
+ * looking at the pointers (empty tensors may have NULL data).
  */
 BWTA_API size_t bwta_gemm_workspace_size(int64_t m, int64_t n, int64_t k, const bwta_opts_t* opts);
 

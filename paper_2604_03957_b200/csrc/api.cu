@@ -262,6 +262,7 @@ bwta_status_t bwta_gemm(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t
     if (a_kind != BWTA_TERNARY && a_kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
     if (!valid_out_dt(y_dt)) return BWTA_ERR_UNSUPPORTED;
     if (m < 0 || n < 0 || k < 0 || k > KMAX) return BWTA_ERR_SHAPE;
+    if (m == 0 || n == 0) return BWTA_OK;  // empty product: nothing to read or write
     if (a_nz == nullptr || w_sgn == nullptr || y == nullptr) return BWTA_ERR_INVALID_VALUE;
     if ((a_kind == BWTA_TERNARY) != (a_sgn != nullptr)) return BWTA_ERR_INVALID_VALUE;
     if (!std::isfinite(a_scale)) return BWTA_ERR_INVALID_VALUE;
@@ -304,6 +305,7 @@ size_t bwta_attn_qk_workspace_size(int64_t batch_heads, int64_t tq, int64_t tk, 
     a.lda = a.ldb = ldw_of(dh);
     a.nb = batch_heads;
     a.nh = 1;
+    a.a_bs = a.b_bs = 4;  // any real stride: the size depends only on the shape
     a.a_nz = a.a_sgn = a.b_nz = a.b_sgn = reinterpret_cast<const uint32_t*>(16);
     a.y_dt = DT_F16;
     return matmul_tc_supported(a) ? matmul_tc_workspace(a) : 0;
@@ -325,6 +327,7 @@ bwta_status_t bwta_attn_qk(const uint32_t* q_sgn, const uint32_t* q_nz, const ui
     bwta_status_t st = check_batch(batch, heads);
     if (st != BWTA_OK) return st;
     if (tq < 0 || tk < 0 || dh < 0 || dh > KMAX) return BWTA_ERR_SHAPE;
+    if (batch == 0 || tq == 0 || tk == 0) return BWTA_OK;
     if (q_sgn == nullptr || q_nz == nullptr || k_sgn == nullptr || s == nullptr) return BWTA_ERR_INVALID_VALUE;
     if (!std::isfinite(alpha)) return BWTA_ERR_INVALID_VALUE;
     const int64_t need = ldw_of(dh);
@@ -372,6 +375,7 @@ size_t bwta_attn_pv_workspace_size(int64_t batch_heads, int64_t tq, int64_t tk, 
     a.lda = a.ldb = ldw_of(tk);
     a.nb = batch_heads;
     a.nh = 1;
+    a.a_bs = a.b_bs = 4;  // any real stride: the size depends only on the shape
     a.a_nz = a.b_nz = a.b_sgn = reinterpret_cast<const uint32_t*>(16);
     a.y_dt = DT_F16;
     return matmul_tc_supported(a) ? matmul_tc_workspace(a) : 0;
@@ -387,6 +391,7 @@ bwta_status_t bwta_attn_pv(const uint32_t* p_sgn, const uint32_t* p_nz, const ui
     bwta_status_t st = check_batch(batch, heads);
     if (st != BWTA_OK) return st;
     if (tq < 0 || tk < 0 || dh < 0 || tk > KMAX) return BWTA_ERR_SHAPE;
+    if (batch == 0 || tq == 0 || dh == 0) return BWTA_OK;
     if (p_nz == nullptr || vt_sgn == nullptr || vt_nz == nullptr || o == nullptr) return BWTA_ERR_INVALID_VALUE;
     if (!std::isfinite(beta)) return BWTA_ERR_INVALID_VALUE;
     const int64_t need = ldw_of(tk);
