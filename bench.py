@@ -1,0 +1,644 @@
+"""bench.py -- BWTA hot path on B200: effective TOPS of the BWTA matmuls (and
+bitpack GB/s) against cuBLAS FP16 on the same GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl bwta|reference]
+                    [--workload bert_layer|llama_prefill|llama_attn|bert_linear]
+
+Metric (BASELINE.json): "BWTA GEMM effective TOPS and speedup vs cuBLAS FP16 on
+B200; bitpack HBM GB/s".  Effective TOPS = 2*M*N*K / t (the paper's
+convention), summed over every BWTA matmul of one step.
+
+Default workload = BASELINE.json configs[1]: one BERT-base layer (batch 32 x
+seq 128, hidden 768, 12 heads x 64, FFN 3072).  A step runs every §8(a) row of
+the hot path once: ternary pack of the layer input, QKV linear, per-head
+ternary packs of Q/K and the transposed ternary pack of V (straight from the
+QKV output, no copies), QK^T, bool pack of the attention probabilities, PV
+(written into the [B, T, H*D] context layout), ternary pack + output
+projection, ternary pack + FFN1, bool pack + FFN2.  The FP operators the
+paper keeps in high precision (softmax, LayerNorm, activation)
+are not part of the BWTA library: their outputs are synthetic tensors with the
+recipe's distributions (bwta_inputs.py), generated outside the timed region.
+
+Timing: each step is one CUDA-graph replay of the library calls, bracketed by
+CUDA events on the capture stream; a 256 MiB buffer (> 126 MB L2) is written
+between steps (outside the events), so every step starts L2-cold.  N > 1 GPUs
+(torchrun): every rank runs its own replica of the workload (independent
+batches: weak scaling, no collective on the data path); time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bwta_inputs as gen  # noqa: E402
+
+METRIC = "BWTA GEMM effective TOPS and speedup vs cuBLAS FP16 on B200; bitpack HBM GB/s"
+UNIT = "TOPS"
+
+
+# ----------------------------------------------------------------------------- utils
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+def peaks():
+    mp = measured_peaks()
+    if mp:
+        return {"hbm_gbs": mp["hbm_gbs"], "bf16_tflops": mp["bf16_tflops"],
+                "bf16_tflops_sustained": mp.get("bf16_tflops_sustained"), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True,
+                                         bufsize=1)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def graph_of(fn, stream):
+    """Capture fn (after one eager warm-up run) into a CUDA graph."""
+    with torch.cuda.stream(stream):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        fn()
+    torch.cuda.synchronize()
+    return g
+
+
+def time_graph(g, flush, reps, warmup, stream):
+    """Median / list of per-replay device times (ms), L2 flushed before each replay."""
+    ts = []
+    with torch.cuda.stream(stream):
+        for i in range(warmup + reps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+            if i >= warmup:
+                ts.append((e0, e1))
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ts]
+
+
+def op_time_ms(fn, flush, stream, reps=20, trials=5):
+    """Device time of one call of fn, L2-cold: a graph of reps x [flush, fn] minus a
+    graph of reps x [flush], so the graph-launch latency is amortised away."""
+    def body():
+        for _ in range(reps):
+            flush.zero_()
+            fn()
+
+    def fl():
+        for _ in range(reps):
+            flush.zero_()
+    g1, g0 = graph_of(body, stream), graph_of(fl, stream)
+    t1 = statistics.median(time_graph(g1, flush[:1], trials, 1, stream))
+    t0 = statistics.median(time_graph(g0, flush[:1], trials, 1, stream))
+    return max(t1 - t0, 0.0) / reps
+
+
+# ----------------------------------------------------------------------------- workloads
+class Op:
+    def __init__(self, name, kind, fn, ops=0, bytes_=0, cublas=None):
+        self.name, self.kind, self.fn, self.ops, self.bytes, self.cublas = name, kind, fn, ops, bytes_, cublas
+
+
+def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=3072):
+    """configs[1]: BERT-base layer, seq 128, batch 32 (M = 4096 tokens)."""
+    M, D = batch * seq, hidden // heads
+    g = lambda s: s + seed  # noqa: E731
+    X = gen.activations((M, hidden), g(0)).to(dev)
+    Xf = gen.activations((M, hidden), g(1)).to(dev)          # LayerNorm output stand-in
+    R = gen.relu_activations((M, ffn), g(2)).to(dev)          # post-ReLU FFN activations
+    P = gen.attention_probs((batch, heads, seq, seq), g(3)).to(dev)  # softmax output stand-in
+    Ws = {"qkv": gen.weights(3 * hidden, hidden, g(4)), "o": gen.weights(hidden, hidden, g(5)),
+          "f1": gen.weights(ffn, hidden, g(6)), "f2": gen.weights(hidden, ffn, g(7))}
+    packed, wsc, w16 = {}, {}, {}
+    for k, w in Ws.items():
+        mu, s_w = gen.weight_stats(w)
+        packed[k] = B.bwta_pack_weight(w.to(dev), mu=mu)      # offline
+        wsc[k] = s_w.to(dev)
+        w16[k] = w.to(dev)
+    s = {"x": gen.act_scale(X), "xf": gen.act_scale(Xf), "r": gen.act_scale(R), "att": float(np.float32(2.0 / seq))}
+    qkv = torch.empty((M, 3 * hidden), dtype=torch.float16, device=dev)
+    S = torch.empty((batch, heads, seq, seq), dtype=torch.float16, device=dev)
+    ctx = torch.empty((M, hidden), dtype=torch.float16, device=dev)
+    y_o = torch.empty((M, hidden), dtype=torch.float16, device=dev)
+    h1 = torch.empty((M, ffn), dtype=torch.float16, device=dev)
+    y2 = torch.empty((M, hidden), dtype=torch.float16, device=dev)
+
+    def heads_view(t, j):  # [B, H, T, D] view of the j-th third of qkv (no copy)
+        return t[:, j * hidden:(j + 1) * hidden].view(batch, seq, heads, D).transpose(1, 2)
+    ctx_v = ctx.view(batch, seq, heads, D).transpose(1, 2)
+
+    # calibration pass (outside any timing): scales of Q, K, V and the context
+    xq = B.bwta_pack_act(X, s["x"])
+    B.bwta_gemm(xq, packed["qkv"], wsc["qkv"], s["x"], out=qkv)
+    torch.cuda.synchronize()
+    for j, n in enumerate("qkv"):
+        s[n] = gen.act_scale(heads_view(qkv, j))
+    s["alpha"] = float(np.float32(s["q"] * s["k"] / np.sqrt(D)))
+    s["beta"] = float(np.float32(s["att"] * s["v"]))
+    st = {}
+
+    def op_pack_x():
+        st["xq"] = B.bwta_pack_act(X, s["x"])
+
+    def op_qkv():
+        B.bwta_gemm(st["xq"], packed["qkv"], wsc["qkv"], s["x"], out=qkv)
+
+    def op_pack_qkv():
+        st["qp"] = B.bwta_pack_act(heads_view(qkv, 0), s["q"])
+        st["kp"] = B.bwta_pack_act(heads_view(qkv, 1), s["k"])
+        st["vt"] = B.bwta_pack_act(heads_view(qkv, 2), s["v"], transpose=True)
+
+    def op_qk():
+        B.bwta_attn_qk(st["qp"], st["kp"], s["alpha"], out=S)
+
+    def op_pack_p():
+        st["pp"] = B.bwta_pack_act(P, s["att"], "bool")
+
+    def op_pv():
+        B.bwta_attn_pv(st["pp"], st["vt"], s["beta"], out=ctx_v)
+
+    def op_o():
+        st["cq"] = B.bwta_pack_act(ctx, s["ctx"])
+        B.bwta_gemm(st["cq"], packed["o"], wsc["o"], s["ctx"], out=y_o)
+
+    def op_f1():
+        st["fq"] = B.bwta_pack_act(Xf, s["xf"])
+        B.bwta_gemm(st["fq"], packed["f1"], wsc["f1"], s["xf"], out=h1)
+
+    def op_f2():
+        st["rq"] = B.bwta_pack_act(R, s["r"], "bool")
+        B.bwta_gemm(st["rq"], packed["f2"], wsc["f2"], s["r"], out=y2)
+
+    op_pack_x(); op_qkv(); op_pack_qkv(); op_qk(); op_pack_p(); op_pv()  # noqa: E702
+    torch.cuda.synchronize()
+    s["ctx"] = gen.act_scale(ctx)   # calibration of the context scale (outside timing)
+
+    # cuBLAS FP16 baselines of the same matmuls (torch -> cuBLASLt)
+    q16, k16, v16 = (heads_view(qkv, j) for j in range(3))
+    cub = {
+        "qkv": lambda: torch.nn.functional.linear(X, w16["qkv"]),
+        "qk": lambda: torch.matmul(q16, k16.transpose(-1, -2)),
+        "pv": lambda: torch.matmul(P, v16),
+        "o": lambda: torch.nn.functional.linear(ctx, w16["o"]),
+        "f1": lambda: torch.nn.functional.linear(Xf, w16["f1"]),
+        "f2": lambda: torch.nn.functional.linear(R, w16["f2"]),
+    }
+    mm = lambda m, n, k: 2 * m * n * k  # noqa: E731
+    pk = lambda n_el, planes: 2 * n_el + n_el * planes / 8  # noqa: E731  fp16 in + planes out
+    ops = [
+        Op("pack_x", "pack", op_pack_x, 0, pk(M * hidden, 2)),
+        Op("gemm_qkv", "gemm", op_qkv, mm(M, 3 * hidden, hidden),
+           M * hidden / 4 + 3 * hidden * hidden / 8 + 2 * M * 3 * hidden, cub["qkv"]),
+        Op("pack_qkv", "pack", op_pack_qkv, 0, 3 * pk(M * hidden, 2)),
+        Op("attn_qk", "qk", op_qk, mm(batch * heads * seq, seq, D),
+           2 * batch * heads * seq * D / 4 + 2 * batch * heads * seq * seq, cub["qk"]),
+        Op("pack_p", "pack", op_pack_p, 0, pk(batch * heads * seq * seq, 1)),
+        Op("attn_pv", "pv", op_pv, mm(batch * heads * seq, D, seq),
+           batch * heads * seq * seq / 8 + batch * heads * D * seq / 4 + 2 * M * hidden, cub["pv"]),
+        Op("pack_gemm_o", "gemm", op_o, mm(M, hidden, hidden),
+           pk(M * hidden, 2) + M * hidden / 4 + hidden * hidden / 8 + 2 * M * hidden, cub["o"]),
+        Op("pack_gemm_ffn1", "gemm", op_f1, mm(M, ffn, hidden),
+           pk(M * hidden, 2) + M * hidden / 4 + ffn * hidden / 8 + 2 * M * ffn, cub["f1"]),
+        Op("pack_gemm_ffn2", "gemm", op_f2, mm(M, hidden, ffn),
+           pk(M * ffn, 1) + M * ffn / 8 + hidden * ffn / 8 + 2 * M * hidden, cub["f2"]),
+    ]
+    host_inputs = {"X": X, "Xf": Xf, "R": R, "P": P}
+    cfg = {"workload": "bert_layer (configs[1]): BERT-base layer, batch 32 x seq 128, hidden 768, "
+                       "12 heads x 64, FFN 3072", "batch": batch, "seq_len": seq, "hidden": hidden,
+           "heads": heads, "ffn": ffn, "tokens": M}
+    return {"ops": ops, "inputs": host_inputs, "output": y2, "cfg": cfg,
+            "oracle_sample": dict(X=X, Xf=Xf, R=R, P=P, Ws=Ws, s=s, heads=heads, D=D, batch=batch, seq=seq)}
+
+
+def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008)):
+    """configs[2]: LLaMA-7B prefill linears, M = 2048 tokens, K = 4096, N = 4096 / 11008."""
+    X = gen.activations((M, K), seed).to(dev)
+    s_x = gen.act_scale(X)
+    ops, st = [], {}
+
+    def op_pack():
+        st["xq"] = B.bwta_pack_act(X, s_x)
+    ops.append(Op("pack_x", "pack", op_pack, 0, 2 * M * K + M * K / 4))
+    for i, N in enumerate(Ns):
+        w = gen.weights(N, K, seed + 1 + i)
+        mu, s_w = gen.weight_stats(w)
+        wp = B.bwta_pack_weight(w.to(dev), mu=mu)
+        sw = s_w.to(dev)
+        y = torch.empty((M, N), dtype=torch.float16, device=dev)
+        w16 = w.to(dev)
+
+        def op_g(wp=wp, sw=sw, y=y):
+            B.bwta_gemm(st["xq"], wp, sw, s_x, out=y)
+        ops.append(Op(f"gemm_n{N}", "gemm", op_g, 2 * M * N * K, M * K / 4 + N * K / 8 + 2 * M * N,
+                      (lambda w16=w16: torch.nn.functional.linear(X, w16))))
+    op_pack()
+    cfg = {"workload": "llama_prefill (configs[2]): LLaMA-7B prefill linears M=2048 K=4096 N=4096/11008",
+           "tokens": M, "k": K, "n": list(Ns)}
+    return {"ops": ops, "inputs": {"X": X}, "output": None, "cfg": cfg, "oracle_sample": None}
+
+
+def llama_attn(B, dev, seed=404, heads=32, seq=2048, D=128):
+    """configs[3]: LLaMA-7B ternary attention QK^T and PV, 32 heads, head_dim 128, seq 2048."""
+    q = gen.activations((1, heads, seq, D), seed).to(dev)
+    k = gen.activations((1, heads, seq, D), seed + 1).to(dev)
+    v = gen.activations((1, heads, seq, D), seed + 2).to(dev)
+    P = gen.attention_probs((1, heads, seq, seq), seed + 3).to(dev)
+    sq, sk, sv = gen.act_scale(q), gen.act_scale(k), gen.act_scale(v)
+    s_att = float(np.float32(2.0 / seq))
+    alpha, beta = float(np.float32(sq * sk / np.sqrt(D))), float(np.float32(s_att * sv))
+    S = torch.empty((1, heads, seq, seq), dtype=torch.float16, device=dev)
+    O = torch.empty((1, heads, seq, D), dtype=torch.float16, device=dev)
+    st = {}
+
+    def op_pack_qkv():
+        st["qp"], st["kp"] = B.bwta_pack_act(q, sq), B.bwta_pack_act(k, sk)
+        st["vt"] = B.bwta_pack_act(v, sv, transpose=True)
+
+    def op_qk():
+        B.bwta_attn_qk(st["qp"], st["kp"], alpha, out=S)
+
+    def op_pack_p():
+        st["pp"] = B.bwta_pack_act(P, s_att, "bool")
+
+    def op_pv():
+        B.bwta_attn_pv(st["pp"], st["vt"], beta, out=O)
+    op_pack_qkv(); op_pack_p()  # noqa: E702
+    n = heads * seq * D
+    ops = [Op("pack_qkv", "pack", op_pack_qkv, 0, 3 * (2 * n + n / 4)),
+           Op("attn_qk", "qk", op_qk, 2 * heads * seq * seq * D, 2 * n / 4 + 2 * heads * seq * seq,
+              lambda: torch.matmul(q, k.transpose(-1, -2))),
+           Op("pack_p", "pack", op_pack_p, 0, 2 * heads * seq * seq + heads * seq * seq / 8),
+           Op("attn_pv", "pv", op_pv, 2 * heads * seq * seq * D, heads * seq * seq / 8 + n / 4 + 2 * n,
+              lambda: torch.matmul(P, v))]
+    cfg = {"workload": "llama_attn (configs[3]): ternary attention, 32 heads, head_dim 128, seq 2048",
+           "heads": heads, "seq_len": seq, "head_dim": D}
+    return {"ops": ops, "inputs": {"P": P}, "output": None, "cfg": cfg, "oracle_sample": None}
+
+
+def bert_linear(B, dev, seed=101):
+    """configs[0]: single BWTA linear M=128 K=768 N=768."""
+    return llama_prefill(B, dev, seed, M=128, K=768, Ns=(768,)) | {
+        "cfg": {"workload": "bert_linear (configs[0]): M=128 K=768 N=768", "tokens": 128, "k": 768, "n": [768]}}
+
+
+WORKLOADS = {"bert_layer": bert_layer, "llama_prefill": llama_prefill, "llama_attn": llama_attn,
+             "bert_linear": bert_linear}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) legs
+def oracle_bert_layer_step(smp, threads, row_frac=1.0):
+    """The BERT layer's BWTA path through the CPU oracle (quantize + dot + epilogue),
+    on the same inputs; row_frac < 1 runs a stated row/head sample.  Returns ops done."""
+    import oracle
+
+    def st(t):
+        t = t.detach().cpu().contiguous()
+        return t.view(torch.int16).numpy().view(np.uint16) if t.dtype in (torch.float16, torch.bfloat16) else t.numpy()
+    s, M = smp["s"], smp["X"].shape[0]
+    rows = max(1, int(M * row_frac))
+    ops = 0
+    qx = oracle.quantize_act(st(smp["X"][:rows]), "f16", s["x"], "ternary")
+    for name, xin, sx, kind in (("qkv", None, s["x"], "ternary"), ("o", smp["X"], s["x"], "ternary"),
+                                ("f1", smp["Xf"], s["xf"], "ternary"), ("f2", smp["R"], s["r"], "bool")):
+        w = smp["Ws"][name]
+        mu, s_w = gen.weight_stats(w)
+        qw = oracle.binarize_weight(st(w), "f16", mu=mu)
+        qa = qx if xin is None else oracle.quantize_act(st(xin[:rows]), "f16", sx, kind)
+        oracle.gemm(qa, qw, s_w.numpy(), sx, "f16", threads=threads)
+        ops += 2 * qa.shape[0] * qw.shape[0] * qw.shape[1]
+    nbh = max(1, int(smp["batch"] * smp["heads"] * row_frac))
+    b = max(1, nbh // smp["heads"])
+    q = gen.activations((b, smp["heads"], smp["seq"], smp["D"]), 1)
+    qq = oracle.quantize_act(st(q).reshape(-1, smp["seq"], smp["D"]), "f16", 1.0, "ternary")
+    oracle.attn_qk(qq, qq, s["alpha"], "f16", threads=threads)
+    pp = oracle.quantize_act(st(smp["P"][:b]).reshape(-1, smp["seq"], smp["seq"]), "f16", s["att"], "bool")
+    oracle.attn_pv(pp, qq, s["beta"], "f16", threads=threads)
+    ops += 2 * 2 * qq.shape[0] * smp["seq"] * smp["seq"] * smp["D"]
+    return ops, f"{rows}/{M} token rows of each BWTA linear + {qq.shape[0]} (batch x head) attention entries"
+
+
+def reference_arm(args):
+    """--impl reference: the CPU oracle, as it stands, on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    threads = oracle.default_threads()
+
+    wl = args.workload
+    if wl != "bert_layer":
+        print(json.dumps({"impl": "reference", "unavailable": f"reference arm implemented for bert_layer only "
+                                                             f"(asked {wl})"}))
+        return 0
+    smp = _bert_inputs_cpu()
+    frac = args.ref_row_frac
+    for _ in range(args.warmup):
+        oracle_bert_layer_step(smp, threads, frac)
+    t0 = time.perf_counter()
+    tot_ops = 0
+    for _ in range(args.steps):
+        o, sample = oracle_bert_layer_step(smp, threads, frac)
+        tot_ops += o
+    dt = time.perf_counter() - t0
+    val = tot_ops / dt / 1e12
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8 (oracle int32 dot)",
+            "data": "synthetic", "config": _bert_cfg() | {"ref_row_frac": frac},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def _bert_cfg():
+    return {"workload": "bert_layer (configs[1]): BERT-base layer, batch 32 x seq 128, hidden 768, "
+                        "12 heads x 64, FFN 3072", "batch": 32, "seq_len": 128, "hidden": 768, "heads": 12,
+            "ffn": 3072, "tokens": 4096}
+
+
+def _bert_inputs_cpu(seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=3072):
+    M = batch * seq
+    g = lambda s: s + seed  # noqa: E731
+    X = gen.activations((M, hidden), g(0))
+    Xf = gen.activations((M, hidden), g(1))
+    R = gen.relu_activations((M, ffn), g(2))
+    P = gen.attention_probs((batch, heads, seq, seq), g(3))
+    Ws = {"qkv": gen.weights(3 * hidden, hidden, g(4)), "o": gen.weights(hidden, hidden, g(5)),
+          "f1": gen.weights(ffn, hidden, g(6)), "f2": gen.weights(hidden, ffn, g(7))}
+    s = {"x": gen.act_scale(X), "xf": gen.act_scale(Xf), "r": gen.act_scale(R), "att": float(np.float32(2.0 / seq)),
+         "alpha": 0.125, "beta": float(np.float32(2.0 / seq))}
+    return dict(X=X, Xf=Xf, R=R, P=P, Ws=Ws, s=s, heads=heads, D=hidden // heads, batch=batch, seq=seq)
+
+
+# ----------------------------------------------------------------------------- main arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="bwta", choices=["bwta", "reference"])
+    ap.add_argument("--workload", default="bert_layer", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-extras", action="store_true", help="skip the configs[2]/[3] side measurements")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline (oracle) leg")
+    ap.add_argument("--ref-row-frac", type=float, default=1.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2604_03957_b200 as B
+
+    pk = peaks()
+    int8_peak = pk["bf16_tflops"] * 2.0   # int8 dense = 2x bf16 dense (nominal 4.5 / 2.25 PF)
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    W = WORKLOADS[args.workload](B, dev)
+    ops = W["ops"]
+
+    def step():
+        for op in ops:
+            op.fn()
+    total_ops = sum(op.ops for op in ops)
+
+    # -------- device-time step (CUDA graph of the library calls)
+    g_step = graph_of(step, stream)
+    l0 = B.lib.bwta_kernel_launches()
+    with torch.cuda.stream(stream):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = B.lib.bwta_kernel_launches() - l0
+
+    clk = ClockSampler(local).__enter__()
+    t_w = time.perf_counter()
+    nw = 0
+    while nw < args.warmup or time.perf_counter() - t_w < 0.5:   # >= W steps and >= 0.5 s under load
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            g_step.replay()
+        nw += 1
+        if nw % 16 == 0:
+            torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    times = time_graph(g_step, flush, args.steps, 0, stream)
+    torch.cuda.synchronize()
+    clk.__exit__()
+    if world > 1:
+        torch.distributed.barrier()
+    t_total = sum(times)  # ms, K steps
+    if world > 1:
+        t = torch.tensor([t_total], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_total = float(t.item())
+    ms_step = t_total / args.steps
+    value = world * total_ops * args.steps / (t_total / 1e3) / 1e12
+
+    # -------- per-op device times, cuBLAS FP16 baselines
+    per_op, cub_ms = {}, {}
+    for op in ops:
+        per_op[op.name] = op_time_ms(op.fn, flush, stream)
+        if op.cublas is not None:
+            cub_ms[op.name] = op_time_ms(op.cublas, flush, stream)
+    cublas_total = sum(cub_ms.values())
+    bwta_mm_only = sum(per_op[n] for n in cub_ms)
+
+    # -------- roofline of the dominant op
+    dom = max(ops, key=lambda o: per_op[o.name])
+    t_dom = per_op[dom.name] / 1e3
+    if dom.kind == "pack":
+        roof = {"bound": "hbm", "achieved": dom.bytes / t_dom / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s"}
+    else:
+        roof = {"bound": "tensor", "achieved": dom.ops / t_dom / 1e12, "peak": int8_peak, "unit": "TOPS"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["kernel"] = dom.name
+    roof["peak_source"] = (f"{pk['source']} bf16 {pk['bf16_tflops']} TFLOP/s x 2 (int8/bf16 nominal ratio)"
+                           if roof["unit"] == "TOPS" else f"{pk['source']} HBM copy")
+    roof["traffic"] = _traffic(dom.name, args.workload)
+
+    # -------- end to end through the public API with host buffers
+    e2e = None
+    if W["inputs"]:
+        hosts = {k: v.detach().cpu().pin_memory() for k, v in W["inputs"].items()}
+        out = W["output"]
+        out_h = torch.empty(out.shape, dtype=out.dtype).pin_memory() if out is not None else None
+        h2d = sum(v.numel() * v.element_size() for v in hosts.values())
+        d2h = out_h.numel() * out_h.element_size() if out_h is not None else 0
+        ev = []
+        with torch.cuda.stream(stream):
+            for i in range(args.warmup + args.steps):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for k, v in hosts.items():
+                    W["inputs"][k].copy_(v, non_blocking=True)
+                g_step.replay()
+                if out_h is not None:
+                    out_h.copy_(out, non_blocking=True)
+                e1.record(stream)
+                if i >= args.warmup:
+                    ev.append((e0, e1))
+        torch.cuda.synchronize()
+        t_e2e = sum(a.elapsed_time(b) for a, b in ev)
+        if world > 1:
+            t = torch.tensor([t_e2e], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            t_e2e = float(t.item())
+        e2e = {"value": world * total_ops * args.steps / (t_e2e / 1e3) / 1e12, "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e / args.steps}
+
+    # -------- side measurements: configs[2] (headline target) and configs[3]
+    extras = {}
+    if not args.no_extras and args.workload == "bert_layer" and rank == 0:
+        for name in ("llama_prefill", "llama_attn"):
+            Wx = WORKLOADS[name](B, dev)
+            res = {}
+            for op in Wx["ops"]:
+                t = op_time_ms(op.fn, flush, stream)
+                r = {"us": t * 1e3}
+                if op.kind == "pack":
+                    r["GB/s"] = op.bytes / (t / 1e3) / 1e9
+                else:
+                    r["TOPS"] = op.ops / (t / 1e3) / 1e12
+                    r["frac_int8_peak"] = r["TOPS"] / int8_peak
+                if op.cublas is not None:
+                    tc = op_time_ms(op.cublas, flush, stream)
+                    r["cublas_fp16_us"] = tc * 1e3
+                    r["speedup_vs_cublas_fp16"] = tc / t
+                res[op.name] = r
+            if name == "llama_prefill":
+                for n in ("gemm_n4096", "gemm_n11008"):
+                    res[n]["speedup_incl_pack"] = res[n]["cublas_fp16_us"] / (res[n]["us"] + res["pack_x"]["us"])
+            extras[name] = res
+            del Wx
+
+    # -------- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if not args.no_cpu and world == 1 and W.get("oracle_sample") is not None:
+        import oracle
+        oracle.build()
+        threads = oracle.default_threads()
+        t0 = time.perf_counter()
+        o, sample = oracle_bert_layer_step(W["oracle_sample"], threads, 1.0)
+        dt = time.perf_counter() - t0
+        cpu = {"value": o / dt / 1e12, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": f"one full step: {sample}; {dt:.2f} s wall"}
+
+    if rank == 0:
+        pack_gbs = {o.name: o.bytes / (per_op[o.name] / 1e3) / 1e9 for o in ops if o.kind == "pack"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int8 (tcgen05 kind::i8, s32 accumulate; fp16 in/out)",
+            "data": "synthetic (seeded, recipe in DESIGN.md)",
+            "config": W["cfg"] | {"parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                                  "l2": "256 MiB flush between steps (outside timed events)",
+            "clock_window": "nvidia-smi every 20 ms over >= 0.5 s of warm-up load + the timed steps"},
+            "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "speedup_vs_cublas_fp16": {"matmuls_only": cublas_total / bwta_mm_only if bwta_mm_only else None,
+                                       "whole_step_incl_packs": cublas_total / ms_step},
+            "per_op_us": {k: v * 1e3 for k, v in per_op.items()},
+            "cublas_fp16_us": {k: v * 1e3 for k, v in cub_ms.items()},
+            "pack_GBps": pack_gbs, "extras": extras,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def _traffic(op_name, workload):
+    """dram bytes per launch of the dominant op from the committed ncu summary, if any."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        return d.get(workload, {}).get(op_name)
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    sys.exit(main())

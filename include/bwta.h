@@ -125,6 +125,11 @@ BWTA_API int bwta_last_design(void);
 /* Library version, e.g. 100 = 0.1.0. */
 BWTA_API int bwta_version(void);
 
+/* Number of device kernels (and memset nodes) this process has enqueued
+ * through the library so far (all threads).  Used by benchmarks to report
+ * how many of the library's kernels ran inside a timed region. */
+BWTA_API uint64_t bwta_kernel_launches(void);
+
 /* ---- activation pack ---------------------------------------------------- */
 /*
  * Quantize and pack FP activations (Sec. 5.2.2).

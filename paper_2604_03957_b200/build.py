@@ -1,6 +1,7 @@
 """Build libbwta.so (the C-ABI library) in-tree with nvcc for sm_100a.
 
-    python -m paper_2604_03957_b200.build [--force]
+    python paper_2604_03957_b200/build.py [--force] [-v]
+(run it by path: importing the package loads libbwta.so, which may be stale)
 
 The CUDA runtime is linked statically and the driver API (TMA descriptors) is
 resolved at run time through cudaGetDriverEntryPoint, so the library loads on

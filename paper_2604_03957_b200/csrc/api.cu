@@ -12,6 +12,10 @@
 
 using namespace bwta;
 
+namespace bwta {
+std::atomic<uint64_t> g_launches{0};
+}
+
 namespace {
 
 thread_local int g_last_cuda_error = 0;
@@ -163,6 +167,7 @@ const char* bwta_status_string(bwta_status_t st) {
 int bwta_last_cuda_error(void) { return g_last_cuda_error; }
 int bwta_last_design(void) { return g_last_design; }
 int bwta_version(void) { return 100; }
+uint64_t bwta_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 bwta_status_t bwta_pack_act(const void* x, bwta_dtype_t x_dt, int64_t batch, int64_t heads, int64_t rows,
                             int64_t cols, int64_t ld_x, int64_t x_bstride, int64_t x_hstride, float scale,
@@ -205,6 +210,12 @@ bwta_status_t bwta_pack_act(const void* x, bwta_dtype_t x_dt, int64_t batch, int
     a.th = make_thresholds(x_dt, scale);
     const int es = esize(x_dt);
     a.vec_ok = aligned16(x) && (ld_x * es) % 16 == 0 && (x_bstride * es) % 16 == 0 && (x_hstride * es) % 16 == 0;
+    const int64_t out_rows = transpose ? cols : rows;
+    a.planes_dense = (heads == 1 || p_hstride == out_rows * ld_words) &&
+                     (batch == 1 || p_bstride == heads * out_rows * ld_words);
+    a.div_ldw = make_fastdiv(uint32_t(ld_words > 0 && ld_words < (1ll << 31) ? ld_words : 1));
+    a.div_rows = make_fastdiv(uint32_t(rows > 0 && rows < (1ll << 31) ? rows : 1));
+    a.div_nh = make_fastdiv(uint32_t(heads < (1ll << 31) ? heads : 1));
     cudaError_t e = transpose ? launch_pack_cols(a, (cudaStream_t)stream) : launch_pack_rows(a, (cudaStream_t)stream);
     return e == cudaSuccess ? BWTA_OK : cuda_fail(e);
 }
@@ -235,6 +246,10 @@ bwta_status_t bwta_pack_weight(const void* w, bwta_dtype_t w_dt, int64_t n, int6
     a.mu = mu;
     a.mu_per_row = mu_per_row;
     a.vec_ok = aligned16(w) && (ld_w * esize(w_dt)) % 16 == 0;
+    a.planes_dense = true;
+    a.div_ldw = make_fastdiv(uint32_t(ld_words > 0 && ld_words < (1ll << 31) ? ld_words : 1));
+    a.div_rows = make_fastdiv(uint32_t(n > 0 && n < (1ll << 31) ? n : 1));
+    a.div_nh = make_fastdiv(1);
     cudaError_t e = launch_pack_rows(a, (cudaStream_t)stream);
     return e == cudaSuccess ? BWTA_OK : cuda_fail(e);
 }

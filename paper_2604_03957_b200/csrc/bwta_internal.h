@@ -3,7 +3,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace bwta {
+
+// process-wide count of enqueued kernels / memsets (bwta_kernel_launches)
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 enum Dt { DT_F16 = 0, DT_BF16 = 1, DT_F32 = 2, DT_I32 = 3 };
 enum Kind { K_BINARY = 0, K_BOOL = 1, K_TERNARY = 2 };
@@ -18,6 +24,19 @@ struct Thresholds {
     float ntnf;
 };
 
+// n / d for 0 <= n < 2^31 with one IMAD.HI (Granlund-Montgomery round-up
+// multiplier): q = (umulhi(n, mul) + n) >> shift.
+struct FastDiv {
+    uint32_t d, mul, shift;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f{d, 0, 0};
+    while ((1ull << f.shift) < d) ++f.shift;
+    f.mul = uint32_t(((1ull << 32) * ((1ull << f.shift) - d)) / d + 1);
+    if (d == 1) f.mul = 0;
+    return f;
+}
+
 struct PackArgs {
     const void* x;
     int dt;
@@ -31,6 +50,8 @@ struct PackArgs {
     int mu_per_row;
     Thresholds th;
     bool vec_ok;  // x rows are 16-byte aligned -> 128-bit loads
+    bool planes_dense;  // planes are [entries][rows][ldw] contiguous -> word offset = flat index
+    FastDiv div_ldw, div_rows, div_nh;  // for the 32-bit index path
 };
 
 cudaError_t launch_pack_rows(const PackArgs& a, cudaStream_t s);

@@ -179,6 +179,7 @@ cudaError_t launch_matmul_cc(const MatmulArgs& a, cudaStream_t s) {
     if (a.M == 0 || a.N == 0 || a.nb * a.nh == 0) return cudaSuccess;
     dim3 grid(unsigned((a.N + BN - 1) / BN), unsigned((a.M + BM - 1) / BM), unsigned(a.nb * a.nh));
     const bool asg = a.a_sgn != nullptr, bnz = a.b_nz != nullptr;
+    count_launch();
     if (asg && bnz) matmul_cc_kernel<true, true><<<grid, NT, 0, s>>>(a);
     else if (asg) matmul_cc_kernel<true, false><<<grid, NT, 0, s>>>(a);
     else if (bnz) matmul_cc_kernel<false, true><<<grid, NT, 0, s>>>(a);

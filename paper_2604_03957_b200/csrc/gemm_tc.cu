@@ -567,6 +567,7 @@ cudaError_t launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb0, const CUte
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    count_launch();
     return cudaLaunchKernelEx(&cfg, kern, ma, mb0, mb1, my, p);
 }
 
@@ -611,6 +612,7 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void* ws, size_t ws_bytes, cud
         const int64_t blocks = (work + 255) / 256;
         const int grid = int(blocks > num_sms() * 8 ? num_sms() * 8 : blocks);
         expand_kernel<<<grid, 256, 0, s>>>(ea);
+        count_launch();
         cudaError_t err = cudaGetLastError();
         if (err != cudaSuccess) return err;
     }

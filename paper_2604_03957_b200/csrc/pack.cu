@@ -6,16 +6,16 @@
 //
 // B200 design (not the paper's in-register IPB, which fuses the
 // pack into its MMA kernel): packing is a standalone HBM-streaming pass.
-//   * Row mode: one warp reads 32 x 16 B fully-coalesced vectors per
-//     "segment" (256 f16 / 128 f32 elements), SEGS segments in flight per
-//     warp.  Each lane turns its 16 B into an E-bit chunk with packed-half
-//     compares (HSET2 via __hge2_mask: 2 elements per instruction, exact,
-//     no division), and 4 (f16/bf16) or 8 (f32) lanes OR their chunks into
-//     one word with warp shuffles.
-//   * Transposed mode (V^T for PV): a warp owns a 128-row x 32-col tile;
-//     lane l packs row l of a 32-row group into a 32-bit word, and a 5-stage
-//     shuffle butterfly transposes the 32x32 bit block so lane j ends up with
-//     column j's word; 4 row groups give one 16-byte store per column.
+//   * Row mode: the output words are walked as one flat list; 4 lanes (8 for
+//     f32) read the 32 elements of one word as 16-byte vectors, so a warp
+//     instruction moves 512 contiguous bytes per 8 words and every warp keeps
+//     U = 4 such vectors per lane in flight.  Each lane turns its 16 B into an
+//     E-bit chunk with packed-half compares (HSET2 via __hge2_mask: 2 elements
+//     per instruction, exact, no division) and the lanes of a word OR their
+//     chunks together with warp shuffles.
+//   * Transposed mode (V^T for PV): a warp owns a 32-row x 32-col tile; lane
+//     l packs row l into a 32-bit word, a 5-stage shuffle butterfly transposes
+//     the 32x32 bit block so lane j ends up with column j's word.
 // Exactness: x/s >= 0.5 <=> x >= s/2 <=> x >= tp, where tp is the smallest
 // value of x's storage type >= s/2 (host-computed, api.cu); x/s < -0.5 <=>
 // x <= -tn, tn = smallest storage value > s/2.  Compares of finite, infinite
@@ -124,90 +124,127 @@ __device__ __forceinline__ uint4 load_chunk(const T* __restrict__ row, int64_t c
     return r;
 }
 
-__device__ __forceinline__ int64_t entry_off(int64_t e, int64_t nh, int64_t bs, int64_t hs) {
-    return (e / nh) * bs + (e % nh) * hs;
+// Division by a launch constant: FastDiv on the 32-bit path, plain otherwise.
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+    return (__umulhi(n, f.mul) + n) >> f.shift;
+}
+__device__ __forceinline__ uint64_t fdiv(uint64_t n, const FastDiv& f) { return n / f.d; }
+
+// ---------------------------------------------------------------------------
+// Row mode: one lane builds one output word.  The planes are walked as a
+// flat list of words gw = (entry*rows + row)*ldw + w; lane gw reads the 32
+// elements of its word as 16-byte vectors (64 B for 2-byte inputs, L1-
+// allocating so the four quarter-line requests of a lane hit the same
+// sectors), compares them with packed-half HSET2 and ORs the results into
+// the word directly -- no cross-lane traffic; 32 lanes store 128 contiguous
+// bytes.  Every lane keeps 2 words in flight and prefetches the next pair
+// before computing.  Padding words (w >= ceil(cols/32)) load nothing.
+// ---------------------------------------------------------------------------
+template <typename T> struct WplOf { static constexpr int v = sizeof(T) == 4 ? 1 : 2; };  // words per lane per iteration
+
+// the 8 compare bits of one 16-byte vector, placed at bit offset `sh`
+template <typename T>
+__device__ __forceinline__ void vec_bits(const uint4& v, const Thresholds& th, int sh, uint32_t& pos, uint32_t& neg) {
+    uint32_t pb, nb;
+    chunk_bits<T>(v, th, pb, nb);
+    pos |= pb << sh;
+    neg |= nb << sh;
 }
 
-// ---------------------------------------------------------------------------
-// Row mode.  Work item = (entry, row, chunk of SEGS segments).
-// ---------------------------------------------------------------------------
-constexpr int SEGS = 4;
+template <typename T, int KIND, bool VEC, typename IDX>
+__global__ void __launch_bounds__(256, 2) pack_rows_kernel(PackArgs p) {
+    constexpr int E = TypeInfo<T>::E;  // elements per 16-byte vector
+    constexpr int NV = 32 / E;         // vectors per word
+    constexpr int WPL = WplOf<T>::v;
+    const IDX ldw = IDX(p.ldw), rows = IDX(p.rows), nh = IDX(p.nh);
+    const IDX total = IDX(p.nb * p.nh) * rows * ldw;
+    const IDX cols = IDX(p.cols);
+    const IDX nthreads = IDX(gridDim.x) * blockDim.x;
+    const IDX tid = IDX(blockIdx.x) * blockDim.x + threadIdx.x;
 
-template <typename T, int KIND, bool VEC>
-__global__ void __launch_bounds__(256) pack_rows_kernel(PackArgs p) {
-    constexpr int E = TypeInfo<T>::E;     // elements per lane per segment
-    constexpr int LPW = 32 / E;           // lanes per output word
-    constexpr int WPS = E;                // words per segment
-    const int lane = threadIdx.x & 31;
-    const int64_t nseg = (p.ldw + WPS - 1) / WPS;
-    const int64_t nchunk = (nseg + SEGS - 1) / SEGS;
-    const int64_t items = p.nb * p.nh * p.rows * nchunk;
-    const int64_t warp0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-
-    for (int64_t it = warp0; it < items; it += nwarps) {
-        const int64_t chunk = it % nchunk;
-        const int64_t rr = it / nchunk;          // entry*rows + row
-        const int64_t r = rr % p.rows;
-        const int64_t e = rr / p.rows;
-        const T* row = reinterpret_cast<const T*>(p.x) + entry_off(e, p.nh, p.x_bs, p.x_hs) + r * p.ld_x;
-        const int64_t poff = entry_off(e, p.nh, p.p_bs, p.p_hs) + r * p.ldw;
-        float mu = 0.f;
-        if (KIND == K_BINARY && p.mu) mu = p.mu_per_row ? p.mu[r] : p.mu[0];
-
-        uint4 v[SEGS];
+    auto issue = [&](IDX gw0, uint4 (&v)[WplOf<T>::v][NV], IDX (&gr)[WplOf<T>::v], IDX (&gwv)[WplOf<T>::v]) {
 #pragma unroll
-        for (int s = 0; s < SEGS; ++s) {
-            const int64_t seg = chunk * SEGS + s;
-            const int64_t c = seg * (32 * E) + lane * E;
-            v[s] = (seg < nseg) ? load_chunk<T, VEC>(row, c, p.cols) : make_uint4(0, 0, 0, 0);
-        }
-        uint32_t nnz = 0;
+        for (int u = 0; u < WPL; ++u) {
+            const IDX gw = gw0 + IDX(u) * nthreads;
+            const IDX r = fdiv(gw < total ? gw : IDX(0), p.div_ldw);  // flat row (entry*rows + row)
+            gr[u] = r;
+            gwv[u] = gw - r * ldw;
+            const IDX c0 = gwv[u] * 32;
 #pragma unroll
-        for (int s = 0; s < SEGS; ++s) {
-            const int64_t seg = chunk * SEGS + s;
-            if (seg >= nseg) break;
-            const int64_t c = seg * (32 * E) + lane * E;
-            uint32_t pos, neg;
-            if (KIND == K_BINARY) {
-                // valid-element mask: elements >= cols must stay 0
-                const int64_t nvalid = p.cols - c;
-                const uint32_t valid = nvalid >= E ? ((1u << E) - 1) : (nvalid <= 0 ? 0u : ((1u << nvalid) - 1));
-                neg = chunk_lt_mu<T>(v[s], mu) & valid;
-                pos = 0;
-            } else {
-                chunk_bits<T>(v[s], p.th, pos, neg);
-            }
-            const int sh = E * (lane % LPW);
-            // nz bits: ternary q != 0; bool q = 1 only for x >= t (binary: unused)
-            uint32_t wn = (KIND == K_BOOL ? pos : (pos | neg)) << sh;
-            uint32_t ws = neg << sh;           // sgn bits
+            for (int q = 0; q < NV; ++q) v[u][q] = make_uint4(0, 0, 0, 0);
+            if (gw < total && c0 < cols) {
+                const IDX e = fdiv(r, p.div_rows), rr = r - e * rows;
+                const IDX eb = fdiv(e, p.div_nh), eh = e - eb * nh;
+                const T* row = reinterpret_cast<const T*>(p.x) + int64_t(eb) * p.x_bs + int64_t(eh) * p.x_hs +
+                               int64_t(rr) * p.ld_x;
+                if (VEC && c0 + 32 <= cols) {
+                    const uint4* src = reinterpret_cast<const uint4*>(row + c0);
 #pragma unroll
-            for (int o = 1; o < LPW; o <<= 1) {
-                wn |= __shfl_xor_sync(FULL, wn, o);
-                ws |= __shfl_xor_sync(FULL, ws, o);
-            }
-            const int64_t widx = seg * WPS + lane / LPW;
-            if ((lane % LPW) == 0 && widx < p.ldw) {
-                if (KIND == K_BINARY) {
-                    p.sgn[poff + widx] = ws;
+                    for (int q = 0; q < NV; ++q) v[u][q] = __ldg(src + q);
                 } else {
-                    p.nz[poff + widx] = wn;
-                    if (KIND == K_TERNARY) p.sgn[poff + widx] = ws;
-                    nnz += __popc(wn);
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) v[u][q] = load_chunk<T, false>(row, int64_t(c0) + q * E, int64_t(cols));
                 }
             }
         }
-        if (KIND != K_BINARY && p.row_nnz) {
+    };
+
+    uint4 v[WPL][NV], vn[WPL][NV];
+    IDX gr[WPL], gwv[WPL], grn[WPL], gwvn[WPL];
+    const IDX step = nthreads * WPL;
+    IDX gw0 = tid;
+    if (gw0 < total) issue(gw0, vn, grn, gwvn);
+    for (; gw0 < total; gw0 += step) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) nnz += __shfl_xor_sync(FULL, nnz, o);
-            if (lane == 0 && nnz) atomicAdd(p.row_nnz + rr, int(nnz));
+        for (int u = 0; u < WPL; ++u) {
+            gr[u] = grn[u];
+            gwv[u] = gwvn[u];
+#pragma unroll
+            for (int q = 0; q < NV; ++q) v[u][q] = vn[u][q];
+        }
+        if (gw0 + step < total) issue(gw0 + step, vn, grn, gwvn);
+#pragma unroll
+        for (int u = 0; u < WPL; ++u) {
+            const IDX gw = gw0 + IDX(u) * nthreads;
+            if (gw >= total) break;
+            uint32_t pos = 0, neg = 0;
+            if (KIND == K_BINARY) {
+                float mu = 0.f;
+                if (p.mu) mu = p.mu_per_row ? p.mu[gr[u] - fdiv(gr[u], p.div_rows) * rows] : p.mu[0];
+#pragma unroll
+                for (int q = 0; q < NV; ++q) neg |= chunk_lt_mu<T>(v[u][q], mu) << (q * E);
+                const int64_t nvalid = int64_t(cols) - int64_t(gwv[u]) * 32;
+                neg &= nvalid >= 32 ? 0xffffffffu : (nvalid <= 0 ? 0u : ((1u << nvalid) - 1u));
+            } else {
+#pragma unroll
+                for (int q = 0; q < NV; ++q) vec_bits<T>(v[u][q], p.th, q * E, pos, neg);
+            }
+            const uint32_t wn = KIND == K_BOOL ? pos : (pos | neg);  // nz: ternary q != 0, bool x >= t
+            const IDX r = gr[u];
+            int64_t poff;
+            if (p.planes_dense) {
+                poff = int64_t(gw);
+            } else {
+                const IDX e = fdiv(r, p.div_rows), rr = r - e * rows;
+                const IDX eb = fdiv(e, p.div_nh), eh = e - eb * nh;
+                poff = int64_t(eb) * p.p_bs + int64_t(eh) * p.p_hs + int64_t(rr) * p.ldw + int64_t(gwv[u]);
+            }
+            if (KIND == K_BINARY) {
+                p.sgn[poff] = neg;
+            } else {
+                p.nz[poff] = wn;
+                if (KIND == K_TERNARY) p.sgn[poff] = neg;
+                if (p.row_nnz && wn) atomicAdd(p.row_nnz + r, __popc(wn));
+            }
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Transposed mode.  Work item = (entry, 128-row tile, 32-col tile).
+// Transposed mode.  Work item = (entry, 32-row group, 32-col tile): lane l
+// packs row l of the group into a 32-bit word (bit c = column c), a 5-stage
+// shuffle butterfly transposes the 32x32 bit block, and lane c stores the
+// word of column c.  Row groups up to ldw cover the zero padding.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
     // 32x32 bit-matrix transpose across a warp: in, lane l holds row l
@@ -223,71 +260,85 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
     return x;
 }
 
-template <typename T, int KIND, bool VEC>
-__global__ void __launch_bounds__(256) pack_cols_kernel(PackArgs p) {
+template <typename T, int KIND, bool VEC, typename IDX>
+__global__ void __launch_bounds__(256, 2) pack_cols_kernel(PackArgs p) {
     constexpr int E = TypeInfo<T>::E;
-    constexpr int NV = 32 / E;            // 16-byte vectors per 32 columns
+    constexpr int NV = 32 / E;  // 16-byte vectors per 32 columns
     const int lane = threadIdx.x & 31;
-    const int64_t ntile_r = p.ldw / 4;    // 128-row tiles (ldw % 4 == 0)
-    const int64_t ntile_c = (p.cols + 31) / 32;
-    const int64_t items = p.nb * p.nh * ntile_r * ntile_c;
-    const int64_t warp0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const IDX ngrp = IDX(p.ldw);                 // 32-row groups (covers padding)
+    const IDX ntile_c = IDX((p.cols + 31) / 32);
+    const IDX nh = IDX(p.nh);
+    const IDX items = IDX(p.nb * p.nh) * ngrp * ntile_c;
+    const IDX warp0 = (IDX(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const IDX nwarps = (IDX(gridDim.x) * blockDim.x) >> 5;
 
-    for (int64_t it = warp0; it < items; it += nwarps) {
-        const int64_t tc = it % ntile_c;
-        const int64_t t2 = it / ntile_c;
-        const int64_t tr = t2 % ntile_r;
-        const int64_t e = t2 / ntile_r;
-        const T* base = reinterpret_cast<const T*>(p.x) + entry_off(e, p.nh, p.x_bs, p.x_hs);
-        const int64_t c0 = tc * 32;
-        uint32_t nzw[4], sgw[4];
+    // loads of item `it` for this lane's row (all zero past the last row)
+    auto issue = [&](IDX it, uint4 (&v)[NV]) {
+        const IDX tc = it % ntile_c, t2 = it / ntile_c;
+        const IDX grp = t2 % ngrp, e = t2 / ngrp;
+        const int64_t r = int64_t(grp) * 32 + lane;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            const int64_t r = tr * 128 + g * 32 + lane;
-            uint32_t pos = 0, neg = 0;
-            if (r < p.rows) {
-                const T* row = base + r * p.ld_x;
-                uint4 v[NV];
+        for (int q = 0; q < NV; ++q) v[q] = make_uint4(0, 0, 0, 0);
+        if (r < p.rows) {
+            const T* row = reinterpret_cast<const T*>(p.x) + int64_t(e / nh) * p.x_bs + int64_t(e % nh) * p.x_hs +
+                           r * p.ld_x;
 #pragma unroll
-                for (int q = 0; q < NV; ++q) v[q] = load_chunk<T, VEC>(row, c0 + q * E, p.cols);
-#pragma unroll
-                for (int q = 0; q < NV; ++q) {
-                    uint32_t pb, nb;
-                    chunk_bits<T>(v[q], p.th, pb, nb);
-                    pos |= pb << (q * E);
-                    neg |= nb << (q * E);
-                }
-            }
-            nzw[g] = transpose32(KIND == K_BOOL ? pos : (pos | neg), lane);
-            sgw[g] = (KIND == K_TERNARY) ? transpose32(neg, lane) : 0u;
+            for (int q = 0; q < NV; ++q) v[q] = load_chunk<T, VEC>(row, int64_t(tc) * 32 + q * E, p.cols);
         }
-        const int64_t col = c0 + lane;
+    };
+    uint4 v[NV], vn[NV];
+    IDX it = warp0;
+    if (it < items) issue(it, vn);
+    for (; it < items; it += nwarps) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) v[q] = vn[q];
+        if (it + nwarps < items) issue(it + nwarps, vn);
+        const IDX tc = it % ntile_c, t2 = it / ntile_c;
+        const IDX grp = t2 % ngrp, e = t2 / ngrp;
+        uint32_t pos = 0, neg = 0;
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            uint32_t pb, nb;
+            chunk_bits<T>(v[q], p.th, pb, nb);
+            pos |= pb << (q * E);
+            neg |= nb << (q * E);
+        }
+        const uint32_t nzw = transpose32(KIND == K_BOOL ? pos : (pos | neg), lane);
+        const uint32_t sgw = (KIND == K_TERNARY) ? transpose32(neg, lane) : 0u;
+        const int64_t col = int64_t(tc) * 32 + lane;
         if (col < p.cols) {
-            const int64_t poff = entry_off(e, p.nh, p.p_bs, p.p_hs) + col * p.ldw + tr * 4;
-            *reinterpret_cast<uint4*>(p.nz + poff) = make_uint4(nzw[0], nzw[1], nzw[2], nzw[3]);
-            if (KIND == K_TERNARY)
-                *reinterpret_cast<uint4*>(p.sgn + poff) = make_uint4(sgw[0], sgw[1], sgw[2], sgw[3]);
-            if (p.row_nnz) {
-                const int n = __popc(nzw[0]) + __popc(nzw[1]) + __popc(nzw[2]) + __popc(nzw[3]);
-                if (n) atomicAdd(p.row_nnz + e * p.cols + col, n);
-            }
+            const int64_t poff = int64_t(e / nh) * p.p_bs + int64_t(e % nh) * p.p_hs + col * p.ldw + int64_t(grp);
+            p.nz[poff] = nzw;
+            if (KIND == K_TERNARY) p.sgn[poff] = sgw;
+            if (p.row_nnz && nzw) atomicAdd(p.row_nnz + int64_t(e) * p.cols + col, __popc(nzw));
         }
     }
 }
 
+int num_sms_pack() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) v = 148;
+        n = v;
+    }
+    return n;
+}
+
+// One resident wave (2 x 256-thread blocks per SM, <= 128 registers); warps loop with prefetch.
 int grid_for(int64_t warp_items) {
     const int64_t blocks = (warp_items + 7) / 8;
-    const int64_t cap = 148 * 16;
+    const int64_t cap = int64_t(num_sms_pack()) * 2;
     return int(blocks < 1 ? 1 : (blocks > cap ? cap : blocks));
 }
 
-template <typename T>
+template <typename T, typename IDX>
 cudaError_t rows_dispatch(const PackArgs& a, cudaStream_t s, int grid) {
-#define BWTA_ROWS(KIND)                                                              \
-    do {                                                                             \
-        if (a.vec_ok) pack_rows_kernel<T, KIND, true><<<grid, 256, 0, s>>>(a);       \
-        else pack_rows_kernel<T, KIND, false><<<grid, 256, 0, s>>>(a);               \
+#define BWTA_ROWS(KIND)                                                                   \
+    do {                                                                                  \
+        if (a.vec_ok) pack_rows_kernel<T, KIND, true, IDX><<<grid, 256, 0, s>>>(a);       \
+        else pack_rows_kernel<T, KIND, false, IDX><<<grid, 256, 0, s>>>(a);               \
     } while (0)
     if (a.kind == K_BINARY) BWTA_ROWS(K_BINARY);
     else if (a.kind == K_BOOL) BWTA_ROWS(K_BOOL);
@@ -296,12 +347,12 @@ cudaError_t rows_dispatch(const PackArgs& a, cudaStream_t s, int grid) {
     return cudaGetLastError();
 }
 
-template <typename T>
+template <typename T, typename IDX>
 cudaError_t cols_dispatch(const PackArgs& a, cudaStream_t s, int grid) {
-#define BWTA_COLS(KIND)                                                              \
-    do {                                                                             \
-        if (a.vec_ok) pack_cols_kernel<T, KIND, true><<<grid, 256, 0, s>>>(a);       \
-        else pack_cols_kernel<T, KIND, false><<<grid, 256, 0, s>>>(a);               \
+#define BWTA_COLS(KIND)                                                                   \
+    do {                                                                                  \
+        if (a.vec_ok) pack_cols_kernel<T, KIND, true, IDX><<<grid, 256, 0, s>>>(a);       \
+        else pack_cols_kernel<T, KIND, false, IDX><<<grid, 256, 0, s>>>(a);               \
     } while (0)
     if (a.kind == K_BOOL) BWTA_COLS(K_BOOL);
     else BWTA_COLS(K_TERNARY);
@@ -309,37 +360,51 @@ cudaError_t cols_dispatch(const PackArgs& a, cudaStream_t s, int grid) {
     return cudaGetLastError();
 }
 
+template <typename T>
+cudaError_t rows_idx(const PackArgs& a, cudaStream_t s, int grid, bool small) {
+    return small ? rows_dispatch<T, uint32_t>(a, s, grid) : rows_dispatch<T, uint64_t>(a, s, grid);
+}
+template <typename T>
+cudaError_t cols_idx(const PackArgs& a, cudaStream_t s, int grid, bool small) {
+    return small ? cols_dispatch<T, uint32_t>(a, s, grid) : cols_dispatch<T, uint64_t>(a, s, grid);
+}
+
 }  // namespace
 
 cudaError_t launch_pack_rows(const PackArgs& a, cudaStream_t s) {
-    const int E = (a.dt == DT_F32) ? 4 : 8;
-    const int64_t nseg = (a.ldw + E - 1) / E;
-    const int64_t items = a.nb * a.nh * a.rows * ((nseg + SEGS - 1) / SEGS);
-    if (items == 0) return cudaSuccess;
+    const int64_t total_words = a.nb * a.nh * a.rows * a.ldw;
+    if (total_words == 0) return cudaSuccess;
     if (a.row_nnz && a.kind != K_BINARY) {
         cudaError_t err = cudaMemsetAsync(a.row_nnz, 0, sizeof(int32_t) * a.nb * a.nh * a.rows, s);
         if (err != cudaSuccess) return err;
+        count_launch();
     }
-    const int grid = grid_for(items);
+    const int grid = grid_for((total_words + 63) / 64);
+    const bool small = total_words + 4 * int64_t(grid) * 256 < (int64_t(1) << 31) &&
+                       a.cols + 32 < (int64_t(1) << 31);
+    count_launch();
     switch (a.dt) {
-        case DT_F16: return rows_dispatch<__half>(a, s, grid);
-        case DT_BF16: return rows_dispatch<__nv_bfloat16>(a, s, grid);
-        default: return rows_dispatch<float>(a, s, grid);
+        case DT_F16: return rows_idx<__half>(a, s, grid, small);
+        case DT_BF16: return rows_idx<__nv_bfloat16>(a, s, grid, small);
+        default: return rows_idx<float>(a, s, grid, small);
     }
 }
 
 cudaError_t launch_pack_cols(const PackArgs& a, cudaStream_t s) {
-    const int64_t items = a.nb * a.nh * (a.ldw / 4) * ((a.cols + 31) / 32);
+    const int64_t items = a.nb * a.nh * a.ldw * ((a.cols + 31) / 32);
     if (items == 0) return cudaSuccess;
     if (a.row_nnz) {
         cudaError_t err = cudaMemsetAsync(a.row_nnz, 0, sizeof(int32_t) * a.nb * a.nh * a.cols, s);
         if (err != cudaSuccess) return err;
+        count_launch();
     }
     const int grid = grid_for(items);
+    const bool small = items + int64_t(grid) * 8 < (int64_t(1) << 31);
+    count_launch();
     switch (a.dt) {
-        case DT_F16: return cols_dispatch<__half>(a, s, grid);
-        case DT_BF16: return cols_dispatch<__nv_bfloat16>(a, s, grid);
-        default: return cols_dispatch<float>(a, s, grid);
+        case DT_F16: return cols_idx<__half>(a, s, grid, small);
+        case DT_BF16: return cols_idx<__nv_bfloat16>(a, s, grid, small);
+        default: return cols_idx<float>(a, s, grid, small);
     }
 }
 

@@ -14,8 +14,8 @@ HEADER = os.path.join(ROOT, "include", "bwta.h")
 
 @pytest.fixture(scope="module")
 def N():
-    from paper_2604_03957_b200 import build
-    build.build()
+    import __graft_entry__
+    __graft_entry__._builder().build()
     from paper_2604_03957_b200 import _native
     return _native
 
