@@ -6,7 +6,7 @@ import ctypes
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libbwta.so")
+LIB_PATH = os.path.join(_PKG, os.environ.get("BWTA_LIB", "libbwta.so"))  # BWTA_LIB: tools only
 
 # enums (include/bwta.h)
 BWTA_OK = 0

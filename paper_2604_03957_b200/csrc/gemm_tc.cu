@@ -84,9 +84,42 @@ struct Cfg {
     static_assert(BNC % 8 == 0, "swizzle atoms are 8 rows");
 };
 
-__device__ __forceinline__ uint32_t spread4(uint32_t x4) { return (x4 * 0x00204081u) & 0x01010101u; }
+// K order inside the int8 operand tiles.  Element k (0..31) of a packed word
+// lands at byte 4*(k%8) + k/8 of its 32-byte group, i.e. code word j
+// (j = 0..7) holds elements {j, 8+j, 16+j, 24+j}.  Both MMA operands use the
+// same permutation (expand_kernel for A, the unpack warps for B), so every
+// dot product is unchanged.
+//
+// Codes are scaled by 64 (int8 0x40 = +64, 0xC0 = -64, 0x00): the nz bit of
+// element 8i+j moves to bit 6 of byte i and the sgn bit to bit 7 by LEFT
+// shifts, which run as IMAD.SHL on the FMA pipe, so a code word costs ~2 FMA
+// + 2 logic instructions instead of a nibble spread (measured in
+// tools/ubench: 230 vs 313 cycles per 128-element ternary row per warp).  The
+// s32 accumulator holds 4096 * dot exactly (|dot| <= K <= 2^18) and the
+// epilogue recovers dot with an arithmetic shift by 12.
+//   binary  (x0 = sgn):           0x40 | sgn << 7          -> +64 / -64
+//   bool    (x0 = nz):            nz << 6                  -> 0 / +64
+//   ternary (x0 = sgn, x1 = nz):  nz << 6 | sgn << 7       -> 0 / +64 / -64
+// (ternary planes are canonical: sgn is a subset of nz, include/bwta.h)
+constexpr int CODE_SHIFT = 12;  // log2(64 * 64)
 
-__device__ __forceinline__ float scaled(uint32_t dot, float c) { return __fmul_rn(__int2float_rn(int32_t(dot)), c); }
+__device__ __forceinline__ uint32_t shl_fma(uint32_t x, int k) {  // x << k as IMAD.SHL (FMA pipe)
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, 0;" : "=r"(r) : "r"(x), "r"(1u << k));
+    return r;
+}
+__device__ __forceinline__ uint32_t to_bit6(uint32_t x, int j) { return j < 7 ? shl_fma(x, 6 - j) : (x >> 1); }
+
+template <int KIND>
+__device__ __forceinline__ uint32_t unpack_word(uint32_t x0, uint32_t x1, int j) {
+    if (KIND == B_BINARY) return (shl_fma(x0, 7 - j) & 0x80808080u) | 0x40404040u;
+    if (KIND == B_BOOL) return to_bit6(x0, j) & 0x40404040u;
+    return (to_bit6(x1, j) & 0x40404040u) | (shl_fma(x0, 7 - j) & 0x80808080u);
+}
+
+// raw s32 accumulator (4096 * dot) -> dot
+__device__ __forceinline__ int32_t dot_of(uint32_t acc) { return int32_t(acc) >> CODE_SHIFT; }
+__device__ __forceinline__ float scaled(uint32_t acc, float c) { return __fmul_rn(__int2float_rn(dot_of(acc)), c); }
 
 __device__ __forceinline__ uint32_t pack2(int dt, float lo, float hi) {
     if (dt == DT_F16) {
@@ -183,7 +216,7 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
                             const uint32_t h2 = pack2(p.y_dt, f[j], 0.f);
                             asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(uint16_t(h2 & 0xffffu)) : "memory");
                         } else {
-                            const uint32_t o = p.y_dt == DT_F32 ? __float_as_uint(f[j]) : v[j];
+                            const uint32_t o = p.y_dt == DT_F32 ? __float_as_uint(f[j]) : uint32_t(dot_of(v[j]));
                             asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(o) : "memory");
                         }
                     }
@@ -205,7 +238,7 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
                         if (p.y_dt == DT_F16) reinterpret_cast<__half*>(p.y)[idx] = __float2half_rn(f[j]);
                         else if (p.y_dt == DT_BF16) reinterpret_cast<__nv_bfloat16*>(p.y)[idx] = __float2bfloat16_rn(f[j]);
                         else if (p.y_dt == DT_F32) reinterpret_cast<float*>(p.y)[idx] = f[j];
-                        else reinterpret_cast<int32_t*>(p.y)[idx] = int32_t(v[j]);
+                        else reinterpret_cast<int32_t*>(p.y)[idx] = dot_of(v[j]);
                     }
                 }
             }
@@ -368,23 +401,12 @@ __global__ void __launch_bounds__(NT, 1)
                         const uint32_t p1[4] = {w1.x, w1.y, w1.z, w1.w};
                         const uint32_t rowaddr = bdst + r * 128;
 #pragma unroll
-                        for (int c = 0; c < 8; ++c) {
-                            const uint32_t x0 = p0[c >> 1] >> (16 * (c & 1));
-                            const uint32_t x1 = p1[c >> 1] >> (16 * (c & 1));
-                            uint32_t o[4];
+                        for (int g = 0; g < 4; ++g) {  // 32-element group = one packed word
+                            uint32_t o[8];
 #pragma unroll
-                            for (int q = 0; q < 4; ++q) {
-                                const uint32_t a4 = (x0 >> (4 * q)) & 0xfu;
-                                if (BKIND == B_BINARY) {
-                                    o[q] = spread4(a4) * 0xfeu + 0x01010101u;
-                                } else if (BKIND == B_BOOL) {
-                                    o[q] = spread4(a4);
-                                } else {
-                                    const uint32_t n4 = (x1 >> (4 * q)) & 0xfu;
-                                    o[q] = spread4(n4) | (spread4(a4 & n4) * 0xfeu);
-                                }
-                            }
-                            sts128(rowaddr + ((c ^ (r & 7)) << 4), o[0], o[1], o[2], o[3]);
+                            for (int j = 0; j < 8; ++j) o[j] = unpack_word<BKIND>(p0[g], p1[g], j);
+                            sts128(rowaddr + (((2 * g) ^ (r & 7)) << 4), o[0], o[1], o[2], o[3]);
+                            sts128(rowaddr + (((2 * g + 1) ^ (r & 7)) << 4), o[4], o[5], o[6], o[7]);
                         }
                     }
                 }
@@ -420,10 +442,9 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Expand packed planes to an int8 image: out[e][r][k] in {-1, 0, +1}, k < Kp.
-// Kind from plane presence: sgn+nz ternary, nz only bool, sgn only binary.
-// spread4(x) moves bit i of a nibble to bit 0 of byte i; the ternary byte is
-// spread(nz) | spread(sgn & nz) * 0xFE (0x01 / 0xFF / 0x00).
+// Expand packed planes to an int8 image out[e][r][k'] of x64 codes in the
+// unpack_word K order.  Kind from plane presence: sgn+nz ternary, nz only bool,
+// sgn only binary (nz = the valid elements of the row).
 // ---------------------------------------------------------------------------
 struct ExpandArgs {
     const uint32_t* sgn;
@@ -431,30 +452,31 @@ struct ExpandArgs {
     int64_t rows, K, ld, bs, hs, nh, entries;
     int64_t kw4;  // words per output row (Kp = 32 * kw4)
     int8_t* out;
+    FastDiv div_kw4, div_rows, div_nh;
 };
 
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
+__device__ __forceinline__ uint64_t fdiv(uint64_t n, const FastDiv& f) { return n / f.d; }
+
+template <typename IDX>
 __global__ void __launch_bounds__(256) expand_kernel(ExpandArgs a) {
-    const int64_t total = a.entries * a.rows * a.kw4;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t w = i % a.kw4;
-        const int64_t rr = i / a.kw4;
-        const int64_t r = rr % a.rows;
-        const int64_t e = rr / a.rows;
-        const int64_t off = (e / a.nh) * a.bs + (e % a.nh) * a.hs + r * a.ld + w;
+    const IDX total = IDX(a.entries * a.rows * a.kw4);
+    const IDX kw4 = IDX(a.kw4), rows = IDX(a.rows), nh = IDX(a.nh);
+    for (IDX i = IDX(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += IDX(gridDim.x) * blockDim.x) {
+        const IDX rr = fdiv(i, a.div_kw4), w = i - rr * kw4;
+        const IDX e = fdiv(rr, a.div_rows), r = rr - e * rows;
+        const IDX eb = fdiv(e, a.div_nh), eh = e - eb * nh;
+        const int64_t off = int64_t(eb) * a.bs + int64_t(eh) * a.hs + int64_t(r) * a.ld + int64_t(w);
         uint32_t nz = a.nz ? __ldg(a.nz + off) : 0xffffffffu;
-        const uint32_t sg = a.sgn ? __ldg(a.sgn + off) : 0u;
+        const uint32_t sg = a.sgn ? __ldg(a.sgn + off) & nz : 0u;
         if (!a.nz) {  // binary: element validity comes from K (no nz plane)
-            const int64_t valid = a.K - w * 32;
+            const int64_t valid = a.K - int64_t(w) * 32;
             nz = valid >= 32 ? 0xffffffffu : (valid <= 0 ? 0u : ((1u << valid) - 1u));
         }
-        const uint32_t s = sg & nz;
         uint32_t o[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const uint32_t n4 = (nz >> (4 * q)) & 0xfu, s4 = (s >> (4 * q)) & 0xfu;
-            o[q] = spread4(n4) | (spread4(s4) * 0xfeu);
-        }
-        uint4* dst = reinterpret_cast<uint4*>(a.out + rr * (a.kw4 * 32) + w * 32);
+        for (int j = 0; j < 8; ++j) o[j] = unpack_word<B_TERNARY>(sg & nz, nz, j);
+        uint4* dst = reinterpret_cast<uint4*>(a.out + int64_t(i) * 32);
         dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
         dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
     }
@@ -590,7 +612,8 @@ size_t matmul_tc_workspace(const MatmulArgs& a) {
 bool matmul_tc_supported(const MatmulArgs& a) {
     if (a.K < 1 || a.M < 1 || a.N < 1) return false;
     if (a.nb * a.nh > 65535 || a.nb > (int64_t(1) << 31) || a.nh > (int64_t(1) << 31)) return false;
-    if (kw4_of(a.K) * 32 > (int64_t(1) << 31) || a.M > (int64_t(1) << 31) || a.N > (int64_t(1) << 31)) return false;
+    if (a.M > (int64_t(1) << 31) || a.N > (int64_t(1) << 31)) return false;
+    if (a.K > (int64_t(1) << 18)) return false;  // 4096 * |dot| must fit the s32 accumulator
     // the bit planes of kernel-B are read by TMA: batch strides must be real strides
     const Plan pl = make_plan(a);
     if ((a.nb > 1 && pl.b_bs <= 0) || (a.nh > 1 && pl.b_hs <= 0)) return false;
@@ -606,12 +629,17 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void* ws, size_t ws_bytes, cud
     int8_t* wa = reinterpret_cast<int8_t*>(ws);
 
     // 1) expand kernel-A planes to an int8 image [entries][Mk][Kp]
-    ExpandArgs ea{pl.a_sgn, pl.a_nz, pl.Mk, a.K, pl.lda, pl.a_bs, pl.a_hs, a.nh, entries, kw4, wa};
+    ExpandArgs ea{pl.a_sgn, pl.a_nz, pl.Mk, a.K, pl.lda, pl.a_bs, pl.a_hs, a.nh, entries, kw4, wa, {}, {}, {}};
     {
         const int64_t work = entries * pl.Mk * kw4;
         const int64_t blocks = (work + 255) / 256;
         const int grid = int(blocks > num_sms() * 8 ? num_sms() * 8 : blocks);
-        expand_kernel<<<grid, 256, 0, s>>>(ea);
+        const bool small = work + int64_t(grid) * 256 < (int64_t(1) << 31);
+        ea.div_kw4 = make_fastdiv(uint32_t(small ? kw4 : 1));
+        ea.div_rows = make_fastdiv(uint32_t(small ? pl.Mk : 1));
+        ea.div_nh = make_fastdiv(uint32_t(small ? a.nh : 1));
+        if (small) expand_kernel<uint32_t><<<grid, 256, 0, s>>>(ea);
+        else expand_kernel<uint64_t><<<grid, 256, 0, s>>>(ea);
         count_launch();
         cudaError_t err = cudaGetLastError();
         if (err != cudaSuccess) return err;
