@@ -195,7 +195,7 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         if (ES == 2) w[j] = pack2(p.y_dt, f[2 * j], f[(2 * j + 1) % CW]);
-                        else w[j] = p.y_dt == DT_F32 ? __float_as_uint(f[j]) : v[j];
+                        else w[j] = p.y_dt == DT_F32 ? __float_as_uint(f[j]) : uint32_t(dot_of(v[j]));
                     }
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
