@@ -11,6 +11,45 @@ namespace bwta {
 extern std::atomic<uint64_t> g_launches;
 inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+// Programmatic dependent launch (PDL).  Every library kernel is launched with
+// programmatic stream serialization: it may start while its predecessor in
+// the stream is still finishing, runs only prologue work (barrier init, TMEM
+// allocation, descriptor prefetch) before pdl_wait(), and performs no global
+// memory access before it.  pdl_wait() returns once the predecessor grid has
+// completed and its memory is visible, so stream order is preserved.
+// pdl_launch_dependents() lets the next kernel start its own prologue early.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
+
+// cudaLaunchKernelEx with the PDL attribute (and an optional cluster size).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              int cluster, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+    if (cluster > 1) {
+        attr[n].id = cudaLaunchAttributeClusterDimension;
+        attr[n].val.clusterDim.x = cluster;
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    count_launch();
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 enum Dt { DT_F16 = 0, DT_BF16 = 1, DT_F32 = 2, DT_I32 = 3 };
 enum Kind { K_BINARY = 0, K_BOOL = 1, K_TERNARY = 2 };
 

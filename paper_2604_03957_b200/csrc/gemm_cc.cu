@@ -44,6 +44,8 @@ __global__ void __launch_bounds__(NT) matmul_cc_kernel(MatmulArgs p) {
     __shared__ __align__(16) uint32_t sBs[2][KW][BN + PAD];
     __shared__ __align__(16) uint32_t sBn[2][KW][BN + PAD];
 
+    pdl_launch_dependents();
+    pdl_wait();  // no global memory access before the predecessor grid completed
     const int t = threadIdx.x;
     const int tx = t & 15, ty = t >> 4;
     const int64_t e = blockIdx.z;
@@ -179,12 +181,10 @@ cudaError_t launch_matmul_cc(const MatmulArgs& a, cudaStream_t s) {
     if (a.M == 0 || a.N == 0 || a.nb * a.nh == 0) return cudaSuccess;
     dim3 grid(unsigned((a.N + BN - 1) / BN), unsigned((a.M + BM - 1) / BM), unsigned(a.nb * a.nh));
     const bool asg = a.a_sgn != nullptr, bnz = a.b_nz != nullptr;
-    count_launch();
-    if (asg && bnz) matmul_cc_kernel<true, true><<<grid, NT, 0, s>>>(a);
-    else if (asg) matmul_cc_kernel<true, false><<<grid, NT, 0, s>>>(a);
-    else if (bnz) matmul_cc_kernel<false, true><<<grid, NT, 0, s>>>(a);
-    else matmul_cc_kernel<false, false><<<grid, NT, 0, s>>>(a);
-    return cudaGetLastError();
+    if (asg && bnz) return launch_pdl(matmul_cc_kernel<true, true>, grid, NT, 0, s, 1, a);
+    if (asg) return launch_pdl(matmul_cc_kernel<true, false>, grid, NT, 0, s, 1, a);
+    if (bnz) return launch_pdl(matmul_cc_kernel<false, true>, grid, NT, 0, s, 1, a);
+    return launch_pdl(matmul_cc_kernel<false, false>, grid, NT, 0, s, 1, a);
 }
 
 }  // namespace bwta

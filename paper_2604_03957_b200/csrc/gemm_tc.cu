@@ -303,6 +303,10 @@ __global__ void __launch_bounds__(NT, 1)
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // prologue done (smem barriers, TMEM, descriptor prefetch): let the next
+    // kernel start its own, then wait for our inputs (predecessor grid)
+    pdl_launch_dependents();
+    pdl_wait();
 
     const int64_t tiles_per_entry = int64_t(p.m_tiles) * p.n_tiles;
     const int64_t total = p.entries * tiles_per_entry;
@@ -462,6 +466,8 @@ template <typename IDX>
 __global__ void __launch_bounds__(256) expand_kernel(ExpandArgs a) {
     const IDX total = IDX(a.entries * a.rows * a.kw4);
     const IDX kw4 = IDX(a.kw4), rows = IDX(a.rows), nh = IDX(a.nh);
+    pdl_launch_dependents();
+    pdl_wait();  // no global memory access before the predecessor grid completed
     for (IDX i = IDX(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += IDX(gridDim.x) * blockDim.x) {
         const IDX rr = fdiv(i, a.div_kw4), w = i - rr * kw4;
         const IDX e = fdiv(rr, a.div_rows), r = rr - e * rows;
@@ -577,20 +583,7 @@ cudaError_t launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb0, const CUte
     const int64_t tiles = p.entries * int64_t(p.m_tiles) * p.n_tiles;
     const int64_t slots = num_sms() / CG;
     const int grid = int((tiles < slots ? tiles : slots) * CG);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = C::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    count_launch();
-    return cudaLaunchKernelEx(&cfg, kern, ma, mb0, mb1, my, p);
+    return launch_pdl(kern, dim3(grid), dim3(NT), size_t(C::SMEM), s, CG, ma, mb0, mb1, my, p);
 }
 
 template <int BN, int CG>
@@ -638,10 +631,8 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void* ws, size_t ws_bytes, cud
         ea.div_kw4 = make_fastdiv(uint32_t(small ? kw4 : 1));
         ea.div_rows = make_fastdiv(uint32_t(small ? pl.Mk : 1));
         ea.div_nh = make_fastdiv(uint32_t(small ? a.nh : 1));
-        if (small) expand_kernel<uint32_t><<<grid, 256, 0, s>>>(ea);
-        else expand_kernel<uint64_t><<<grid, 256, 0, s>>>(ea);
-        count_launch();
-        cudaError_t err = cudaGetLastError();
+        cudaError_t err = small ? launch_pdl(expand_kernel<uint32_t>, grid, 256, 0, s, 1, ea)
+                                : launch_pdl(expand_kernel<uint64_t>, grid, 256, 0, s, 1, ea);
         if (err != cudaSuccess) return err;
     }
 

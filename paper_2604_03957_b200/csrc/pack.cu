@@ -161,6 +161,8 @@ __global__ void __launch_bounds__(256, 2) pack_rows_kernel(PackArgs p) {
     const IDX cols = IDX(p.cols);
     const IDX nthreads = IDX(gridDim.x) * blockDim.x;
     const IDX tid = IDX(blockIdx.x) * blockDim.x + threadIdx.x;
+    pdl_launch_dependents();
+    pdl_wait();  // no global memory access before the predecessor grid completed
 
     auto issue = [&](IDX gw0, uint4 (&v)[WplOf<T>::v][NV], IDX (&gr)[WplOf<T>::v], IDX (&gwv)[WplOf<T>::v]) {
 #pragma unroll
@@ -271,6 +273,8 @@ __global__ void __launch_bounds__(256, 2) pack_cols_kernel(PackArgs p) {
     const IDX items = IDX(p.nb * p.nh) * ngrp * ntile_c;
     const IDX warp0 = (IDX(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const IDX nwarps = (IDX(gridDim.x) * blockDim.x) >> 5;
+    pdl_launch_dependents();
+    pdl_wait();  // no global memory access before the predecessor grid completed
 
     // loads of item `it` for this lane's row (all zero past the last row)
     auto issue = [&](IDX it, uint4 (&v)[NV]) {
@@ -335,29 +339,31 @@ int grid_for(int64_t warp_items) {
 
 template <typename T, typename IDX>
 cudaError_t rows_dispatch(const PackArgs& a, cudaStream_t s, int grid) {
+    cudaError_t err = cudaSuccess;
 #define BWTA_ROWS(KIND)                                                                   \
     do {                                                                                  \
-        if (a.vec_ok) pack_rows_kernel<T, KIND, true, IDX><<<grid, 256, 0, s>>>(a);       \
-        else pack_rows_kernel<T, KIND, false, IDX><<<grid, 256, 0, s>>>(a);               \
+        if (a.vec_ok) err = launch_pdl(pack_rows_kernel<T, KIND, true, IDX>, grid, 256, 0, s, 1, a);  \
+        else err = launch_pdl(pack_rows_kernel<T, KIND, false, IDX>, grid, 256, 0, s, 1, a);         \
     } while (0)
     if (a.kind == K_BINARY) BWTA_ROWS(K_BINARY);
     else if (a.kind == K_BOOL) BWTA_ROWS(K_BOOL);
     else BWTA_ROWS(K_TERNARY);
 #undef BWTA_ROWS
-    return cudaGetLastError();
+    return err;
 }
 
 template <typename T, typename IDX>
 cudaError_t cols_dispatch(const PackArgs& a, cudaStream_t s, int grid) {
+    cudaError_t err = cudaSuccess;
 #define BWTA_COLS(KIND)                                                                   \
     do {                                                                                  \
-        if (a.vec_ok) pack_cols_kernel<T, KIND, true, IDX><<<grid, 256, 0, s>>>(a);       \
-        else pack_cols_kernel<T, KIND, false, IDX><<<grid, 256, 0, s>>>(a);               \
+        if (a.vec_ok) err = launch_pdl(pack_cols_kernel<T, KIND, true, IDX>, grid, 256, 0, s, 1, a);  \
+        else err = launch_pdl(pack_cols_kernel<T, KIND, false, IDX>, grid, 256, 0, s, 1, a);         \
     } while (0)
     if (a.kind == K_BOOL) BWTA_COLS(K_BOOL);
     else BWTA_COLS(K_TERNARY);
 #undef BWTA_COLS
-    return cudaGetLastError();
+    return err;
 }
 
 template <typename T>
@@ -382,7 +388,6 @@ cudaError_t launch_pack_rows(const PackArgs& a, cudaStream_t s) {
     const int grid = grid_for((total_words + 63) / 64);
     const bool small = total_words + 4 * int64_t(grid) * 256 < (int64_t(1) << 31) &&
                        a.cols + 32 < (int64_t(1) << 31);
-    count_launch();
     switch (a.dt) {
         case DT_F16: return rows_idx<__half>(a, s, grid, small);
         case DT_BF16: return rows_idx<__nv_bfloat16>(a, s, grid, small);
@@ -400,7 +405,6 @@ cudaError_t launch_pack_cols(const PackArgs& a, cudaStream_t s) {
     }
     const int grid = grid_for(items);
     const bool small = items + int64_t(grid) * 8 < (int64_t(1) << 31);
-    count_launch();
     switch (a.dt) {
         case DT_F16: return cols_idx<__half>(a, s, grid, small);
         case DT_BF16: return cols_idx<__nv_bfloat16>(a, s, grid, small);

@@ -306,3 +306,22 @@ def test_llama_prefill_full_size_sampled(B, n):
     # planes of sampled rows
     sgn, nz, _ = oracle.pack_act(storage(x[rows]), "f16", s_a, "ternary")
     assert np.array_equal(words(a.nz)[rows], nz) and np.array_equal(words(a.sgn)[rows], sgn)
+
+
+def test_nshard_gemm_single_rank_matches_full(B):
+    """dist.gemm_nshard with world = 1 runs the real local path (bwta_gemm with
+    y_transposed) and must reproduce the unsharded Y^T bit for bit; the rank
+    logic itself is covered by tests/test_dist.py (gloo, world 2)."""
+    from paper_2604_03957_b200 import dist as D
+    a, wp, s_a, s_w, qa, qw = _gemm_case(B, 200, 300, 768, 4242)
+    yt = D.gemm_nshard(a, wp, s_w.cuda(), s_a, 300, 1, 0, out_dtype=torch.float16)
+    d = oracle.dot(qa, qw, threads=oracle.default_threads())
+    assert_out_equal(yt, oracle.epilogue_linear(d, s_w.numpy(), s_a, "f16").T.copy(), "nshard")
+    # two local shards computed on one GPU and concatenated equal the full output
+    n = 300
+    parts = []
+    for r in range(2):
+        s0, e0 = D.shard_bounds(n, 2, r)
+        w_r = type(wp)(wp.sgn[s0:e0], None, "binary", wp.cols)
+        parts.append(B.bwta_gemm(a, w_r, s_w[s0:e0].cuda(), s_a, out_dtype=torch.float16, y_transposed=True))
+    assert torch.equal(torch.cat(parts, 0).cpu(), yt.cpu())
