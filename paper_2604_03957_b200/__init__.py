@@ -79,9 +79,12 @@ def _stream(stream) -> ctypes.c_void_p:
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def _opts(design: str):
+def _opts(design: str, tile=None):
+    """tile: optional (tile_n, cta_group) override of design (b)'s tile choice."""
     o = N.Opts()
     o.design = _DESIGN[design]
+    if tile is not None:
+        o.tile_n, o.cta_group = int(tile[0]), int(tile[1])
     return ctypes.byref(o)
 
 
@@ -163,7 +166,7 @@ def bwta_pack_weight(w: torch.Tensor, mu=None, stream=None) -> Packed:
 
 def bwta_gemm(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: float,
               out_dtype=torch.float16, y_transposed: bool = False, out: Optional[torch.Tensor] = None,
-              design: str = "auto", stream=None) -> torch.Tensor:
+              design: str = "auto", stream=None, tile=None) -> torch.Tensor:
     """Y = s_W s_A (sign(W - mu) (x) quant(A^T, s_A)).
 
     a: Packed activations [M, lda] (ternary or bool); w: Packed weights [N, ldw].
@@ -175,7 +178,7 @@ def bwta_gemm(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: fl
     dev = ar.device
     if out is None:
         out = torch.empty((n, m) if y_transposed else (m, n), dtype=out_dtype, device=dev)
-    o = _opts(design)
+    o = _opts(design, tile)
     ws, wsb = _workspace(lib.bwta_gemm_workspace_size(m, n, k, o), dev)
     ws_scale = None if w_scale is None else w_scale.to(device=dev, dtype=torch.float32).contiguous()
     st = lib.bwta_gemm(_ptr(a.sgn), _ptr(a.nz), _KIND[a.kind], m, ar.stride(-2), _ptr(w.sgn), n,
@@ -186,7 +189,7 @@ def bwta_gemm(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: fl
 
 
 def bwta_attn_qk(q: Packed, k: Packed, alpha: float, out_dtype=torch.float16,
-                 out: Optional[torch.Tensor] = None, design: str = "auto", stream=None) -> torch.Tensor:
+                 out: Optional[torch.Tensor] = None, design: str = "auto", stream=None, tile=None) -> torch.Tensor:
     """S = alpha * ternary(Q) (x) ternary(K)^T per (batch, head).
 
     q: Packed [B, H, Tq, ld] (or [B, Tq, ld] / [Tq, ld]); k: Packed ternary or binary
@@ -200,7 +203,7 @@ def bwta_attn_qk(q: Packed, k: Packed, alpha: float, out_dtype=torch.float16,
     if out is None:
         out = torch.empty(tuple(qr.shape[:-2]) + (tq, tk), dtype=out_dtype, device=qr.device)
     _, _, obs, ohs = _batch_dims(out)
-    o = _opts(design)
+    o = _opts(design, tile)
     ws, wsb = _workspace(lib.bwta_attn_qk_workspace_size(b * h, tq, tk, dh, o), qr.device)
     k_nz = k.nz if k.kind == "ternary" else None
     st = lib.bwta_attn_qk(_ptr(q.sgn), _ptr(q.nz), _ptr(k.sgn), _ptr(k_nz), b, h, tq, tk, dh,
@@ -212,7 +215,7 @@ def bwta_attn_qk(q: Packed, k: Packed, alpha: float, out_dtype=torch.float16,
 
 
 def bwta_attn_pv(p: Packed, vt: Packed, beta: float, out_dtype=torch.float16,
-                 out: Optional[torch.Tensor] = None, design: str = "auto", stream=None) -> torch.Tensor:
+                 out: Optional[torch.Tensor] = None, design: str = "auto", stream=None, tile=None) -> torch.Tensor:
     """O = beta * bool(Att) (x) ternary(V) per (batch, head)   (P:969-975).
 
     p: Packed bool (or ternary) [..., Tq, ldp] over Tk; vt: Packed ternary
@@ -226,7 +229,7 @@ def bwta_attn_pv(p: Packed, vt: Packed, beta: float, out_dtype=torch.float16,
     if out is None:
         out = torch.empty(tuple(pr.shape[:-2]) + (tq, dh), dtype=out_dtype, device=pr.device)
     _, _, obs, ohs = _batch_dims(out)
-    o = _opts(design)
+    o = _opts(design, tile)
     ws, wsb = _workspace(lib.bwta_attn_pv_workspace_size(b * h, tq, tk, dh, o), pr.device)
     p_sgn = p.sgn if p.kind == "ternary" else None
     st = lib.bwta_attn_pv(_ptr(p_sgn), _ptr(p.nz), _ptr(vt.sgn), _ptr(vt.nz), b, h, tq, tk, dh,

@@ -23,7 +23,8 @@ EXPORTS = ("bwta_ld_words", "bwta_status_string", "bwta_last_cuda_error", "bwta_
 
 
 class Opts(ctypes.Structure):
-    _fields_ = [("design", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+    _fields_ = [("design", ctypes.c_int32), ("tile_n", ctypes.c_int32), ("cta_group", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 5)]
 
 
 def _declare(L):

@@ -116,12 +116,19 @@ const bwta_opts_t* opts_or_default(const bwta_opts_t* o) {
 }
 
 // Run a matmul description with the requested design.
-bwta_status_t run_matmul(const MatmulArgs& a, void* ws, size_t ws_bytes, const bwta_opts_t* opts,
+bwta_status_t run_matmul(const MatmulArgs& a0, void* ws, size_t ws_bytes, const bwta_opts_t* opts,
                          cudaStream_t s) {
     opts = opts_or_default(opts);
     if (opts->design < 0 || opts->design > 2) return BWTA_ERR_INVALID_VALUE;
     for (int r : opts->reserved)
         if (r != 0) return BWTA_ERR_INVALID_VALUE;
+    if (!(opts->tile_n == 0 || opts->tile_n == 64 || opts->tile_n == 128 || opts->tile_n == 192 ||
+          opts->tile_n == 256) ||
+        opts->cta_group < 0 || opts->cta_group > 2)
+        return BWTA_ERR_INVALID_VALUE;
+    MatmulArgs a = a0;
+    a.tile_n = opts->tile_n;
+    a.cta_group = opts->cta_group;
     bool use_tc = false;
     if (opts->design == BWTA_DESIGN_TCGEN05) {
         if (!matmul_tc_supported(a)) return BWTA_ERR_UNSUPPORTED;

@@ -119,6 +119,7 @@ struct MatmulArgs {
     int y_trans;              // store Y^T (y[j*ldy + i])
     const float* col_scale;   // [N] or null
     float scalar;
+    int tile_n = 0, cta_group = 0;  // design (b) tile overrides (0 = auto)
 };
 
 cudaError_t launch_matmul_cc(const MatmulArgs& a, cudaStream_t s);

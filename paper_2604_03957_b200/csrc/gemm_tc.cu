@@ -7,26 +7,30 @@
 // compute; the epilogue applies c = fl32(scale[n] * scalar)
 // (w_scale * a_scale, or alpha / beta) exactly as design (a).
 //
-// Operand roles.  The kernel computes D[i][j] = sum_k A8[i][k] * B[j][k] with
-//   kernel-A : int8 image of the SMALLER operand, expanded once per call into
-//              the workspace by expand_kernel (L2-resident), loaded by TMA;
-//   kernel-B : the LARGER operand, read as packed bit planes by TMA (N*K/8
-//              bytes for binary weights) and unpacked to int8 in shared memory
-//              by 4 unpack warps, straight into the UMMA 128B-swizzled
-//              K-major layout.  No int8 copy of it ever touches HBM.
-// If the caller's A is the larger operand the roles swap and the epilogue
+// Operand roles.  The kernel computes D[i][j] = sum_k A[i][k] * B[j][k] with
+// BOTH operands read as packed bit planes by TMA (box 4 words x rows: 2 bits
+// per ternary element, 1 per bool/binary) and unpacked to int8 codes in
+// shared memory by 8 unpack warps, straight into the UMMA 128B-swizzled
+// K-major layout.  No int8 copy of either operand touches L2 or HBM: the
+// L2 -> SM traffic is the bit planes only (measured on B200: an int8 operand
+// image streamed by TMA capped the mainloop at ~740 cycles per 128-K stage,
+// ~24 B/clk/SM of L2 reads, against the 512-cycle tensor floor).  The
+// caller's A (M side) and W (N side) swap roles when M > N; the epilogue then
 // stores D^T (Y[m][n] = D[n][m]).
 //
-// CTA (one per SM, persistent over tiles of 128 x BN), 12 warps:
-//   warp 0     TMA producer: A8 tile (16 KB) + B bit tiles into a STAGES ring
+// CTA (one per SM, persistent over tiles of 128 x BN, or 256 x BN for a CTA
+// pair), 20 warps:
+//   warp 0     TMA producer: A and B bit-plane slices into a STAGES ring
 //   warp 1     MMA issuer: 4 x tcgen05.mma (128 x BN x 32) per 128-K stage,
 //              accumulators double-buffered in TMEM (2 x BN columns)
 //   warp 2     TMEM allocator
-//   warps 4-7  epilogue: tcgen05.ld 32x32b -> fp32 scale -> fp16/bf16/fp32/
-//              i32 -> 128B-swizzled staging -> TMA tensor store (clips tails)
-//   warps 8-11 unpack: bits (smem) -> int8 codes (smem), fence.proxy.async
-// Barriers: full (TMA tx), bready (unpack done), empty (MMA commit),
-// tfull (accumulator ready), tempty (epilogue drained TMEM).
+//   warps 4-7, 12-15  epilogue (two warps per TMEM lane quarter, alternate
+//              64-column chunks): tcgen05.ld -> fp32 scale -> fp16/bf16/fp32/
+//              i32 -> smem staging (stmatrix) -> TMA tensor store (clips tails)
+//   warps 8-11 unpack B rows, warps 16-19 unpack A rows: bits (smem) ->
+//              int8 codes (smem), fence.proxy.async
+// Barriers: full (TMA tx), bready (8 unpack warps x CG), empty (MMA commit),
+// tfull (accumulator ready), tempty (8 epilogue warps x CG drained TMEM).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -45,16 +49,17 @@ using namespace sm100;
 constexpr int BM = 128;     // MMA M (kernel-A rows per tile), cta_group::1
 constexpr int BK = 128;     // K elements (= int8 bytes) per stage: one 128B swizzle row
 constexpr int UMMA_K = 32;  // K per tcgen05.mma for 8-bit inputs
-constexpr int NT = 384;     // 12 warps
+constexpr int NT = 640;     // 20 warps
 constexpr int OUT_BUF = 4096;
 
-enum BKind { B_BINARY = 0, B_BOOL = 1, B_TERNARY = 2 };
+enum BKind { B_BINARY = 0, B_BOOL = 1, B_TERNARY = 2 };  // operand kinds (A or B)
 
 struct TcParams {
     int64_t M, N;  // kernel rows (A side) / cols (B side) per entry
     int num_kb;
     int64_t nh, entries;
     int m_tiles, n_tiles;
+    int a_kind, b_kind;  // B_BINARY / B_BOOL / B_TERNARY
     // epilogue
     void* y;
     int y_dt;
@@ -66,22 +71,29 @@ struct TcParams {
     float scalar;
 };
 
-template <int BN, int BKIND, int CG>
+__host__ __device__ constexpr int nplanes_of(int kind) { return kind == B_TERNARY ? 2 : 1; }
+
+template <int BN, int CG>
 struct Cfg {
     static constexpr int BNC = BN / CG;          // kernel-B rows held (and unpacked) per CTA
-    static constexpr int A_BYTES = BM * BK;
+    static constexpr int A_BYTES = BM * BK;      // int8 codes
     static constexpr int B_BYTES = BNC * BK;
-    static constexpr int PLANE_BYTES = BNC * 16;  // 4 words per row per stage
-    static constexpr int NPLANES = BKIND == B_TERNARY ? 2 : 1;
-    static constexpr int STAGE = A_BYTES + B_BYTES + NPLANES * PLANE_BYTES;
-    static constexpr int OUT_BYTES = 4 * 2 * OUT_BUF;
-    static constexpr int STAGES_FIT = (210 * 1024 - OUT_BYTES) / STAGE;
+    static constexpr int ABITS = 2 * BM * 16;    // up to 2 planes x 4 words per row
+    static constexpr int BBITS = 2 * BNC * 16;
+    static constexpr int STAGE = A_BYTES + B_BYTES + ABITS + BBITS;
+    static constexpr int OUT_BYTES = 8 * OUT_BUF;                           // one staging buffer per epilogue warp
+    static constexpr int SCALE_COLS = (BN + 127) / 128 * 64;                 // columns per epilogue warp
+    static constexpr int SCALE_BYTES = 8 * SCALE_COLS * 4;                  // per-warp column scales
+    static constexpr int STAGES_FIT = (210 * 1024 - OUT_BYTES - SCALE_BYTES) / STAGE;
     static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
     static constexpr int BAR_BYTES = 256;
-    static constexpr int SMEM = 1024 + STAGES * STAGE + OUT_BYTES + BAR_BYTES;
-    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int SMEM = 1024 + STAGES * STAGE + OUT_BYTES + SCALE_BYTES + BAR_BYTES;
+    static constexpr int TMEM_COLS = 2 * BN <= 128 ? 2 * BN : (2 * BN <= 256 ? 256 : 512);  // power of 2
     static_assert(STAGES >= 2, "pipeline too shallow");
     static_assert(BNC % 8 == 0, "swizzle atoms are 8 rows");
+    static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0 && OUT_BYTES % 1024 == 0 && SCALE_BYTES % 128 == 0 &&
+                      ABITS % 128 == 0 && BBITS % 128 == 0,
+                  "smem region alignment");
 };
 
 // K order inside the int8 operand tiles.  Element k (0..31) of a packed word
@@ -102,6 +114,20 @@ struct Cfg {
 //   ternary (x0 = sgn, x1 = nz):  nz << 6 | sgn << 7       -> 0 / +64 / -64
 // (ternary planes are canonical: sgn is a subset of nz, include/bwta.h)
 constexpr int CODE_SHIFT = 12;  // log2(64 * 64)
+
+// Timeline hooks (tools/trace_gemm.py; compiled only with -DBWTA_TRACE)
+#ifdef BWTA_TRACE
+// one writer per (CTA, event, index): plain stores, no atomics on the hot path
+__device__ unsigned long long g_trace[2][16][1024];
+#define TRACE(ev, idx, cond)                                                             \
+    do {                                                                                 \
+        if ((cond) && blockIdx.x < 2 && (idx) < 1024) g_trace[blockIdx.x][ev][idx] = clock64(); \
+    } while (0)
+#else
+#define TRACE(ev, idx, cond) \
+    do {                     \
+    } while (0)
+#endif
 
 __device__ __forceinline__ uint32_t shl_fma(uint32_t x, int k) {  // x << k as IMAD.SHL (FMA pipe)
     uint32_t r;
@@ -134,84 +160,88 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
-// Epilogue warp `ew` owns TMEM lanes 32*ew .. 32*ew+31 (kernel rows).  ES =
-// output element size; a chunk is CW = 128/ES columns = one 128-byte row.
-template <int BN, int ES, int CG>
-__device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& tmY, uint32_t tmem_base, uint8_t* sOut,
-                                         uint64_t* tfull, uint64_t* tempty, int ew, int lane,
-                                         int64_t tiles_per_entry, int64_t total, int rank, int64_t t0,
-                                         int64_t tstep) {
+// ---------------------------------------------------------------------------
+// Epilogue.  8 warps: warp (h, q) (warps 4+q and 12+q) owns TMEM lane quarter
+// q (kernel rows 32q..32q+31 of the CTA's 128) and the column chunks
+// c = h, h+2, ... of CW = 128/ES columns (one 128-byte output row each).
+// A chunk is staged in the warp's own 4 KB smem buffer and written by one
+// TMA tensor store (which clips the M/N tails).
+//
+// Fast path (fp16/bf16 out, TMA store): tcgen05.ld.16x256b puts the
+// accumulators in the mma.sync m16n8 fragment layout, two adjacent columns
+// per register pair, so a pair converts to one f16x2 / bf16x2 word and
+// stmatrix (.trans for D^T) writes 8x8 blocks -- 1 shared store per 8
+// outputs per thread, no shuffles.  Scaling: acc = 4096 * dot exactly and
+// float(acc) is exact (|dot| <= 2^24), so fl(float(acc) * (c * 2^-12)) ==
+// fl(float(dot) * c) (R5) whenever c * 2^-12 is exact, i.e. |c| >= 2^-114, c
+// = 0 or c non-finite.  A tile with any other scale takes the generic path.
+// ---------------------------------------------------------------------------
+constexpr float INV4096 = 1.0f / 4096.0f;
+
+__device__ __forceinline__ bool scale_ok(float c) {
+    const float a = fabsf(c);
+    return !(a < 0x1p-114f) || a == 0.f;  // NaN compares false -> ok
+}
+
+// generic tile: 32x32b loads, any output type, TMA or direct stores.  A
+// chunk (one 128-byte output row per thread, CW columns) is processed in
+// 32-column halves to bound register use.
+template <int BN, int ES>
+__device__ __forceinline__ void epi_tile_generic(const TcParams& p, const CUtensorMap& tmY, uint32_t tacc,
+                                                 uint8_t* stg, int q, int h, int lane, int64_t mrow0, int nt,
+                                                 int eb, int eh) {
     constexpr int CW = 128 / ES;
-    uint8_t* stg_base = sOut + ew * 2 * OUT_BUF;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    uint32_t nchunk = 0;
-    for (int64_t t = t0; t < total; t += tstep) {
-        const int64_t e = t / tiles_per_entry;
-        const int64_t r = t % tiles_per_entry;
-        const int mt = int(r % p.m_tiles), nt = int(r / p.m_tiles);
-        const int eb = int(e / p.nh), eh = int(e % p.nh);
-        mbar_wait(&tfull[acc], acc_phase);
-        tc_fence_after();
-        const int64_t mrow0 = int64_t(mt) * BM * CG + rank * BM;  // first kernel row of this CTA
-        const int64_t row = mrow0 + ew * 32 + lane;               // kernel row of this thread
-        const bool rok = row < p.M;
-        float crow = p.scalar;
-        if (p.scale_on_rows && p.scale) crow = __fmul_rn(__ldg(p.scale + (rok ? row : 0)), p.scalar);
-        const bool col_scaled = !p.scale_on_rows && p.scale;
-        const int64_t ybase = int64_t(eb) * p.y_bs + int64_t(eh) * p.y_hs;
+    const int64_t row = mrow0 + q * 32 + lane;  // kernel row of this thread
+    const bool rok = row < p.M;
+    float crow = p.scalar;
+    if (p.scale_on_rows && p.scale) crow = __fmul_rn(__ldg(p.scale + (rok ? row : 0)), p.scalar);
+    const bool col_scaled = !p.scale_on_rows && p.scale;
+    const int64_t ybase = int64_t(eb) * p.y_bs + int64_t(eh) * p.y_hs;
+    const uint32_t sbase = smem_u32(stg);
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += CW) {
-            const int64_t n0 = int64_t(nt) * BN + c0;
-            uint32_t v[CW];
-            tmem_ld_32x32b_x32(tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN + c0),
-                               *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-            if (CW == 64)
-                tmem_ld_32x32b_x32(tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN + c0 + 32),
-                                   *reinterpret_cast<uint32_t(*)[32]>(&v[CW == 64 ? 32 : 0]));
+    for (int c0 = h * CW; c0 < BN; c0 += 2 * CW) {
+        const int64_t n0 = int64_t(nt) * BN + c0;
+        if (n0 >= p.N) break;
+        if (p.use_tma_store) {
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+        }
+#pragma unroll 1
+        for (int u = 0; u < CW / 32; ++u) {
+            uint32_t v[32];
+            tmem_ld_32x32b_x32(tacc + (uint32_t(q * 32) << 16) + uint32_t(c0 + 32 * u), v);
             tmem_wait_ld();
-            if (n0 >= p.N) continue;
-            // per-column scale: lane j holds the scale of column n0 + j (+ 32)
-            float cl[CW / 32];
+            const int64_t nl = n0 + 32 * u + lane;
+            const float cl = col_scaled ? __fmul_rn(__ldg(p.scale + (nl < p.N ? nl : 0)), p.scalar) : crow;
+            float f[32];
 #pragma unroll
-            for (int u = 0; u < CW / 32; ++u) {
-                const int64_t n = n0 + 32 * u + lane;
-                cl[u] = col_scaled ? __fmul_rn(__ldg(p.scale + (n < p.N ? n : 0)), p.scalar) : crow;
-            }
-            float f[CW];
-#pragma unroll
-            for (int j = 0; j < CW; ++j) {
-                const float c = col_scaled ? __shfl_sync(0xffffffffu, cl[j / 32], j % 32) : crow;
-                f[j] = scaled(v[j], c);
-            }
+            for (int j = 0; j < 32; ++j) f[j] = scaled(v[j], col_scaled ? __shfl_sync(0xffffffffu, cl, j) : crow);
             if (p.use_tma_store) {
-                uint8_t* stg = stg_base + (nchunk & 1) * OUT_BUF;
-                if (lane == 0) bulk_wait_read<1>();
-                __syncwarp();
-                const uint32_t sbase = smem_u32(stg);
                 if (!p.out_trans) {
-                    // row `lane` of a [32 rows x 128 B] box, 128B-swizzled
-                    uint32_t w[32];
+                    // row `lane` of a [32 rows x 128 B] box, 128B-swizzled (fp16/bf16: this half = 64 B)
+                    if (ES == 2) {
+                        uint32_t w[16];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        if (ES == 2) w[j] = pack2(p.y_dt, f[2 * j], f[(2 * j + 1) % CW]);
-                        else w[j] = p.y_dt == DT_F32 ? __float_as_uint(f[j]) : uint32_t(dot_of(v[j]));
-                    }
+                        for (int j = 0; j < 16; ++j) w[j] = pack2(p.y_dt, f[2 * j], f[2 * j + 1]);
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        sts128(sbase + lane * 128 + ((q ^ (lane & 7)) << 4), w[4 * q], w[4 * q + 1], w[4 * q + 2],
-                               w[4 * q + 3]);
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        tma_store_4d(&tmY, stg, int(n0), int(mrow0 + ew * 32), eh, eb);
-                        bulk_commit();
+                        for (int qq = 0; qq < 4; ++qq)
+                            sts128(sbase + lane * 128 + (((4 * u + qq) ^ (lane & 7)) << 4), w[4 * qq], w[4 * qq + 1],
+                                   w[4 * qq + 2], w[4 * qq + 3]);
+                    } else {
+#pragma unroll
+                        for (int qq = 0; qq < 8; ++qq) {
+                            uint32_t o[4];
+#pragma unroll
+                            for (int x = 0; x < 4; ++x)
+                                o[x] = p.y_dt == DT_F32 ? __float_as_uint(f[4 * qq + x]) : uint32_t(dot_of(v[4 * qq + x]));
+                            sts128(sbase + lane * 128 + ((qq ^ (lane & 7)) << 4), o[0], o[1], o[2], o[3]);
+                        }
                     }
                 } else {
                     // box [CW kernel-cols][32 kernel-rows]: lane is the contiguous index
 #pragma unroll
-                    for (int j = 0; j < CW; ++j) {
-                        const uint32_t a = sbase + j * 32 * ES + lane * ES;
+                    for (int j = 0; j < 32; ++j) {
+                        const uint32_t a = sbase + (32 * u + j) * 32 * ES + lane * ES;
                         if (ES == 2) {
                             const uint32_t h2 = pack2(p.y_dt, f[j], 0.f);
                             asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(uint16_t(h2 & 0xffffu)) : "memory");
@@ -220,19 +250,12 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
                             asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(o) : "memory");
                         }
                     }
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        tma_store_4d(&tmY, stg, int(mrow0 + ew * 32), int(n0), eh, eb);
-                        bulk_commit();
-                    }
                 }
-                ++nchunk;
             } else {
                 // direct stores (outputs whose layout TMA cannot describe)
 #pragma unroll
-                for (int j = 0; j < CW; ++j) {
-                    const int64_t n = n0 + j;
+                for (int j = 0; j < 32; ++j) {
+                    const int64_t n = n0 + 32 * u + j;
                     if (rok && n < p.N) {
                         const int64_t idx = ybase + (p.out_trans ? n * p.ldy + row : row * p.ldy + n);
                         if (p.y_dt == DT_F16) reinterpret_cast<__half*>(p.y)[idx] = __float2half_rn(f[j]);
@@ -243,8 +266,152 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
                 }
             }
         }
+        if (p.use_tma_store) {
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                if (!p.out_trans) tma_store_4d(&tmY, stg, int(n0), int(mrow0 + q * 32), eh, eb);
+                else tma_store_4d(&tmY, stg, int(mrow0 + q * 32), int(n0), eh, eb);
+                bulk_commit();
+            }
+        }
+    }
+}
+
+// fast tile: fp16/bf16 output through TMA (see above).  cs = this warp's
+// column scales (c * 2^-12, 64 per chunk) when column-scaled; cr = the
+// thread's four row scales (rows 16b + 8i + lane/4) when row-scaled.
+template <int BN, bool BF16>
+__device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorMap& tmY, uint32_t tacc, uint8_t* stg,
+                                              const float* cs, bool col_scaled, const float (&cr)[4], int q, int h,
+                                              int lane, int64_t mrow0, int nt, int eb, int eh, int tix) {
+    constexpr int CW = 64;
+    const bool tr = h == 0 && q == 0 && lane == 0;
+    (void)tr;
+    (void)tix;
+    const int t0 = lane & 3;
+    const uint32_t sbase = smem_u32(stg);
+    // stmatrix addresses: matrix mi = lane/8 (column group offset mi/2, row half mi%2), line li = lane%8
+    const int mi = lane >> 3, li = lane & 7;
+#pragma unroll 1
+    for (int i = 0, c0 = h * CW; c0 < BN; ++i, c0 += 2 * CW) {
+        const int64_t n0 = int64_t(nt) * BN + c0;
+        if (n0 >= p.N) break;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {  // 16-lane block b: rows 16b .. 16b+15 of the warp's 32
+            uint32_t v[32];
+            tmem_ld_16x256b_x8(tacc + (uint32_t(q * 32 + 16 * b) << 16) + uint32_t(c0), v);
+            tmem_wait_ld();
+            TRACE(9, tix * 8 + i * 2 + b, tr);
+            // pk[2g + i2]: rows 16b + 8*i2 + lane/4, columns 8g + 2*t0, +1
+            uint32_t pk[16];
+#pragma unroll
+            for (int g = 0; g < 8; ++g) {
+                float ca = 0.f, cb = 0.f;
+                if (col_scaled) {
+                    const float2 c2 = *reinterpret_cast<const float2*>(cs + i * CW + 8 * g + 2 * t0);
+                    ca = c2.x;
+                    cb = c2.y;
+                }
+#pragma unroll
+                for (int i2 = 0; i2 < 2; ++i2) {
+                    const float c_lo = col_scaled ? ca : cr[2 * b + i2];
+                    const float c_hi = col_scaled ? cb : cr[2 * b + i2];
+                    const float f0 = __fmul_rn(__int2float_rn(int32_t(v[4 * g + 2 * i2])), c_lo);
+                    const float f1 = __fmul_rn(__int2float_rn(int32_t(v[4 * g + 2 * i2 + 1])), c_hi);
+                    pk[2 * g + i2] = pack2(BF16 ? DT_BF16 : DT_F16, f0, f1);
+                }
+            }
+            if (b == 0) {
+                if (lane == 0) bulk_wait_read<0>();  // the previous store has read the buffer
+                __syncwarp();
+            }
+#pragma unroll
+            for (int gp = 0; gp < 4; ++gp) {
+                const int g = 2 * gp + (mi >> 1);
+                const int r = 16 * b + 8 * (mi & 1);  // first row of this thread's matrix
+                if (!p.out_trans) {
+                    const int row = r + li;
+                    stmatrix_x4(sbase + row * 128 + ((g ^ (row & 7)) << 4), pk[4 * gp], pk[4 * gp + 1],
+                                pk[4 * gp + 2], pk[4 * gp + 3]);
+                } else {
+                    stmatrix_x4_trans(sbase + (8 * g + li) * 64 + r * 2, pk[4 * gp], pk[4 * gp + 1], pk[4 * gp + 2],
+                                      pk[4 * gp + 3]);
+                }
+            }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        TRACE(12, tix * 4 + i, tr);
+        if (lane == 0) {
+            if (!p.out_trans) tma_store_4d(&tmY, stg, int(n0), int(mrow0 + q * 32), eh, eb);
+            else tma_store_4d(&tmY, stg, int(mrow0 + q * 32), int(n0), eh, eb);
+            bulk_commit();
+        }
+    }
+}
+
+template <int BN, int ES, int CG>
+__device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& tmY, uint32_t tmem_base, uint8_t* sOut,
+                                         float* sScale, uint64_t* tfull, uint64_t* tempty, int q, int h, int lane,
+                                         int64_t tiles_per_entry, int64_t total, int rank, int64_t t0,
+                                         int64_t tstep) {
+    uint8_t* stg = sOut + (h * 4 + q) * OUT_BUF;
+    float* cs = sScale + (h * 4 + q) * Cfg<BN, CG>::SCALE_COLS;
+    const bool fast_ok = ES == 2 && p.use_tma_store;
+    const bool col_scaled = !p.scale_on_rows && p.scale;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int tix = 0;
+    for (int64_t t = t0; t < total; t += tstep, ++tix) {
+        const int64_t e = t / tiles_per_entry;
+        const int64_t r = t % tiles_per_entry;
+        const int mt = int(r % p.m_tiles), nt = int(r / p.m_tiles);
+        const int eb = int(e / p.nh), eh = int(e % p.nh);
+        const int64_t mrow0 = int64_t(mt) * BM * CG + rank * BM;  // first kernel row of this CTA
+        // scales of this tile (loaded before the accumulator is ready)
+        bool ok = fast_ok;
+        float cr[4] = {0.f, 0.f, 0.f, 0.f};
+        if (fast_ok) {
+            if (col_scaled) {
+                // this warp's chunks: columns nt*BN + (2i + h)*64 + [0, 64)
+                for (int i = 0, c0 = h * 64; c0 < BN; ++i, c0 += 128) {
+                    const int64_t n = int64_t(nt) * BN + c0 + 2 * lane;
+                    const float a = __fmul_rn(__ldg(p.scale + (n < p.N ? n : 0)), p.scalar);
+                    const float b = __fmul_rn(__ldg(p.scale + (n + 1 < p.N ? n + 1 : 0)), p.scalar);
+                    ok = ok && scale_ok(a) && scale_ok(b);
+                    *reinterpret_cast<float2*>(cs + i * 64 + 2 * lane) = make_float2(a * INV4096, b * INV4096);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    float c = p.scalar;
+                    if (p.scale_on_rows && p.scale) {
+                        const int64_t row = mrow0 + q * 32 + 16 * (k >> 1) + 8 * (k & 1) + (lane >> 2);
+                        c = __fmul_rn(__ldg(p.scale + (row < p.M ? row : 0)), p.scalar);
+                    }
+                    ok = ok && scale_ok(c);
+                    cr[k] = c * INV4096;
+                }
+            }
+            ok = __all_sync(0xffffffffu, ok);
+            __syncwarp();
+        }
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        TRACE(5, tix, h == 0 && q == 0 && lane == 0);
+        const uint32_t tacc = tmem_base + uint32_t(acc * BN);
+        if (ok) {
+            if (p.y_dt == DT_BF16)
+                epi_tile_fast<BN, true>(p, tmY, tacc, stg, cs, col_scaled, cr, q, h, lane, mrow0, nt, eb, eh, tix);
+            else
+                epi_tile_fast<BN, false>(p, tmY, tacc, stg, cs, col_scaled, cr, q, h, lane, mrow0, nt, eb, eh, tix);
+        } else {
+            epi_tile_generic<BN, ES>(p, tmY, tacc, stg, q, h, lane, mrow0, nt, eb, eh);
+        }
         tc_fence_before();
         __syncwarp();
+        TRACE(6, tix, h == 0 && q == 0 && lane == 0);
         if (lane == 0) {
             if (CG == 1) mbar_arrive(&tempty[acc]);
             else mbar_arrive_cluster(mapa_smem(&tempty[acc], 0));  // the leader owns the MMA
@@ -255,18 +422,59 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
     if (lane == 0) bulk_wait_all();
 }
 
-template <int BN, int BKIND, int CG>
+// One operand row (128 K-elements = 4 words per plane) -> 128 int8 codes at
+// rowaddr in the UMMA 128B-swizzled K-major layout (row r of its 8-row atom).
+// p0: sgn (binary, ternary) or nz (bool); p1: nz (ternary).
+template <int KIND>
+__device__ __forceinline__ void unpack_row(uint32_t p0addr, uint32_t p1addr, uint32_t rowaddr, int r) {
+    const uint4 w0 = lds128(p0addr);
+    uint4 w1 = make_uint4(0, 0, 0, 0);
+    if (KIND == B_TERNARY) w1 = lds128(p1addr);
+    uint32_t x0[4] = {w0.x, w0.y, w0.z, w0.w};
+    const uint32_t x1[4] = {w1.x, w1.y, w1.z, w1.w};
+    if (KIND == B_TERNARY) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) x0[g] &= x1[g];  // canonical sgn (subset of nz)
+    }
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {  // 32-element group = one packed word
+        uint32_t o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = unpack_word<KIND>(x0[g], x1[g], j);
+        sts128(rowaddr + (((2 * g) ^ (r & 7)) << 4), o[0], o[1], o[2], o[3]);
+        sts128(rowaddr + (((2 * g + 1) ^ (r & 7)) << 4), o[4], o[5], o[6], o[7]);
+    }
+}
+
+// rows [r0, rows) step `step` of one operand slice (warp-uniform kind)
+__device__ __forceinline__ void unpack_rows(int kind, uint32_t bits, int plane_bytes, uint32_t dst, int r0, int rows,
+                                            int step) {
+    if (kind == B_TERNARY) {
+        for (int r = r0; r < rows; r += step) unpack_row<B_TERNARY>(bits + r * 16, bits + plane_bytes + r * 16, dst + r * 128, r);
+    } else if (kind == B_BOOL) {
+        for (int r = r0; r < rows; r += step) unpack_row<B_BOOL>(bits + r * 16, 0, dst + r * 128, r);
+    } else {
+        for (int r = r0; r < rows; r += step) unpack_row<B_BINARY>(bits + r * 16, 0, dst + r * 128, r);
+    }
+}
+
+template <int BN, int CG>
 __global__ void __launch_bounds__(NT, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
-                   const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmY, TcParams p) {
-    using C = Cfg<BN, BKIND, CG>;
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
+                   const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
+                   const __grid_constant__ CUtensorMap tmY, TcParams p) {
+    using C = Cfg<BN, CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned regions first (SW128 operand tiles, SW128 output
+    // staging), then the 128-byte aligned bit-plane stages, then barriers
     uint8_t* sA = smem;
     uint8_t* sB = sA + C::STAGES * C::A_BYTES;
-    uint8_t* sBits = sB + C::STAGES * C::B_BYTES;  // [stage][plane][BNC rows][16 B]
-    uint8_t* sOut = sBits + C::STAGES * C::NPLANES * C::PLANE_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sOut + C::OUT_BYTES);
+    uint8_t* sOut = sB + C::STAGES * C::B_BYTES;
+    float* sScale = reinterpret_cast<float*>(sOut + C::OUT_BYTES);
+    uint8_t* sABits = sOut + C::OUT_BYTES + C::SCALE_BYTES;  // [stage][plane][128 rows][16 B]
+    uint8_t* sBBits = sABits + C::STAGES * C::ABITS;         // [stage][plane][BNC rows][16 B]
+    uint64_t* full = reinterpret_cast<uint64_t*>(sBBits + C::STAGES * C::BBITS);
     uint64_t* bready = full + C::STAGES;
     uint64_t* empty = bready + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;
@@ -277,20 +485,22 @@ __global__ void __launch_bounds__(NT, 1)
     const int lane = threadIdx.x & 31;
     const int rank = CG == 2 ? int(cluster_ctarank()) : 0;
     const bool leader = rank == 0;
+    const int a_planes = nplanes_of(p.a_kind), b_planes = nplanes_of(p.b_kind);
 
     if (warp == 0 && lane == 0) {
-        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmA0);
+        if (a_planes == 2) tma_prefetch_desc(&tmA1);
         tma_prefetch_desc(&tmB0);
-        if (C::NPLANES == 2) tma_prefetch_desc(&tmB1);
+        if (b_planes == 2) tma_prefetch_desc(&tmB1);
         if (p.use_tma_store) tma_prefetch_desc(&tmY);
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&bready[s], 4 * CG);  // unpack warps of every CTA of the pair
+            mbar_init(&bready[s], 8 * CG);  // A and B unpack warps of every CTA of the pair
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4 * CG);  // epilogue warps of every CTA of the pair
+            mbar_init(&tempty[a], 8 * CG);  // epilogue warps of every CTA of the pair
         }
         fence_barrier_init();
     }
@@ -307,6 +517,7 @@ __global__ void __launch_bounds__(NT, 1)
     // kernel start its own, then wait for our inputs (predecessor grid)
     pdl_launch_dependents();
     pdl_wait();
+    TRACE(0, 0, threadIdx.x == 0);
 
     const int64_t tiles_per_entry = int64_t(p.m_tiles) * p.n_tiles;
     const int64_t total = p.entries * tiles_per_entry;
@@ -314,8 +525,10 @@ __global__ void __launch_bounds__(NT, 1)
 
     if (warp == 0) {
         // ------------------------------ TMA producer ------------------------------
+        const uint32_t tx = uint32_t(a_planes * BM * 16 + b_planes * C::BNC * 16);
         int stage = 0;
         uint32_t phase = 0;
+        int it = 0;
         for (int64_t t = t0; t < total; t += tstep) {
             const int64_t e = t / tiles_per_entry;
             const int64_t r = t % tiles_per_entry;
@@ -325,12 +538,16 @@ __global__ void __launch_bounds__(NT, 1)
             const int brow = nt * BN + rank * C::BNC;
             for (int kb = 0; kb < p.num_kb; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1);
+                TRACE(1, it, lane == 0);
+                ++it;
                 if (lane == 0) {
-                    mbar_arrive_expect_tx(&full[stage], C::A_BYTES + C::NPLANES * C::PLANE_BYTES);
-                    tma_load_3d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, arow, int(e));
-                    uint8_t* bits = sBits + stage * C::NPLANES * C::PLANE_BYTES;
-                    tma_load_4d(bits, &tmB0, &full[stage], kb * 4, brow, eh, eb);
-                    if (C::NPLANES == 2) tma_load_4d(bits + C::PLANE_BYTES, &tmB1, &full[stage], kb * 4, brow, eh, eb);
+                    mbar_arrive_expect_tx(&full[stage], tx);
+                    uint8_t* ab = sABits + stage * C::ABITS;
+                    tma_load_4d(ab, &tmA0, &full[stage], kb * 4, arow, eh, eb);
+                    if (a_planes == 2) tma_load_4d(ab + BM * 16, &tmA1, &full[stage], kb * 4, arow, eh, eb);
+                    uint8_t* bb = sBBits + stage * C::BBITS;
+                    tma_load_4d(bb, &tmB0, &full[stage], kb * 4, brow, eh, eb);
+                    if (b_planes == 2) tma_load_4d(bb + C::BNC * 16, &tmB1, &full[stage], kb * 4, brow, eh, eb);
                 }
                 __syncwarp();
                 if (++stage == C::STAGES) {
@@ -347,14 +564,16 @@ __global__ void __launch_bounds__(NT, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
+            int it = 0;
             for (int64_t t = t0; t < total; t += tstep) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + uint32_t(acc * BN);
                 for (int kb = 0; kb < p.num_kb; ++kb) {
-                    mbar_wait(&full[stage], phase);
                     mbar_wait(&bready[stage], phase);
                     tc_fence_after();
+                    TRACE(4, it, lane == 0);
+                    ++it;
                     if (lane == 0) {
                         const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
                         const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
@@ -382,40 +601,27 @@ __global__ void __launch_bounds__(NT, 1)
                 if (acc == 0) acc_phase ^= 1;
             }
         }
-    } else if (warp >= 8) {
-        // ------------------------------ unpack ------------------------------
-        const int ut = threadIdx.x - 256;  // 0..127
+    } else if ((warp >= 8 && warp < 12) || warp >= 16) {
+        // ------------------------------ unpack (8-11: B rows, 16-19: A rows) ------------------------------
+        const bool is_a = warp >= 16;
+        const int ut = threadIdx.x - (is_a ? 512 : 256);  // 0..127
+        const int kind = is_a ? p.a_kind : p.b_kind;
+        const int rows = is_a ? BM : C::BNC;
+        const int plane_bytes = is_a ? BM * 16 : C::BNC * 16;
         const uint32_t bready_addr0 = CG == 2 ? mapa_smem(&bready[0], 0) : 0u;
         int stage = 0;
         uint32_t phase = 0;
+        int it = 0;
         for (int64_t t = t0; t < total; t += tstep) {
-            for (int kb = 0; kb < p.num_kb; ++kb) {
+            for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
                 mbar_wait(&full[stage], phase);
-                const uint32_t bits = smem_u32(sBits + stage * C::NPLANES * C::PLANE_BYTES);
-                const uint32_t bdst = smem_u32(sB + stage * C::B_BYTES);
-#pragma unroll
-                for (int i = 0; i < (C::BNC + 127) / 128; ++i) {
-                    const int r = ut + 128 * i;
-                    if (r < C::BNC) {
-                        // plane 0: sgn (binary/ternary) or nz (bool); plane 1: nz (ternary)
-                        const uint4 w0 = lds128(bits + r * 16);
-                        uint4 w1 = make_uint4(0, 0, 0, 0);
-                        if (BKIND == B_TERNARY) w1 = lds128(bits + C::PLANE_BYTES + r * 16);
-                        const uint32_t p0[4] = {w0.x, w0.y, w0.z, w0.w};
-                        const uint32_t p1[4] = {w1.x, w1.y, w1.z, w1.w};
-                        const uint32_t rowaddr = bdst + r * 128;
-#pragma unroll
-                        for (int g = 0; g < 4; ++g) {  // 32-element group = one packed word
-                            uint32_t o[8];
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) o[j] = unpack_word<BKIND>(p0[g], p1[g], j);
-                            sts128(rowaddr + (((2 * g) ^ (r & 7)) << 4), o[0], o[1], o[2], o[3]);
-                            sts128(rowaddr + (((2 * g + 1) ^ (r & 7)) << 4), o[4], o[5], o[6], o[7]);
-                        }
-                    }
-                }
+                TRACE(is_a ? 10 : 2, it, ut == 0);
+                const uint32_t bits = is_a ? smem_u32(sABits + stage * C::ABITS) : smem_u32(sBBits + stage * C::BBITS);
+                const uint32_t dst = is_a ? smem_u32(sA + stage * C::A_BYTES) : smem_u32(sB + stage * C::B_BYTES);
+                unpack_rows(kind, bits, plane_bytes, dst, ut, rows, 128);
                 fence_proxy_async_smem();
                 __syncwarp();
+                TRACE(is_a ? 11 : 3, it, ut == 0);
                 if (lane == 0) {
                     if (CG == 1) mbar_arrive(&bready[stage]);
                     else mbar_arrive_cluster(bready_addr0 + stage * 8);
@@ -427,64 +633,24 @@ __global__ void __launch_bounds__(NT, 1)
             }
         }
     } else if (warp >= 4) {
-        // ------------------------------ epilogue ------------------------------
+        // ------------------------------ epilogue (warps 4-7 and 12-15) ------------------------------
+        const int q = warp & 3, h = warp >= 12 ? 1 : 0;
         if (p.y_dt == DT_F16 || p.y_dt == DT_BF16)
-            epilogue<BN, 2, CG>(p, tmY, tmem_base, sOut, tfull, tempty, warp - 4, lane, tiles_per_entry, total, rank,
-                                t0, tstep);
+            epilogue<BN, 2, CG>(p, tmY, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
+                                rank, t0, tstep);
         else
-            epilogue<BN, 4, CG>(p, tmY, tmem_base, sOut, tfull, tempty, warp - 4, lane, tiles_per_entry, total, rank,
-                                t0, tstep);
+            epilogue<BN, 4, CG>(p, tmY, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
+                                rank, t0, tstep);
     }
+    TRACE(7, 0, warp == 4 && lane == 0);
     tc_fence_before();
     if (CG == 2) cluster_sync();
     else __syncthreads();
+    TRACE(8, 0, threadIdx.x == 0);
     if (warp == 2) {
         tc_fence_after();
         if (CG == 1) tmem_dealloc(tmem_base, C::TMEM_COLS);
         else tmem_dealloc2(tmem_base, C::TMEM_COLS);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Expand packed planes to an int8 image out[e][r][k'] of x64 codes in the
-// unpack_word K order.  Kind from plane presence: sgn+nz ternary, nz only bool,
-// sgn only binary (nz = the valid elements of the row).
-// ---------------------------------------------------------------------------
-struct ExpandArgs {
-    const uint32_t* sgn;
-    const uint32_t* nz;
-    int64_t rows, K, ld, bs, hs, nh, entries;
-    int64_t kw4;  // words per output row (Kp = 32 * kw4)
-    int8_t* out;
-    FastDiv div_kw4, div_rows, div_nh;
-};
-
-__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
-__device__ __forceinline__ uint64_t fdiv(uint64_t n, const FastDiv& f) { return n / f.d; }
-
-template <typename IDX>
-__global__ void __launch_bounds__(256) expand_kernel(ExpandArgs a) {
-    const IDX total = IDX(a.entries * a.rows * a.kw4);
-    const IDX kw4 = IDX(a.kw4), rows = IDX(a.rows), nh = IDX(a.nh);
-    pdl_launch_dependents();
-    pdl_wait();  // no global memory access before the predecessor grid completed
-    for (IDX i = IDX(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += IDX(gridDim.x) * blockDim.x) {
-        const IDX rr = fdiv(i, a.div_kw4), w = i - rr * kw4;
-        const IDX e = fdiv(rr, a.div_rows), r = rr - e * rows;
-        const IDX eb = fdiv(e, a.div_nh), eh = e - eb * nh;
-        const int64_t off = int64_t(eb) * a.bs + int64_t(eh) * a.hs + int64_t(r) * a.ld + int64_t(w);
-        uint32_t nz = a.nz ? __ldg(a.nz + off) : 0xffffffffu;
-        const uint32_t sg = a.sgn ? __ldg(a.sgn + off) & nz : 0u;
-        if (!a.nz) {  // binary: element validity comes from K (no nz plane)
-            const int64_t valid = a.K - int64_t(w) * 32;
-            nz = valid >= 32 ? 0xffffffffu : (valid <= 0 ? 0u : ((1u << valid) - 1u));
-        }
-        uint32_t o[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = unpack_word<B_TERNARY>(sg & nz, nz, j);
-        uint4* dst = reinterpret_cast<uint4*>(a.out + int64_t(i) * 32);
-        dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-        dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
     }
 }
 
@@ -536,7 +702,6 @@ int num_sms() {
 }
 
 int64_t kw4_of(int64_t K) { return ((K + 31) / 32 + 3) / 4 * 4; }
-size_t round1k(size_t x) { return (x + 1023) & ~size_t(1023); }
 
 // A stride for a batch dimension of extent `count`: TMA needs a multiple of 16
 // bytes even when the dimension is degenerate.
@@ -567,13 +732,39 @@ Plan make_plan(const MatmulArgs& a) {
     return p;
 }
 
-int pick_bn(int64_t N) { return N > 128 ? 256 : (N > 64 ? 128 : 64); }
+// Tile shape: minimise (rounds of the persistent grid) x (per-tile cost).
+// The per-CTA MMA time of a tile is proportional to BN, plus a fixed
+// per-tile overhead (~48 columns' worth); CTA pairs halve the B-side unpack
+// and shared-memory operand traffic per MAC, so single CTAs pay 25 % more.
+struct TileChoice {
+    int bn, cg;
+};
+TileChoice choose_tile(int64_t Mk, int64_t Nk, int64_t entries) {
+    TileChoice best{64, 1};
+    double best_cost = 1e300;
+    const int bns[4] = {256, 192, 128, 64};
+    for (int cg = 2; cg >= 1; --cg) {
+        if (cg == 2 && Mk <= BM) continue;
+        for (int bn : bns) {
+            if (bn > 64 && Nk <= bn - 64) continue;  // a narrower tile covers N just as well
+            const int64_t tiles = entries * ((Mk + BM * cg - 1) / (BM * cg)) * ((Nk + bn - 1) / bn);
+            const int64_t slots = num_sms() / cg;
+            const int64_t rounds = (tiles + slots - 1) / slots;
+            const double cost = double(rounds) * (bn + 48) * (cg == 2 ? 1.0 : 1.25);
+            if (cost < best_cost - 1e-9) {
+                best_cost = cost;
+                best = TileChoice{bn, cg};
+            }
+        }
+    }
+    return best;
+}
 
-template <int BN, int BKIND, int CG>
-cudaError_t launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb0, const CUtensorMap& mb1, const CUtensorMap& my,
-                       const TcParams& p, cudaStream_t s) {
-    using C = Cfg<BN, BKIND, CG>;
-    auto kern = tc_gemm_kernel<BN, BKIND, CG>;
+template <int BN, int CG>
+cudaError_t launch_cfg(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUtensorMap& mb0, const CUtensorMap& mb1,
+                       const CUtensorMap& my, const TcParams& p, cudaStream_t s) {
+    using C = Cfg<BN, CG>;
+    auto kern = tc_gemm_kernel<BN, CG>;
     static bool attr_set = false;  // benign race: the same value may be set twice
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -583,93 +774,84 @@ cudaError_t launch_cfg(const CUtensorMap& ma, const CUtensorMap& mb0, const CUte
     const int64_t tiles = p.entries * int64_t(p.m_tiles) * p.n_tiles;
     const int64_t slots = num_sms() / CG;
     const int grid = int((tiles < slots ? tiles : slots) * CG);
-    return launch_pdl(kern, dim3(grid), dim3(NT), size_t(C::SMEM), s, CG, ma, mb0, mb1, my, p);
-}
-
-template <int BN, int CG>
-cudaError_t launch_bn(int bkind, const CUtensorMap& ma, const CUtensorMap& mb0, const CUtensorMap& mb1,
-                      const CUtensorMap& my, const TcParams& p, cudaStream_t s) {
-    if (bkind == B_BINARY) return launch_cfg<BN, B_BINARY, CG>(ma, mb0, mb1, my, p, s);
-    if (bkind == B_BOOL) return launch_cfg<BN, B_BOOL, CG>(ma, mb0, mb1, my, p, s);
-    return launch_cfg<BN, B_TERNARY, CG>(ma, mb0, mb1, my, p, s);
+    return launch_pdl(kern, dim3(grid), dim3(NT), size_t(C::SMEM), s, CG, ma0, ma1, mb0, mb1, my, p);
 }
 
 }  // namespace
 
-size_t matmul_tc_workspace(const MatmulArgs& a) {
-    const Plan pl = make_plan(a);
-    const size_t kp = size_t(kw4_of(a.K)) * 32;
-    return round1k(size_t(a.nb * a.nh) * pl.Mk * kp);
+#ifdef BWTA_TRACE
+// copy the timeline to the host and reset it (tools/trace_gemm.py)
+extern "C" __attribute__((visibility("default"))) int bwta_trace_fetch(unsigned long long* buf) {
+    if (cudaMemcpyFromSymbol(buf, g_trace, sizeof(g_trace)) != cudaSuccess) return 1;
+    static unsigned long long zero[2][16][1024] = {};
+    return cudaMemcpyToSymbol(g_trace, zero, sizeof(zero)) != cudaSuccess;
 }
+#endif
+
+size_t matmul_tc_workspace(const MatmulArgs&) { return 0; }  // both operands are unpacked in-kernel
 
 bool matmul_tc_supported(const MatmulArgs& a) {
     if (a.K < 1 || a.M < 1 || a.N < 1) return false;
-    if (a.nb * a.nh > 65535 || a.nb > (int64_t(1) << 31) || a.nh > (int64_t(1) << 31)) return false;
+    if (a.nb > (int64_t(1) << 31) || a.nh > (int64_t(1) << 31)) return false;
     if (a.M > (int64_t(1) << 31) || a.N > (int64_t(1) << 31)) return false;
     if (a.K > (int64_t(1) << 18)) return false;  // 4096 * |dot| must fit the s32 accumulator
-    // the bit planes of kernel-B are read by TMA: batch strides must be real strides
-    const Plan pl = make_plan(a);
-    if ((a.nb > 1 && pl.b_bs <= 0) || (a.nh > 1 && pl.b_hs <= 0)) return false;
+    // both operands' bit planes are read by TMA: batch strides must be real strides
+    if ((a.nb > 1 && (a.a_bs <= 0 || a.b_bs <= 0)) || (a.nh > 1 && (a.a_hs <= 0 || a.b_hs <= 0))) return false;
     return encode_fn() != nullptr;
 }
 
-cudaError_t launch_matmul_tc(const MatmulArgs& a, void* ws, size_t ws_bytes, cudaStream_t s) {
+namespace {
+// 4-D tensor map over a packed operand: dims {ld words, rows, heads, batch},
+// box {4 words, box_rows, 1, 1} (one 128-element K slice of box_rows rows)
+bool encode_planes(CUtensorMap* m, const uint32_t* base, int64_t ld, int64_t rows, int64_t hs, int64_t bs,
+                   int64_t nh, int64_t nb, int box_rows) {
+    const uint64_t row_b = uint64_t(ld) * 4;
+    const uint64_t dims[4] = {uint64_t(ld), uint64_t(rows), uint64_t(nh), uint64_t(nb)};
+    const uint64_t hsb = bstride(nh, hs * 4, row_b * rows);
+    const uint64_t str[3] = {row_b, hsb, bstride(nb, bs * 4, hsb * nh)};
+    const uint32_t box[4] = {4, uint32_t(box_rows), 1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint32_t*>(base), dims, str, box,
+                  CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+int kind_of(const uint32_t* sgn, const uint32_t* nz) { return (sgn && nz) ? B_TERNARY : (nz ? B_BOOL : B_BINARY); }
+}  // namespace
+
+cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s) {
     const int64_t entries = a.nb * a.nh;
     const int64_t kw4 = kw4_of(a.K);
-    const int64_t kp = kw4 * 32;
     const Plan pl = make_plan(a);
-    if (ws_bytes < matmul_tc_workspace(a)) return cudaErrorInvalidValue;
-    int8_t* wa = reinterpret_cast<int8_t*>(ws);
 
-    // 1) expand kernel-A planes to an int8 image [entries][Mk][Kp]
-    ExpandArgs ea{pl.a_sgn, pl.a_nz, pl.Mk, a.K, pl.lda, pl.a_bs, pl.a_hs, a.nh, entries, kw4, wa, {}, {}, {}};
-    {
-        const int64_t work = entries * pl.Mk * kw4;
-        const int64_t blocks = (work + 255) / 256;
-        const int grid = int(blocks > num_sms() * 8 ? num_sms() * 8 : blocks);
-        const bool small = work + int64_t(grid) * 256 < (int64_t(1) << 31);
-        ea.div_kw4 = make_fastdiv(uint32_t(small ? kw4 : 1));
-        ea.div_rows = make_fastdiv(uint32_t(small ? pl.Mk : 1));
-        ea.div_nh = make_fastdiv(uint32_t(small ? a.nh : 1));
-        cudaError_t err = small ? launch_pdl(expand_kernel<uint32_t>, grid, 256, 0, s, 1, ea)
-                                : launch_pdl(expand_kernel<uint64_t>, grid, 256, 0, s, 1, ea);
-        if (err != cudaSuccess) return err;
-    }
+    // tile shape and CTA pairing (cta_group::2, M = 256 per pair)
+    TileChoice tc = choose_tile(pl.Mk, pl.Nk, entries);
+    if (a.tile_n) tc.bn = a.tile_n;
+    if (a.cta_group) tc.cg = a.cta_group;
+    if (tc.cg == 2 && pl.Mk <= BM) tc.cg = 1;  // a pair needs two 128-row halves of kernel-A
+    const int bn = tc.bn, cg = tc.cg;
 
-    // 2) tensor maps.  CTA pairs (cta_group::2, M = 256) whenever kernel-A has
-    //    more than one 128-row block and kernel-B fills a 256-wide tile.
-    const int bn = pick_bn(pl.Nk);
-    const int cg = (pl.Mk > BM && bn == 256) ? 2 : 1;
-    CUtensorMap ma, mb0, mb1, my;
+    // bit-plane tensor maps: plane 0 = sgn (binary/ternary) or nz (bool), plane 1 = nz (ternary)
+    const int akind = kind_of(pl.a_sgn, pl.a_nz), bkind = kind_of(pl.b_sgn, pl.b_nz);
+    CUtensorMap ma0, ma1, mb0, mb1, my;
     {
-        const uint64_t dims[3] = {uint64_t(kp), uint64_t(pl.Mk), uint64_t(entries)};
-        const uint64_t str[2] = {uint64_t(kp), uint64_t(kp) * pl.Mk};
-        const uint32_t box[3] = {uint32_t(BK), uint32_t(BM), 1};
-        if (!encode(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, wa, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B))
-            return cudaErrorInvalidValue;
-    }
-    {
-        const uint64_t row_b = uint64_t(pl.ldb) * 4;
-        const uint64_t dims[4] = {uint64_t(pl.ldb), uint64_t(pl.Nk), uint64_t(a.nh), uint64_t(a.nb)};
-        const uint64_t hsb = bstride(a.nh, pl.b_hs * 4, row_b * pl.Nk);
-        const uint64_t str[3] = {row_b, hsb, bstride(a.nb, pl.b_bs * 4, hsb * a.nh)};
-        const uint32_t box[4] = {4, uint32_t(bn / cg), 1, 1};
-        const uint32_t* p0 = pl.bkind == B_BOOL ? pl.b_nz : pl.b_sgn;
-        const uint32_t* p1 = pl.bkind == B_TERNARY ? pl.b_nz : p0;
-        if (!encode(&mb0, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint32_t*>(p0), dims, str, box,
-                    CU_TENSOR_MAP_SWIZZLE_NONE) ||
-            !encode(&mb1, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint32_t*>(p1), dims, str, box,
-                    CU_TENSOR_MAP_SWIZZLE_NONE))
+        const uint32_t* a0 = akind == B_BOOL ? pl.a_nz : pl.a_sgn;
+        const uint32_t* a1 = akind == B_TERNARY ? pl.a_nz : a0;
+        const uint32_t* b0 = bkind == B_BOOL ? pl.b_nz : pl.b_sgn;
+        const uint32_t* b1 = bkind == B_TERNARY ? pl.b_nz : b0;
+        if (!encode_planes(&ma0, a0, pl.lda, pl.Mk, pl.a_hs, pl.a_bs, a.nh, a.nb, BM) ||
+            !encode_planes(&ma1, a1, pl.lda, pl.Mk, pl.a_hs, pl.a_bs, a.nh, a.nb, BM) ||
+            !encode_planes(&mb0, b0, pl.ldb, pl.Nk, pl.b_hs, pl.b_bs, a.nh, a.nb, bn / cg) ||
+            !encode_planes(&mb1, b1, pl.ldb, pl.Nk, pl.b_hs, pl.b_bs, a.nh, a.nb, bn / cg))
             return cudaErrorInvalidValue;
     }
     TcParams p{};
     p.M = pl.Mk;
     p.N = pl.Nk;
-    p.num_kb = int(kp / BK);
+    p.num_kb = int(kw4 / 4);
     p.entries = entries;
     p.nh = a.nh;
     p.m_tiles = int((pl.Mk + BM * cg - 1) / (BM * cg));
     p.n_tiles = int((pl.Nk + bn - 1) / bn);
+    p.a_kind = akind;
+    p.b_kind = bkind;
     p.y = a.y;
     p.y_dt = a.y_dt;
     p.ldy = a.ldy;
@@ -699,12 +881,18 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void* ws, size_t ws_bytes, cud
                              : encode(&my, dt, 4, a.y, dims, str, box_nt, CU_TENSOR_MAP_SWIZZLE_128B);
         }
         p.use_tma_store = ok ? 1 : 0;
-        if (!ok) my = ma;  // unused
+        if (!ok) my = ma0;  // unused
     }
-    if (bn == 256 && cg == 2) return launch_bn<256, 2>(pl.bkind, ma, mb0, mb1, my, p, s);
-    if (bn == 256) return launch_bn<256, 1>(pl.bkind, ma, mb0, mb1, my, p, s);
-    if (bn == 128) return launch_bn<128, 1>(pl.bkind, ma, mb0, mb1, my, p, s);
-    return launch_bn<64, 1>(pl.bkind, ma, mb0, mb1, my, p, s);
+    if (cg == 2) {
+        if (bn == 256) return launch_cfg<256, 2>(ma0, ma1, mb0, mb1, my, p, s);
+        if (bn == 192) return launch_cfg<192, 2>(ma0, ma1, mb0, mb1, my, p, s);
+        if (bn == 128) return launch_cfg<128, 2>(ma0, ma1, mb0, mb1, my, p, s);
+        return launch_cfg<64, 2>(ma0, ma1, mb0, mb1, my, p, s);
+    }
+    if (bn == 256) return launch_cfg<256, 1>(ma0, ma1, mb0, mb1, my, p, s);
+    if (bn == 192) return launch_cfg<192, 1>(ma0, ma1, mb0, mb1, my, p, s);
+    if (bn == 128) return launch_cfg<128, 1>(ma0, ma1, mb0, mb1, my, p, s);
+    return launch_cfg<64, 1>(ma0, ma1, mb0, mb1, my, p, s);
 }
 
 }  // namespace bwta

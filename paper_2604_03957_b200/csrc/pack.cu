@@ -6,13 +6,13 @@
 //
 // B200 design (not the paper's in-register IPB, which fuses the
 // pack into its MMA kernel): packing is a standalone HBM-streaming pass.
-//   * Row mode: the output words are walked as one flat list; 4 lanes (8 for
-//     f32) read the 32 elements of one word as 16-byte vectors, so a warp
-//     instruction moves 512 contiguous bytes per 8 words and every warp keeps
-//     U = 4 such vectors per lane in flight.  Each lane turns its 16 B into an
-//     E-bit chunk with packed-half compares (HSET2 via __hge2_mask: 2 elements
-//     per instruction, exact, no division) and the lanes of a word OR their
-//     chunks together with warp shuffles.
+//   * Row mode: the output words are walked as one flat list; one lane owns
+//     one output word and reads its 32 elements as 16-byte vectors (64 B for
+//     2-byte inputs), 2 words per lane in flight plus a prefetch of the next
+//     pair.  Each 16 B vector becomes 8 compare bits through packed-half
+//     compares (HSET2 via __hge2_mask: 2 elements per instruction, exact, no
+//     division); no cross-lane traffic, and 32 lanes store 128 contiguous
+//     bytes of plane.
 //   * Transposed mode (V^T for PV): a warp owns a 32-row x 32-col tile; lane
 //     l packs row l into a 32-bit word, a 5-stage shuffle butterfly transposes
 //     the 32x32 bit block so lane j ends up with column j's word.

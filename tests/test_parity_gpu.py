@@ -190,6 +190,40 @@ def test_gemm_parity(B, design):
             assert_out_equal(y1, oracle.epilogue_linear(d, None, s_a, "f32"), "no w_scale")
 
 
+@pytest.mark.parametrize("tile", [(64, 1), (128, 1), (192, 1), (256, 1), (64, 2), (128, 2), (192, 2), (256, 2)])
+def test_gemm_parity_every_tile(B, tile):
+    """Every design-(b) tile shape (tile_n x CTA group), both operand roles
+    (M < N: activations expanded; M > N: roles swapped, D^T epilogue), ragged
+    M/N/K tails, per-column / per-row scales, both output orientations."""
+    for i, (m, n, k, a_kind) in enumerate([(300, 517, 421, "ternary"), (517, 300, 421, "bool"),
+                                           (130, 1000, 2000, "bool"), (1000, 130, 300, "ternary")]):
+        a, wp, s_a, s_w, qa, qw = _gemm_case(B, m, n, k, 2500 + i, a_kind)
+        d = oracle.dot(qa, qw, threads=oracle.default_threads())
+        yi = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.int32, design="tcgen05", tile=tile)
+        assert np.array_equal(yi.cpu().numpy(), d), (m, n, k, a_kind, tile)
+        ref = oracle.epilogue_linear(d, s_w.numpy(), s_a, "f16")
+        y = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.float16, design="tcgen05", tile=tile)
+        assert_out_equal(y, ref, f"{m}x{n}x{k} {tile}")
+        yt = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.float16, y_transposed=True, design="tcgen05",
+                         tile=tile)
+        assert_out_equal(yt, ref.T.copy(), f"{m}x{n}x{k} {tile} transposed")
+        yb = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.bfloat16, design="tcgen05", tile=tile)
+        assert_out_equal(yb, oracle.epilogue_linear(d, s_w.numpy(), s_a, "bf16"), f"{m}x{n}x{k} {tile} bf16")
+
+
+def test_gemm_tiny_scales_take_exact_path(B):
+    """Per-channel scales below 2^-114 make c * 2^-12 inexact; those tiles must
+    fall back to the generic epilogue and still match R5 exactly."""
+    m, n, k = 200, 300, 256
+    a, wp, s_a, s_w, qa, qw = _gemm_case(B, m, n, k, 2600)
+    d = oracle.dot(qa, qw)
+    s_w = s_w.clone()
+    s_w[::7] = torch.tensor(3e-36)  # subnormal-range products
+    for dt, name in ((torch.float16, "f16"), (torch.float32, "f32")):
+        y = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=dt, design="tcgen05")
+        assert_out_equal(y, oracle.epilogue_linear(d, s_w.numpy(), s_a, name), name)
+
+
 def test_gemm_exhaustive_k6(B):
     """All 3^6 ternary x 2^6 binary (and bool) vectors at K=6, also shifted to
     straddle a word boundary (offset 29): dot equals the oracle's triple loop."""

@@ -1,22 +1,53 @@
-"""Timeline of one tcgen05 GEMM launch (CTAs 0/1) from the BWTA_TRACE build.
-    BWTA_LIB=libbwta_trace.so python tools/trace_gemm.py M K N"""
-import sys, os, ctypes
+"""Timeline of one tcgen05 GEMM launch (CTAs 0 and 1) from the -DBWTA_TRACE build.
+
+    python paper_2604_03957_b200/build.py --trace
+    BWTA_LIB=libbwta_trace.so python tools/trace_gemm.py M K N [ternary|bool]
+
+Prints, per CTA, the clock64 (SM cycles, relative to the CTA's first event)
+of every hook in gemm_tc.cu, and per-k-block intervals for the first tile."""
+import os
+import sys
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch, bwta_inputs as gen, paper_2604_03957_b200 as B
+import numpy as np
+import torch
+
+import bwta_inputs as gen
+import paper_2604_03957_b200 as B
+
 m, k, n = (int(v) for v in sys.argv[1:4])
-x = gen.activations((m, k), 1).cuda(); w = gen.weights(n, k, 2).cuda()
-a = B.bwta_pack_act(x, 1.6); wp = B.bwta_pack_weight(w)
+kind = sys.argv[4] if len(sys.argv) > 4 else "ternary"
+x = gen.activations((m, k), 1).cuda()
+if kind == "bool":
+    x = torch.relu(x)
+w = gen.weights(n, k, 2).cuda()
+a = B.bwta_pack_act(x, 1.6, kind=kind)
+wp = B.bwta_pack_weight(w)
 y = torch.empty((m, n), dtype=torch.float16, device="cuda")
-buf = np.zeros((2, 14, 1024), np.uint64); cnt = np.zeros((2, 14), np.int32)
+buf = np.zeros((2, 16, 1024), np.uint64)
 f = B.lib.bwta_trace_fetch
 for it in range(3):
-    torch.cuda.synchronize(); f(buf.ctypes.data, cnt.ctypes.data)
-    B.bwta_gemm(a, wp, None, 1.0, out=y, design="tcgen05"); torch.cuda.synchronize()
-    f(buf.ctypes.data, cnt.ctypes.data)
-names = ["start", "tma", "unpackB_in", "unpackB_out", "mma", "epi_in", "epi_out", "end", "unpackA_in", "unpackA_out", "a_lds", "a_wait_st_done", "a_st_issued", "b_math_done"]
+    torch.cuda.synchronize()
+    f(buf.ctypes.data)
+    B.bwta_gemm(a, wp, None, 1.0, out=y, design="tcgen05")
+    torch.cuda.synchronize()
+    f(buf.ctypes.data)
+cnt = (buf != 0).sum(-1)
+names = ["start", "tma_issue", "unp_full", "unp_done", "mma_bready", "epi_tfull", "epi_done", "end_work", "exit",
+         "e_ld", "unpA_full", "unpA_done", "e_st"]
 for c in range(2):
-    t0 = buf[c][0][0]   # per-CTA clock64 origin (SM-local counters)
-    print(f"CTA {c}: counts", dict(zip(names, cnt[c].tolist())))
+    t0 = int(buf[c][0][0])
+    print(f"CTA {c}: counts", dict(zip(names, cnt[c][:len(names)].tolist())))
+    ev = {}
     for r, nm in enumerate(names):
-        v = (buf[c][r][:min(cnt[c][r], 1024)].astype(np.int64) - int(t0)) / 1965.0  # cycles -> us at 1965 MHz
-        if len(v): print(f"  {nm:10s}", " ".join(f"{x:7.2f}" for x in np.sort(v)[:40]))
+        v = buf[c][r][: cnt[c][r]].astype(np.int64) - t0
+        ev[nm] = v
+        if len(v):
+            print(f"  {nm:11s}", " ".join(f"{x:6d}" for x in v[:48]))
+    for a_, b_ in (("tma_issue", "unp_full"), ("unp_full", "unp_done"), ("unp_done", "mma_bready")):
+        if len(ev[a_]) and len(ev[b_]):
+            n_ = min(len(ev[a_]), len(ev[b_]))
+            print(f"  {a_}->{b_}: median {np.median(ev[b_][:n_] - ev[a_][:n_]):.0f} cycles")
+    for nm in ("tma_issue", "unp_done", "mma_bready"):
+        if len(ev[nm]) > 2:
+            print(f"  {nm} period: median {np.median(np.diff(ev[nm])):.0f} cycles")
