@@ -103,7 +103,7 @@ typedef enum {
 /* Options for the matmul entry points; NULL = all defaults (zero-initialised). */
 typedef struct {
     int32_t design;      /* bwta_design_t */
-    int32_t tile_n;      /* design (b) only: 0 = auto, else the tile width 64 | 128 | 192 | 256 */
+    int32_t tile_n;      /* design (b) only: 0 = auto, else the tile width 64 | 128 | 192 */
     int32_t cta_group;   /* design (b) only: 0 = auto, 1 = single CTA, 2 = CTA pair (cta_group::2) */
     int32_t reserved[5]; /* must be 0 */
 } bwta_opts_t;

@@ -122,8 +122,7 @@ bwta_status_t run_matmul(const MatmulArgs& a0, void* ws, size_t ws_bytes, const 
     if (opts->design < 0 || opts->design > 2) return BWTA_ERR_INVALID_VALUE;
     for (int r : opts->reserved)
         if (r != 0) return BWTA_ERR_INVALID_VALUE;
-    if (!(opts->tile_n == 0 || opts->tile_n == 64 || opts->tile_n == 128 || opts->tile_n == 192 ||
-          opts->tile_n == 256) ||
+    if (!(opts->tile_n == 0 || opts->tile_n == 64 || opts->tile_n == 128 || opts->tile_n == 192) ||
         opts->cta_group < 0 || opts->cta_group > 2)
         return BWTA_ERR_INVALID_VALUE;
     MatmulArgs a = a0;

@@ -47,8 +47,10 @@ namespace {
 using namespace sm100;
 
 constexpr int BM = 128;     // MMA M (kernel-A rows per tile), cta_group::1
-constexpr int BK = 128;     // K elements (= int8 bytes) per stage: one 128B swizzle row
-constexpr int UMMA_K = 32;  // K per tcgen05.mma for 8-bit inputs
+constexpr int BK = 256;     // K elements per stage: one 128-byte swizzle row of packed E2M1 codes
+constexpr int ROWB = 128;   // bytes per operand row per stage
+constexpr int UMMA_KB = 32; // bytes of K per tcgen05.mma (K = 64 four-bit elements)
+constexpr int WPS = BK / 32;  // packed words per row per plane per stage (8)
 constexpr int NT = 640;     // 20 warps
 constexpr int OUT_BUF = 4096;
 
@@ -76,10 +78,10 @@ __host__ __device__ constexpr int nplanes_of(int kind) { return kind == B_TERNAR
 template <int BN, int CG>
 struct Cfg {
     static constexpr int BNC = BN / CG;          // kernel-B rows held (and unpacked) per CTA
-    static constexpr int A_BYTES = BM * BK;      // int8 codes
-    static constexpr int B_BYTES = BNC * BK;
-    static constexpr int ABITS = 2 * BM * 16;    // up to 2 planes x 4 words per row
-    static constexpr int BBITS = 2 * BNC * 16;
+    static constexpr int A_BYTES = BM * ROWB;     // E2M1 codes, 2 per byte
+    static constexpr int B_BYTES = BNC * ROWB;
+    static constexpr int ABITS = 2 * BM * WPS * 4;  // up to 2 planes x 8 words per row
+    static constexpr int BBITS = 2 * BNC * WPS * 4;
     static constexpr int STAGE = A_BYTES + B_BYTES + ABITS + BBITS;
     static constexpr int OUT_BYTES = 8 * OUT_BUF;                           // one staging buffer per epilogue warp
     static constexpr int SCALE_COLS = (BN + 127) / 128 * 64;                 // columns per epilogue warp
@@ -88,7 +90,12 @@ struct Cfg {
     static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
     static constexpr int BAR_BYTES = 256;
     static constexpr int SMEM = 1024 + STAGES * STAGE + OUT_BYTES + SCALE_BYTES + BAR_BYTES;
-    static constexpr int TMEM_COLS = 2 * BN <= 128 ? 2 * BN : (2 * BN <= 256 ? 256 : 512);  // power of 2
+    // TMEM: two f32 accumulators of BN columns, then the UE8M0 scale factors
+    // (all 1.0): SFA at SF_COL (4 columns used for M = 128), SFB at SF_COL + 8
+    // (up to 8 columns).
+    static constexpr int SF_COL = 2 * BN;
+    static constexpr int TMEM_COLS = 512;
+    static_assert(SF_COL + 16 <= TMEM_COLS, "accumulators + scale factors exceed TMEM");
     static_assert(STAGES >= 2, "pipeline too shallow");
     static_assert(BNC % 8 == 0, "swizzle atoms are 8 rows");
     static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0 && OUT_BYTES % 1024 == 0 && SCALE_BYTES % 128 == 0 &&
@@ -96,25 +103,18 @@ struct Cfg {
                   "smem region alignment");
 };
 
-// K order inside the int8 operand tiles.  Element k (0..31) of a packed word
-// lands at byte 4*(k%8) + k/8 of its 32-byte group, i.e. code word j
-// (j = 0..7) holds elements {j, 8+j, 16+j, 24+j}.  Both MMA operands use the
-// same permutation (expand_kernel for A, the unpack warps for B), so every
-// dot product is unchanged.
-//
-// Codes are scaled by 64 (int8 0x40 = +64, 0xC0 = -64, 0x00): the nz bit of
-// element 8i+j moves to bit 6 of byte i and the sgn bit to bit 7 by LEFT
-// shifts, which run as IMAD.SHL on the FMA pipe, so a code word costs ~2 FMA
-// + 2 logic instructions instead of a nibble spread (measured in
-// tools/ubench: 230 vs 313 cycles per 128-element ternary row per warp).  The
-// s32 accumulator holds 4096 * dot exactly (|dot| <= K <= 2^18) and the
-// epilogue recovers dot with an arithmetic shift by 12.
-//   binary  (x0 = sgn):           0x40 | sgn << 7          -> +64 / -64
-//   bool    (x0 = nz):            nz << 6                  -> 0 / +64
-//   ternary (x0 = sgn, x1 = nz):  nz << 6 | sgn << 7       -> 0 / +64 / -64
-// (ternary planes are canonical: sgn is a subset of nz, include/bwta.h)
-constexpr int CODE_SHIFT = 12;  // log2(64 * 64)
-
+// Operand codes: E2M1 nibbles, +1.0 = 0x2, -1.0 = 0xA, 0 = 0x0, fed to
+// tcgen05.mma.kind::mxf4 with every UE8M0 block scale = 1.0 (0x7F), so each
+// product is exactly q_a * q_w and the f32 accumulator holds the integer dot
+// exactly (|dot| <= K <= 2^24).  K order inside a 32-element group: code word
+// j (j = 0..3, 8 nibbles) holds elements {j, 4+j, ..., 28+j}, nibble i =
+// element 4i + j, so the nz bit of element 4i+j moves to bit 4i+1 and the sgn
+// bit to bit 4i+3 by one shift each (left shifts issued as IMAD.SHL on the FMA
+// pipe).  Both operands use the same permutation, so every dot is unchanged.
+//   binary  (x0 = sgn):           0x2 | sgn << 3            -> +1 / -1
+//   bool    (x0 = nz):            nz << 1                   -> 0 / +1
+//   ternary (x0 = sgn, x1 = nz):  nz << 1 | sgn << 3        -> 0 / +1 / -1
+// (ternary sgn is masked to the canonical subset of nz)
 // Timeline hooks (tools/trace_gemm.py; compiled only with -DBWTA_TRACE)
 #ifdef BWTA_TRACE
 // one writer per (CTA, event, index): plain stores, no atomics on the hot path
@@ -134,18 +134,20 @@ __device__ __forceinline__ uint32_t shl_fma(uint32_t x, int k) {  // x << k as I
     asm("mad.lo.u32 %0, %1, %2, 0;" : "=r"(r) : "r"(x), "r"(1u << k));
     return r;
 }
-__device__ __forceinline__ uint32_t to_bit6(uint32_t x, int j) { return j < 7 ? shl_fma(x, 6 - j) : (x >> 1); }
+// bit 4i+j -> bit 4i+1 (nz) / 4i+3 (sgn)
+__device__ __forceinline__ uint32_t nz_to_bit1(uint32_t x, int j) { return j == 0 ? shl_fma(x, 1) : (j == 1 ? x : x >> (j - 1)); }
+__device__ __forceinline__ uint32_t sg_to_bit3(uint32_t x, int j) { return j == 3 ? x : shl_fma(x, 3 - j); }
 
 template <int KIND>
 __device__ __forceinline__ uint32_t unpack_word(uint32_t x0, uint32_t x1, int j) {
-    if (KIND == B_BINARY) return (shl_fma(x0, 7 - j) & 0x80808080u) | 0x40404040u;
-    if (KIND == B_BOOL) return to_bit6(x0, j) & 0x40404040u;
-    return (to_bit6(x1, j) & 0x40404040u) | (shl_fma(x0, 7 - j) & 0x80808080u);
+    if (KIND == B_BINARY) return (sg_to_bit3(x0, j) & 0x88888888u) | 0x22222222u;
+    if (KIND == B_BOOL) return nz_to_bit1(x0, j) & 0x22222222u;
+    return (nz_to_bit1(x1, j) & 0x22222222u) | (sg_to_bit3(x0, j) & 0x88888888u);
 }
 
-// raw s32 accumulator (4096 * dot) -> dot
-__device__ __forceinline__ int32_t dot_of(uint32_t acc) { return int32_t(acc) >> CODE_SHIFT; }
-__device__ __forceinline__ float scaled(uint32_t acc, float c) { return __fmul_rn(__int2float_rn(dot_of(acc)), c); }
+// f32 accumulator (the exact integer dot) -> dot / scaled output (R5)
+__device__ __forceinline__ int32_t dot_of(uint32_t acc) { return __float2int_rn(__uint_as_float(acc)); }
+__device__ __forceinline__ float scaled(uint32_t acc, float c) { return __fmul_rn(__uint_as_float(acc), c); }
 
 __device__ __forceinline__ uint32_t pack2(int dt, float lo, float hi) {
     if (dt == DT_F16) {
@@ -171,17 +173,9 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, ui
 // accumulators in the mma.sync m16n8 fragment layout, two adjacent columns
 // per register pair, so a pair converts to one f16x2 / bf16x2 word and
 // stmatrix (.trans for D^T) writes 8x8 blocks -- 1 shared store per 8
-// outputs per thread, no shuffles.  Scaling: acc = 4096 * dot exactly and
-// float(acc) is exact (|dot| <= 2^24), so fl(float(acc) * (c * 2^-12)) ==
-// fl(float(dot) * c) (R5) whenever c * 2^-12 is exact, i.e. |c| >= 2^-114, c
-// = 0 or c non-finite.  A tile with any other scale takes the generic path.
+// outputs per thread, no shuffles.  Scaling: the f32 accumulator is the
+// exact dot, so y = fl(acc * c) is R5's fl(float(dot) * c) with one FMUL.
 // ---------------------------------------------------------------------------
-constexpr float INV4096 = 1.0f / 4096.0f;
-
-__device__ __forceinline__ bool scale_ok(float c) {
-    const float a = fabsf(c);
-    return !(a < 0x1p-114f) || a == 0.f;  // NaN compares false -> ok
-}
 
 // generic tile: 32x32b loads, any output type, TMA or direct stores.  A
 // chunk (one 128-byte output row per thread, CW columns) is processed in
@@ -317,8 +311,8 @@ __device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorM
                 for (int i2 = 0; i2 < 2; ++i2) {
                     const float c_lo = col_scaled ? ca : cr[2 * b + i2];
                     const float c_hi = col_scaled ? cb : cr[2 * b + i2];
-                    const float f0 = __fmul_rn(__int2float_rn(int32_t(v[4 * g + 2 * i2])), c_lo);
-                    const float f1 = __fmul_rn(__int2float_rn(int32_t(v[4 * g + 2 * i2 + 1])), c_hi);
+                    const float f0 = scaled(v[4 * g + 2 * i2], c_lo);
+                    const float f1 = scaled(v[4 * g + 2 * i2 + 1], c_hi);
                     pk[2 * g + i2] = pack2(BF16 ? DT_BF16 : DT_F16, f0, f1);
                 }
             }
@@ -370,7 +364,7 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
         const int eb = int(e / p.nh), eh = int(e % p.nh);
         const int64_t mrow0 = int64_t(mt) * BM * CG + rank * BM;  // first kernel row of this CTA
         // scales of this tile (loaded before the accumulator is ready)
-        bool ok = fast_ok;
+        const bool ok = fast_ok;
         float cr[4] = {0.f, 0.f, 0.f, 0.f};
         if (fast_ok) {
             if (col_scaled) {
@@ -379,8 +373,7 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
                     const int64_t n = int64_t(nt) * BN + c0 + 2 * lane;
                     const float a = __fmul_rn(__ldg(p.scale + (n < p.N ? n : 0)), p.scalar);
                     const float b = __fmul_rn(__ldg(p.scale + (n + 1 < p.N ? n + 1 : 0)), p.scalar);
-                    ok = ok && scale_ok(a) && scale_ok(b);
-                    *reinterpret_cast<float2*>(cs + i * 64 + 2 * lane) = make_float2(a * INV4096, b * INV4096);
+                    *reinterpret_cast<float2*>(cs + i * 64 + 2 * lane) = make_float2(a, b);
                 }
             } else {
 #pragma unroll
@@ -390,11 +383,9 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
                         const int64_t row = mrow0 + q * 32 + 16 * (k >> 1) + 8 * (k & 1) + (lane >> 2);
                         c = __fmul_rn(__ldg(p.scale + (row < p.M ? row : 0)), p.scalar);
                     }
-                    ok = ok && scale_ok(c);
-                    cr[k] = c * INV4096;
+                    cr[k] = c;
                 }
             }
-            ok = __all_sync(0xffffffffu, ok);
             __syncwarp();
         }
         mbar_wait(&tfull[acc], acc_phase);
@@ -422,39 +413,43 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
     if (lane == 0) bulk_wait_all();
 }
 
-// One operand row (128 K-elements = 4 words per plane) -> 128 int8 codes at
-// rowaddr in the UMMA 128B-swizzled K-major layout (row r of its 8-row atom).
+// One operand row (256 K-elements = 8 words per plane) -> 128 bytes of E2M1
+// codes at rowaddr in the UMMA 128B-swizzled K-major layout (row r of its
+// 8-row atom): packed word g becomes the 16-byte chunk g.
 // p0: sgn (binary, ternary) or nz (bool); p1: nz (ternary).
 template <int KIND>
 __device__ __forceinline__ void unpack_row(uint32_t p0addr, uint32_t p1addr, uint32_t rowaddr, int r) {
-    const uint4 w0 = lds128(p0addr);
-    uint4 w1 = make_uint4(0, 0, 0, 0);
-    if (KIND == B_TERNARY) w1 = lds128(p1addr);
-    uint32_t x0[4] = {w0.x, w0.y, w0.z, w0.w};
-    const uint32_t x1[4] = {w1.x, w1.y, w1.z, w1.w};
-    if (KIND == B_TERNARY) {
 #pragma unroll
-        for (int g = 0; g < 4; ++g) x0[g] &= x1[g];  // canonical sgn (subset of nz)
-    }
+    for (int h = 0; h < 2; ++h) {  // words 4h .. 4h+3
+        const uint4 w0 = lds128(p0addr + 16 * h);
+        uint4 w1 = make_uint4(0, 0, 0, 0);
+        if (KIND == B_TERNARY) w1 = lds128(p1addr + 16 * h);
+        uint32_t x0[4] = {w0.x, w0.y, w0.z, w0.w};
+        const uint32_t x1[4] = {w1.x, w1.y, w1.z, w1.w};
+        if (KIND == B_TERNARY) {
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {  // 32-element group = one packed word
-        uint32_t o[8];
+            for (int g = 0; g < 4; ++g) x0[g] &= x1[g];  // canonical sgn (subset of nz)
+        }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = unpack_word<KIND>(x0[g], x1[g], j);
-        sts128(rowaddr + (((2 * g) ^ (r & 7)) << 4), o[0], o[1], o[2], o[3]);
-        sts128(rowaddr + (((2 * g + 1) ^ (r & 7)) << 4), o[4], o[5], o[6], o[7]);
+        for (int g = 0; g < 4; ++g) {
+            uint32_t o[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = unpack_word<KIND>(x0[g], x1[g], j);
+            sts128(rowaddr + (((4 * h + g) ^ (r & 7)) << 4), o[0], o[1], o[2], o[3]);
+        }
     }
 }
 
 // rows [r0, rows) step `step` of one operand slice (warp-uniform kind)
 __device__ __forceinline__ void unpack_rows(int kind, uint32_t bits, int plane_bytes, uint32_t dst, int r0, int rows,
                                             int step) {
+    constexpr int RB = WPS * 4;  // bit bytes per row per plane
     if (kind == B_TERNARY) {
-        for (int r = r0; r < rows; r += step) unpack_row<B_TERNARY>(bits + r * 16, bits + plane_bytes + r * 16, dst + r * 128, r);
+        for (int r = r0; r < rows; r += step) unpack_row<B_TERNARY>(bits + r * RB, bits + plane_bytes + r * RB, dst + r * ROWB, r);
     } else if (kind == B_BOOL) {
-        for (int r = r0; r < rows; r += step) unpack_row<B_BOOL>(bits + r * 16, 0, dst + r * 128, r);
+        for (int r = r0; r < rows; r += step) unpack_row<B_BOOL>(bits + r * RB, 0, dst + r * ROWB, r);
     } else {
-        for (int r = r0; r < rows; r += step) unpack_row<B_BINARY>(bits + r * 16, 0, dst + r * 128, r);
+        for (int r = r0; r < rows; r += step) unpack_row<B_BINARY>(bits + r * RB, 0, dst + r * ROWB, r);
     }
 }
 
@@ -513,6 +508,18 @@ __global__ void __launch_bounds__(NT, 1)
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (warp >= 4 && warp < 8) {
+        // UE8M0 scale factors = 1.0 (0x7F) in columns SF_COL .. SF_COL + 15 of every lane
+        uint32_t ones[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) ones[i] = 0x7F7F7F7Fu;
+        tmem_st_32x32b_x16(tmem_base + (uint32_t((warp & 3) * 32) << 16) + uint32_t(C::SF_COL), ones);
+        tmem_wait_st();
+    }
+    tc_fence_before();
+    if (CG == 2) cluster_sync();
+    else __syncthreads();
+    tc_fence_after();
     // prologue done (smem barriers, TMEM, descriptor prefetch): let the next
     // kernel start its own, then wait for our inputs (predecessor grid)
     pdl_launch_dependents();
@@ -525,7 +532,7 @@ __global__ void __launch_bounds__(NT, 1)
 
     if (warp == 0) {
         // ------------------------------ TMA producer ------------------------------
-        const uint32_t tx = uint32_t(a_planes * BM * 16 + b_planes * C::BNC * 16);
+        const uint32_t tx = uint32_t((a_planes * BM + b_planes * C::BNC) * WPS * 4);
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
@@ -543,11 +550,12 @@ __global__ void __launch_bounds__(NT, 1)
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&full[stage], tx);
                     uint8_t* ab = sABits + stage * C::ABITS;
-                    tma_load_4d(ab, &tmA0, &full[stage], kb * 4, arow, eh, eb);
-                    if (a_planes == 2) tma_load_4d(ab + BM * 16, &tmA1, &full[stage], kb * 4, arow, eh, eb);
+                    tma_load_4d(ab, &tmA0, &full[stage], kb * WPS, arow, eh, eb);
+                    if (a_planes == 2) tma_load_4d(ab + BM * WPS * 4, &tmA1, &full[stage], kb * WPS, arow, eh, eb);
                     uint8_t* bb = sBBits + stage * C::BBITS;
-                    tma_load_4d(bb, &tmB0, &full[stage], kb * 4, brow, eh, eb);
-                    if (b_planes == 2) tma_load_4d(bb + C::BNC * 16, &tmB1, &full[stage], kb * 4, brow, eh, eb);
+                    tma_load_4d(bb, &tmB0, &full[stage], kb * WPS, brow, eh, eb);
+                    if (b_planes == 2)
+                        tma_load_4d(bb + C::BNC * WPS * 4, &tmB1, &full[stage], kb * WPS, brow, eh, eb);
                 }
                 __syncwarp();
                 if (++stage == C::STAGES) {
@@ -559,7 +567,8 @@ __global__ void __launch_bounds__(NT, 1)
     } else if (warp == 1) {
         // ------------------------------ MMA issuer (leader CTA) ------------------------------
         if (leader) {
-            constexpr uint32_t idesc = idesc_i8(BM * CG, BN);
+            constexpr uint32_t idesc = idesc_mxf4(BM * CG, BN);
+            const uint32_t sfa = tmem_base + uint32_t(C::SF_COL), sfb = tmem_base + uint32_t(C::SF_COL + 8);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -578,10 +587,10 @@ __global__ void __launch_bounds__(NT, 1)
                         const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
                         const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
-                        for (int k = 0; k < BK / UMMA_K; ++k) {
-                            const uint64_t ad = smem_desc_sw128(a0 + k * UMMA_K), bd = smem_desc_sw128(b0 + k * UMMA_K);
-                            if (CG == 1) mma_i8(d, ad, bd, idesc, (kb | k) != 0);
-                            else mma_i8_cg2(d, ad, bd, idesc, (kb | k) != 0);
+                        for (int k = 0; k < ROWB / UMMA_KB; ++k) {
+                            const uint64_t ad = smem_desc_sw128(a0 + k * UMMA_KB), bd = smem_desc_sw128(b0 + k * UMMA_KB);
+                            if (CG == 1) mma_mxf4(d, ad, bd, idesc, sfa, sfb, (kb | k) != 0);
+                            else mma_mxf4_cg2(d, ad, bd, idesc, sfa, sfb, (kb | k) != 0);
                         }
                         if (CG == 1) tc_commit(&empty[stage]);
                         else tc_commit2_mc(&empty[stage], 0x3);
@@ -607,7 +616,7 @@ __global__ void __launch_bounds__(NT, 1)
         const int ut = threadIdx.x - (is_a ? 512 : 256);  // 0..127
         const int kind = is_a ? p.a_kind : p.b_kind;
         const int rows = is_a ? BM : C::BNC;
-        const int plane_bytes = is_a ? BM * 16 : C::BNC * 16;
+        const int plane_bytes = (is_a ? BM : C::BNC) * WPS * 4;
         const uint32_t bready_addr0 = CG == 2 ? mapa_smem(&bready[0], 0) : 0u;
         int stage = 0;
         uint32_t phase = 0;
@@ -742,7 +751,7 @@ struct TileChoice {
 TileChoice choose_tile(int64_t Mk, int64_t Nk, int64_t entries) {
     TileChoice best{64, 1};
     double best_cost = 1e300;
-    const int bns[4] = {256, 192, 128, 64};
+    const int bns[3] = {192, 128, 64};
     for (int cg = 2; cg >= 1; --cg) {
         if (cg == 2 && Mk <= BM) continue;
         for (int bn : bns) {
@@ -794,7 +803,7 @@ bool matmul_tc_supported(const MatmulArgs& a) {
     if (a.K < 1 || a.M < 1 || a.N < 1) return false;
     if (a.nb > (int64_t(1) << 31) || a.nh > (int64_t(1) << 31)) return false;
     if (a.M > (int64_t(1) << 31) || a.N > (int64_t(1) << 31)) return false;
-    if (a.K > (int64_t(1) << 18)) return false;  // 4096 * |dot| must fit the s32 accumulator
+    if (a.K > (int64_t(1) << 24)) return false;  // |dot| <= K must be exact in the f32 accumulator
     // both operands' bit planes are read by TMA: batch strides must be real strides
     if ((a.nb > 1 && (a.a_bs <= 0 || a.b_bs <= 0)) || (a.nh > 1 && (a.a_hs <= 0 || a.b_hs <= 0))) return false;
     return encode_fn() != nullptr;
@@ -802,14 +811,14 @@ bool matmul_tc_supported(const MatmulArgs& a) {
 
 namespace {
 // 4-D tensor map over a packed operand: dims {ld words, rows, heads, batch},
-// box {4 words, box_rows, 1, 1} (one 128-element K slice of box_rows rows)
+// box {8 words, box_rows, 1, 1} (one 256-element K slice of box_rows rows)
 bool encode_planes(CUtensorMap* m, const uint32_t* base, int64_t ld, int64_t rows, int64_t hs, int64_t bs,
                    int64_t nh, int64_t nb, int box_rows) {
     const uint64_t row_b = uint64_t(ld) * 4;
     const uint64_t dims[4] = {uint64_t(ld), uint64_t(rows), uint64_t(nh), uint64_t(nb)};
     const uint64_t hsb = bstride(nh, hs * 4, row_b * rows);
     const uint64_t str[3] = {row_b, hsb, bstride(nb, bs * 4, hsb * nh)};
-    const uint32_t box[4] = {4, uint32_t(box_rows), 1, 1};
+    const uint32_t box[4] = {uint32_t(WPS), uint32_t(box_rows), 1, 1};
     return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint32_t*>(base), dims, str, box,
                   CU_TENSOR_MAP_SWIZZLE_NONE);
 }
@@ -845,7 +854,7 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     TcParams p{};
     p.M = pl.Mk;
     p.N = pl.Nk;
-    p.num_kb = int(kw4 / 4);
+    p.num_kb = int((kw4 + WPS - 1) / WPS);
     p.entries = entries;
     p.nh = a.nh;
     p.m_tiles = int((pl.Mk + BM * cg - 1) / (BM * cg));
@@ -884,12 +893,10 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
         if (!ok) my = ma0;  // unused
     }
     if (cg == 2) {
-        if (bn == 256) return launch_cfg<256, 2>(ma0, ma1, mb0, mb1, my, p, s);
         if (bn == 192) return launch_cfg<192, 2>(ma0, ma1, mb0, mb1, my, p, s);
         if (bn == 128) return launch_cfg<128, 2>(ma0, ma1, mb0, mb1, my, p, s);
         return launch_cfg<64, 2>(ma0, ma1, mb0, mb1, my, p, s);
     }
-    if (bn == 256) return launch_cfg<256, 1>(ma0, ma1, mb0, mb1, my, p, s);
     if (bn == 192) return launch_cfg<192, 1>(ma0, ma1, mb0, mb1, my, p, s);
     if (bn == 128) return launch_cfg<128, 1>(ma0, ma1, mb0, mb1, my, p, s);
     return launch_cfg<64, 1>(ma0, ma1, mb0, mb1, my, p, s);

@@ -190,7 +190,7 @@ def test_gemm_parity(B, design):
             assert_out_equal(y1, oracle.epilogue_linear(d, None, s_a, "f32"), "no w_scale")
 
 
-@pytest.mark.parametrize("tile", [(64, 1), (128, 1), (192, 1), (256, 1), (64, 2), (128, 2), (192, 2), (256, 2)])
+@pytest.mark.parametrize("tile", [(64, 1), (128, 1), (192, 1), (64, 2), (128, 2), (192, 2)])
 def test_gemm_parity_every_tile(B, tile):
     """Every design-(b) tile shape (tile_n x CTA group), both operand roles
     (M < N: activations expanded; M > N: roles swapped, D^T epilogue), ragged
@@ -211,9 +211,8 @@ def test_gemm_parity_every_tile(B, tile):
         assert_out_equal(yb, oracle.epilogue_linear(d, s_w.numpy(), s_a, "bf16"), f"{m}x{n}x{k} {tile} bf16")
 
 
-def test_gemm_tiny_scales_take_exact_path(B):
-    """Per-channel scales below 2^-114 make c * 2^-12 inexact; those tiles must
-    fall back to the generic epilogue and still match R5 exactly."""
+def test_gemm_tiny_scales(B):
+    """Per-channel scales in the subnormal product range still follow R5 exactly."""
     m, n, k = 200, 300, 256
     a, wp, s_a, s_w, qa, qw = _gemm_case(B, m, n, k, 2600)
     d = oracle.dot(qa, qw)
