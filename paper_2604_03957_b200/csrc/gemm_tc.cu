@@ -56,6 +56,28 @@ constexpr int OUT_BUF = 4096;
 
 enum BKind { B_BINARY = 0, B_BOOL = 1, B_TERNARY = 2 };  // operand kinds (A or B)
 
+extern __shared__ __align__(16) uint8_t smem_raw[];  // dynamic shared memory of tc_gemm_kernel
+
+// Timeline hooks (tools/trace_gemm.py; compiled only with -DBWTA_TRACE).
+// Timestamps go to shared memory (a global store would be waited on by the
+// next fence.proxy.async, i.e. MEMBAR.ALL.CTA, and distort the timeline);
+// thread 0 copies them out at kernel exit for CTAs 0 and 1.
+#ifdef BWTA_TRACE
+constexpr int TRACE_EV = 16, TRACE_N = 64;
+constexpr int TRACE_BYTES = TRACE_EV * TRACE_N * 8;
+__device__ unsigned long long g_trace[2][TRACE_EV][TRACE_N];
+#define TRACE(ev, idx, cond)                                                                          \
+    do {                                                                                              \
+        if ((cond) && (idx) < TRACE_N)                                                                \
+            reinterpret_cast<unsigned long long*>(smem_raw)[(ev) * TRACE_N + (idx)] = clock64();      \
+    } while (0)
+#else
+constexpr int TRACE_BYTES = 0;  // (dynamic smem then starts with the operand ring)
+#define TRACE(ev, idx, cond) \
+    do {                     \
+    } while (0)
+#endif
+
 struct TcParams {
     int64_t M, N;  // kernel rows (A side) / cols (B side) per entry
     int num_kb;
@@ -86,10 +108,10 @@ struct Cfg {
     static constexpr int OUT_BYTES = 8 * OUT_BUF;                           // one staging buffer per epilogue warp
     static constexpr int SCALE_COLS = (BN + 127) / 128 * 64;                 // columns per epilogue warp
     static constexpr int SCALE_BYTES = 8 * SCALE_COLS * 4;                  // per-warp column scales
-    static constexpr int STAGES_FIT = (210 * 1024 - OUT_BYTES - SCALE_BYTES) / STAGE;
+    static constexpr int STAGES_FIT = (210 * 1024 - OUT_BYTES - SCALE_BYTES - TRACE_BYTES) / STAGE;
     static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
     static constexpr int BAR_BYTES = 256;
-    static constexpr int SMEM = 1024 + STAGES * STAGE + OUT_BYTES + SCALE_BYTES + BAR_BYTES;
+    static constexpr int SMEM = 1024 + STAGES * STAGE + OUT_BYTES + SCALE_BYTES + BAR_BYTES + TRACE_BYTES;
     // TMEM: two f32 accumulators of BN columns, then the UE8M0 scale factors
     // (all 1.0): SFA at SF_COL (4 columns used for M = 128), SFB at SF_COL + 8
     // (up to 8 columns).
@@ -115,19 +137,6 @@ struct Cfg {
 //   bool    (x0 = nz):            nz << 1                   -> 0 / +1
 //   ternary (x0 = sgn, x1 = nz):  nz << 1 | sgn << 3        -> 0 / +1 / -1
 // (ternary sgn is masked to the canonical subset of nz)
-// Timeline hooks (tools/trace_gemm.py; compiled only with -DBWTA_TRACE)
-#ifdef BWTA_TRACE
-// one writer per (CTA, event, index): plain stores, no atomics on the hot path
-__device__ unsigned long long g_trace[2][16][1024];
-#define TRACE(ev, idx, cond)                                                             \
-    do {                                                                                 \
-        if ((cond) && blockIdx.x < 2 && (idx) < 1024) g_trace[blockIdx.x][ev][idx] = clock64(); \
-    } while (0)
-#else
-#define TRACE(ev, idx, cond) \
-    do {                     \
-    } while (0)
-#endif
 
 __device__ __forceinline__ uint32_t shl_fma(uint32_t x, int k) {  // x << k as IMAD.SHL (FMA pipe)
     uint32_t r;
@@ -317,8 +326,10 @@ __device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorM
                 }
             }
             if (b == 0) {
+                TRACE(13, tix * 4 + i, tr);
                 if (lane == 0) bulk_wait_read<0>();  // the previous store has read the buffer
                 __syncwarp();
+                TRACE(14, tix * 4 + i, tr);
             }
 #pragma unroll
             for (int gp = 0; gp < 4; ++gp) {
@@ -333,6 +344,7 @@ __device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorM
                                       pk[4 * gp + 3]);
                 }
             }
+            if (b == 0) TRACE(15, tix * 4 + i, tr);
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -363,13 +375,16 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
         const int mt = int(r % p.m_tiles), nt = int(r / p.m_tiles);
         const int eb = int(e / p.nh), eh = int(e % p.nh);
         const int64_t mrow0 = int64_t(mt) * BM * CG + rank * BM;  // first kernel row of this CTA
+        // with an odd number of 64-column chunks the two warps of a lane
+        // quarter alternate which of them takes the extra chunk
+        const int hh = ((BN / 64) & 1) ? (h ^ (tix & 1)) : h;
         // scales of this tile (loaded before the accumulator is ready)
         const bool ok = fast_ok;
         float cr[4] = {0.f, 0.f, 0.f, 0.f};
         if (fast_ok) {
             if (col_scaled) {
                 // this warp's chunks: columns nt*BN + (2i + h)*64 + [0, 64)
-                for (int i = 0, c0 = h * 64; c0 < BN; ++i, c0 += 128) {
+                for (int i = 0, c0 = hh * 64; c0 < BN; ++i, c0 += 128) {
                     const int64_t n = int64_t(nt) * BN + c0 + 2 * lane;
                     const float a = __fmul_rn(__ldg(p.scale + (n < p.N ? n : 0)), p.scalar);
                     const float b = __fmul_rn(__ldg(p.scale + (n + 1 < p.N ? n + 1 : 0)), p.scalar);
@@ -394,11 +409,11 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
         const uint32_t tacc = tmem_base + uint32_t(acc * BN);
         if (ok) {
             if (p.y_dt == DT_BF16)
-                epi_tile_fast<BN, true>(p, tmY, tacc, stg, cs, col_scaled, cr, q, h, lane, mrow0, nt, eb, eh, tix);
+                epi_tile_fast<BN, true>(p, tmY, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix);
             else
-                epi_tile_fast<BN, false>(p, tmY, tacc, stg, cs, col_scaled, cr, q, h, lane, mrow0, nt, eb, eh, tix);
+                epi_tile_fast<BN, false>(p, tmY, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix);
         } else {
-            epi_tile_generic<BN, ES>(p, tmY, tacc, stg, q, h, lane, mrow0, nt, eb, eh);
+            epi_tile_generic<BN, ES>(p, tmY, tacc, stg, q, hh, lane, mrow0, nt, eb, eh);
         }
         tc_fence_before();
         __syncwarp();
@@ -459,8 +474,8 @@ __global__ void __launch_bounds__(NT, 1)
                    const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
                    const __grid_constant__ CUtensorMap tmY, TcParams p) {
     using C = Cfg<BN, CG>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem =
+        reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw + TRACE_BYTES) + 1023) & ~uintptr_t(1023));
     // 1024-byte aligned regions first (SW128 operand tiles, SW128 output
     // staging), then the 128-byte aligned bit-plane stages, then barriers
     uint8_t* sA = smem;
@@ -475,6 +490,9 @@ __global__ void __launch_bounds__(NT, 1)
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+#ifdef BWTA_TRACE
+    for (int i = threadIdx.x; i < TRACE_EV * TRACE_N; i += blockDim.x) reinterpret_cast<unsigned long long*>(smem_raw)[i] = 0;
+#endif
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -656,6 +674,12 @@ __global__ void __launch_bounds__(NT, 1)
     if (CG == 2) cluster_sync();
     else __syncthreads();
     TRACE(8, 0, threadIdx.x == 0);
+#ifdef BWTA_TRACE
+    __syncthreads();
+    if (blockIdx.x < 2)
+        for (int i = threadIdx.x; i < TRACE_EV * TRACE_N; i += blockDim.x)
+            (&g_trace[blockIdx.x][0][0])[i] = reinterpret_cast<unsigned long long*>(smem_raw)[i];
+#endif
     if (warp == 2) {
         tc_fence_after();
         if (CG == 1) tmem_dealloc(tmem_base, C::TMEM_COLS);
@@ -742,9 +766,10 @@ Plan make_plan(const MatmulArgs& a) {
 }
 
 // Tile shape: minimise (rounds of the persistent grid) x (per-tile cost).
-// The per-CTA MMA time of a tile is proportional to BN, plus a fixed
-// per-tile overhead (~48 columns' worth); CTA pairs halve the B-side unpack
-// and shared-memory operand traffic per MAC, so single CTAs pay 25 % more.
+// The mainloop is bound by shared-memory traffic (unpacked codes written
+// and read back by the MMA), which per CTA and stage is proportional to the
+// rows it unpacks: 128 A rows + BN / cg B rows; plus a fixed per-tile
+// overhead (~64 rows' worth: fill, epilogue drain).
 struct TileChoice {
     int bn, cg;
 };
@@ -759,7 +784,7 @@ TileChoice choose_tile(int64_t Mk, int64_t Nk, int64_t entries) {
             const int64_t tiles = entries * ((Mk + BM * cg - 1) / (BM * cg)) * ((Nk + bn - 1) / bn);
             const int64_t slots = num_sms() / cg;
             const int64_t rounds = (tiles + slots - 1) / slots;
-            const double cost = double(rounds) * (bn + 48) * (cg == 2 ? 1.0 : 1.25);
+            const double cost = double(rounds) * (BM + bn / cg + 64);
             if (cost < best_cost - 1e-9) {
                 best_cost = cost;
                 best = TileChoice{bn, cg};
@@ -792,7 +817,7 @@ cudaError_t launch_cfg(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUt
 // copy the timeline to the host and reset it (tools/trace_gemm.py)
 extern "C" __attribute__((visibility("default"))) int bwta_trace_fetch(unsigned long long* buf) {
     if (cudaMemcpyFromSymbol(buf, g_trace, sizeof(g_trace)) != cudaSuccess) return 1;
-    static unsigned long long zero[2][16][1024] = {};
+    static unsigned long long zero[2][TRACE_EV][TRACE_N] = {};
     return cudaMemcpyToSymbol(g_trace, zero, sizeof(zero)) != cudaSuccess;
 }
 #endif

@@ -15,35 +15,44 @@ import torch
 import bwta_inputs as gen
 import paper_2604_03957_b200 as B
 
-m, k, n = (int(v) for v in sys.argv[1:4])
-kind = sys.argv[4] if len(sys.argv) > 4 else "ternary"
-x = gen.activations((m, k), 1).cuda()
-if kind == "bool":
-    x = torch.relu(x)
-w = gen.weights(n, k, 2).cuda()
-a = B.bwta_pack_act(x, 1.6, kind=kind)
-wp = B.bwta_pack_weight(w)
-y = torch.empty((m, n), dtype=torch.float16, device="cuda")
-buf = np.zeros((2, 16, 1024), np.uint64)
+if sys.argv[1] == "qk":   # attention QK^T: qk BH T D
+    bh, t, d = (int(v) for v in sys.argv[2:5])
+    qp = B.bwta_pack_act(torch.randn(bh, t, d, device="cuda", dtype=torch.float16), 1.6)
+    kp = B.bwta_pack_act(torch.randn(bh, t, d, device="cuda", dtype=torch.float16), 1.6)
+    s_ = torch.empty(bh, t, t, device="cuda", dtype=torch.float16)
+    run = lambda: B.bwta_attn_qk(qp, kp, 0.1, out=s_, design="tcgen05")
+else:
+    m, k, n = (int(v) for v in sys.argv[1:4])
+    kind = sys.argv[4] if len(sys.argv) > 4 else "ternary"
+    x = gen.activations((m, k), 1).cuda()
+    if kind == "bool":
+        x = torch.relu(x)
+    w = gen.weights(n, k, 2).cuda()
+    a = B.bwta_pack_act(x, 1.6, kind=kind)
+    wp = B.bwta_pack_weight(w)
+    y = torch.empty((m, n), dtype=torch.float16, device="cuda")
+    run = lambda: B.bwta_gemm(a, wp, None, 1.0, out=y, design="tcgen05")
+buf = np.zeros((2, 16, 64), np.uint64)
 f = B.lib.bwta_trace_fetch
 for it in range(3):
     torch.cuda.synchronize()
     f(buf.ctypes.data)
-    B.bwta_gemm(a, wp, None, 1.0, out=y, design="tcgen05")
+    run()
     torch.cuda.synchronize()
     f(buf.ctypes.data)
 cnt = (buf != 0).sum(-1)
 names = ["start", "tma_issue", "unp_full", "unp_done", "mma_bready", "epi_tfull", "epi_done", "end_work", "exit",
-         "e_ld", "unpA_full", "unpA_done", "e_st"]
+         "e_ld", "unpA_full", "unpA_done", "e_st", "e_cvt0", "e_wrd0", "e_stm0"]
 for c in range(2):
     t0 = int(buf[c][0][0])
     print(f"CTA {c}: counts", dict(zip(names, cnt[c][:len(names)].tolist())))
     ev = {}
     for r, nm in enumerate(names):
-        v = buf[c][r][: cnt[c][r]].astype(np.int64) - t0
+        v = buf[c][r].astype(np.int64)
+        v = v[buf[c][r] != 0] - t0
         ev[nm] = v
         if len(v):
-            print(f"  {nm:11s}", " ".join(f"{x:6d}" for x in v[:48]))
+            print(f"  {nm:11s}", " ".join(f"{x:6d}" for x in v[:24]))
     for a_, b_ in (("tma_issue", "unp_full"), ("unp_full", "unp_done"), ("unp_done", "mma_bready")):
         if len(ev[a_]) and len(ev[b_]):
             n_ = min(len(ev[a_]), len(ev[b_]))
