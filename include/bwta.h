@@ -159,6 +159,33 @@ BWTA_API bwta_status_t bwta_pack_act(const void* x, bwta_dtype_t x_dt,
                             int64_t p_bstride, int64_t p_hstride,
                             int32_t* row_nnz, void* stream);
 
+/* ---- several activation packs in one launch ------------------------------ */
+/*
+ * bwta_pack_act_batch(descs, count, stream) == calling bwta_pack_act on
+ * descs[0..count) in order (same arguments, same results, same errors), but
+ * enqueued as ONE kernel launch when every desc has the same x_dt (otherwise
+ * one launch per desc).  Intended for the per-head Q, K and V^T packs of an
+ * attention layer, whose individual launches are latency-bound.
+ * 0 <= count <= BWTA_PACK_BATCH_MAX; descs is a HOST array.  All descs are
+ * validated before anything is enqueued.  The outputs of different descs
+ * must not alias each other or any input.
+ */
+#define BWTA_PACK_BATCH_MAX 4
+typedef struct {
+    const void* x;
+    bwta_dtype_t x_dt;
+    int64_t batch, heads, rows, cols, ld_x, x_bstride, x_hstride;
+    float scale;
+    bwta_kind_t kind;
+    int transpose;
+    uint32_t* sgn;
+    uint32_t* nz;
+    int64_t ld_words, p_bstride, p_hstride;
+    int32_t* row_nnz;
+} bwta_pack_desc_t;
+
+BWTA_API bwta_status_t bwta_pack_act_batch(const bwta_pack_desc_t* descs, int count, void* stream);
+
 /* ---- weight pack (offline) ---------------------------------------------- */
 /*
  * sgn[r] bit c = 1 <=> sign(W[r][c] - mu) = -1.

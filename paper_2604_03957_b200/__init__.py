@@ -21,7 +21,7 @@ from . import _native as N
 from ._native import lib
 
 __all__ = ["Packed", "BwtaError", "bwta_ld_words", "bwta_pack_act", "bwta_pack_weight",
-           "bwta_gemm", "bwta_attn_qk", "bwta_attn_pv", "last_design", "lib"]
+           "bwta_pack_act_batch", "bwta_gemm", "bwta_attn_qk", "bwta_attn_pv", "last_design", "lib"]
 
 
 class BwtaError(RuntimeError):
@@ -114,15 +114,12 @@ def _workspace(nbytes: int, device) -> tuple:
 
 
 # ----------------------------------------------------------------------------
-def bwta_pack_act(x: torch.Tensor, scale: float, kind: str = "ternary", transpose: bool = False,
-                  row_nnz: bool = False, stream=None) -> Packed:
-    """Quantize (P:911-930) and bit-pack activations.
-
-    x: CUDA tensor (f16/bf16/f32) [rows, cols], [B, rows, cols] or
-    [B, H, rows, cols] (any batch/head/row strides, unit column stride).
-    transpose=True packs along rows (planes of x^T; used for V^T in PV)."""
+def _pack_desc(x: torch.Tensor, scale: float, kind: str, transpose: bool, row_nnz: bool):
+    """(bwta_pack_desc_t, Packed) for one activation pack; allocates the planes."""
     if x.stride(-1) != 1:
         raise ValueError("x must have unit stride in its last dimension")
+    if kind not in _KIND:
+        raise ValueError(f"unknown kind {kind!r}")
     b, h, xbs, xhs = _batch_dims(x)
     rows, cols = x.shape[-2], x.shape[-1]
     out_rows, plen = (cols, rows) if transpose else (rows, cols)
@@ -136,11 +133,42 @@ def bwta_pack_act(x: torch.Tensor, scale: float, kind: str = "ternary", transpos
     phs = out_rows * ldw if x.dim() == 4 else 0
     if x.dim() == 2:
         pbs = 0
-    st = lib.bwta_pack_act(_ptr(x), _DT[x.dtype], b, h, rows, cols, x.stride(-2), xbs, xhs,
-                           ctypes.c_float(scale), _KIND[kind], int(transpose), _ptr(sgn), _ptr(nz),
-                           ldw, pbs, phs, _ptr(rn), _stream(stream))
+    d = N.PackDesc(_ptr(x), _DT[x.dtype], b, h, rows, cols, x.stride(-2), xbs, xhs, float(scale), _KIND[kind],
+                   int(transpose), _ptr(sgn), _ptr(nz), ldw, pbs, phs, _ptr(rn))
+    return d, Packed(sgn, nz, kind, plen, rn)
+
+
+def bwta_pack_act(x: torch.Tensor, scale: float, kind: str = "ternary", transpose: bool = False,
+                  row_nnz: bool = False, stream=None) -> Packed:
+    """Quantize (P:911-930) and bit-pack activations.
+
+    x: CUDA tensor (f16/bf16/f32) [rows, cols], [B, rows, cols] or
+    [B, H, rows, cols] (any batch/head/row strides, unit column stride).
+    transpose=True packs along rows (planes of x^T; used for V^T in PV)."""
+    d, out = _pack_desc(x, scale, kind, transpose, row_nnz)
+    st = lib.bwta_pack_act(d.x, d.x_dt, d.batch, d.heads, d.rows, d.cols, d.ld_x, d.x_bstride, d.x_hstride,
+                           ctypes.c_float(scale), d.kind, d.transpose, d.sgn, d.nz, d.ld_words, d.p_bstride,
+                           d.p_hstride, d.row_nnz, _stream(stream))
     _check(st, "bwta_pack_act")
-    return Packed(sgn, nz, kind, plen, rn)
+    return out
+
+
+def bwta_pack_act_batch(items, stream=None) -> list:
+    """Several bwta_pack_act calls in one kernel launch (<= 4; the per-head Q,
+    K and V^T packs of an attention layer).  items: sequence of
+    (x, scale, kind, transpose) tuples; returns the Packed results in order."""
+    items = list(items)
+    if len(items) > 4:
+        raise ValueError("at most 4 packs per batch")
+    descs, outs = [], []
+    for x, scale, kind, transpose in items:
+        d, o = _pack_desc(x, scale, kind, transpose, False)
+        descs.append(d)
+        outs.append(o)
+    arr = (N.PackDesc * max(len(descs), 1))(*descs)
+    _check(lib.bwta_pack_act_batch(ctypes.cast(arr, ctypes.c_void_p), len(descs), _stream(stream)),
+           "bwta_pack_act_batch")
+    return outs
 
 
 def bwta_pack_weight(w: torch.Tensor, mu=None, stream=None) -> Packed:

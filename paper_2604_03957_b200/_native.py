@@ -17,7 +17,8 @@ BINARY, BOOL, TERNARY = 0, 1, 2
 DESIGN_AUTO, DESIGN_CUDA_CORE, DESIGN_TCGEN05 = 0, 1, 2
 
 EXPORTS = ("bwta_ld_words", "bwta_status_string", "bwta_last_cuda_error", "bwta_last_design",
-           "bwta_version", "bwta_kernel_launches", "bwta_pack_act", "bwta_pack_weight", "bwta_gemm_workspace_size",
+           "bwta_version", "bwta_kernel_launches", "bwta_pack_act", "bwta_pack_act_batch", "bwta_pack_weight",
+           "bwta_gemm_workspace_size",
            "bwta_gemm", "bwta_attn_qk_workspace_size", "bwta_attn_qk",
            "bwta_attn_pv_workspace_size", "bwta_attn_pv")
 
@@ -25,6 +26,16 @@ EXPORTS = ("bwta_ld_words", "bwta_status_string", "bwta_last_cuda_error", "bwta_
 class Opts(ctypes.Structure):
     _fields_ = [("design", ctypes.c_int32), ("tile_n", ctypes.c_int32), ("cta_group", ctypes.c_int32),
                 ("reserved", ctypes.c_int32 * 5)]
+
+
+class PackDesc(ctypes.Structure):
+    """bwta_pack_desc_t (include/bwta.h)."""
+    _fields_ = [("x", ctypes.c_void_p), ("x_dt", ctypes.c_int32), ("batch", ctypes.c_int64),
+                ("heads", ctypes.c_int64), ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
+                ("ld_x", ctypes.c_int64), ("x_bstride", ctypes.c_int64), ("x_hstride", ctypes.c_int64),
+                ("scale", ctypes.c_float), ("kind", ctypes.c_int32), ("transpose", ctypes.c_int32),
+                ("sgn", ctypes.c_void_p), ("nz", ctypes.c_void_p), ("ld_words", ctypes.c_int64),
+                ("p_bstride", ctypes.c_int64), ("p_hstride", ctypes.c_int64), ("row_nnz", ctypes.c_void_p)]
 
 
 def _declare(L):
@@ -46,6 +57,8 @@ def _declare(L):
     L.bwta_version.argtypes = []
     L.bwta_kernel_launches.restype = ctypes.c_uint64
     L.bwta_kernel_launches.argtypes = []
+    L.bwta_pack_act_batch.restype = i32
+    L.bwta_pack_act_batch.argtypes = [P, i32, P]
     L.bwta_pack_act.restype = i32
     L.bwta_pack_act.argtypes = [P, i32, i64, i64, i64, i64, i64, i64, i64, f32, i32, i32,
                                 P, P, i64, i64, i64, P, P]

@@ -175,10 +175,19 @@ int bwta_last_design(void) { return g_last_design; }
 int bwta_version(void) { return 100; }
 uint64_t bwta_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
-bwta_status_t bwta_pack_act(const void* x, bwta_dtype_t x_dt, int64_t batch, int64_t heads, int64_t rows,
-                            int64_t cols, int64_t ld_x, int64_t x_bstride, int64_t x_hstride, float scale,
-                            bwta_kind_t kind, int transpose, uint32_t* sgn, uint32_t* nz, int64_t ld_words,
-                            int64_t p_bstride, int64_t p_hstride, int32_t* row_nnz, void* stream) {
+namespace {
+// Validate one activation pack and describe it; `empty` = nothing to write.
+bwta_status_t prepare_pack(const bwta_pack_desc_t& d, PackArgs& a, bool& empty) {
+    const void* x = d.x;
+    const bwta_dtype_t x_dt = d.x_dt;
+    const int64_t batch = d.batch, heads = d.heads, rows = d.rows, cols = d.cols, ld_x = d.ld_x;
+    const int64_t x_bstride = d.x_bstride, x_hstride = d.x_hstride;
+    const float scale = d.scale;
+    const bwta_kind_t kind = d.kind;
+    const int transpose = d.transpose;
+    uint32_t* sgn = d.sgn;
+    uint32_t* nz = d.nz;
+    const int64_t ld_words = d.ld_words, p_bstride = d.p_bstride, p_hstride = d.p_hstride;
     if (x_dt != BWTA_F16 && x_dt != BWTA_BF16 && x_dt != BWTA_F32) return BWTA_ERR_UNSUPPORTED;
     if (kind != BWTA_TERNARY && kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
     if (!scale_ok_pos(scale)) return BWTA_ERR_INVALID_VALUE;
@@ -191,12 +200,10 @@ bwta_status_t bwta_pack_act(const void* x, bwta_dtype_t x_dt, int64_t batch, int
     if (x_bstride < 0 || x_hstride < 0 || p_bstride < 0 || p_hstride < 0) return BWTA_ERR_SHAPE;
     if (ld_words % 4 || p_bstride % 4 || p_hstride % 4 || !aligned16(nz) || (sgn && !aligned16(sgn)))
         return BWTA_ERR_ALIGNMENT;
-    bwta_status_t st = check_device();
-    if (st != BWTA_OK) return st;
     // No packed rows at all -> nothing to write.  (Packed rows whose length
     // is 0 are all padding and are still written as zero words.)
-    if (batch == 0 || (transpose ? cols : rows) == 0) return BWTA_OK;
-    PackArgs a{};
+    empty = batch == 0 || (transpose ? cols : rows) == 0;
+    a = PackArgs{};
     a.x = x;
     a.dt = x_dt;
     a.nb = batch;
@@ -212,7 +219,7 @@ bwta_status_t bwta_pack_act(const void* x, bwta_dtype_t x_dt, int64_t batch, int
     a.ldw = ld_words;
     a.p_bs = p_bstride;
     a.p_hs = p_hstride;
-    a.row_nnz = row_nnz;
+    a.row_nnz = d.row_nnz;
     a.th = make_thresholds(x_dt, scale);
     const int es = esize(x_dt);
     a.vec_ok = aligned16(x) && (ld_x * es) % 16 == 0 && (x_bstride * es) % 16 == 0 && (x_hstride * es) % 16 == 0;
@@ -222,7 +229,42 @@ bwta_status_t bwta_pack_act(const void* x, bwta_dtype_t x_dt, int64_t batch, int
     a.div_ldw = make_fastdiv(uint32_t(ld_words > 0 && ld_words < (1ll << 31) ? ld_words : 1));
     a.div_rows = make_fastdiv(uint32_t(rows > 0 && rows < (1ll << 31) ? rows : 1));
     a.div_nh = make_fastdiv(uint32_t(heads < (1ll << 31) ? heads : 1));
+    return BWTA_OK;
+}
+}  // namespace
+
+bwta_status_t bwta_pack_act(const void* x, bwta_dtype_t x_dt, int64_t batch, int64_t heads, int64_t rows,
+                            int64_t cols, int64_t ld_x, int64_t x_bstride, int64_t x_hstride, float scale,
+                            bwta_kind_t kind, int transpose, uint32_t* sgn, uint32_t* nz, int64_t ld_words,
+                            int64_t p_bstride, int64_t p_hstride, int32_t* row_nnz, void* stream) {
+    const bwta_pack_desc_t d{x,     x_dt,  batch, heads,     rows,     cols,      ld_x,      x_bstride, x_hstride,
+                             scale, kind, transpose, sgn, nz, ld_words, p_bstride, p_hstride, row_nnz};
+    PackArgs a;
+    bool empty = false;
+    bwta_status_t st = prepare_pack(d, a, empty);
+    if (st != BWTA_OK) return st;
+    st = check_device();
+    if (st != BWTA_OK || empty) return st;
     cudaError_t e = transpose ? launch_pack_cols(a, (cudaStream_t)stream) : launch_pack_rows(a, (cudaStream_t)stream);
+    return e == cudaSuccess ? BWTA_OK : cuda_fail(e);
+}
+
+bwta_status_t bwta_pack_act_batch(const bwta_pack_desc_t* descs, int count, void* stream) {
+    if (count < 0 || count > BWTA_PACK_BATCH_MAX) return BWTA_ERR_INVALID_VALUE;
+    if (count == 0) return BWTA_OK;
+    if (descs == nullptr) return BWTA_ERR_INVALID_VALUE;
+    PackArgs a[BWTA_PACK_BATCH_MAX];
+    int tr[BWTA_PACK_BATCH_MAX];
+    int n = 0;
+    for (int i = 0; i < count; ++i) {  // validate everything before enqueueing anything
+        bool empty = false;
+        bwta_status_t st = prepare_pack(descs[i], a[n], empty);
+        if (st != BWTA_OK) return st;
+        if (!empty) tr[n++] = descs[i].transpose;
+    }
+    bwta_status_t st = check_device();
+    if (st != BWTA_OK || n == 0) return st;
+    cudaError_t e = launch_pack_group(a, tr, n, (cudaStream_t)stream);
     return e == cudaSuccess ? BWTA_OK : cuda_fail(e);
 }
 

@@ -95,6 +95,9 @@ struct PackArgs {
 
 cudaError_t launch_pack_rows(const PackArgs& a, cudaStream_t s);
 cudaError_t launch_pack_cols(const PackArgs& a, cudaStream_t s);
+constexpr int PACK_GROUP_MAX = 4;
+// several activation packs in one launch (falls back to one launch each)
+cudaError_t launch_pack_group(const PackArgs* a, const int* transpose, int n, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // Bit-serial matmul (design (a)) and the generic matmul description shared by

@@ -151,18 +151,17 @@ __device__ __forceinline__ void vec_bits(const uint4& v, const Thresholds& th, i
     neg |= nb << sh;
 }
 
+// Body of the row-mode pack for block `vb` of a grid of `vg` blocks (256 threads).
 template <typename T, int KIND, bool VEC, typename IDX>
-__global__ void __launch_bounds__(256, 2) pack_rows_kernel(PackArgs p) {
+__device__ __forceinline__ void pack_rows_body(const PackArgs& p, unsigned vb, unsigned vg) {
     constexpr int E = TypeInfo<T>::E;  // elements per 16-byte vector
     constexpr int NV = 32 / E;         // vectors per word
     constexpr int WPL = WplOf<T>::v;
     const IDX ldw = IDX(p.ldw), rows = IDX(p.rows), nh = IDX(p.nh);
     const IDX total = IDX(p.nb * p.nh) * rows * ldw;
     const IDX cols = IDX(p.cols);
-    const IDX nthreads = IDX(gridDim.x) * blockDim.x;
-    const IDX tid = IDX(blockIdx.x) * blockDim.x + threadIdx.x;
-    pdl_launch_dependents();
-    pdl_wait();  // no global memory access before the predecessor grid completed
+    const IDX nthreads = IDX(vg) * blockDim.x;
+    const IDX tid = IDX(vb) * blockDim.x + threadIdx.x;
 
     auto issue = [&](IDX gw0, uint4 (&v)[WplOf<T>::v][NV], IDX (&gr)[WplOf<T>::v], IDX (&gwv)[WplOf<T>::v]) {
 #pragma unroll
@@ -262,8 +261,9 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
     return x;
 }
 
+// Body of the transposed pack for block `vb` of a grid of `vg` blocks.
 template <typename T, int KIND, bool VEC, typename IDX>
-__global__ void __launch_bounds__(256, 2) pack_cols_kernel(PackArgs p) {
+__device__ __forceinline__ void pack_cols_body(const PackArgs& p, unsigned vb, unsigned vg) {
     constexpr int E = TypeInfo<T>::E;
     constexpr int NV = 32 / E;  // 16-byte vectors per 32 columns
     const int lane = threadIdx.x & 31;
@@ -271,10 +271,8 @@ __global__ void __launch_bounds__(256, 2) pack_cols_kernel(PackArgs p) {
     const IDX ntile_c = IDX((p.cols + 31) / 32);
     const IDX nh = IDX(p.nh);
     const IDX items = IDX(p.nb * p.nh) * ngrp * ntile_c;
-    const IDX warp0 = (IDX(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const IDX nwarps = (IDX(gridDim.x) * blockDim.x) >> 5;
-    pdl_launch_dependents();
-    pdl_wait();  // no global memory access before the predecessor grid completed
+    const IDX warp0 = (IDX(vb) * blockDim.x + threadIdx.x) >> 5;
+    const IDX nwarps = (IDX(vg) * blockDim.x) >> 5;
 
     // loads of item `it` for this lane's row (all zero past the last row)
     auto issue = [&](IDX it, uint4 (&v)[NV]) {
@@ -290,32 +288,98 @@ __global__ void __launch_bounds__(256, 2) pack_cols_kernel(PackArgs p) {
             for (int q = 0; q < NV; ++q) v[q] = load_chunk<T, VEC>(row, int64_t(tc) * 32 + q * E, p.cols);
         }
     };
-    uint4 v[NV], vn[NV];
+    // two items per warp per iteration and a prefetch of the next two: 4 x 64 B
+    // of loads in flight per lane (the transposed pack is latency-bound at
+    // the per-head sizes of an attention layer)
+    constexpr int CPL = sizeof(T) == 4 ? 1 : 2;  // f32 rows are twice the bytes
+    uint4 v[CPL][NV], vn[CPL][NV];
+    const IDX step = nwarps * CPL;
     IDX it = warp0;
-    if (it < items) issue(it, vn);
-    for (; it < items; it += nwarps) {
 #pragma unroll
-        for (int q = 0; q < NV; ++q) v[q] = vn[q];
-        if (it + nwarps < items) issue(it + nwarps, vn);
-        const IDX tc = it % ntile_c, t2 = it / ntile_c;
-        const IDX grp = t2 % ngrp, e = t2 / ngrp;
-        uint32_t pos = 0, neg = 0;
+    for (int u = 0; u < CPL; ++u)
+        if (it + IDX(u) * nwarps < items) issue(it + IDX(u) * nwarps, vn[u]);
+    for (; it < items; it += step) {
 #pragma unroll
-        for (int q = 0; q < NV; ++q) {
-            uint32_t pb, nb;
-            chunk_bits<T>(v[q], p.th, pb, nb);
-            pos |= pb << (q * E);
-            neg |= nb << (q * E);
+        for (int u = 0; u < CPL; ++u)
+#pragma unroll
+            for (int q = 0; q < NV; ++q) v[u][q] = vn[u][q];
+#pragma unroll
+        for (int u = 0; u < CPL; ++u)
+            if (it + step + IDX(u) * nwarps < items) issue(it + step + IDX(u) * nwarps, vn[u]);
+#pragma unroll
+        for (int u = 0; u < CPL; ++u) {
+            const IDX iu = it + IDX(u) * nwarps;
+            if (iu >= items) break;
+            const IDX tc = iu % ntile_c, t2 = iu / ntile_c;
+            const IDX grp = t2 % ngrp, e = t2 / ngrp;
+            uint32_t pos = 0, neg = 0;
+#pragma unroll
+            for (int q = 0; q < NV; ++q) {
+                uint32_t pb, nb;
+                chunk_bits<T>(v[u][q], p.th, pb, nb);
+                pos |= pb << (q * E);
+                neg |= nb << (q * E);
+            }
+            const uint32_t nzw = transpose32(KIND == K_BOOL ? pos : (pos | neg), lane);
+            const uint32_t sgw = (KIND == K_TERNARY) ? transpose32(neg, lane) : 0u;
+            const int64_t col = int64_t(tc) * 32 + lane;
+            if (col < p.cols) {
+                const int64_t poff = int64_t(e / nh) * p.p_bs + int64_t(e % nh) * p.p_hs + col * p.ldw + int64_t(grp);
+                p.nz[poff] = nzw;
+                if (KIND == K_TERNARY) p.sgn[poff] = sgw;
+                if (p.row_nnz && nzw) atomicAdd(p.row_nnz + int64_t(e) * p.cols + col, __popc(nzw));
+            }
         }
-        const uint32_t nzw = transpose32(KIND == K_BOOL ? pos : (pos | neg), lane);
-        const uint32_t sgw = (KIND == K_TERNARY) ? transpose32(neg, lane) : 0u;
-        const int64_t col = int64_t(tc) * 32 + lane;
-        if (col < p.cols) {
-            const int64_t poff = int64_t(e / nh) * p.p_bs + int64_t(e % nh) * p.p_hs + col * p.ldw + int64_t(grp);
-            p.nz[poff] = nzw;
-            if (KIND == K_TERNARY) p.sgn[poff] = sgw;
-            if (p.row_nnz && nzw) atomicAdd(p.row_nnz + int64_t(e) * p.cols + col, __popc(nzw));
-        }
+    }
+}
+
+template <typename T, int KIND, bool VEC, typename IDX>
+__global__ void __launch_bounds__(256, 2) pack_rows_kernel(PackArgs p) {
+    pdl_launch_dependents();
+    pdl_wait();  // no global memory access before the predecessor grid completed
+    pack_rows_body<T, KIND, VEC, IDX>(p, blockIdx.x, gridDim.x);
+}
+
+template <typename T, int KIND, bool VEC, typename IDX>
+__global__ void __launch_bounds__(256, 2) pack_cols_kernel(PackArgs p) {
+    pdl_launch_dependents();
+    pdl_wait();
+    pack_cols_body<T, KIND, VEC, IDX>(p, blockIdx.x, gridDim.x);
+}
+
+// Several activation packs (same input dtype, 32-bit indexing) in one launch:
+// block b runs the pack whose block range [end[d-1], end[d]) contains b.
+// Saves the per-launch ramp and drain of the small per-head packs (Q, K and
+// V^T of an attention layer).
+struct PackGroup {
+    PackArgs a[PACK_GROUP_MAX];
+    int transpose[PACK_GROUP_MAX];
+    int block_end[PACK_GROUP_MAX];
+    int n;
+};
+
+template <typename T, int KIND, bool VEC>
+__device__ __forceinline__ void group_body(const PackArgs& p, int transpose, unsigned vb, unsigned vg) {
+    if (transpose) pack_cols_body<T, KIND == K_BINARY ? K_TERNARY : KIND, VEC, uint32_t>(p, vb, vg);
+    else pack_rows_body<T, KIND, VEC, uint32_t>(p, vb, vg);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 2) pack_group_kernel(const __grid_constant__ PackGroup g) {
+    pdl_launch_dependents();
+    pdl_wait();
+    int d = 0;
+    while (d + 1 < g.n && int(blockIdx.x) >= g.block_end[d]) ++d;
+    const int b0 = d ? g.block_end[d - 1] : 0;
+    const unsigned vb = blockIdx.x - b0, vg = g.block_end[d] - b0;
+    const PackArgs& p = g.a[d];
+    const int tr = g.transpose[d];
+    if (p.kind == K_BOOL) {
+        if (p.vec_ok) group_body<T, K_BOOL, true>(p, tr, vb, vg);
+        else group_body<T, K_BOOL, false>(p, tr, vb, vg);
+    } else {
+        if (p.vec_ok) group_body<T, K_TERNARY, true>(p, tr, vb, vg);
+        else group_body<T, K_TERNARY, false>(p, tr, vb, vg);
     }
 }
 
@@ -409,6 +473,60 @@ cudaError_t launch_pack_cols(const PackArgs& a, cudaStream_t s) {
         case DT_F16: return cols_idx<__half>(a, s, grid, small);
         case DT_BF16: return cols_idx<__nv_bfloat16>(a, s, grid, small);
         default: return cols_idx<float>(a, s, grid, small);
+    }
+}
+
+namespace {
+int64_t pack_work(const PackArgs& a, int transpose) {
+    return transpose ? a.nb * a.nh * a.ldw * ((a.cols + 31) / 32) * 32 : a.nb * a.nh * a.rows * a.ldw;
+}
+bool pack_small(const PackArgs& a, int transpose, int grid) {
+    if (transpose) return pack_work(a, 1) / 32 + int64_t(grid) * 8 < (int64_t(1) << 31);
+    return pack_work(a, 0) + 4 * int64_t(grid) * 256 < (int64_t(1) << 31) && a.cols + 32 < (int64_t(1) << 31);
+}
+}  // namespace
+
+cudaError_t launch_pack_group(const PackArgs* a, const int* transpose, int n, cudaStream_t s) {
+    // one pack, mixed dtypes or 64-bit indexing: ordinary launches, in order
+    bool fuse = n > 1 && n <= PACK_GROUP_MAX;
+    for (int i = 0; i < n && fuse; ++i)
+        fuse = a[i].dt == a[0].dt && a[i].kind != K_BINARY && pack_small(a[i], transpose[i], 2 * num_sms_pack());
+    if (!fuse) {
+        for (int i = 0; i < n; ++i) {
+            cudaError_t e = transpose[i] ? launch_pack_cols(a[i], s) : launch_pack_rows(a[i], s);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
+    PackGroup g{};
+    g.n = n;
+    int64_t total = 0, work[PACK_GROUP_MAX];
+    for (int i = 0; i < n; ++i) {
+        g.a[i] = a[i];
+        g.transpose[i] = transpose[i];
+        work[i] = pack_work(a[i], transpose[i]);
+        total += work[i];
+        if (a[i].row_nnz) {
+            const int64_t cnt = a[i].nb * a[i].nh * (transpose[i] ? a[i].cols : a[i].rows);
+            cudaError_t e = cudaMemsetAsync(a[i].row_nnz, 0, sizeof(int32_t) * cnt, s);
+            if (e != cudaSuccess) return e;
+            count_launch();
+        }
+    }
+    // one resident wave shared in proportion to the words each pack writes
+    const int wave = 2 * num_sms_pack();
+    int end = 0;
+    for (int i = 0; i < n; ++i) {
+        int64_t b = total > 0 ? (work[i] * wave + total - 1) / total : 1;
+        const int64_t need = transpose[i] ? (work[i] / 32 + 7) / 8 : (work[i] + 511) / 512;
+        if (b > need) b = need;
+        end += int(b < 1 ? 1 : b);
+        g.block_end[i] = end;
+    }
+    switch (a[0].dt) {
+        case DT_F16: return launch_pdl(pack_group_kernel<__half>, end, 256, 0, s, 1, g);
+        case DT_BF16: return launch_pdl(pack_group_kernel<__nv_bfloat16>, end, 256, 0, s, 1, g);
+        default: return launch_pdl(pack_group_kernel<float>, end, 256, 0, s, 1, g);
     }
 }
 

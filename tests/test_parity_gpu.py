@@ -129,6 +129,28 @@ def test_pack_act_strided_heads_and_unaligned(B, transpose):
         assert np.array_equal(words(p.sgn).reshape(sgn.shape), sgn)
 
 
+def test_pack_act_batch_matches_single_calls(B):
+    """bwta_pack_act_batch (one launch) == the individual packs == the oracle:
+    strided per-head Q, K (rows), V^T (transposed) and a bool P with ragged sizes."""
+    Bsz, T, H, D = 2, 37, 3, 64
+    qkv = gen.activations((Bsz, T, 3 * H * D), 91).cuda()
+    P = gen.attention_probs((Bsz, H, T, T), 92).cuda()
+    views = [qkv[:, :, j * H * D:(j + 1) * H * D].unflatten(-1, (H, D)).transpose(1, 2) for j in range(3)]
+    items = [(views[0], 1.1, "ternary", False), (views[1], 0.9, "ternary", False),
+             (views[2], 1.3, "ternary", True), (P, 2.0 / T, "bool", False)]
+    got = B.bwta_pack_act_batch(items)
+    for (x, s, kind, tr), g in zip(items, got):
+        ref = B.bwta_pack_act(x, s, kind, transpose=tr)
+        assert torch.equal(g.nz, ref.nz)
+        sgn, nz, _ = oracle.pack_act(storage(x.contiguous()).reshape(-1, x.shape[-2], x.shape[-1]), "f16", s, kind,
+                                     transpose=tr)
+        assert np.array_equal(words(g.nz).reshape(nz.shape), nz)
+        if kind == "ternary":
+            assert torch.equal(g.sgn, ref.sgn)
+            assert np.array_equal(words(g.sgn).reshape(sgn.shape), sgn)
+    assert B.bwta_pack_act_batch([]) == []
+
+
 def test_pack_act_tiny_and_huge_scales(B):
     x = gen.activations((4, 300), 5, torch.float16)
     x[0, :8] = torch.tensor([6e-8, -6e-8, 1e-5, -1e-5, 65504, -65504, 3e-8, -3e-8], dtype=torch.float16)

@@ -20,7 +20,7 @@ def tg(g, n=10):
     return statistics.median(ts)
 R = 20
 def per_op(fn, style):
-    fl = (lambda: fbuf.zero_()) if style == "write" else (lambda: fbuf.sum())
+    fl = (lambda: fbuf.zero_()) if style == "write" else ((lambda: fbuf.sum()) if style == "read" else (lambda: fbuf[:1].zero_()))
     def rep():
         for _ in range(R): fl(); fn()
     def fonly():
@@ -35,6 +35,9 @@ cases = [("C3 X 2048x4096", x3, lambda: B.bwta_pack_act(x3, 1.6)),
          ("C2 X 4096x768", xb, lambda: B.bwta_pack_act(xb, 1.6)),
          ("C2 Q heads view", hv(0), lambda: B.bwta_pack_act(hv(0), 1.6)),
          ("C2 V^T heads view", hv(2), lambda: B.bwta_pack_act(hv(2), 1.6, transpose=True)),
+         ("C2 Q+K+V^T one launch", qkv, lambda: B.bwta_pack_act_batch([(hv(0), 1.6, "ternary", False),
+                                                                         (hv(1), 1.6, "ternary", False),
+                                                                         (hv(2), 1.6, "ternary", True)])),
          ("C2 P bool", P, lambda: B.bwta_pack_act(P, 2/128, "bool")),
          ("C2 R bool 4096x3072", Rr, lambda: B.bwta_pack_act(Rr, 0.8, "bool")),
          ("C4 P bool 32x2048^2", Pc4, lambda: B.bwta_pack_act(Pc4, 2/2048, "bool")),
@@ -42,7 +45,7 @@ cases = [("C3 X 2048x4096", x3, lambda: B.bwta_pack_act(x3, 1.6)),
 for name, x, fn in cases:
     nb = x.numel() * 2
     out = []
-    for style in ("write", "read"):
+    for style in ("write", "none"):
         tp = per_op(fn, style); tc = per_op(lambda: x.clone(), style)
         out.append(f"[{style}-flush] pack {tp:6.2f}us {nb*1.125/tp/1e3:5.0f}GB/s clone {tc:6.2f}us {2*nb/tc/1e3:5.0f}GB/s")
     print(f"{name:22s} {nb/1e6:6.1f}MB " + " | ".join(out))
