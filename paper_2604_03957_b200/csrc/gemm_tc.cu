@@ -47,10 +47,15 @@ namespace {
 using namespace sm100;
 
 constexpr int BM = 128;     // MMA M (kernel-A rows per tile), cta_group::1
-constexpr int BK = 256;     // K elements per stage: one 128-byte swizzle row of packed E2M1 codes
-constexpr int ROWB = 128;   // bytes per operand row per stage
+// K elements per stage, KS = 256 (one 128-byte SW128 row of packed E2M1
+// codes per operand row) or KS = 128 (a 64-byte SW64 row) for K <= 128 --
+// attention with head_dim <= 128 -- so no stage is half padding.
+template <int KS> struct Stage {
+    static constexpr int ROWB = KS / 2;       // bytes per operand row per stage
+    static constexpr int WPS = KS / 32;       // packed words per row per plane per stage
+    static constexpr int NMMA = ROWB / 32;    // tcgen05.mma per stage (K = 64 each)
+};
 constexpr int UMMA_KB = 32; // bytes of K per tcgen05.mma (K = 64 four-bit elements)
-constexpr int WPS = BK / 32;  // packed words per row per plane per stage (8)
 constexpr int NT = 640;     // 20 warps
 constexpr int OUT_BUF = 4096;
 
@@ -97,13 +102,14 @@ struct TcParams {
 
 __host__ __device__ constexpr int nplanes_of(int kind) { return kind == B_TERNARY ? 2 : 1; }
 
-template <int BN, int CG>
+template <int BN, int CG, int KS = 256>
 struct Cfg {
+    using S = Stage<KS>;
     static constexpr int BNC = BN / CG;          // kernel-B rows held (and unpacked) per CTA
-    static constexpr int A_BYTES = BM * ROWB;     // E2M1 codes, 2 per byte
-    static constexpr int B_BYTES = BNC * ROWB;
-    static constexpr int ABITS = 2 * BM * WPS * 4;  // up to 2 planes x 8 words per row
-    static constexpr int BBITS = 2 * BNC * WPS * 4;
+    static constexpr int A_BYTES = BM * S::ROWB;     // E2M1 codes, 2 per byte
+    static constexpr int B_BYTES = BNC * S::ROWB;
+    static constexpr int ABITS = 2 * BM * S::WPS * 4;  // up to 2 planes x WPS words per row
+    static constexpr int BBITS = 2 * BNC * S::WPS * 4;
     static constexpr int STAGE = A_BYTES + B_BYTES + ABITS + BBITS;
     static constexpr int OUT_BYTES = 8 * OUT_BUF;                           // one staging buffer per epilogue warp
     static constexpr int SCALE_COLS = (BN + 127) / 128 * 64;                 // columns per epilogue warp
@@ -428,14 +434,16 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
     if (lane == 0) bulk_wait_all();
 }
 
-// One operand row (256 K-elements = 8 words per plane) -> 128 bytes of E2M1
-// codes at rowaddr in the UMMA 128B-swizzled K-major layout (row r of its
-// 8-row atom): packed word g becomes the 16-byte chunk g.
+// One operand row (KS K-elements = KS/32 words per plane) -> KS/2 bytes of
+// E2M1 codes at rowaddr in the UMMA K-major layout: packed word g becomes the
+// 16-byte chunk g, placed by the 128B swizzle (chunk ^ (r & 7), 8-row atoms
+// of 1024 B) or the 64B swizzle (chunk ^ ((r >> 1) & 3), 8-row atoms of 512 B).
 // p0: sgn (binary, ternary) or nz (bool); p1: nz (ternary).
-template <int KIND>
+template <int KIND, int KS>
 __device__ __forceinline__ void unpack_row(uint32_t p0addr, uint32_t p1addr, uint32_t rowaddr, int r) {
+    const int sw = KS == 256 ? (r & 7) : ((r >> 1) & 3);
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {  // words 4h .. 4h+3
+    for (int h = 0; h < Stage<KS>::WPS / 4; ++h) {  // words 4h .. 4h+3
         const uint4 w0 = lds128(p0addr + 16 * h);
         uint4 w1 = make_uint4(0, 0, 0, 0);
         if (KIND == B_TERNARY) w1 = lds128(p1addr + 16 * h);
@@ -450,30 +458,41 @@ __device__ __forceinline__ void unpack_row(uint32_t p0addr, uint32_t p1addr, uin
             uint32_t o[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) o[j] = unpack_word<KIND>(x0[g], x1[g], j);
-            sts128(rowaddr + (((4 * h + g) ^ (r & 7)) << 4), o[0], o[1], o[2], o[3]);
+            sts128(rowaddr + (((4 * h + g) ^ sw) << 4), o[0], o[1], o[2], o[3]);
         }
     }
 }
 
 // rows [r0, rows) step `step` of one operand slice (warp-uniform kind)
+template <int KS>
 __device__ __forceinline__ void unpack_rows(int kind, uint32_t bits, int plane_bytes, uint32_t dst, int r0, int rows,
                                             int step) {
-    constexpr int RB = WPS * 4;  // bit bytes per row per plane
+    constexpr int RB = Stage<KS>::WPS * 4;  // bit bytes per row per plane
+    constexpr int ROWB = Stage<KS>::ROWB;
     if (kind == B_TERNARY) {
-        for (int r = r0; r < rows; r += step) unpack_row<B_TERNARY>(bits + r * RB, bits + plane_bytes + r * RB, dst + r * ROWB, r);
+        for (int r = r0; r < rows; r += step)
+            unpack_row<B_TERNARY, KS>(bits + r * RB, bits + plane_bytes + r * RB, dst + r * ROWB, r);
     } else if (kind == B_BOOL) {
-        for (int r = r0; r < rows; r += step) unpack_row<B_BOOL>(bits + r * RB, 0, dst + r * ROWB, r);
+        for (int r = r0; r < rows; r += step) unpack_row<B_BOOL, KS>(bits + r * RB, 0, dst + r * ROWB, r);
     } else {
-        for (int r = r0; r < rows; r += step) unpack_row<B_BINARY>(bits + r * RB, 0, dst + r * ROWB, r);
+        for (int r = r0; r < rows; r += step) unpack_row<B_BINARY, KS>(bits + r * RB, 0, dst + r * ROWB, r);
     }
 }
 
-template <int BN, int CG>
+// UMMA shared-memory descriptor of a K-major operand tile for the stage layout
+template <int KS>
+__device__ __forceinline__ uint64_t smem_desc_stage(uint32_t saddr) {
+    if (KS == 256) return smem_desc_sw128(saddr);
+    return smem_desc_sw64(saddr);
+}
+
+template <int BN, int CG, int KS>
 __global__ void __launch_bounds__(NT, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
                    const __grid_constant__ CUtensorMap tmY, TcParams p) {
-    using C = Cfg<BN, CG>;
+    using C = Cfg<BN, CG, KS>;
+    constexpr int WPS = Stage<KS>::WPS;
     uint8_t* smem =
         reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw + TRACE_BYTES) + 1023) & ~uintptr_t(1023));
     // 1024-byte aligned regions first (SW128 operand tiles, SW128 output
@@ -605,8 +624,9 @@ __global__ void __launch_bounds__(NT, 1)
                         const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
                         const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
 #pragma unroll
-                        for (int k = 0; k < ROWB / UMMA_KB; ++k) {
-                            const uint64_t ad = smem_desc_sw128(a0 + k * UMMA_KB), bd = smem_desc_sw128(b0 + k * UMMA_KB);
+                        for (int k = 0; k < Stage<KS>::NMMA; ++k) {
+                            const uint64_t ad = smem_desc_stage<KS>(a0 + k * UMMA_KB);
+                            const uint64_t bd = smem_desc_stage<KS>(b0 + k * UMMA_KB);
                             if (CG == 1) mma_mxf4(d, ad, bd, idesc, sfa, sfb, (kb | k) != 0);
                             else mma_mxf4_cg2(d, ad, bd, idesc, sfa, sfb, (kb | k) != 0);
                         }
@@ -645,7 +665,7 @@ __global__ void __launch_bounds__(NT, 1)
                 TRACE(is_a ? 10 : 2, it, ut == 0);
                 const uint32_t bits = is_a ? smem_u32(sABits + stage * C::ABITS) : smem_u32(sBBits + stage * C::BBITS);
                 const uint32_t dst = is_a ? smem_u32(sA + stage * C::A_BYTES) : smem_u32(sB + stage * C::B_BYTES);
-                unpack_rows(kind, bits, plane_bytes, dst, ut, rows, 128);
+                unpack_rows<KS>(kind, bits, plane_bytes, dst, ut, rows, 128);
                 fence_proxy_async_smem();
                 __syncwarp();
                 TRACE(is_a ? 11 : 3, it, ut == 0);
@@ -794,11 +814,11 @@ TileChoice choose_tile(int64_t Mk, int64_t Nk, int64_t entries) {
     return best;
 }
 
-template <int BN, int CG>
-cudaError_t launch_cfg(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUtensorMap& mb0, const CUtensorMap& mb1,
-                       const CUtensorMap& my, const TcParams& p, cudaStream_t s) {
-    using C = Cfg<BN, CG>;
-    auto kern = tc_gemm_kernel<BN, CG>;
+template <int BN, int CG, int KS>
+cudaError_t launch_ks(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUtensorMap& mb0, const CUtensorMap& mb1,
+                      const CUtensorMap& my, const TcParams& p, cudaStream_t s) {
+    using C = Cfg<BN, CG, KS>;
+    auto kern = tc_gemm_kernel<BN, CG, KS>;
     static bool attr_set = false;  // benign race: the same value may be set twice
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -809,6 +829,13 @@ cudaError_t launch_cfg(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUt
     const int64_t slots = num_sms() / CG;
     const int grid = int((tiles < slots ? tiles : slots) * CG);
     return launch_pdl(kern, dim3(grid), dim3(NT), size_t(C::SMEM), s, CG, ma0, ma1, mb0, mb1, my, p);
+}
+
+template <int BN, int CG>
+cudaError_t launch_cfg(int ks, const CUtensorMap& ma0, const CUtensorMap& ma1, const CUtensorMap& mb0,
+                       const CUtensorMap& mb1, const CUtensorMap& my, const TcParams& p, cudaStream_t s) {
+    return ks == 128 ? launch_ks<BN, CG, 128>(ma0, ma1, mb0, mb1, my, p, s)
+                     : launch_ks<BN, CG, 256>(ma0, ma1, mb0, mb1, my, p, s);
 }
 
 }  // namespace
@@ -836,14 +863,14 @@ bool matmul_tc_supported(const MatmulArgs& a) {
 
 namespace {
 // 4-D tensor map over a packed operand: dims {ld words, rows, heads, batch},
-// box {8 words, box_rows, 1, 1} (one 256-element K slice of box_rows rows)
+// box {wps words, box_rows, 1, 1} (one 32*wps-element K slice of box_rows rows)
 bool encode_planes(CUtensorMap* m, const uint32_t* base, int64_t ld, int64_t rows, int64_t hs, int64_t bs,
-                   int64_t nh, int64_t nb, int box_rows) {
+                   int64_t nh, int64_t nb, int box_rows, int wps) {
     const uint64_t row_b = uint64_t(ld) * 4;
     const uint64_t dims[4] = {uint64_t(ld), uint64_t(rows), uint64_t(nh), uint64_t(nb)};
     const uint64_t hsb = bstride(nh, hs * 4, row_b * rows);
     const uint64_t str[3] = {row_b, hsb, bstride(nb, bs * 4, hsb * nh)};
-    const uint32_t box[4] = {uint32_t(WPS), uint32_t(box_rows), 1, 1};
+    const uint32_t box[4] = {uint32_t(wps), uint32_t(box_rows), 1, 1};
     return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint32_t*>(base), dims, str, box,
                   CU_TENSOR_MAP_SWIZZLE_NONE);
 }
@@ -862,6 +889,9 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     if (tc.cg == 2 && pl.Mk <= BM) tc.cg = 1;  // a pair needs two 128-row halves of kernel-A
     const int bn = tc.bn, cg = tc.cg;
 
+    // stage depth along K: 128 when the whole reduction fits (attention, head_dim <= 128)
+    const int ks = kw4 <= 4 ? 128 : 256;
+    const int wps = ks / 32;
     // bit-plane tensor maps: plane 0 = sgn (binary/ternary) or nz (bool), plane 1 = nz (ternary)
     const int akind = kind_of(pl.a_sgn, pl.a_nz), bkind = kind_of(pl.b_sgn, pl.b_nz);
     CUtensorMap ma0, ma1, mb0, mb1, my;
@@ -870,16 +900,16 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
         const uint32_t* a1 = akind == B_TERNARY ? pl.a_nz : a0;
         const uint32_t* b0 = bkind == B_BOOL ? pl.b_nz : pl.b_sgn;
         const uint32_t* b1 = bkind == B_TERNARY ? pl.b_nz : b0;
-        if (!encode_planes(&ma0, a0, pl.lda, pl.Mk, pl.a_hs, pl.a_bs, a.nh, a.nb, BM) ||
-            !encode_planes(&ma1, a1, pl.lda, pl.Mk, pl.a_hs, pl.a_bs, a.nh, a.nb, BM) ||
-            !encode_planes(&mb0, b0, pl.ldb, pl.Nk, pl.b_hs, pl.b_bs, a.nh, a.nb, bn / cg) ||
-            !encode_planes(&mb1, b1, pl.ldb, pl.Nk, pl.b_hs, pl.b_bs, a.nh, a.nb, bn / cg))
+        if (!encode_planes(&ma0, a0, pl.lda, pl.Mk, pl.a_hs, pl.a_bs, a.nh, a.nb, BM, wps) ||
+            !encode_planes(&ma1, a1, pl.lda, pl.Mk, pl.a_hs, pl.a_bs, a.nh, a.nb, BM, wps) ||
+            !encode_planes(&mb0, b0, pl.ldb, pl.Nk, pl.b_hs, pl.b_bs, a.nh, a.nb, bn / cg, wps) ||
+            !encode_planes(&mb1, b1, pl.ldb, pl.Nk, pl.b_hs, pl.b_bs, a.nh, a.nb, bn / cg, wps))
             return cudaErrorInvalidValue;
     }
     TcParams p{};
     p.M = pl.Mk;
     p.N = pl.Nk;
-    p.num_kb = int((kw4 + WPS - 1) / WPS);
+    p.num_kb = int((kw4 + wps - 1) / wps);
     p.entries = entries;
     p.nh = a.nh;
     p.m_tiles = int((pl.Mk + BM * cg - 1) / (BM * cg));
@@ -918,13 +948,13 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
         if (!ok) my = ma0;  // unused
     }
     if (cg == 2) {
-        if (bn == 192) return launch_cfg<192, 2>(ma0, ma1, mb0, mb1, my, p, s);
-        if (bn == 128) return launch_cfg<128, 2>(ma0, ma1, mb0, mb1, my, p, s);
-        return launch_cfg<64, 2>(ma0, ma1, mb0, mb1, my, p, s);
+        if (bn == 192) return launch_cfg<192, 2>(ks, ma0, ma1, mb0, mb1, my, p, s);
+        if (bn == 128) return launch_cfg<128, 2>(ks, ma0, ma1, mb0, mb1, my, p, s);
+        return launch_cfg<64, 2>(ks, ma0, ma1, mb0, mb1, my, p, s);
     }
-    if (bn == 192) return launch_cfg<192, 1>(ma0, ma1, mb0, mb1, my, p, s);
-    if (bn == 128) return launch_cfg<128, 1>(ma0, ma1, mb0, mb1, my, p, s);
-    return launch_cfg<64, 1>(ma0, ma1, mb0, mb1, my, p, s);
+    if (bn == 192) return launch_cfg<192, 1>(ks, ma0, ma1, mb0, mb1, my, p, s);
+    if (bn == 128) return launch_cfg<128, 1>(ks, ma0, ma1, mb0, mb1, my, p, s);
+    return launch_cfg<64, 1>(ks, ma0, ma1, mb0, mb1, my, p, s);
 }
 
 }  // namespace bwta

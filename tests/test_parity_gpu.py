@@ -218,7 +218,8 @@ def test_gemm_parity_every_tile(B, tile):
     (M < N: activations expanded; M > N: roles swapped, D^T epilogue), ragged
     M/N/K tails, per-column / per-row scales, both output orientations."""
     for i, (m, n, k, a_kind) in enumerate([(300, 517, 421, "ternary"), (517, 300, 421, "bool"),
-                                           (130, 1000, 2000, "bool"), (1000, 130, 300, "ternary")]):
+                                           (130, 1000, 2000, "bool"), (1000, 130, 300, "ternary"),
+                                           (300, 517, 128, "ternary"), (517, 300, 97, "bool")]):  # 128-K stages
         a, wp, s_a, s_w, qa, qw = _gemm_case(B, m, n, k, 2500 + i, a_kind)
         d = oracle.dot(qa, qw, threads=oracle.default_threads())
         yi = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.int32, design="tcgen05", tile=tile)
