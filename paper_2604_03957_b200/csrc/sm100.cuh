@@ -172,8 +172,13 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
+// Cluster-wide execution barrier with a RELAXED arrive: the .release form
+// compiles to MEMBAR.ALL.GPU.  What crosses it in this library is ordered
+// explicitly -- mbarrier inits by fence.mbarrier_init.release.cluster, TMEM
+// writes and allocations by tcgen05.fence::before/after_thread_sync -- as in
+// CUTLASS's cluster_arrive_relaxed() + cluster_wait().
 __device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
 }
 // shared::cluster address of the same smem offset in CTA `rank` of the cluster
 __device__ __forceinline__ uint32_t mapa_smem(const void* p, uint32_t rank) {

@@ -8,7 +8,10 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
            "smsp__issue_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
            "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
-           "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "lts__t_bytes.sum"]
+           "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "lts__t_bytes.sum",
+           "sm__cycles_active.avg", "sm__cycles_elapsed.avg", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+           "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+           "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio"]
 
 def report(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -39,7 +42,8 @@ if __name__ == "__main__":
     else:
         L = launches(path)
         ids = sorted(L)
-        half = ids[len(ids) // 2:]          # second step (first is warm-up)
+        last = int(sys.argv[3]) if len(sys.argv) > 3 else len(ids) // 2
+        half = ids[-last:]                   # the last step (earlier launches: calibration, warm-up)
         tot = sum(L[i][2] for i in half)
         agg = collections.defaultdict(float)
         print(f"{'id':>4} {'ns':>9} {'share':>6}  kernel (grid)")
