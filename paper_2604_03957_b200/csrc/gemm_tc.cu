@@ -769,9 +769,9 @@ struct Plan {
     int bkind;
 };
 
-Plan make_plan(const MatmulArgs& a) {
+Plan make_plan(const MatmulArgs& a, bool swap) {
     Plan p{};
-    p.swap = a.M > a.N;
+    p.swap = swap;
     if (!p.swap) {
         p.a_sgn = a.a_sgn; p.a_nz = a.a_nz; p.b_sgn = a.b_sgn; p.b_nz = a.b_nz;
         p.Mk = a.M; p.Nk = a.N; p.lda = a.lda; p.ldb = a.ldb;
@@ -792,10 +792,10 @@ Plan make_plan(const MatmulArgs& a) {
 // overhead (~64 rows' worth: fill, epilogue drain).
 struct TileChoice {
     int bn, cg;
+    double cost;
 };
 TileChoice choose_tile(int64_t Mk, int64_t Nk, int64_t entries) {
-    TileChoice best{64, 1};
-    double best_cost = 1e300;
+    TileChoice best{64, 1, 1e300};
     const int bns[3] = {192, 128, 64};
     for (int cg = 2; cg >= 1; --cg) {
         if (cg == 2 && Mk <= BM) continue;
@@ -805,10 +805,7 @@ TileChoice choose_tile(int64_t Mk, int64_t Nk, int64_t entries) {
             const int64_t slots = num_sms() / cg;
             const int64_t rounds = (tiles + slots - 1) / slots;
             const double cost = double(rounds) * (BM + bn / cg + 64);
-            if (cost < best_cost - 1e-9) {
-                best_cost = cost;
-                best = TileChoice{bn, cg};
-            }
+            if (cost < best.cost - 1e-9) best = TileChoice{bn, cg, cost};
         }
     }
     return best;
@@ -880,10 +877,13 @@ int kind_of(const uint32_t* sgn, const uint32_t* nz) { return (sgn && nz) ? B_TE
 cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s) {
     const int64_t entries = a.nb * a.nh;
     const int64_t kw4 = kw4_of(a.K);
-    const Plan pl = make_plan(a);
-
-    // tile shape and CTA pairing (cta_group::2, M = 256 per pair)
-    TileChoice tc = choose_tile(pl.Mk, pl.Nk, entries);
+    // operand roles and tile shape: the caller's A on the MMA M side (kernel-A)
+    // or swapped (W on the M side, the epilogue stores D^T), whichever tiles
+    // the persistent grid better -- e.g. a skinny M = 16 goes on the N side
+    const TileChoice t_ns = choose_tile(a.M, a.N, entries), t_sw = choose_tile(a.N, a.M, entries);
+    const bool swap = t_sw.cost < t_ns.cost - 1e-9 || (!(t_ns.cost < t_sw.cost - 1e-9) && a.M > a.N);
+    const Plan pl = make_plan(a, swap);
+    TileChoice tc = swap ? t_sw : t_ns;
     if (a.tile_n) tc.bn = a.tile_n;
     if (a.cta_group) tc.cg = a.cta_group;
     if (tc.cg == 2 && pl.Mk <= BM) tc.cg = 1;  // a pair needs two 128-row halves of kernel-A
