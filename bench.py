@@ -215,10 +215,10 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
     def op_qkv():
         B.bwta_gemm(st["xq"], packed["qkv"], wsc["qkv"], s["x"], out=qkv)
 
-    def op_pack_qkv():  # per-head Q and K packs in one launch, then V^T
-        st["qp"], st["kp"] = B.bwta_pack_act_batch(
-            [(heads_view(qkv, 0), s["q"], "ternary", False), (heads_view(qkv, 1), s["k"], "ternary", False)])
-        st["vt"] = B.bwta_pack_act(heads_view(qkv, 2), s["v"], transpose=True)
+    def op_pack_qkv():  # the per-head Q, K and V^T packs in one launch
+        st["qp"], st["kp"], st["vt"] = B.bwta_pack_act_batch(
+            [(heads_view(qkv, 0), s["q"], "ternary", False), (heads_view(qkv, 1), s["k"], "ternary", False),
+             (heads_view(qkv, 2), s["v"], "ternary", True)])
 
     def op_qk():
         B.bwta_attn_qk(st["qp"], st["kp"], s["alpha"], out=S)

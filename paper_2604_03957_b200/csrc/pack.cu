@@ -262,72 +262,68 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x, int lane) {
 }
 
 // Body of the transposed pack for block `vb` of a grid of `vg` blocks.
+// Work item = (entry, 32-column tile, 4 consecutive 32-row groups): lane l
+// loads row 32*g + l of each of the 4 groups (4 x 64 B in flight per lane),
+// packs and transposes each 32x32 bit block, and lane c then holds 4
+// consecutive words of output row c, stored as one 16-byte vector per plane
+// (ld is a multiple of 4 words, so the vector never crosses a row).
 template <typename T, int KIND, bool VEC, typename IDX>
 __device__ __forceinline__ void pack_cols_body(const PackArgs& p, unsigned vb, unsigned vg) {
     constexpr int E = TypeInfo<T>::E;
     constexpr int NV = 32 / E;  // 16-byte vectors per 32 columns
+    constexpr int G = 4;        // row groups per item
     const int lane = threadIdx.x & 31;
-    const IDX ngrp = IDX(p.ldw);                 // 32-row groups (covers padding)
+    const IDX ngq = IDX(p.ldw / G);               // 128-row quads (ld covers the padding)
     const IDX ntile_c = IDX((p.cols + 31) / 32);
     const IDX nh = IDX(p.nh);
-    const IDX items = IDX(p.nb * p.nh) * ngrp * ntile_c;
+    const IDX items = IDX(p.nb * p.nh) * ngq * ntile_c;
     const IDX warp0 = (IDX(vb) * blockDim.x + threadIdx.x) >> 5;
     const IDX nwarps = (IDX(vg) * blockDim.x) >> 5;
-
-    // loads of item `it` for this lane's row (all zero past the last row)
-    auto issue = [&](IDX it, uint4 (&v)[NV]) {
+    for (IDX it = warp0; it < items; it += nwarps) {
         const IDX tc = it % ntile_c, t2 = it / ntile_c;
-        const IDX grp = t2 % ngrp, e = t2 / ngrp;
-        const int64_t r = int64_t(grp) * 32 + lane;
+        const IDX gq = t2 % ngq, e = t2 / ngq;
+        const T* base = reinterpret_cast<const T*>(p.x) + int64_t(e / nh) * p.x_bs + int64_t(e % nh) * p.x_hs;
+        // 2-byte inputs: all 4 groups' loads in flight at once; f32 (twice the
+        // registers) one group at a time
+        constexpr int GL = sizeof(T) == 4 ? 1 : G;
+        uint32_t nzw[G], sgw[G];
 #pragma unroll
-        for (int q = 0; q < NV; ++q) v[q] = make_uint4(0, 0, 0, 0);
-        if (r < p.rows) {
-            const T* row = reinterpret_cast<const T*>(p.x) + int64_t(e / nh) * p.x_bs + int64_t(e % nh) * p.x_hs +
-                           r * p.ld_x;
+        for (int g0 = 0; g0 < G; g0 += GL) {
+            uint4 v[GL][NV];
 #pragma unroll
-            for (int q = 0; q < NV; ++q) v[q] = load_chunk<T, VEC>(row, int64_t(tc) * 32 + q * E, p.cols);
-        }
-    };
-    // two items per warp per iteration and a prefetch of the next two: 4 x 64 B
-    // of loads in flight per lane (the transposed pack is latency-bound at
-    // the per-head sizes of an attention layer)
-    constexpr int CPL = sizeof(T) == 4 ? 1 : 2;  // f32 rows are twice the bytes
-    uint4 v[CPL][NV], vn[CPL][NV];
-    const IDX step = nwarps * CPL;
-    IDX it = warp0;
+            for (int g = 0; g < GL; ++g) {
+                const int64_t r = (int64_t(gq) * G + g0 + g) * 32 + lane;
 #pragma unroll
-    for (int u = 0; u < CPL; ++u)
-        if (it + IDX(u) * nwarps < items) issue(it + IDX(u) * nwarps, vn[u]);
-    for (; it < items; it += step) {
+                for (int q = 0; q < NV; ++q) v[g][q] = make_uint4(0, 0, 0, 0);
+                if (r < p.rows) {
+                    const T* row = base + r * p.ld_x;
 #pragma unroll
-        for (int u = 0; u < CPL; ++u)
-#pragma unroll
-            for (int q = 0; q < NV; ++q) v[u][q] = vn[u][q];
-#pragma unroll
-        for (int u = 0; u < CPL; ++u)
-            if (it + step + IDX(u) * nwarps < items) issue(it + step + IDX(u) * nwarps, vn[u]);
-#pragma unroll
-        for (int u = 0; u < CPL; ++u) {
-            const IDX iu = it + IDX(u) * nwarps;
-            if (iu >= items) break;
-            const IDX tc = iu % ntile_c, t2 = iu / ntile_c;
-            const IDX grp = t2 % ngrp, e = t2 / ngrp;
-            uint32_t pos = 0, neg = 0;
-#pragma unroll
-            for (int q = 0; q < NV; ++q) {
-                uint32_t pb, nb;
-                chunk_bits<T>(v[u][q], p.th, pb, nb);
-                pos |= pb << (q * E);
-                neg |= nb << (q * E);
+                    for (int q = 0; q < NV; ++q) v[g][q] = load_chunk<T, VEC>(row, int64_t(tc) * 32 + q * E, p.cols);
+                }
             }
-            const uint32_t nzw = transpose32(KIND == K_BOOL ? pos : (pos | neg), lane);
-            const uint32_t sgw = (KIND == K_TERNARY) ? transpose32(neg, lane) : 0u;
-            const int64_t col = int64_t(tc) * 32 + lane;
-            if (col < p.cols) {
-                const int64_t poff = int64_t(e / nh) * p.p_bs + int64_t(e % nh) * p.p_hs + col * p.ldw + int64_t(grp);
-                p.nz[poff] = nzw;
-                if (KIND == K_TERNARY) p.sgn[poff] = sgw;
-                if (p.row_nnz && nzw) atomicAdd(p.row_nnz + int64_t(e) * p.cols + col, __popc(nzw));
+#pragma unroll
+            for (int g = 0; g < GL; ++g) {
+                uint32_t pos = 0, neg = 0;
+#pragma unroll
+                for (int q = 0; q < NV; ++q) {
+                    uint32_t pb, nb;
+                    chunk_bits<T>(v[g][q], p.th, pb, nb);
+                    pos |= pb << (q * E);
+                    neg |= nb << (q * E);
+                }
+                nzw[g0 + g] = transpose32(KIND == K_BOOL ? pos : (pos | neg), lane);
+                sgw[g0 + g] = (KIND == K_TERNARY) ? transpose32(neg, lane) : 0u;
+            }
+        }
+        const int64_t col = int64_t(tc) * 32 + lane;
+        if (col < p.cols) {
+            const int64_t poff = int64_t(e / nh) * p.p_bs + int64_t(e % nh) * p.p_hs + col * p.ldw + int64_t(gq) * G;
+            *reinterpret_cast<uint4*>(p.nz + poff) = make_uint4(nzw[0], nzw[1], nzw[2], nzw[3]);
+            if (KIND == K_TERNARY)
+                *reinterpret_cast<uint4*>(p.sgn + poff) = make_uint4(sgw[0], sgw[1], sgw[2], sgw[3]);
+            if (p.row_nnz) {
+                const int c = __popc(nzw[0]) + __popc(nzw[1]) + __popc(nzw[2]) + __popc(nzw[3]);
+                if (c) atomicAdd(p.row_nnz + int64_t(e) * p.cols + col, c);
             }
         }
     }
@@ -460,7 +456,7 @@ cudaError_t launch_pack_rows(const PackArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_pack_cols(const PackArgs& a, cudaStream_t s) {
-    const int64_t items = a.nb * a.nh * a.ldw * ((a.cols + 31) / 32);
+    const int64_t items = a.nb * a.nh * (a.ldw / 4) * ((a.cols + 31) / 32);
     if (items == 0) return cudaSuccess;
     if (a.row_nnz) {
         cudaError_t err = cudaMemsetAsync(a.row_nnz, 0, sizeof(int32_t) * a.nb * a.nh * a.cols, s);
@@ -518,7 +514,7 @@ cudaError_t launch_pack_group(const PackArgs* a, const int* transpose, int n, cu
     int end = 0;
     for (int i = 0; i < n; ++i) {
         int64_t b = total > 0 ? (work[i] * wave + total - 1) / total : 1;
-        const int64_t need = transpose[i] ? (work[i] / 32 + 7) / 8 : (work[i] + 511) / 512;
+        const int64_t need = transpose[i] ? (work[i] / 128 + 7) / 8 : (work[i] + 511) / 512;  // warp items
         if (b > need) b = need;
         end += int(b < 1 ? 1 : b);
         g.block_end[i] = end;
