@@ -541,8 +541,8 @@ __global__ void __launch_bounds__(NT, 1)
         else tmem_alloc2(tmem_slot, C::TMEM_COLS);
     }
     tc_fence_before();
-    if (CG == 2) cluster_sync();
-    else __syncthreads();
+    __syncthreads();               // CTA-local smem order (TMEM address slot, barrier inits)
+    if (CG == 2) cluster_sync();   // the pair: relaxed arrive, tcgen05 fences order TMEM
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (warp >= 4 && warp < 8) {
@@ -554,8 +554,8 @@ __global__ void __launch_bounds__(NT, 1)
         tmem_wait_st();
     }
     tc_fence_before();
-    if (CG == 2) cluster_sync();
-    else __syncthreads();
+    __syncthreads();               // CTA-local smem order (TMEM address slot, barrier inits)
+    if (CG == 2) cluster_sync();   // the pair: relaxed arrive, tcgen05 fences order TMEM
     tc_fence_after();
     // prologue done (smem barriers, TMEM, descriptor prefetch): let the next
     // kernel start its own, then wait for our inputs (predecessor grid)
@@ -691,8 +691,8 @@ __global__ void __launch_bounds__(NT, 1)
     }
     TRACE(7, 0, warp == 4 && lane == 0);
     tc_fence_before();
-    if (CG == 2) cluster_sync();
-    else __syncthreads();
+    __syncthreads();               // CTA-local smem order (TMEM address slot, barrier inits)
+    if (CG == 2) cluster_sync();   // the pair: relaxed arrive, tcgen05 fences order TMEM
     TRACE(8, 0, threadIdx.x == 0);
 #ifdef BWTA_TRACE
     __syncthreads();

@@ -1,0 +1,32 @@
+"""Small calls of every entry point, for compute-sanitizer (memcheck / racecheck / initcheck)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import bwta_inputs as gen
+import paper_2604_03957_b200 as B
+
+x = gen.activations((130, 300), 1).cuda()
+w = gen.weights(200, 300, 2).cuda()
+a = B.bwta_pack_act(x, 1.6)
+ab = B.bwta_pack_act(torch.relu(x), 1.6, "bool")
+wp = B.bwta_pack_weight(w)
+for d in ("cuda_core", "tcgen05"):
+    B.bwta_gemm(a, wp, None, 1.0, design=d)
+    B.bwta_gemm(ab, wp, None, 1.0, design=d, y_transposed=True)
+    B.bwta_gemm(a, wp, None, 1.0, design=d, out_dtype=torch.int32)
+q = gen.activations((2, 3, 37, 64), 3).cuda()
+k = gen.activations((2, 3, 41, 64), 4).cuda()
+v = gen.activations((2, 3, 41, 64), 5).cuda()
+p = gen.attention_probs((2, 3, 37, 41), 6).cuda()
+qp, kp = B.bwta_pack_act(q, 1.6), B.bwta_pack_act(k, 1.6)
+vt = B.bwta_pack_act(v, 1.6, transpose=True)
+pp = B.bwta_pack_act(p, 0.05, "bool")
+g = B.bwta_pack_act_batch([(q, 1.6, "ternary", False), (v, 1.6, "ternary", True)])
+for d in ("cuda_core", "tcgen05"):
+    B.bwta_attn_qk(qp, kp, 0.1, design=d)
+    B.bwta_attn_pv(pp, vt, 0.1, design=d)
+torch.cuda.synchronize()
+print("ok")
