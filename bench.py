@@ -171,13 +171,13 @@ class Op:
         self.name, self.kind, self.fn, self.ops, self.bytes, self.cublas = name, kind, fn, ops, bytes_, cublas
 
 
-def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=3072):
+def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=3072, fuse_ffn=True,
+               qkv_packs="group2"):
     """configs[1]: BERT-base layer, seq 128, batch 32 (M = 4096 tokens)."""
     M, D = batch * seq, hidden // heads
     g = lambda s: s + seed  # noqa: E731
     X = gen.activations((M, hidden), g(0)).to(dev)
     Xf = gen.activations((M, hidden), g(1)).to(dev)          # LayerNorm output stand-in
-    R = gen.relu_activations((M, ffn), g(2)).to(dev)          # post-ReLU FFN activations
     P = gen.attention_probs((batch, heads, seq, seq), g(3)).to(dev)  # softmax output stand-in
     Ws = {"qkv": gen.weights(3 * hidden, hidden, g(4)), "o": gen.weights(hidden, hidden, g(5)),
           "f1": gen.weights(ffn, hidden, g(6)), "f2": gen.weights(hidden, ffn, g(7))}
@@ -187,7 +187,7 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
         packed[k] = B.bwta_pack_weight(w.to(dev), mu=mu)      # offline
         wsc[k] = s_w.to(dev)
         w16[k] = w.to(dev)
-    s = {"x": gen.act_scale(X), "xf": gen.act_scale(Xf), "r": gen.act_scale(R), "att": float(np.float32(2.0 / seq))}
+    s = {"x": gen.act_scale(X), "xf": gen.act_scale(Xf), "att": float(np.float32(2.0 / seq))}
     qkv = torch.empty((M, 3 * hidden), dtype=torch.float16, device=dev)
     S = torch.empty((batch, heads, seq, seq), dtype=torch.float16, device=dev)
     ctx = torch.empty((M, hidden), dtype=torch.float16, device=dev)
@@ -215,10 +215,16 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
     def op_qkv():
         B.bwta_gemm(st["xq"], packed["qkv"], wsc["qkv"], s["x"], out=qkv)
 
-    def op_pack_qkv():  # the per-head Q, K and V^T packs in one launch
-        st["qp"], st["kp"], st["vt"] = B.bwta_pack_act_batch(
-            [(heads_view(qkv, 0), s["q"], "ternary", False), (heads_view(qkv, 1), s["k"], "ternary", False),
-             (heads_view(qkv, 2), s["v"], "ternary", True)])
+    def op_pack_qkv():  # the per-head Q, K and V^T packs (one launch by default)
+        qa, ka, va = ((heads_view(qkv, 0), s["q"], "ternary", False), (heads_view(qkv, 1), s["k"], "ternary", False),
+                      (heads_view(qkv, 2), s["v"], "ternary", True))
+        if qkv_packs == "group3":
+            st["qp"], st["kp"], st["vt"] = B.bwta_pack_act_batch([qa, ka, va])
+        elif qkv_packs == "group2":
+            st["qp"], st["kp"] = B.bwta_pack_act_batch([qa, ka])
+            st["vt"] = B.bwta_pack_act(va[0], va[1], transpose=True)
+        else:
+            st["qp"], st["kp"], st["vt"] = (B.bwta_pack_act(x[0], x[1], transpose=x[3]) for x in (qa, ka, va))
 
     def op_qk():
         B.bwta_attn_qk(st["qp"], st["kp"], s["alpha"], out=S)
@@ -238,11 +244,14 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
     def op_pack_xf():
         st["fq"] = B.bwta_pack_act(Xf, s["xf"])
 
-    def op_f1():
+    def op_f1():  # FFN1 emits FFN2's bool input planes directly (fused pack, no h1 write)
+        st["rq"] = B.bwta_gemm_pack(st["fq"], packed["f1"], wsc["f1"], s["xf"], s["r"], "bool")
+
+    def op_f1_unfused():  # the same planes through fp16 h1 + a standalone pack
         B.bwta_gemm(st["fq"], packed["f1"], wsc["f1"], s["xf"], out=h1)
 
-    def op_pack_r():
-        st["rq"] = B.bwta_pack_act(R, s["r"], "bool")
+    def op_pack_h1():
+        st["rq"] = B.bwta_pack_act(h1, s["r"], "bool")
 
     def op_f2():
         B.bwta_gemm(st["rq"], packed["f2"], wsc["f2"], s["r"], out=y2)
@@ -250,6 +259,12 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
     op_pack_x(); op_qkv(); op_pack_qkv(); op_qk(); op_pack_p(); op_pv()  # noqa: E702
     torch.cuda.synchronize()
     s["ctx"] = gen.act_scale(ctx)   # calibration of the context scale (outside timing)
+    # calibration of FFN2's input scale on the (unfused) FFN1 output: s_r = 2 mean relu(h1)
+    op_pack_xf()
+    B.bwta_gemm(st["fq"], packed["f1"], wsc["f1"], s["xf"], out=h1)
+    torch.cuda.synchronize()
+    R = torch.relu(h1)              # the post-ReLU FFN activations (cuBLAS baseline input)
+    s["r"] = gen.act_scale(R)
 
     # cuBLAS FP16 baselines of the same matmuls (torch -> cuBLASLt)
     q16, k16, v16 = (heads_view(qkv, j) for j in range(3))
@@ -277,13 +292,19 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
         Op("gemm_o", "gemm", op_o, mm(M, hidden, hidden),
            M * hidden / 4 + hidden * hidden / 8 + 2 * M * hidden, cub["o"]),
         Op("pack_xf", "pack", op_pack_xf, 0, pk(M * hidden, 2)),
-        Op("gemm_ffn1", "gemm", op_f1, mm(M, ffn, hidden),
-           M * hidden / 4 + ffn * hidden / 8 + 2 * M * ffn, cub["f1"]),
-        Op("pack_r", "pack", op_pack_r, 0, pk(M * ffn, 1)),
+    ]
+    if fuse_ffn:
+        ops.append(Op("gemm_ffn1", "gemm", op_f1, mm(M, ffn, hidden),
+                      M * hidden / 4 + ffn * hidden / 8 + M * ffn / 8, cub["f1"]))  # writes FFN2's bool planes
+    else:
+        ops += [Op("gemm_ffn1", "gemm", op_f1_unfused, mm(M, ffn, hidden),
+                   M * hidden / 4 + ffn * hidden / 8 + 2 * M * ffn, cub["f1"]),
+                Op("pack_h1", "pack", op_pack_h1, 0, pk(M * ffn, 1))]
+    ops += [
         Op("gemm_ffn2", "gemm", op_f2, mm(M, hidden, ffn),
            M * ffn / 8 + hidden * ffn / 8 + 2 * M * hidden, cub["f2"]),
     ]
-    host_inputs = {"X": X, "Xf": Xf, "R": R, "P": P}
+    host_inputs = {"X": X, "Xf": Xf, "P": P}
     cfg = {"workload": "bert_layer (configs[1]): BERT-base layer, batch 32 x seq 128, hidden 768, "
                        "12 heads x 64, FFN 3072", "batch": batch, "seq_len": seq, "hidden": hidden,
            "heads": heads, "ffn": ffn, "tokens": M}
@@ -379,13 +400,21 @@ def oracle_bert_layer_step(smp, threads, row_frac=1.0):
     rows = max(1, int(M * row_frac))
     ops = 0
     qx = oracle.quantize_act(st(smp["X"][:rows]), "f16", s["x"], "ternary")
+    y_f1 = None
     for name, xin, sx, kind in (("qkv", None, s["x"], "ternary"), ("o", smp["X"], s["x"], "ternary"),
-                                ("f1", smp["Xf"], s["xf"], "ternary"), ("f2", smp["R"], s["r"], "bool")):
+                                ("f1", smp["Xf"], s["xf"], "ternary"), ("f2", "f1", s["r"], "bool")):
         w = smp["Ws"][name]
         mu, s_w = gen.weight_stats(w)
         qw = oracle.binarize_weight(st(w), "f16", mu=mu)
-        qa = qx if xin is None else oracle.quantize_act(st(xin[:rows]), "f16", sx, kind)
-        oracle.gemm(qa, qw, s_w.numpy(), sx, "f16", threads=threads)
+        if xin is None:
+            qa = qx
+        elif isinstance(xin, str):   # FFN2 consumes bool(FFN1 output): relu(y) >= t <=> y >= t
+            qa = oracle.quantize_act(y_f1, "f16", sx, kind)
+        else:
+            qa = oracle.quantize_act(st(xin[:rows]), "f16", sx, kind)
+        y = oracle.gemm(qa, qw, s_w.numpy(), sx, "f16", threads=threads)
+        if name == "f1":
+            y_f1 = y
         ops += 2 * qa.shape[0] * qw.shape[0] * qw.shape[1]
     nbh = max(1, int(smp["batch"] * smp["heads"] * row_frac))
     b = max(1, nbh // smp["heads"])
@@ -444,7 +473,7 @@ def _bert_inputs_cpu(seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=3072
     g = lambda s: s + seed  # noqa: E731
     X = gen.activations((M, hidden), g(0))
     Xf = gen.activations((M, hidden), g(1))
-    R = gen.relu_activations((M, ffn), g(2))
+    R = gen.relu_activations((M, ffn), g(2))  # stand-in for the FFN1 output (timing only)
     P = gen.attention_probs((batch, heads, seq, seq), g(3))
     Ws = {"qkv": gen.weights(3 * hidden, hidden, g(4)), "o": gen.weights(hidden, hidden, g(5)),
           "f1": gen.weights(ffn, hidden, g(6)), "f2": gen.weights(hidden, ffn, g(7))}

@@ -223,6 +223,27 @@ BWTA_API bwta_status_t bwta_gemm(const uint32_t* a_sgn, const uint32_t* a_nz, bw
                         void* workspace, size_t workspace_bytes,
                         const bwta_opts_t* opts, void* stream);
 
+/* ---- BWTA linear with the next layer's pack fused into the epilogue ------ */
+/*
+ * out = bwta_pack_act(Y, y_dt, out_scale, out_kind), Y = bwta_gemm(...) in
+ * y_dt, BIT-EXACTLY -- without writing Y: the epilogue rounds each
+ * y = fl32(dot * c) (R5) to y_dt (F16 | BF16) and quantizes it with the
+ * exact thresholds of out_scale (R1-R3), writing the planes of Y's rows
+ * (bits along n): out_nz (+ out_sgn for TERNARY) [m x out_ld_words],
+ * out_ld_words >= bwta_ld_words(n), padding zero.  Typical use: the FFN1
+ * linear emitting the BOOL planes FFN2 consumes (relu(y) >= t <=> y >= t
+ * for t > 0), 2 bits instead of 16 per activation and no pack launch
+ * (SURVEY §8(f) N2).  Design (b) only (opts->design CUDA_CORE ->
+ * BWTA_ERR_UNSUPPORTED); no row_nnz.  Other arguments as bwta_gemm.
+ */
+BWTA_API bwta_status_t bwta_gemm_pack(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t a_kind,
+                                      int64_t m, int64_t lda_words,
+                                      const uint32_t* w_sgn, int64_t n, int64_t ldw_words, int64_t k,
+                                      const float* w_scale, float a_scale, bwta_dtype_t y_dt,
+                                      float out_scale, bwta_kind_t out_kind,
+                                      uint32_t* out_sgn, uint32_t* out_nz, int64_t out_ld_words,
+                                      const bwta_opts_t* opts, void* stream);
+
 /* ---- attention QK^T (Case 3) -------------------------------------------- */
 /*
  * S_e[i][j] = fl32(float(sum_d q[i][d] k[j][d]) * alpha)

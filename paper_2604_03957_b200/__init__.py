@@ -21,7 +21,7 @@ from . import _native as N
 from ._native import lib
 
 __all__ = ["Packed", "BwtaError", "bwta_ld_words", "bwta_pack_act", "bwta_pack_weight",
-           "bwta_pack_act_batch", "bwta_gemm", "bwta_attn_qk", "bwta_attn_pv", "last_design", "lib"]
+           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "last_design", "lib"]
 
 
 class BwtaError(RuntimeError):
@@ -214,6 +214,31 @@ def bwta_gemm(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: fl
                        _DT[out.dtype], out.stride(0), int(y_transposed), _ptr(ws), wsb, o, _stream(stream))
     _check(st, "bwta_gemm")
     return out
+
+
+def bwta_gemm_pack(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: float, out_scale: float,
+                   out_kind: str = "ternary", y_dtype=torch.float16, design: str = "auto", stream=None,
+                   tile=None) -> Packed:
+    """bwta_pack_act(bwta_gemm(a, w, ...) in y_dtype, out_scale, out_kind) with the pack
+    fused into the GEMM epilogue (Y is never written).  Returns the Packed planes
+    of Y's rows [M, ld(N)] -- e.g. FFN1 emitting FFN2's bool input."""
+    if a.kind not in ("ternary", "bool") or w.kind != "binary" or a.cols != w.cols:
+        raise ValueError("bwta_gemm_pack expects ternary/bool activations and binary weights of equal K")
+    if out_kind not in ("ternary", "bool"):
+        raise ValueError("out_kind must be 'ternary' or 'bool'")
+    ar = a.ref
+    m, n, k = ar.shape[-2], w.sgn.shape[-2], a.cols
+    dev = ar.device
+    ldw = bwta_ld_words(n)
+    nz = torch.empty((m, ldw), dtype=torch.int32, device=dev)
+    sgn = torch.empty((m, ldw), dtype=torch.int32, device=dev) if out_kind == "ternary" else None
+    ws_scale = None if w_scale is None else w_scale.to(device=dev, dtype=torch.float32).contiguous()
+    st = lib.bwta_gemm_pack(_ptr(a.sgn), _ptr(a.nz), _KIND[a.kind], m, ar.stride(-2), _ptr(w.sgn), n,
+                            w.sgn.stride(-2), k, _ptr(ws_scale), ctypes.c_float(a_scale), _DT[y_dtype],
+                            ctypes.c_float(out_scale), _KIND[out_kind], _ptr(sgn), _ptr(nz), ldw,
+                            _opts(design, tile), _stream(stream))
+    _check(st, "bwta_gemm_pack")
+    return Packed(sgn, nz, out_kind, n)
 
 
 def bwta_attn_qk(q: Packed, k: Packed, alpha: float, out_dtype=torch.float16,

@@ -18,7 +18,7 @@ DESIGN_AUTO, DESIGN_CUDA_CORE, DESIGN_TCGEN05 = 0, 1, 2
 
 EXPORTS = ("bwta_ld_words", "bwta_status_string", "bwta_last_cuda_error", "bwta_last_design",
            "bwta_version", "bwta_kernel_launches", "bwta_pack_act", "bwta_pack_act_batch", "bwta_pack_weight",
-           "bwta_gemm_workspace_size",
+           "bwta_gemm_workspace_size", "bwta_gemm_pack",
            "bwta_gemm", "bwta_attn_qk_workspace_size", "bwta_attn_qk",
            "bwta_attn_pv_workspace_size", "bwta_attn_pv")
 
@@ -57,6 +57,8 @@ def _declare(L):
     L.bwta_version.argtypes = []
     L.bwta_kernel_launches.restype = ctypes.c_uint64
     L.bwta_kernel_launches.argtypes = []
+    L.bwta_gemm_pack.restype = i32
+    L.bwta_gemm_pack.argtypes = [P, P, i32, i64, i64, P, i64, i64, i64, P, f32, i32, f32, i32, P, P, i64, P, P]
     L.bwta_pack_act_batch.restype = i32
     L.bwta_pack_act_batch.argtypes = [P, i32, P]
     L.bwta_pack_act.restype = i32

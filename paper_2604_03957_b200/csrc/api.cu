@@ -89,6 +89,31 @@ uint16_t smallest_pattern(double t, bool strict, bool bf16) {
     return uint16_t(lo);
 }
 
+// The smallest float f with RNE_to_y_dt(f) >= value(pattern) (pattern > 0):
+// the epilogue of bwta_gemm_pack compares the fp32 product against it, which
+// is exactly "round to f16/bf16, then compare with the storage threshold".
+// The rounding boundary is the midpoint m of pattern and its predecessor (for
+// the infinity pattern: max finite + half an ulp); a tie at m rounds to the
+// even mantissa, so m itself qualifies iff the pattern's mantissa is even
+// (for infinity: the virtual successor of max finite is even -> yes).
+float rounding_threshold(uint16_t pattern, bool bf16) {
+    const uint16_t inf = bf16 ? 0x7f80u : 0x7c00u;
+    const double prev = bf16 ? bf16_value(uint16_t(pattern - 1)) : f16_value(uint16_t(pattern - 1));
+    double m;
+    bool inclusive;
+    if (pattern >= inf) {
+        const double ulp = bf16 ? std::ldexp(1.0, 127 - 7) : std::ldexp(1.0, 15 - 10);  // at max finite
+        m = prev + ulp / 2;
+        inclusive = true;
+    } else {
+        const double v = bf16 ? bf16_value(pattern) : f16_value(pattern);
+        m = (prev + v) / 2;
+        inclusive = (pattern & 1u) == 0;
+    }
+    const float lo = float(m);  // exact: at most one bit more than the 16-bit type
+    return inclusive ? lo : std::nextafter(lo, INFINITY);
+}
+
 Thresholds make_thresholds(int dt, float scale) {
     Thresholds th{};
     const double t = 0.5 * double(scale);  // exact
@@ -356,6 +381,70 @@ bwta_status_t bwta_gemm(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t
     a.col_scale = w_scale;
     a.scalar = a_scale;
     return run_matmul(a, workspace, workspace_bytes, opts, (cudaStream_t)stream);
+}
+
+bwta_status_t bwta_gemm_pack(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t a_kind, int64_t m,
+                             int64_t lda_words, const uint32_t* w_sgn, int64_t n, int64_t ldw_words, int64_t k,
+                             const float* w_scale, float a_scale, bwta_dtype_t y_dt, float out_scale,
+                             bwta_kind_t out_kind, uint32_t* out_sgn, uint32_t* out_nz, int64_t out_ld_words,
+                             const bwta_opts_t* opts, void* stream) {
+    if (a_kind != BWTA_TERNARY && a_kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
+    if (out_kind != BWTA_TERNARY && out_kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
+    if (y_dt != BWTA_F16 && y_dt != BWTA_BF16) return BWTA_ERR_UNSUPPORTED;
+    if (m < 0 || n < 0 || k < 0 || k > KMAX) return BWTA_ERR_SHAPE;
+    if (m == 0 || n == 0) return BWTA_OK;
+    if (a_nz == nullptr || w_sgn == nullptr || out_nz == nullptr) return BWTA_ERR_INVALID_VALUE;
+    if ((a_kind == BWTA_TERNARY) != (a_sgn != nullptr)) return BWTA_ERR_INVALID_VALUE;
+    if ((out_kind == BWTA_TERNARY) != (out_sgn != nullptr)) return BWTA_ERR_INVALID_VALUE;
+    if (!std::isfinite(a_scale) || !scale_ok_pos(out_scale)) return BWTA_ERR_INVALID_VALUE;
+    const int64_t need = ldw_of(k);
+    if (lda_words < need || ldw_words < need || out_ld_words < ldw_of(n)) return BWTA_ERR_SHAPE;
+    if (lda_words % 4 || ldw_words % 4 || out_ld_words % 4 || !aligned16(a_nz) || (a_sgn && !aligned16(a_sgn)) ||
+        !aligned16(w_sgn) || !aligned16(out_nz) || (out_sgn && !aligned16(out_sgn)))
+        return BWTA_ERR_ALIGNMENT;
+    const bwta_opts_t* o = opts_or_default(opts);
+    if (o->design == BWTA_DESIGN_CUDA_CORE) return BWTA_ERR_UNSUPPORTED;  // fused pack: design (b) only
+    bwta_status_t st = check_device();
+    if (st != BWTA_OK) return st;
+    MatmulArgs a{};
+    a.a_sgn = a_sgn;
+    a.a_nz = a_nz;
+    a.b_sgn = w_sgn;
+    a.M = m;
+    a.N = n;
+    a.K = k;
+    a.lda = lda_words;
+    a.ldb = ldw_words;
+    a.nb = a.nh = 1;
+    a.y_dt = y_dt;
+    a.col_scale = w_scale;
+    a.scalar = a_scale;
+    a.pack_out = 1;
+    a.po_kind = out_kind;
+    a.po_sgn = out_sgn;
+    a.po_nz = out_nz;
+    a.po_ld = out_ld_words;
+    const double t = 0.5 * double(out_scale);  // exact
+    const bool bf = y_dt == BWTA_BF16;
+    a.po_tp = rounding_threshold(smallest_pattern(t, false, bf), bf);
+    a.po_tn = rounding_threshold(smallest_pattern(t, true, bf), bf);
+    if (!matmul_tc_supported(a)) return BWTA_ERR_UNSUPPORTED;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (out_ld_words * 32 > n) {
+        // words past ceil(n/32) are padding the kernel does not visit: zero the planes first
+        cudaError_t e = cudaMemsetAsync(out_nz, 0, sizeof(uint32_t) * size_t(m) * size_t(out_ld_words), s);
+        if (e == cudaSuccess && out_sgn)
+            e = cudaMemsetAsync(out_sgn, 0, sizeof(uint32_t) * size_t(m) * size_t(out_ld_words), s);
+        if (e != cudaSuccess) return cuda_fail(e);
+    }
+    a.tile_n = o->tile_n;
+    a.cta_group = o->cta_group;
+    for (int r : o->reserved)
+        if (r != 0) return BWTA_ERR_INVALID_VALUE;
+    cudaError_t e = launch_matmul_tc(a, nullptr, 0, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_last_design = BWTA_DESIGN_TCGEN05;
+    return BWTA_OK;
 }
 
 size_t bwta_attn_qk_workspace_size(int64_t batch_heads, int64_t tq, int64_t tk, int64_t dh, const bwta_opts_t* opts) {

@@ -123,6 +123,14 @@ struct MatmulArgs {
     const float* col_scale;   // [N] or null
     float scalar;
     int tile_n = 0, cta_group = 0;  // design (b) tile overrides (0 = auto)
+    // fused next-layer pack (bwta_gemm_pack): instead of writing Y, quantize
+    // round(Y to y_dt) with the next layer's thresholds and write its planes
+    int pack_out = 0;
+    int po_kind = 0;          // K_TERNARY / K_BOOL
+    uint32_t* po_sgn = nullptr;
+    uint32_t* po_nz = nullptr;
+    int64_t po_ld = 0;        // words per packed row (rows = the M rows of Y)
+    float po_tp = 0.f, po_tn = 0.f;  // +1 iff y >= po_tp; -1 iff y <= -po_tn (exact storage values)
 };
 
 cudaError_t launch_matmul_cc(const MatmulArgs& a, cudaStream_t s);

@@ -98,6 +98,12 @@ struct TcParams {
     const float* scale;  // per kernel column (or per kernel row if scale_on_rows), may be null
     int scale_on_rows;
     float scalar;
+    // fused pack of the output (MatmulArgs::pack_out)
+    int pack_out, po_kind;
+    uint32_t* po_sgn;
+    uint32_t* po_nz;
+    int64_t po_ld;
+    float po_tp, po_tn;
 };
 
 __host__ __device__ constexpr int nplanes_of(int kind) { return kind == B_TERNARY ? 2 : 1; }
@@ -363,6 +369,114 @@ __device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorM
     }
 }
 
+// Fused next-layer pack: the tile's outputs y = fl32(dot * c) (R5) are
+// quantized exactly as bwta_pack_act would quantize the stored Y (y rounded
+// to fp16 / bf16, then R1-R3): the host turns the storage thresholds into fp32
+// rounding boundaries (api.cu rounding_threshold), so +1 iff y >= po_tp and
+// -1 iff y <= -po_tn on the fp32 value, NaN -> 0; the bits
+// go straight into the next layer's planes (rows = the M rows of Y, bits
+// along N).  32x32b TMEM loads: thread = kernel row, 32 kernel columns.
+//  * not swapped (kernel row = m): a thread owns 32 consecutive n of its row
+//    -> one word per plane per thread;
+//  * swapped (kernel row = n): a warp's 32 lanes are 32 consecutive n ->
+//    one __ballot_sync per kernel column (= output row m), lane j stores
+//    the word of column j.
+// smallest integer d (|d| <= 2^25) with fl32(d * c) >= t, for c > 0 finite
+__device__ __forceinline__ float int_threshold_ge(float t, float c) {
+    float d = ceilf(t / c);
+    d = fminf(fmaxf(d, -33554432.f), 33554432.f);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        if (__fmul_rn(d, c) < t) d += 1.f;
+        else if (__fmul_rn(d - 1.f, c) >= t) d -= 1.f;
+    }
+    return d;
+}
+
+template <int BN>
+__device__ __forceinline__ void epi_tile_pack(const TcParams& p, uint32_t tacc, uint8_t* scratch, int q, int h,
+                                              int lane, int64_t mrow0, int nt) {
+    const bool ternary = p.po_kind == K_TERNARY;
+    const int64_t row = mrow0 + q * 32 + lane;  // kernel row of this thread
+    const bool rok = row < p.M;
+    float crow = p.scalar;
+    if (p.scale_on_rows && p.scale) crow = __fmul_rn(__ldg(p.scale + (rok ? row : 0)), p.scalar);
+    const bool col_scaled = !p.scale_on_rows && p.scale;
+    // integer thresholds of the swapped orientation (per-lane scale), when every c > 0 is finite:
+    // y >= tp <=> acc >= tpi;  y <= -tn <=> -acc*c >= tn <=> -acc >= tni' <=> acc <= tni
+    const bool c_pos = !col_scaled && crow > 0.f && crow <= 3.4e38f;
+    const bool ith = p.out_trans && __all_sync(0xffffffffu, c_pos);
+    float tpi = 0.f, tni = 0.f;
+    if (ith) {
+        tpi = int_threshold_ge(p.po_tp, crow);
+        tni = -int_threshold_ge(p.po_tn, crow);
+    }
+#pragma unroll 1
+    for (int c0 = h * 32; c0 < BN; c0 += 64) {
+        const int64_t n0 = int64_t(nt) * BN + c0;  // first kernel column (a multiple of 32)
+        if (n0 >= p.N) break;
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tacc + (uint32_t(q * 32) << 16) + uint32_t(c0), v);
+        tmem_wait_ld();
+        float cl = crow;
+        if (col_scaled) {
+            const int64_t nl = n0 + lane;
+            cl = __fmul_rn(__ldg(p.scale + (nl < p.N ? nl : 0)), p.scalar);
+        }
+        if (!p.out_trans) {
+            // this thread's 32 columns are 32 consecutive elements of its output row
+            uint32_t pos = 0, neg = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float c = col_scaled ? __shfl_sync(0xffffffffu, cl, j) : crow;
+                const float y = scaled(v[j], c);
+                const bool valid = n0 + j < p.N;
+                pos |= uint32_t(valid && y >= p.po_tp) << j;
+                neg |= uint32_t(valid && y <= -p.po_tn) << j;
+            }
+            if (rok) {
+                const int64_t off = row * p.po_ld + n0 / 32;
+                p.po_nz[off] = ternary ? (pos | neg) : pos;
+                if (ternary) p.po_sgn[off] = neg;
+            }
+        } else {
+            // lanes are 32 consecutive elements (kernel rows) of output row n0 + j:
+            // one ballot per column and plane; the (warp-uniform) ballot words go
+            // through the warp's scratch so lane j picks up column j's word.
+            // With a per-lane scale c > 0 the tests run on the exact integer
+            // accumulator against integer thresholds (fl(d * c) is monotonic in d).
+            uint32_t* sc = reinterpret_cast<uint32_t*>(scratch);
+            if (ith) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float acc = __uint_as_float(v[j]);
+                    const uint32_t wp = __ballot_sync(0xffffffffu, rok && acc >= tpi);
+                    sc[j] = wp;
+                    if (ternary) sc[32 + j] = __ballot_sync(0xffffffffu, rok && acc <= tni);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float c = col_scaled ? __shfl_sync(0xffffffffu, cl, j) : crow;
+                    const float y = scaled(v[j], c);
+                    sc[j] = __ballot_sync(0xffffffffu, rok && y >= p.po_tp);
+                    if (ternary) sc[32 + j] = __ballot_sync(0xffffffffu, rok && y <= -p.po_tn);
+                }
+            }
+            __syncwarp();
+            const uint32_t my_pos = sc[lane];
+            const uint32_t my_neg = ternary ? sc[32 + lane] : 0u;
+            __syncwarp();
+            // (a word past the last valid element is padding: zeroed by the host)
+            if (n0 + lane < p.N && mrow0 + q * 32 < p.M) {
+                const int64_t off = (n0 + lane) * p.po_ld + (mrow0 + q * 32) / 32;
+                p.po_nz[off] = ternary ? (my_pos | my_neg) : my_pos;
+                if (ternary) p.po_sgn[off] = my_neg;
+            }
+        }
+    }
+}
+
 template <int BN, int ES, int CG>
 __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& tmY, uint32_t tmem_base, uint8_t* sOut,
                                          float* sScale, uint64_t* tfull, uint64_t* tempty, int q, int h, int lane,
@@ -413,7 +527,9 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
         tc_fence_after();
         TRACE(5, tix, h == 0 && q == 0 && lane == 0);
         const uint32_t tacc = tmem_base + uint32_t(acc * BN);
-        if (ok) {
+        if (p.pack_out) {
+            epi_tile_pack<BN>(p, tacc, reinterpret_cast<uint8_t*>(cs), q, hh, lane, mrow0, nt);
+        } else if (ok) {
             if (p.y_dt == DT_BF16)
                 epi_tile_fast<BN, true>(p, tmY, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix);
             else
@@ -925,6 +1041,13 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     p.scale = a.col_scale;
     p.scale_on_rows = pl.swap ? 1 : 0;
     p.scalar = a.scalar;
+    p.pack_out = a.pack_out;
+    p.po_kind = a.po_kind;
+    p.po_sgn = a.po_sgn;
+    p.po_nz = a.po_nz;
+    p.po_ld = a.po_ld;
+    p.po_tp = a.po_tp;
+    p.po_tn = a.po_tn;
     // output tensor map (TMA store) when the layout allows it
     {
         const int es = (a.y_dt == DT_F16 || a.y_dt == DT_BF16) ? 2 : 4;
@@ -932,7 +1055,8 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
         const int64_t inner = p.out_trans ? pl.Mk : pl.Nk, outer = p.out_trans ? pl.Nk : pl.Mk;
         const uint64_t hsb = bstride(a.nh, a.y_hs * es, ldb_ * outer);
         const uint64_t bsb = bstride(a.nb, a.y_bs * es, hsb * a.nh);
-        bool ok = (reinterpret_cast<uintptr_t>(a.y) % 16 == 0) && ldb_ % 16 == 0 && hsb % 16 == 0 && bsb % 16 == 0 &&
+        bool ok = !a.pack_out && (reinterpret_cast<uintptr_t>(a.y) % 16 == 0) && ldb_ % 16 == 0 && hsb % 16 == 0 &&
+                  bsb % 16 == 0 &&
                   ldb_ < (uint64_t(1) << 40) && hsb < (uint64_t(1) << 40) && bsb < (uint64_t(1) << 40);
         if (ok) {
             const uint64_t dims[4] = {uint64_t(inner), uint64_t(outer), uint64_t(a.nh), uint64_t(a.nb)};

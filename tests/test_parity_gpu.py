@@ -234,6 +234,55 @@ def test_gemm_parity_every_tile(B, tile):
         assert_out_equal(yb, oracle.epilogue_linear(d, s_w.numpy(), s_a, "bf16"), f"{m}x{n}x{k} {tile} bf16")
 
 
+@pytest.mark.parametrize("tile", [None, (64, 1), (192, 2)])
+def test_gemm_pack_fused_equals_gemm_then_pack(B, tile):
+    """bwta_gemm_pack == bwta_pack_act(bwta_gemm(...)) bit-exactly (and == the
+    oracle's quantization of the oracle's Y), both operand orientations,
+    ternary and bool outputs, f16 and bf16 rounding, ragged N (padding bits
+    and padding words), with and without per-channel scales."""
+    for i, (m, n, k, a_kind) in enumerate([(300, 517, 421, "ternary"), (517, 300, 421, "bool"),
+                                           (1000, 130, 300, "ternary"), (64, 2000, 768, "bool")]):
+        a, wp, s_a, s_w, qa, qw = _gemm_case(B, m, n, k, 2700 + i, a_kind)
+        d = oracle.dot(qa, qw, threads=oracle.default_threads())
+        for y_dt, name in ((torch.float16, "f16"), (torch.bfloat16, "bf16")):
+            for sw in (s_w, None):
+                y = B.bwta_gemm(a, wp, None if sw is None else sw.cuda(), s_a, out_dtype=y_dt)
+                yref = oracle.epilogue_linear(d, None if sw is None else sw.numpy(), s_a, name)
+                s_out = float(torch.tensor(2.0) * y.float().abs().mean()) or 1.0
+                for kind in ("ternary", "bool"):
+                    got = B.bwta_gemm_pack(a, wp, None if sw is None else sw.cuda(), s_a, s_out, kind, y_dt,
+                                           design="tcgen05", tile=tile)
+                    ref = B.bwta_pack_act(y, s_out, kind)
+                    assert torch.equal(got.nz, ref.nz), (m, n, k, name, kind)
+                    if kind == "ternary":
+                        assert torch.equal(got.sgn, ref.sgn), (m, n, k, name, kind)
+                    osg, onz, _ = oracle.pack_act(yref, name, s_out, kind)
+                    assert np.array_equal(words(got.nz), onz), (m, n, k, name, kind, "oracle")
+
+
+def test_gemm_pack_rounding_ties(B):
+    """Outputs placed exactly on the f16/bf16 rounding midpoint below the
+    quantization threshold (and one float ulp either side): the fused pack
+    must round-to-nearest-even first, like bwta_gemm + bwta_pack_act."""
+    m, n, k = 256, 192, 300
+    a, wp, s_a, s_w, qa, qw = _gemm_case(B, m, n, k, 2800)
+    d = oracle.dot(qa, qw)
+    for y_dt, name, t in ((torch.float16, "f16", 1.0), (torch.float16, "f16", 1.0009765625),
+                          (torch.bfloat16, "bf16", 1.0), (torch.bfloat16, "bf16", 1.0078125)):
+        prev = float(torch.tensor(t, dtype=y_dt).view(torch.int16).sub(1).view(y_dt).float())
+        mid = (prev + t) / 2
+        for lo in (np.nextafter(np.float32(mid), np.float32(0)), np.float32(mid), np.nextafter(np.float32(mid), np.float32(2))):
+            sw = torch.full((n,), float(lo) / 4.0, dtype=torch.float32)     # y = lo exactly where dot = 4
+            assert (d == 4).sum() > 0
+            for kind in ("ternary", "bool"):
+                got = B.bwta_gemm_pack(a, wp, sw.cuda(), 1.0, 2.0 * t, kind, y_dt, design="tcgen05")
+                y = B.bwta_gemm(a, wp, sw.cuda(), 1.0, out_dtype=y_dt)
+                ref = B.bwta_pack_act(y, 2.0 * t, kind)
+                assert torch.equal(got.nz, ref.nz), (name, t, float(lo), kind)
+                _, onz, _ = oracle.pack_act(oracle.epilogue_linear(d, sw.numpy(), 1.0, name), name, 2.0 * t, kind)
+                assert np.array_equal(words(got.nz), onz), (name, t, float(lo), kind)
+
+
 def test_gemm_tiny_scales(B):
     """Per-channel scales in the subnormal product range still follow R5 exactly."""
     m, n, k = 200, 300, 256
