@@ -140,5 +140,9 @@ cudaError_t launch_matmul_cc(const MatmulArgs& a, cudaStream_t s);
 size_t matmul_tc_workspace(const MatmulArgs& a);
 bool matmul_tc_supported(const MatmulArgs& a);
 cudaError_t launch_matmul_tc(const MatmulArgs& a, void* ws, size_t ws_bytes, cudaStream_t s);
+// skinny products (smaller side <= 32 rows, gemv_tc.cu); launch_matmul_tc
+// routes eligible shapes there
+bool matmul_gemv_eligible(const MatmulArgs& a);
+cudaError_t launch_matmul_gemv(const MatmulArgs& a, cudaStream_t s);
 
 }  // namespace bwta

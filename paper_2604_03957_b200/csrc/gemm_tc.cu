@@ -40,6 +40,7 @@
 
 #include "bwta_internal.h"
 #include "sm100.cuh"
+#include "tc_codes.cuh"
 
 namespace bwta {
 namespace {
@@ -59,7 +60,7 @@ constexpr int UMMA_KB = 32; // bytes of K per tcgen05.mma (K = 64 four-bit eleme
 constexpr int NT = 640;     // 20 warps
 constexpr int OUT_BUF = 4096;
 
-enum BKind { B_BINARY = 0, B_BOOL = 1, B_TERNARY = 2 };  // operand kinds (A or B)
+using namespace tc;
 
 extern __shared__ __align__(16) uint8_t smem_raw[];  // dynamic shared memory of tc_gemm_kernel
 
@@ -137,35 +138,6 @@ struct Cfg {
                   "smem region alignment");
 };
 
-// Operand codes: E2M1 nibbles, +1.0 = 0x2, -1.0 = 0xA, 0 = 0x0, fed to
-// tcgen05.mma.kind::mxf4 with every UE8M0 block scale = 1.0 (0x7F), so each
-// product is exactly q_a * q_w and the f32 accumulator holds the integer dot
-// exactly (|dot| <= K <= 2^24).  K order inside a 32-element group: code word
-// j (j = 0..3, 8 nibbles) holds elements {j, 4+j, ..., 28+j}, nibble i =
-// element 4i + j, so the nz bit of element 4i+j moves to bit 4i+1 and the sgn
-// bit to bit 4i+3 by one shift each (left shifts issued as IMAD.SHL on the FMA
-// pipe).  Both operands use the same permutation, so every dot is unchanged.
-//   binary  (x0 = sgn):           0x2 | sgn << 3            -> +1 / -1
-//   bool    (x0 = nz):            nz << 1                   -> 0 / +1
-//   ternary (x0 = sgn, x1 = nz):  nz << 1 | sgn << 3        -> 0 / +1 / -1
-// (ternary sgn is masked to the canonical subset of nz)
-
-__device__ __forceinline__ uint32_t shl_fma(uint32_t x, int k) {  // x << k as IMAD.SHL (FMA pipe)
-    uint32_t r;
-    asm("mad.lo.u32 %0, %1, %2, 0;" : "=r"(r) : "r"(x), "r"(1u << k));
-    return r;
-}
-// bit 4i+j -> bit 4i+1 (nz) / 4i+3 (sgn)
-__device__ __forceinline__ uint32_t nz_to_bit1(uint32_t x, int j) { return j == 0 ? shl_fma(x, 1) : (j == 1 ? x : x >> (j - 1)); }
-__device__ __forceinline__ uint32_t sg_to_bit3(uint32_t x, int j) { return j == 3 ? x : shl_fma(x, 3 - j); }
-
-template <int KIND>
-__device__ __forceinline__ uint32_t unpack_word(uint32_t x0, uint32_t x1, int j) {
-    if (KIND == B_BINARY) return (sg_to_bit3(x0, j) & 0x88888888u) | 0x22222222u;
-    if (KIND == B_BOOL) return nz_to_bit1(x0, j) & 0x22222222u;
-    return (nz_to_bit1(x1, j) & 0x22222222u) | (sg_to_bit3(x0, j) & 0x88888888u);
-}
-
 // f32 accumulator (the exact integer dot) -> dot / scaled output (R5)
 __device__ __forceinline__ int32_t dot_of(uint32_t acc) { return __float2int_rn(__uint_as_float(acc)); }
 __device__ __forceinline__ float scaled(uint32_t acc, float c) { return __fmul_rn(__uint_as_float(acc), c); }
@@ -179,9 +151,6 @@ __device__ __forceinline__ uint32_t pack2(int dt, float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
-__device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
-}
 
 // ---------------------------------------------------------------------------
 // Epilogue.  8 warps: warp (h, q) (warps 4+q and 12+q) owns TMEM lane quarter
@@ -826,8 +795,10 @@ __global__ void __launch_bounds__(NT, 1)
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
-std::once_flag g_encode_once;
+}  // namespace
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     std::call_once(g_encode_once, [] {
@@ -877,6 +848,8 @@ int64_t kw4_of(int64_t K) { return ((K + 31) / 32 + 3) / 4 * 4; }
 uint64_t bstride(int64_t count, int64_t stride_bytes, uint64_t fallback) {
     return (count <= 1 || stride_bytes <= 0) ? fallback : uint64_t(stride_bytes);
 }
+
+namespace {
 
 struct Plan {
     bool swap;
@@ -974,23 +947,22 @@ bool matmul_tc_supported(const MatmulArgs& a) {
     return encode_fn() != nullptr;
 }
 
-namespace {
 // 4-D tensor map over a packed operand: dims {ld words, rows, heads, batch},
 // box {wps words, box_rows, 1, 1} (one 32*wps-element K slice of box_rows rows)
 bool encode_planes(CUtensorMap* m, const uint32_t* base, int64_t ld, int64_t rows, int64_t hs, int64_t bs,
-                   int64_t nh, int64_t nb, int box_rows, int wps) {
+                   int64_t nh, int64_t nb, int box_rows, int wps, CUtensorMapSwizzle sw) {
     const uint64_t row_b = uint64_t(ld) * 4;
     const uint64_t dims[4] = {uint64_t(ld), uint64_t(rows), uint64_t(nh), uint64_t(nb)};
     const uint64_t hsb = bstride(nh, hs * 4, row_b * rows);
     const uint64_t str[3] = {row_b, hsb, bstride(nb, bs * 4, hsb * nh)};
     const uint32_t box[4] = {uint32_t(wps), uint32_t(box_rows), 1, 1};
     return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<uint32_t*>(base), dims, str, box,
-                  CU_TENSOR_MAP_SWIZZLE_NONE);
+                  sw);
 }
 int kind_of(const uint32_t* sgn, const uint32_t* nz) { return (sgn && nz) ? B_TERNARY : (nz ? B_BOOL : B_BINARY); }
-}  // namespace
 
 cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s) {
+    if (matmul_gemv_eligible(a)) return launch_matmul_gemv(a, s);
     const int64_t entries = a.nb * a.nh;
     const int64_t kw4 = kw4_of(a.K);
     // operand roles and tile shape: the caller's A on the MMA M side (kernel-A)

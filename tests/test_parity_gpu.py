@@ -430,3 +430,81 @@ def test_nshard_gemm_single_rank_matches_full(B):
         w_r = type(wp)(wp.sgn[s0:e0], None, "binary", wp.cols)
         parts.append(B.bwta_gemm(a, w_r, s_w[s0:e0].cuda(), s_a, out_dtype=torch.float16, y_transposed=True))
     assert torch.equal(torch.cat(parts, 0).cpu(), yt.cpu())
+
+
+# --------------------------------------------------- skinny (decode) GEMM ----
+# The smaller side has <= 32 rows -> the skinny tcgen05 kernel (gemv_tc.cu):
+# kernel-A (the large side) codes in TMEM, the small side in shared memory.
+SKINNY = [(1, 300, 1000, "ternary"), (5, 1000, 777, "bool"), (16, 1000, 2048, "ternary"),
+          (17, 517, 300, "bool"), (32, 129, 3000, "ternary"), (2000, 9, 333, "ternary"),
+          (3000, 32, 1000, "bool"), (1, 1, 40, "ternary"), (24, 4100, 96, "ternary")]
+
+
+@pytest.mark.parametrize("case", range(len(SKINNY)))
+def test_gemm_skinny_parity(B, case):
+    m, n, k, a_kind = SKINNY[case]
+    a, wp, s_a, s_w, qa, qw = _gemm_case(B, m, n, k, 4000 + case, a_kind)
+    d = oracle.dot(qa, qw, threads=oracle.default_threads())
+    yi = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.int32)
+    assert np.array_equal(yi.cpu().numpy(), d), (m, n, k, a_kind)
+    for dt, name in ((torch.float16, "f16"), (torch.bfloat16, "bf16"), (torch.float32, "f32")):
+        y = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=dt)
+        assert_out_equal(y, oracle.epilogue_linear(d, s_w.numpy(), s_a, name), f"{m}x{n}x{k} {name}")
+    yt = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.float16, y_transposed=True)
+    assert_out_equal(yt, oracle.epilogue_linear(d, s_w.numpy(), s_a, "f16").T.copy(), "transposed")
+    y1 = B.bwta_gemm(a, wp, None, s_a, out_dtype=torch.float32)
+    assert_out_equal(y1, oracle.epilogue_linear(d, None, s_a, "f32"), "no w_scale")
+    # the general tile kernel (forced tile) gives the same result
+    yg = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.float16, tile=(64, 1))
+    assert torch.equal(yg.view(torch.int16), B.bwta_gemm(a, wp, s_w.cuda(), s_a).view(torch.int16))
+
+
+def test_attention_decode_parity(B):
+    """Decode attention (Tq = 1 and 3): QK^T and PV on the skinny kernel, batched heads."""
+    for i, (b, h, tq, tk, dh) in enumerate([(2, 3, 1, 1000, 128), (1, 4, 3, 300, 64)]):
+        seed = 4500 + 10 * i
+        q = gen.activations((b, h, tq, dh), seed)
+        k = gen.activations((b, h, tk, dh), seed + 1)
+        v = gen.activations((b, h, tk, dh), seed + 2)
+        sq, sk, sv = gen.act_scale(q), gen.act_scale(k), gen.act_scale(v)
+        alpha = float(np.float32(sq * sk / np.sqrt(dh)))
+        qp = B.bwta_pack_act(q.cuda(), sq, "ternary")
+        kp = B.bwta_pack_act(k.cuda(), sk, "ternary")
+        oq = oracle.quantize_act(storage(q).reshape(b * h, tq, dh), "f16", sq, "ternary")
+        ok = oracle.quantize_act(storage(k).reshape(b * h, tk, dh), "f16", sk, "ternary")
+        for dt, name in ((torch.int32, "i32"), (torch.float16, "f16")):
+            s = B.bwta_attn_qk(qp, kp, alpha, out_dtype=dt)
+            assert_out_equal(s, oracle.attn_qk(oq, ok, alpha, name, threads=4).reshape(b, h, tq, tk), f"qk {name}")
+        p = gen.attention_probs((b, h, tq, tk), seed + 3)
+        s_att = float(np.float32(2.0 / tk))
+        beta = float(np.float32(s_att * sv))
+        pp = B.bwta_pack_act(p.cuda(), s_att, "bool")
+        vt = B.bwta_pack_act(v.cuda(), sv, "ternary", transpose=True)
+        op = oracle.quantize_act(storage(p).reshape(b * h, tq, tk), "f16", s_att, "bool")
+        ov = oracle.quantize_act(storage(v).reshape(b * h, tk, dh), "f16", sv, "ternary")
+        for dt, name in ((torch.int32, "i32"), (torch.float16, "f16")):
+            o = B.bwta_attn_pv(pp, vt, beta, out_dtype=dt)
+            assert_out_equal(o, oracle.attn_pv(op, ov, beta, name, threads=4).reshape(b, h, tq, dh), f"pv {name}")
+
+
+@pytest.mark.parametrize("m", [1, 16])
+def test_decode_full_size_sampled(B, m):
+    """configs[4]-shaped decode linear at full size (K = 8192, N = 28672) in the
+    bench's launch configuration; a random sample of 384 output columns (plus the
+    first and last) is checked against the oracle."""
+    k, n = 8192, 28672
+    x = gen.activations((m, k), 5050 + m)
+    w = gen.weights(n, k, 5051)
+    s_a = gen.act_scale(x)
+    mu, s_w = gen.weight_stats(w)
+    a = B.bwta_pack_act(x.cuda(), s_a, "ternary")
+    wp = B.bwta_pack_weight(w.cuda(), mu=mu)
+    y = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.float16)
+    yi = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.int32)
+    cols = np.concatenate([np.random.default_rng(2).choice(n, 384, replace=False), [0, n - 1]])
+    qa = oracle.quantize_act(storage(x), "f16", s_a, "ternary")
+    qw = oracle.binarize_weight(storage(w[torch.from_numpy(cols)]), "f16", mu=mu)
+    d = oracle.dot(qa, qw, threads=oracle.default_threads())
+    assert np.array_equal(yi.cpu().numpy()[:, cols], d)
+    assert_out_equal(y[:, torch.from_numpy(cols).cuda()].contiguous(),
+                     oracle.epilogue_linear(d, s_w.numpy()[cols], s_a, "f16"), "decode")

@@ -68,7 +68,7 @@ int main() {
         }
         cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice);
         for (int cg = 1; cg <= 2; ++cg)
-            for (int n : {64, 128, 192, 256}) {
+            for (int n : {16, 32, 64, 128, 256}) {
                 const int iters = 2000;
                 for (int grid : {cg, 148}) {
                     cudaLaunchConfig_t cfg = {};
