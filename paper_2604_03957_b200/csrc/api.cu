@@ -153,6 +153,16 @@ bwta_status_t run_matmul(const MatmulArgs& a0, void* ws, size_t ws_bytes, const 
     MatmulArgs a = a0;
     a.tile_n = opts->tile_n;
     a.cta_group = opts->cta_group;
+    // decode-sized products (<= 4 rows on one side): the CUDA-core GEMV (design (a)
+    // family) streams the large side at HBM rate; AUTO prefers it unless a tile
+    // shape was forced
+    if (matmul_gemv_cc_eligible(a) && (opts->design == BWTA_DESIGN_CUDA_CORE ||
+                                       (opts->design == BWTA_DESIGN_AUTO && !a.tile_n && !a.cta_group))) {
+        cudaError_t e = launch_matmul_gemv_cc(a, s);
+        if (e != cudaSuccess) return cuda_fail(e);
+        g_last_design = BWTA_DESIGN_CUDA_CORE;
+        return BWTA_OK;
+    }
     bool use_tc = false;
     if (opts->design == BWTA_DESIGN_TCGEN05) {
         if (!matmul_tc_supported(a)) return BWTA_ERR_UNSUPPORTED;

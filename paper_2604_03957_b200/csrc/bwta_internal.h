@@ -144,5 +144,8 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void* ws, size_t ws_bytes, cud
 // routes eligible shapes there
 bool matmul_gemv_eligible(const MatmulArgs& a);
 cudaError_t launch_matmul_gemv(const MatmulArgs& a, cudaStream_t s);
+// decode-sized products (smaller side <= 4 rows) on CUDA cores (gemv_cc.cu)
+bool matmul_gemv_cc_eligible(const MatmulArgs& a);
+cudaError_t launch_matmul_gemv_cc(const MatmulArgs& a, cudaStream_t s);
 
 }  // namespace bwta

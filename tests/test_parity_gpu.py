@@ -435,9 +435,12 @@ def test_nshard_gemm_single_rank_matches_full(B):
 # --------------------------------------------------- skinny (decode) GEMM ----
 # The smaller side has <= 32 rows -> the skinny tcgen05 kernel (gemv_tc.cu):
 # kernel-A (the large side) codes in TMEM, the small side in shared memory.
+# <= 4 rows: also the CUDA-core GEMV (gemv_cc.cu), the AUTO choice there.
 SKINNY = [(1, 300, 1000, "ternary"), (5, 1000, 777, "bool"), (16, 1000, 2048, "ternary"),
           (17, 517, 300, "bool"), (32, 129, 3000, "ternary"), (2000, 9, 333, "ternary"),
-          (3000, 32, 1000, "bool"), (1, 1, 40, "ternary"), (24, 4100, 96, "ternary")]
+          (3000, 32, 1000, "bool"), (1, 1, 40, "ternary"), (24, 4100, 96, "ternary"),
+          (2, 777, 4100, "bool"), (3, 1030, 513, "ternary"), (4, 65, 8192, "ternary"), (1000, 3, 260, "bool"),
+          (700, 1, 129, "ternary")]
 
 
 @pytest.mark.parametrize("case", range(len(SKINNY)))
@@ -454,14 +457,19 @@ def test_gemm_skinny_parity(B, case):
     assert_out_equal(yt, oracle.epilogue_linear(d, s_w.numpy(), s_a, "f16").T.copy(), "transposed")
     y1 = B.bwta_gemm(a, wp, None, s_a, out_dtype=torch.float32)
     assert_out_equal(y1, oracle.epilogue_linear(d, None, s_a, "f32"), "no w_scale")
-    # the general tile kernel (forced tile) gives the same result
-    yg = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.float16, tile=(64, 1))
-    assert torch.equal(yg.view(torch.int16), B.bwta_gemm(a, wp, s_w.cuda(), s_a).view(torch.int16))
+    # every other path gives the same result: the general tile kernel (forced tile), the
+    # tcgen05 skinny kernel, the CUDA-core path (GEMV when <= 4 rows)
+    ref16 = B.bwta_gemm(a, wp, s_w.cuda(), s_a).view(torch.int16)
+    for kw in (dict(tile=(64, 1)), dict(design="tcgen05"), dict(design="cuda_core")):
+        yg = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.float16, **kw)
+        assert torch.equal(yg.view(torch.int16), ref16), kw
+        yi2 = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.int32, **kw)
+        assert np.array_equal(yi2.cpu().numpy(), d), kw
 
 
 def test_attention_decode_parity(B):
     """Decode attention (Tq = 1 and 3): QK^T and PV on the skinny kernel, batched heads."""
-    for i, (b, h, tq, tk, dh) in enumerate([(2, 3, 1, 1000, 128), (1, 4, 3, 300, 64)]):
+    for i, (b, h, tq, tk, dh) in enumerate([(2, 3, 1, 1000, 128), (1, 4, 3, 300, 64), (2, 2, 20, 333, 128)]):
         seed = 4500 + 10 * i
         q = gen.activations((b, h, tq, dh), seed)
         k = gen.activations((b, h, tk, dh), seed + 1)
@@ -472,9 +480,11 @@ def test_attention_decode_parity(B):
         kp = B.bwta_pack_act(k.cuda(), sk, "ternary")
         oq = oracle.quantize_act(storage(q).reshape(b * h, tq, dh), "f16", sq, "ternary")
         ok = oracle.quantize_act(storage(k).reshape(b * h, tk, dh), "f16", sk, "ternary")
-        for dt, name in ((torch.int32, "i32"), (torch.float16, "f16")):
-            s = B.bwta_attn_qk(qp, kp, alpha, out_dtype=dt)
-            assert_out_equal(s, oracle.attn_qk(oq, ok, alpha, name, threads=4).reshape(b, h, tq, tk), f"qk {name}")
+        for design in ("auto", "tcgen05", "cuda_core"):
+            for dt, name in ((torch.int32, "i32"), (torch.float16, "f16")):
+                s = B.bwta_attn_qk(qp, kp, alpha, out_dtype=dt, design=design)
+                assert_out_equal(s, oracle.attn_qk(oq, ok, alpha, name, threads=4).reshape(b, h, tq, tk),
+                                 f"qk {name} {design}")
         p = gen.attention_probs((b, h, tq, tk), seed + 3)
         s_att = float(np.float32(2.0 / tk))
         beta = float(np.float32(s_att * sv))
@@ -482,9 +492,11 @@ def test_attention_decode_parity(B):
         vt = B.bwta_pack_act(v.cuda(), sv, "ternary", transpose=True)
         op = oracle.quantize_act(storage(p).reshape(b * h, tq, tk), "f16", s_att, "bool")
         ov = oracle.quantize_act(storage(v).reshape(b * h, tk, dh), "f16", sv, "ternary")
-        for dt, name in ((torch.int32, "i32"), (torch.float16, "f16")):
-            o = B.bwta_attn_pv(pp, vt, beta, out_dtype=dt)
-            assert_out_equal(o, oracle.attn_pv(op, ov, beta, name, threads=4).reshape(b, h, tq, dh), f"pv {name}")
+        for design in ("auto", "tcgen05", "cuda_core"):
+            for dt, name in ((torch.int32, "i32"), (torch.float16, "f16")):
+                o = B.bwta_attn_pv(pp, vt, beta, out_dtype=dt, design=design)
+                assert_out_equal(o, oracle.attn_pv(op, ov, beta, name, threads=4).reshape(b, h, tq, dh),
+                                 f"pv {name} {design}")
 
 
 @pytest.mark.parametrize("m", [1, 16])
