@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -261,7 +262,8 @@ bwta_status_t prepare_pack(const bwta_pack_desc_t& d, PackArgs& a, bool& empty) 
     const int64_t out_rows = transpose ? cols : rows;
     a.planes_dense = (heads == 1 || p_hstride == out_rows * ld_words) &&
                      (batch == 1 || p_bstride == heads * out_rows * ld_words);
-    a.div_ldw = make_fastdiv(uint32_t(ld_words > 0 && ld_words < (1ll << 31) ? ld_words : 1));
+    a.nwd = std::max<int64_t>(1, (cols + 31) / 32);
+    a.div_nwd = make_fastdiv(uint32_t(a.nwd < (1ll << 31) ? a.nwd : 1));
     a.div_rows = make_fastdiv(uint32_t(rows > 0 && rows < (1ll << 31) ? rows : 1));
     a.div_nh = make_fastdiv(uint32_t(heads < (1ll << 31) ? heads : 1));
     return BWTA_OK;
@@ -330,7 +332,8 @@ bwta_status_t bwta_pack_weight(const void* w, bwta_dtype_t w_dt, int64_t n, int6
     a.mu_per_row = mu_per_row;
     a.vec_ok = aligned16(w) && (ld_w * esize(w_dt)) % 16 == 0;
     a.planes_dense = true;
-    a.div_ldw = make_fastdiv(uint32_t(ld_words > 0 && ld_words < (1ll << 31) ? ld_words : 1));
+    a.nwd = std::max<int64_t>(1, (k + 31) / 32);
+    a.div_nwd = make_fastdiv(uint32_t(a.nwd < (1ll << 31) ? a.nwd : 1));
     a.div_rows = make_fastdiv(uint32_t(n > 0 && n < (1ll << 31) ? n : 1));
     a.div_nh = make_fastdiv(1);
     cudaError_t e = launch_pack_rows(a, (cudaStream_t)stream);

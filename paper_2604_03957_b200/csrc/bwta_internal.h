@@ -90,7 +90,8 @@ struct PackArgs {
     Thresholds th;
     bool vec_ok;  // x rows are 16-byte aligned -> 128-bit loads
     bool planes_dense;  // planes are [entries][rows][ldw] contiguous -> word offset = flat index
-    FastDiv div_ldw, div_rows, div_nh;  // for the 32-bit index path
+    int64_t nwd;        // data words per packed row, max(1, ceil(cols / 32)); lanes own data words only
+    FastDiv div_nwd, div_rows, div_nh;  // for the 32-bit index path
 };
 
 cudaError_t launch_pack_rows(const PackArgs& a, cudaStream_t s);

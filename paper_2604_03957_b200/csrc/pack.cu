@@ -138,7 +138,9 @@ __device__ __forceinline__ uint64_t fdiv(uint64_t n, const FastDiv& f) { return 
 // sectors), compares them with packed-half HSET2 and ORs the results into
 // the word directly -- no cross-lane traffic; 32 lanes store 128 contiguous
 // bytes.  Every lane keeps 2 words in flight and prefetches the next pair
-// before computing.  Padding words (w >= ceil(cols/32)) load nothing.
+// before computing.  Lanes own data words only (w < ceil(cols/32)); the lane of
+// a row's last data word also zeroes its padding words (head_dim 64 rows: 2
+// data + 2 padding words -- no lane idles on padding).
 // ---------------------------------------------------------------------------
 template <typename T> struct WplOf { static constexpr int v = sizeof(T) == 4 ? 1 : 2; };  // words per lane per iteration
 
@@ -157,8 +159,8 @@ __device__ __forceinline__ void pack_rows_body(const PackArgs& p, unsigned vb, u
     constexpr int E = TypeInfo<T>::E;  // elements per 16-byte vector
     constexpr int NV = 32 / E;         // vectors per word
     constexpr int WPL = WplOf<T>::v;
-    const IDX ldw = IDX(p.ldw), rows = IDX(p.rows), nh = IDX(p.nh);
-    const IDX total = IDX(p.nb * p.nh) * rows * ldw;
+    const IDX ldw = IDX(p.ldw), rows = IDX(p.rows), nh = IDX(p.nh), nwd = IDX(p.nwd);
+    const IDX total = IDX(p.nb * p.nh) * rows * nwd;  // data words; their lanes also zero the row's padding
     const IDX cols = IDX(p.cols);
     const IDX nthreads = IDX(vg) * blockDim.x;
     const IDX tid = IDX(vb) * blockDim.x + threadIdx.x;
@@ -167,9 +169,9 @@ __device__ __forceinline__ void pack_rows_body(const PackArgs& p, unsigned vb, u
 #pragma unroll
         for (int u = 0; u < WPL; ++u) {
             const IDX gw = gw0 + IDX(u) * nthreads;
-            const IDX r = fdiv(gw < total ? gw : IDX(0), p.div_ldw);  // flat row (entry*rows + row)
+            const IDX r = fdiv(gw < total ? gw : IDX(0), p.div_nwd);  // flat row (entry*rows + row)
             gr[u] = r;
-            gwv[u] = gw - r * ldw;
+            gwv[u] = gw - r * nwd;
             const IDX c0 = gwv[u] * 32;
 #pragma unroll
             for (int q = 0; q < NV; ++q) v[u][q] = make_uint4(0, 0, 0, 0);
@@ -224,7 +226,7 @@ __device__ __forceinline__ void pack_rows_body(const PackArgs& p, unsigned vb, u
             const IDX r = gr[u];
             int64_t poff;
             if (p.planes_dense) {
-                poff = int64_t(gw);
+                poff = int64_t(r) * int64_t(ldw) + int64_t(gwv[u]);
             } else {
                 const IDX e = fdiv(r, p.div_rows), rr = r - e * rows;
                 const IDX eb = fdiv(e, p.div_nh), eh = e - eb * nh;
@@ -236,6 +238,13 @@ __device__ __forceinline__ void pack_rows_body(const PackArgs& p, unsigned vb, u
                 p.nz[poff] = wn;
                 if (KIND == K_TERNARY) p.sgn[poff] = neg;
                 if (p.row_nnz && wn) atomicAdd(p.row_nnz + r, __popc(wn));
+            }
+            if (gwv[u] + 1 == nwd) {  // the row's last data word: zero the padding words
+                for (IDX w = nwd; w < ldw; ++w) {
+                    const int64_t o = poff + int64_t(w - gwv[u]);
+                    if (KIND == K_BINARY || KIND == K_TERNARY) p.sgn[o] = 0u;
+                    if (KIND != K_BINARY) p.nz[o] = 0u;
+                }
             }
         }
     }
@@ -438,7 +447,7 @@ cudaError_t cols_idx(const PackArgs& a, cudaStream_t s, int grid, bool small) {
 }  // namespace
 
 cudaError_t launch_pack_rows(const PackArgs& a, cudaStream_t s) {
-    const int64_t total_words = a.nb * a.nh * a.rows * a.ldw;
+    const int64_t total_words = a.nb * a.nh * a.rows * a.nwd;
     if (total_words == 0) return cudaSuccess;
     if (a.row_nnz && a.kind != K_BINARY) {
         cudaError_t err = cudaMemsetAsync(a.row_nnz, 0, sizeof(int32_t) * a.nb * a.nh * a.rows, s);
@@ -474,7 +483,7 @@ cudaError_t launch_pack_cols(const PackArgs& a, cudaStream_t s) {
 
 namespace {
 int64_t pack_work(const PackArgs& a, int transpose) {
-    return transpose ? a.nb * a.nh * a.ldw * ((a.cols + 31) / 32) * 32 : a.nb * a.nh * a.rows * a.ldw;
+    return transpose ? a.nb * a.nh * a.ldw * ((a.cols + 31) / 32) * 32 : a.nb * a.nh * a.rows * a.nwd;
 }
 bool pack_small(const PackArgs& a, int transpose, int grid) {
     if (transpose) return pack_work(a, 1) / 32 + int64_t(grid) * 8 < (int64_t(1) << 31);
