@@ -331,6 +331,16 @@ __device__ __forceinline__ void mma_mxf4_ts(uint32_t d_tmem, uint32_t a_tmem, ui
         : "memory");
 }
 
+__device__ __forceinline__ void mma_mxf4_ts_cg2(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t sfa, uint32_t sfb, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+        : "memory");
+}
+
 // Instruction descriptor for kind::mxf4 (block-scaled layout): A/B format
 // E2M1 = 1 at [7,10) / [10,13), both K-major, N >> 3 at [17,23), scale format
 // UE8M0 = 1 at bit 23, M >> 4 at [24,29), scale-factor ids 0, K = 64 (bit 31 = 0).
