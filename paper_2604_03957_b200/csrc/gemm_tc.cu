@@ -115,7 +115,9 @@ template <int BN, int CG, int KS = 256>
 struct Cfg {
     using S = Stage<KS>;
     static constexpr int BNC = BN / CG;          // kernel-B rows held (and unpacked) per CTA
-    static constexpr int A_BYTES = BM * S::ROWB;     // E2M1 codes, 2 per byte
+    // E2M1 codes, 2 per byte; none for 256-K stages (kernel-A codes live in TMEM there), which
+    // deepens the bit/B-code ring (the stage chain TMA -> unpack -> MMA -> commit is latency-bound)
+    static constexpr int A_BYTES = KS == 256 ? 0 : BM * S::ROWB;
     static constexpr int B_BYTES = BNC * S::ROWB;
     static constexpr int ABITS = 2 * BM * S::WPS * 4;  // up to 2 planes x WPS words per row
     static constexpr int BBITS = 2 * BNC * S::WPS * 4;

@@ -12,8 +12,9 @@
 // kernel is bound by ~100 cycles per tcgen05.mma instruction at N <= 128,
 // tools/ubench/mxf4_ubench.cu), so CUDA cores win here.
 //
-// Warp task = RW consecutive large-side rows (RW * MS = 16 outputs, 8 when the
-// large side is ternary).  Lane l owns word quads
+// Warp task = RW consecutive large-side rows (4-8, halved when the large side is
+// ternary); the loads of the next 32-quad iteration are in flight
+// while the current one is counted.  Lane l owns word quads
 // q = l, l + 32, ... (16-byte loads, coalesced 512 B per warp and row); for
 // each quad it loads the small side's quad once (L1-resident, reused across
 // the RW rows) and the RW large-side quads (RW independent 16-byte loads in
@@ -88,8 +89,10 @@ template <int MS, int LP, int SP>
 __global__ void __launch_bounds__(GC_NT, GC_CTAS) cc_gemv_kernel(GcParams p) {
     constexpr bool L_SGN = LP & 1, L_NZ = LP & 2, S_SGN = SP & 1, S_NZ = SP & 2;
     constexpr bool HOIST = !L_NZ;  // m = nz_small: popc(m) summed once per small row
-    constexpr int RW = (L_NZ ? 8 : 16) / MS;
-    constexpr int NV = RW * MS;     // 16 or 8 outputs per task
+    // rows per task: enough to reuse the small side's L1 loads, few enough for two iterations of
+    // large-side loads in registers
+    constexpr int RW = (MS == 1 ? 8 : 4) / (L_NZ ? 2 : 1);
+    constexpr int NV = RW * MS;
     pdl_launch_dependents();
     pdl_wait();
     const int lane = threadIdx.x & 31;
@@ -116,10 +119,26 @@ __global__ void __launch_bounds__(GC_NT, GC_CTAS) cc_gemv_kernel(GcParams p) {
             lsg[r] = L_SGN ? p.l_sgn + o : nullptr;
             lnz[r] = L_NZ ? p.l_nz + o : nullptr;
         }
+        // large side quads of the RW rows for quad iteration qi (RW x 16 B in flight per plane);
+        // the next iteration's loads are issued before the current one is consumed
+        uint4 ls[RW], ln[RW];
+        auto load_large = [&](int qi, uint4 (&s_)[RW], uint4 (&n_)[RW]) {
+            const int q = qi * 32 + lane;
+            const bool qok = q < p.nq;
+#pragma unroll
+            for (int r = 0; r < RW; ++r) {
+                const bool ok = qok && r0 + r < p.L;
+                s_[r] = L_SGN && ok ? ldg_nc4(lsg[r] + 4 * q) : make_uint4(0, 0, 0, 0);
+                n_[r] = L_NZ && ok ? ldg_nc4(lnz[r] + 4 * q) : make_uint4(0, 0, 0, 0);
+            }
+        };
+        load_large(0, ls, ln);
         for (int qi = 0; qi < nqi; ++qi) {
             const int q = qi * 32 + lane;
             const bool qok = q < p.nq;
-            // small side quads (the same for every large row of the task)
+            uint4 lsn[RW], lnn[RW];
+            if (qi + 1 < nqi) load_large(qi + 1, lsn, lnn);
+            // small side quads (the same for every large row of the task; L1-resident)
             uint4 ss[MS], sn[MS];
 #pragma unroll
             for (int m = 0; m < MS; ++m) {
@@ -127,14 +146,6 @@ __global__ void __launch_bounds__(GC_NT, GC_CTAS) cc_gemv_kernel(GcParams p) {
                 const int64_t o = soff + int64_t(m < p.S ? m : 0) * p.lds + 4 * q;
                 ss[m] = S_SGN && ok ? ldg4(p.s_sgn + o) : make_uint4(0, 0, 0, 0);
                 sn[m] = !ok ? make_uint4(0, 0, 0, 0) : S_NZ ? ldg4(p.s_nz + o) : make_uint4(~0u, ~0u, ~0u, ~0u);
-            }
-            // large side quads of the RW rows (all loads first: RW x 16 B in flight per plane)
-            uint4 ls[RW], ln[RW];
-#pragma unroll
-            for (int r = 0; r < RW; ++r) {
-                const bool ok = qok && r0 + r < p.L;
-                ls[r] = L_SGN && ok ? ldg_nc4(lsg[r] + 4 * q) : make_uint4(0, 0, 0, 0);
-                ln[r] = L_NZ && ok ? ldg_nc4(lnz[r] + 4 * q) : make_uint4(0, 0, 0, 0);
             }
             if (HOIST) {
 #pragma unroll
@@ -152,6 +163,13 @@ __global__ void __launch_bounds__(GC_NT, GC_CTAS) cc_gemv_kernel(GcParams p) {
                         cneg[r * MS + m] += __popc(mm & (w_of(ss[m], i) ^ w_of(ls[r], i)));
                         if (!HOIST) cpos[r * MS + m] += __popc(mm);
                     }
+            if (qi + 1 < nqi) {
+#pragma unroll
+                for (int r = 0; r < RW; ++r) {
+                    ls[r] = lsn[r];
+                    ln[r] = lnn[r];
+                }
+            }
         }
         int32_t v[NV];
 #pragma unroll
