@@ -60,6 +60,7 @@ template <int KS> struct Stage {
 constexpr int UMMA_KB = 32; // bytes of K per tcgen05.mma (K = 64 four-bit elements)
 constexpr int NT = 640;     // 20 warps
 constexpr int OUT_BUF = 4096;
+constexpr int OUT_NBUF = 2;  // staging buffers per epilogue warp (fast path: store k overlaps the staging of k + 1)
 
 using namespace tc;
 
@@ -122,7 +123,7 @@ struct Cfg {
     static constexpr int ABITS = 2 * BM * S::WPS * 4;  // up to 2 planes x WPS words per row
     static constexpr int BBITS = 2 * BNC * S::WPS * 4;
     static constexpr int STAGE = A_BYTES + B_BYTES + ABITS + BBITS;
-    static constexpr int OUT_BYTES = 8 * OUT_BUF;                           // one staging buffer per epilogue warp
+    static constexpr int OUT_BYTES = 8 * OUT_NBUF * OUT_BUF;                // OUT_NBUF staging buffers per epilogue warp
     static constexpr int SCALE_COLS = (BN + 127) / 128 * 64;                 // columns per epilogue warp
     static constexpr int SCALE_BYTES = 8 * SCALE_COLS * 4;                  // per-warp column scales
     static constexpr int STAGES_FIT = (210 * 1024 - OUT_BYTES - SCALE_BYTES - TRACE_BYTES) / STAGE;
@@ -274,21 +275,23 @@ __device__ __forceinline__ void epi_tile_generic(const TcParams& p, const CUtens
 // column scales (c * 2^-12, 64 per chunk) when column-scaled; cr = the
 // thread's four row scales (rows 16b + 8i + lane/4) when row-scaled.
 template <int BN, bool BF16>
-__device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorMap& tmY, uint32_t tacc, uint8_t* stg,
+__device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorMap& tmY, uint32_t tacc, uint8_t* stg0,
                                               const float* cs, bool col_scaled, const float (&cr)[4], int q, int h,
-                                              int lane, int64_t mrow0, int nt, int eb, int eh, int tix) {
+                                              int lane, int64_t mrow0, int nt, int eb, int eh, int tix, int& nstore) {
     constexpr int CW = 64;
     const bool tr = h == 0 && q == 0 && lane == 0;
     (void)tr;
     (void)tix;
     const int t0 = lane & 3;
-    const uint32_t sbase = smem_u32(stg);
     // stmatrix addresses: matrix mi = lane/8 (column group offset mi/2, row half mi%2), line li = lane%8
     const int mi = lane >> 3, li = lane & 7;
 #pragma unroll 1
     for (int i = 0, c0 = h * CW; c0 < BN; ++i, c0 += 2 * CW) {
         const int64_t n0 = int64_t(nt) * BN + c0;
         if (n0 >= p.N) break;
+        uint8_t* stg = stg0 + (nstore % OUT_NBUF) * OUT_BUF;
+        const uint32_t sbase = smem_u32(stg);
+        ++nstore;
 #pragma unroll
         for (int b = 0; b < 2; ++b) {  // 16-lane block b: rows 16b .. 16b+15 of the warp's 32
             uint32_t v[32];
@@ -316,7 +319,7 @@ __device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorM
             }
             if (b == 0) {
                 TRACE(13, tix * 4 + i, tr);
-                if (lane == 0) bulk_wait_read<0>();  // the previous store has read the buffer
+                if (lane == 0) bulk_wait_read<OUT_NBUF - 1>();  // the store that last used this buffer has read it
                 __syncwarp();
                 TRACE(14, tix * 4 + i, tr);
             }
@@ -459,7 +462,8 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
                                          float* sScale, uint64_t* tfull, uint64_t* tempty, int q, int h, int lane,
                                          int64_t tiles_per_entry, int64_t total, int rank, int64_t t0,
                                          int64_t tstep) {
-    uint8_t* stg = sOut + (h * 4 + q) * OUT_BUF;
+    uint8_t* stg = sOut + (h * 4 + q) * OUT_NBUF * OUT_BUF;
+    int nstore = 0;  // fast path: chunks stored by this warp (selects the staging buffer)
     float* cs = sScale + (h * 4 + q) * Cfg<BN, CG>::SCALE_COLS;
     const bool fast_ok = ES == 2 && p.use_tma_store;
     const bool col_scaled = !p.scale_on_rows && p.scale;
@@ -508,9 +512,11 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
             epi_tile_pack<BN>(p, tacc, reinterpret_cast<uint8_t*>(cs), q, hh, lane, mrow0, nt);
         } else if (ok) {
             if (p.y_dt == DT_BF16)
-                epi_tile_fast<BN, true>(p, tmY, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix);
+                epi_tile_fast<BN, true>(p, tmY, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix,
+                                        nstore);
             else
-                epi_tile_fast<BN, false>(p, tmY, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix);
+                epi_tile_fast<BN, false>(p, tmY, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix,
+                                         nstore);
         } else {
             epi_tile_generic<BN, ES>(p, tmY, tacc, stg, q, hh, lane, mrow0, nt, eb, eh);
         }
