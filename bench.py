@@ -180,7 +180,7 @@ class Op:
 
 
 def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=3072, fuse_ffn=True,
-               qkv_packs="overlap"):
+               qkv_packs="overlap", fuse_ctx=True):
     """configs[1]: BERT-base layer, seq 128, batch 32 (M = 4096 tokens)."""
     M, D = batch * seq, hidden // heads
     g = lambda s: s + seed  # noqa: E731
@@ -259,6 +259,9 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
     def op_pv():
         B.bwta_attn_pv(st["pp"], st["vt"], s["beta"], out=ctx_v)
 
+    def op_pv_pack():  # PV emitting the O-projection's ternary input planes (fused pack, no ctx write)
+        st["cq"] = B.bwta_attn_pv_pack(st["pp"], st["vt"], s["beta"], s["ctx"], "ternary")
+
     def op_pack_ctx():
         st["cq"] = B.bwta_pack_act(ctx, s["ctx"])
 
@@ -310,9 +313,14 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
         Op("attn_qk", "qk", op_qk, mm(batch * heads * seq, seq, D),
            2 * batch * heads * seq * D / 4 + 2 * batch * heads * seq * seq, cub["qk"]),
         Op("pack_p", "pack", op_pack_p, 0, pk(batch * heads * seq * seq, 1)),
+    ] + ([
+        Op("attn_pv_pack", "pv", op_pv_pack, mm(batch * heads * seq, D, seq),
+           batch * heads * seq * seq / 8 + batch * heads * D * seq / 4 + M * hidden / 4, cub["pv"]),
+    ] if fuse_ctx else [
         Op("attn_pv", "pv", op_pv, mm(batch * heads * seq, D, seq),
            batch * heads * seq * seq / 8 + batch * heads * D * seq / 4 + 2 * M * hidden, cub["pv"]),
         Op("pack_ctx", "pack", op_pack_ctx, 0, pk(M * hidden, 2)),
+    ]) + [
         Op("gemm_o", "gemm", op_o, mm(M, hidden, hidden),
            M * hidden / 4 + hidden * hidden / 8 + 2 * M * hidden, cub["o"]),
         Op("pack_xf", "pack", op_pack_xf, 0, pk(M * hidden, 2)),

@@ -287,6 +287,29 @@ BWTA_API bwta_status_t bwta_attn_pv(const uint32_t* p_sgn, const uint32_t* p_nz,
                            void* workspace, size_t workspace_bytes,
                            const bwta_opts_t* opts, void* stream);
 
+/* ---- attention PV with the next layer's pack fused into the epilogue ----- */
+/*
+ * bwta_pack_act(C, out_scale, out_kind) of the attention context
+ *   C[b, t, h*dh + d] = round_{o_dt}(O_{b,h}[t][d]),   O as bwta_attn_pv computes it
+ * (P:969-975 then P:911-930): the O-projection's input planes come
+ * straight out of the PV epilogue, O is never written.  Output planes: batch*tq rows
+ * (token-major, b then t) of out_ld_words words, head h owning words
+ * [h dh/32, (h+1) dh/32) of every row -- exactly the planes bwta_pack_act writes for
+ * the [batch*tq, heads*dh] context.  Requires dh % 32 == 0, o_dt F16 | BF16,
+ * out_kind TERNARY | BOOL, out_ld_words >= bwta_ld_words(heads*dh) (padding words are
+ * zeroed by a memset on `stream`), design (b); the products the skinny kernels serve
+ * (<= 32 rows on one side) return BWTA_ERR_UNSUPPORTED.  Other arguments and errors
+ * as bwta_attn_pv.
+ */
+BWTA_API bwta_status_t bwta_attn_pv_pack(const uint32_t* p_sgn, const uint32_t* p_nz,
+                           const uint32_t* vt_sgn, const uint32_t* vt_nz,
+                           int64_t batch, int64_t heads, int64_t tq, int64_t tk, int64_t dh,
+                           int64_t ldp_words, int64_t p_bstride, int64_t p_hstride,
+                           int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
+                           float beta, bwta_dtype_t o_dt, float out_scale, bwta_kind_t out_kind,
+                           uint32_t* out_sgn, uint32_t* out_nz, int64_t out_ld_words,
+                           const bwta_opts_t* opts, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,7 @@ from . import _native as N
 from ._native import lib
 
 __all__ = ["Packed", "BwtaError", "bwta_ld_words", "bwta_pack_act", "bwta_pack_weight",
-           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "last_design", "lib"]
+           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "bwta_attn_pv_pack", "last_design", "lib"]
 
 
 class BwtaError(RuntimeError):
@@ -291,3 +291,29 @@ def bwta_attn_pv(p: Packed, vt: Packed, beta: float, out_dtype=torch.float16,
                           _stream(stream))
     _check(st, "bwta_attn_pv")
     return out
+
+
+def bwta_attn_pv_pack(p: Packed, vt: Packed, beta: float, out_scale: float, out_kind: str = "ternary",
+                      o_dtype=torch.float16, design: str = "auto", stream=None, tile=None) -> Packed:
+    """bwta_pack_act(C, out_scale, out_kind) of the attention context C[b, t, h*Dh + d] =
+    round(O_{b,h}[t][d]) with the pack fused into the PV epilogue (O is never written):
+    the O-projection's input planes [B*Tq, ld(H*Dh)].  p / vt as bwta_attn_pv, 4-D
+    [B, H, ...] (or 3-D [H, ...] / 2-D)."""
+    if out_kind not in ("ternary", "bool"):
+        raise ValueError("out_kind must be 'ternary' or 'bool'")
+    pr, vr = p.ref, vt.ref
+    b, h, pbs, phs = _batch_dims(pr)
+    _, _, vbs, vhs = _batch_dims(vr)
+    tq, dh, tk = pr.shape[-2], vr.shape[-2], p.cols
+    if vt.cols != tk or vt.kind != "ternary":
+        raise ValueError("V^T must be ternary planes over the same Tk as P")
+    ldo = bwta_ld_words(h * dh)
+    nz = torch.empty((b * tq, ldo), dtype=torch.int32, device=pr.device)
+    sgn = torch.empty((b * tq, ldo), dtype=torch.int32, device=pr.device) if out_kind == "ternary" else None
+    p_sgn = p.sgn if p.kind == "ternary" else None
+    st = lib.bwta_attn_pv_pack(_ptr(p_sgn), _ptr(p.nz), _ptr(vt.sgn), _ptr(vt.nz), b, h, tq, tk, dh,
+                               pr.stride(-2), pbs, phs, vr.stride(-2), vbs, vhs, ctypes.c_float(beta),
+                               _DT[o_dtype], ctypes.c_float(out_scale), _KIND[out_kind], _ptr(sgn), _ptr(nz), ldo,
+                               _opts(design, tile), _stream(stream))
+    _check(st, "bwta_attn_pv_pack")
+    return Packed(sgn, nz, out_kind, h * dh)

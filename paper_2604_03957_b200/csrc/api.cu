@@ -546,6 +546,82 @@ size_t bwta_attn_pv_workspace_size(int64_t batch_heads, int64_t tq, int64_t tk, 
     return matmul_tc_supported(a) ? matmul_tc_workspace(a) : 0;
 }
 
+bwta_status_t bwta_attn_pv_pack(const uint32_t* p_sgn, const uint32_t* p_nz, const uint32_t* vt_sgn,
+                                const uint32_t* vt_nz, int64_t batch, int64_t heads, int64_t tq, int64_t tk, int64_t dh,
+                                int64_t ldp_words, int64_t p_bstride, int64_t p_hstride, int64_t ldv_words,
+                                int64_t v_bstride, int64_t v_hstride, float beta, bwta_dtype_t o_dt, float out_scale,
+                                bwta_kind_t out_kind, uint32_t* out_sgn, uint32_t* out_nz, int64_t out_ld_words,
+                                const bwta_opts_t* opts, void* stream) {
+    if (o_dt != BWTA_F16 && o_dt != BWTA_BF16) return BWTA_ERR_UNSUPPORTED;
+    if (out_kind != BWTA_TERNARY && out_kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
+    bwta_status_t st = check_batch(batch, heads);
+    if (st != BWTA_OK) return st;
+    if (tq < 0 || tk < 0 || dh < 0 || tk > KMAX) return BWTA_ERR_SHAPE;
+    if (batch == 0 || tq == 0 || dh == 0) return BWTA_OK;
+    if (p_nz == nullptr || vt_sgn == nullptr || vt_nz == nullptr || out_nz == nullptr) return BWTA_ERR_INVALID_VALUE;
+    if ((out_kind == BWTA_TERNARY) != (out_sgn != nullptr)) return BWTA_ERR_INVALID_VALUE;
+    if (!std::isfinite(beta) || !scale_ok_pos(out_scale)) return BWTA_ERR_INVALID_VALUE;
+    if (dh % 32) return BWTA_ERR_UNSUPPORTED;  // a head must own whole words of the context row
+    const int64_t need = ldw_of(tk);
+    if (ldp_words < need || ldv_words < need || out_ld_words < ldw_of(heads * dh)) return BWTA_ERR_SHAPE;
+    if (p_bstride < 0 || p_hstride < 0 || v_bstride < 0 || v_hstride < 0) return BWTA_ERR_SHAPE;
+    if (ldp_words % 4 || ldv_words % 4 || out_ld_words % 4 || p_bstride % 4 || p_hstride % 4 || v_bstride % 4 ||
+        v_hstride % 4 || !aligned16(p_nz) || (p_sgn && !aligned16(p_sgn)) || !aligned16(vt_sgn) ||
+        !aligned16(vt_nz) || !aligned16(out_nz) || (out_sgn && !aligned16(out_sgn)))
+        return BWTA_ERR_ALIGNMENT;
+    const bwta_opts_t* o = opts_or_default(opts);
+    if (o->design == BWTA_DESIGN_CUDA_CORE) return BWTA_ERR_UNSUPPORTED;  // fused pack: design (b) only
+    for (int r : o->reserved)
+        if (r != 0) return BWTA_ERR_INVALID_VALUE;
+    st = check_device();
+    if (st != BWTA_OK) return st;
+    MatmulArgs a{};
+    a.a_sgn = p_sgn;
+    a.a_nz = p_nz;
+    a.b_sgn = vt_sgn;
+    a.b_nz = vt_nz;
+    a.M = tq;
+    a.N = dh;
+    a.K = tk;
+    a.lda = ldp_words;
+    a.ldb = ldv_words;
+    a.a_bs = p_bstride;
+    a.a_hs = p_hstride;
+    a.b_bs = v_bstride;
+    a.b_hs = v_hstride;
+    a.nb = batch;
+    a.nh = heads;
+    a.y_dt = o_dt;
+    a.scalar = beta;
+    a.pack_out = 1;
+    a.po_kind = out_kind;
+    a.po_sgn = out_sgn;
+    a.po_nz = out_nz;
+    a.po_ld = out_ld_words;           // one packed row per token (b, t): the heads' contexts concatenated
+    a.po_bs = tq * out_ld_words;
+    a.po_hs = dh / 32;                // head h owns words [h dh / 32, (h + 1) dh / 32) of the row
+    const double t = 0.5 * double(out_scale);  // exact
+    const bool bf = o_dt == BWTA_BF16;
+    a.po_tp = rounding_threshold(smallest_pattern(t, false, bf), bf);
+    a.po_tn = rounding_threshold(smallest_pattern(t, true, bf), bf);
+    a.tile_n = o->tile_n;
+    a.cta_group = o->cta_group;
+    if (!matmul_tc_supported(a) || matmul_gemv_eligible(a)) return BWTA_ERR_UNSUPPORTED;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (out_ld_words * 32 > heads * dh) {
+        // padding words of the context rows: no head writes them
+        const size_t bytes = sizeof(uint32_t) * size_t(batch) * size_t(tq) * size_t(out_ld_words);
+        cudaError_t e = cudaMemsetAsync(out_nz, 0, bytes, s);
+        if (e == cudaSuccess && out_sgn) e = cudaMemsetAsync(out_sgn, 0, bytes, s);
+        if (e != cudaSuccess) return cuda_fail(e);
+        count_launch(out_sgn ? 2 : 1);
+    }
+    cudaError_t e = launch_matmul_tc(a, nullptr, 0, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_last_design = BWTA_DESIGN_TCGEN05;
+    return BWTA_OK;
+}
+
 bwta_status_t bwta_attn_pv(const uint32_t* p_sgn, const uint32_t* p_nz, const uint32_t* vt_sgn, const uint32_t* vt_nz,
                            int64_t batch, int64_t heads, int64_t tq, int64_t tk, int64_t dh, int64_t ldp_words,
                            int64_t p_bstride, int64_t p_hstride, int64_t ldv_words, int64_t v_bstride,

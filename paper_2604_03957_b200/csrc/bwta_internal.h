@@ -131,6 +131,7 @@ struct MatmulArgs {
     uint32_t* po_sgn = nullptr;
     uint32_t* po_nz = nullptr;
     int64_t po_ld = 0;        // words per packed row (rows = the M rows of Y)
+    int64_t po_bs = 0, po_hs = 0;  // words between the planes of consecutive batch / head entries
     float po_tp = 0.f, po_tn = 0.f;  // +1 iff y >= po_tp; -1 iff y <= -po_tn (exact storage values)
 };
 

@@ -107,6 +107,7 @@ struct TcParams {
     uint32_t* po_sgn;
     uint32_t* po_nz;
     int64_t po_ld;
+    int64_t po_bs, po_hs;  // words between the planes of consecutive batch / head entries
     float po_tp, po_tn;
 };
 
@@ -375,7 +376,7 @@ __device__ __forceinline__ float int_threshold_ge(float t, float c) {
 
 template <int BN>
 __device__ __forceinline__ void epi_tile_pack(const TcParams& p, uint32_t tacc, uint8_t* scratch, int q, int h,
-                                              int lane, int64_t mrow0, int nt) {
+                                              int lane, int64_t mrow0, int nt, int64_t eoff) {
     const bool ternary = p.po_kind == K_TERNARY;
     const int64_t row = mrow0 + q * 32 + lane;  // kernel row of this thread
     const bool rok = row < p.M;
@@ -415,7 +416,7 @@ __device__ __forceinline__ void epi_tile_pack(const TcParams& p, uint32_t tacc, 
                 neg |= uint32_t(valid && y <= -p.po_tn) << j;
             }
             if (rok) {
-                const int64_t off = row * p.po_ld + n0 / 32;
+                const int64_t off = eoff + row * p.po_ld + n0 / 32;
                 p.po_nz[off] = ternary ? (pos | neg) : pos;
                 if (ternary) p.po_sgn[off] = neg;
             }
@@ -449,7 +450,7 @@ __device__ __forceinline__ void epi_tile_pack(const TcParams& p, uint32_t tacc, 
             __syncwarp();
             // (a word past the last valid element is padding: zeroed by the host)
             if (n0 + lane < p.N && mrow0 + q * 32 < p.M) {
-                const int64_t off = (n0 + lane) * p.po_ld + (mrow0 + q * 32) / 32;
+                const int64_t off = eoff + (n0 + lane) * p.po_ld + (mrow0 + q * 32) / 32;
                 p.po_nz[off] = ternary ? (my_pos | my_neg) : my_pos;
                 if (ternary) p.po_sgn[off] = my_neg;
             }
@@ -509,7 +510,8 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
         TRACE(5, tix, h == 0 && q == 0 && lane == 0);
         const uint32_t tacc = tmem_base + uint32_t(acc * BN);
         if (p.pack_out) {
-            epi_tile_pack<BN>(p, tacc, reinterpret_cast<uint8_t*>(cs), q, hh, lane, mrow0, nt);
+            epi_tile_pack<BN>(p, tacc, reinterpret_cast<uint8_t*>(cs), q, hh, lane, mrow0, nt,
+                              int64_t(eb) * p.po_bs + int64_t(eh) * p.po_hs);
         } else if (ok) {
             if (p.y_dt == DT_BF16)
                 epi_tile_fast<BN, true>(p, tmY, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix,
@@ -1093,6 +1095,8 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     p.po_sgn = a.po_sgn;
     p.po_nz = a.po_nz;
     p.po_ld = a.po_ld;
+    p.po_bs = a.po_bs;
+    p.po_hs = a.po_hs;
     p.po_tp = a.po_tp;
     p.po_tn = a.po_tn;
     // output tensor map (TMA store) when the layout allows it

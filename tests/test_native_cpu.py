@@ -146,3 +146,28 @@ def test_product_package_never_touches_the_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
                 assert "bwta_oracle" not in text and "liborc" not in text, f
+
+
+def test_attn_pv_pack_validation(N):
+    """bwta_attn_pv_pack: host validation before any device work (no GPU here)."""
+    L = N.lib
+
+    def pvp(**kw):
+        a = dict(p_sgn=None, p_nz=32, vs=48, vn=64, b=1, h=2, tq=4, tk=100, dh=64, ldp=4, ldv=4, beta=0.1,
+                 o_dt=0, s_o=1.0, kind=2, o_sgn=80, o_nz=96, ldo=4)
+        a.update(kw)
+        return L.bwta_attn_pv_pack(a["p_sgn"], a["p_nz"], a["vs"], a["vn"], a["b"], a["h"], a["tq"], a["tk"],
+                                   a["dh"], a["ldp"], 0, 0, a["ldv"], 0, 0, ctypes.c_float(a["beta"]), a["o_dt"],
+                                   ctypes.c_float(a["s_o"]), a["kind"], a["o_sgn"], a["o_nz"], a["ldo"], None, None)
+    assert pvp() == 4                       # valid, but no sm_100 device here
+    assert pvp(dh=48) == 4                  # a head must own whole words of the context row
+    assert pvp(o_dt=2) == 4                 # fused pack rounds to f16 / bf16 only
+    assert pvp(kind=0) == 4                 # the next layer's activations are ternary or bool
+    assert pvp(o_nz=None) == 1
+    assert pvp(kind=1) == 1                 # BOOL output has no sgn plane
+    assert pvp(s_o=0.0) == 1
+    assert pvp(s_o=float("inf")) == 1
+    assert pvp(ldo=0) == 2                  # < bwta_ld_words(heads * dh)
+    assert pvp(ldp=0) == 2
+    assert pvp(o_nz=100) == 3               # 16-byte alignment
+    assert pvp(b=0) == 0                    # empty problem

@@ -520,3 +520,41 @@ def test_decode_full_size_sampled(B, m):
     assert np.array_equal(yi.cpu().numpy()[:, cols], d)
     assert_out_equal(y[:, torch.from_numpy(cols).cuda()].contiguous(),
                      oracle.epilogue_linear(d, s_w.numpy()[cols], s_a, "f16"), "decode")
+
+
+# ------------------------------------------------ PV with the context pack fused ----
+@pytest.mark.parametrize("kind", ["ternary", "bool"])
+@pytest.mark.parametrize("o_dtype", [torch.float16, torch.bfloat16])
+def test_attn_pv_pack_equals_pv_then_pack(B, kind, o_dtype):
+    """bwta_attn_pv_pack == bwta_pack_act(context of bwta_attn_pv) bit-exactly, and == the
+    oracle's quantization of the oracle's rounded context; the heads' words interleave in
+    the token rows, ragged Tq/Tk, several tile shapes."""
+    for i, (b, h, tq, tk, dh) in enumerate([(2, 3, 37, 41, 64), (1, 2, 130, 129, 128), (4, 12, 128, 128, 64),
+                                            (1, 5, 200, 300, 32)]):
+        seed = 6000 + 10 * i
+        v = gen.activations((b, h, tk, dh), seed)
+        p = gen.attention_probs((b, h, tq, tk), seed + 1)
+        sv = gen.act_scale(v)
+        s_att = float(np.float32(2.0 / tk))
+        beta = float(np.float32(s_att * sv))
+        pp = B.bwta_pack_act(p.cuda(), s_att, "bool")
+        vt = B.bwta_pack_act(v.cuda(), sv, "ternary", transpose=True)
+        o = B.bwta_attn_pv(pp, vt, beta, out_dtype=o_dtype)
+        ctx = o.transpose(1, 2).reshape(b * tq, h * dh).contiguous()
+        s_ctx = gen.act_scale(ctx) or 1.0
+        ref = B.bwta_pack_act(ctx, s_ctx, kind)
+        for tile in (None, (64, 1), (128, 2)):
+            got = B.bwta_attn_pv_pack(pp, vt, beta, s_ctx, kind, o_dtype=o_dtype, tile=tile)
+            assert torch.equal(got.nz, ref.nz), (b, h, tq, tk, dh, tile)
+            if kind == "ternary":
+                assert torch.equal(got.sgn, ref.sgn), (b, h, tq, tk, dh, tile)
+        # oracle: PV in the oracle, rounded to o_dtype, quantized with the oracle's pack
+        op = oracle.quantize_act(storage(p).reshape(b * h, tq, tk), "f16", s_att, "bool")
+        ov = oracle.quantize_act(storage(v).reshape(b * h, tk, dh), "f16", sv, "ternary")
+        name = DT[o_dtype]
+        oo = oracle.attn_pv(op, ov, beta, name, threads=4).reshape(b, h, tq, dh)
+        octx = np.ascontiguousarray(oo.transpose(0, 2, 1, 3).reshape(b * tq, h * dh))
+        sgn, nz, _ = oracle.pack_act(octx, name, s_ctx, kind)
+        assert np.array_equal(words(got.nz), nz)
+        if kind == "ternary":
+            assert np.array_equal(words(got.sgn), sgn)
