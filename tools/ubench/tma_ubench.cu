@@ -26,7 +26,8 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 }
 
 __global__ void __launch_bounds__(64, 1) kern(const __grid_constant__ CUtensorMap m0, const __grid_constant__ CUtensorMap m1,
-                                              const __grid_constant__ CUtensorMap m4, const uint32_t* w, int ld, int mode,
+                                              const __grid_constant__ CUtensorMap m4, const __grid_constant__ CUtensorMap m8,
+                                              const uint32_t* w, int ld, int mode,
                                               int slabs_per_cta, unsigned long long* out) {
     extern __shared__ __align__(1024) uint8_t raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
@@ -58,8 +59,10 @@ __global__ void __launch_bounds__(64, 1) kern(const __grid_constant__ CUtensorMa
                     bulk_g2s(smem_u32(dst + r * 128), w + size_t(slab * 128 + r) * ld + j * 32, 128, &full[s]);
             } else if (mode == 3) {
                 if (lane == 0) bulk_g2s(smem_u32(dst), w + size_t(slab) * 128 * ld + size_t(j) * (STAGE / 4), STAGE, &full[s]);
-            } else {
+            } else if (mode == 4) {
                 if (lane == 0) tma_load_4d(dst, &m4, &full[s], (j % 4) * 64, slab * 128 + (j / 4) * 64, 0, 0);
+            } else {  // mode 5: four 8-word x 128-row boxes (32 B per row, the tile kernel's 256-K slices)
+                if (lane < 4) tma_load_4d(dst + lane * 4096, &m8, &full[s], (j * 4 + lane) * 8, slab * 128, 0, 0);
             }
         }
     } else if (lane == 0) {
@@ -91,19 +94,19 @@ int main() {
     PFN_cuTensorMapEncodeTiled_v12000 enc;
     cudaDriverEntryPointQueryResult q;
     cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
-    CUtensorMap m[3];
-    const uint32_t boxes[3][2] = {{32, 128}, {32, 32}, {64, 64}};
-    for (int i = 0; i < 3; ++i) {
+    CUtensorMap m[4];
+    const uint32_t boxes[4][2] = {{32, 128}, {32, 32}, {64, 64}, {8, 128}};
+    for (int i = 0; i < 4; ++i) {
         cuuint64_t d[4] = {cuuint64_t(ld), cuuint64_t(N), 1, 1};
         cuuint64_t st[3] = {cuuint64_t(ld) * 4, cuuint64_t(ld) * 4 * N, cuuint64_t(ld) * 4 * N};
         cuuint32_t b[4] = {boxes[i][0], boxes[i][1], 1, 1}, es[4] = {1, 1, 1, 1};
         CUresult r = enc(&m[i], CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, w, d, st, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         i == 2 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         i >= 2 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) { printf("encode %d failed %d\n", i, r); return 1; }
     }
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, STAGES * STAGE + 1024);
-    const char* names[5] = {"2D box 32w x 128r", "2D box 32w x 32r x4", "1D bulk 128 B x 128 rows", "1D bulk 16 KB contiguous", "2D box 64w x 64r"};
+    const char* names[6] = {"2D box 32w x 128r", "2D box 32w x 32r x4", "1D bulk 128 B x 128 rows", "1D bulk 16 KB contiguous", "2D box 64w x 64r", "2D box 8w x 128r x4"};
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     for (int carve = 0; carve <= 0; ++carve) {
     // carve = 1: the flush kernel asks for the max shared-memory carveout too,
@@ -111,13 +114,13 @@ int main() {
     cudaFuncSetAttribute(readflush, cudaFuncAttributePreferredSharedMemoryCarveout, carve ? 100 : -1);
     printf("flush kernel carveout %s\n", carve ? "max shared" : "default");
     for (int g : {1, 8, 148})
-    for (int mode = 0; mode < 5; ++mode) {
+    for (int mode = 0; mode < 6; ++mode) {
         if (mode == 2) continue;
         for (int rep = 0; rep < 3; ++rep) {
             if (rep < 2) cudaMemset(fl, rep, 512 << 20);  // (dirty L2) ...
             readflush<<<592, 512>>>(reinterpret_cast<const uint4*>(fl), (512u << 20) / 16, reinterpret_cast<unsigned*>(o));  // ... evicted clean
             cudaEventRecord(e0);
-            kern<<<g, 64, STAGES * STAGE + 1024>>>(m[0], m[1], m[2], w, ld, mode, slabs_per_cta, o);
+            kern<<<g, 64, STAGES * STAGE + 1024>>>(m[0], m[1], m[2], m[3], w, ld, mode, slabs_per_cta, o);
             cudaEventRecord(e1);
             if (cudaDeviceSynchronize() != cudaSuccess) { printf("error %s\n", cudaGetErrorString(cudaGetLastError())); return 1; }
             float ms; cudaEventElapsedTime(&ms, e0, e1);
