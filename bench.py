@@ -180,7 +180,7 @@ class Op:
 
 
 def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=3072, fuse_ffn=True,
-               qkv_packs="overlap", fuse_ctx=True):
+               qkv_packs="overlap_sep", fuse_ctx=True):
     """configs[1]: BERT-base layer, seq 128, batch 32 (M = 4096 tokens)."""
     M, D = batch * seq, hidden // heads
     g = lambda s: s + seed  # noqa: E731
@@ -228,12 +228,15 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
     def op_pack_qkv():  # the per-head Q, K and V^T packs (one launch by default)
         qa, ka, va = ((heads_view(qkv, 0), s["q"], "ternary", False), (heads_view(qkv, 1), s["k"], "ternary", False),
                       (heads_view(qkv, 2), s["v"], "ternary", True))
-        if qkv_packs == "overlap":
-            # Q + K packs (one launch) on the step's stream; the V^T pack -- needed only by PV --
-            # on a side stream, so it overlaps the Q/K pack and the QK^T kernel (joined before PV)
+        if qkv_packs in ("overlap", "overlap_sep"):
+            # Q + K packs (one launch, or two) on the step's stream; the V^T pack -- needed only by
+            # PV -- on a side stream, so it overlaps the Q/K packs and QK^T (joined before PV)
             cur = torch.cuda.current_stream()
             side.wait_stream(cur)
-            st["qp"], st["kp"] = B.bwta_pack_act_batch([qa, ka])
+            if qkv_packs == "overlap":
+                st["qp"], st["kp"] = B.bwta_pack_act_batch([qa, ka])
+            else:
+                st["qp"], st["kp"] = (B.bwta_pack_act(x[0], x[1]) for x in (qa, ka))
             with torch.cuda.stream(side):
                 st["vt"] = B.bwta_pack_act(va[0], va[1], transpose=True)
             if st.get("defer_join"):
