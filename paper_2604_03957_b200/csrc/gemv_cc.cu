@@ -12,7 +12,7 @@
 // kernel is bound by ~100 cycles per tcgen05.mma instruction at N <= 128,
 // tools/ubench/mxf4_ubench.cu), so CUDA cores win here.
 //
-// Warp task = RW consecutive large-side rows (4-8, halved when the large side is
+// Warp task = RW consecutive large-side rows (4, halved when the large side is
 // ternary); the loads of the next 32-quad iteration are in flight
 // while the current one is counted.  Lane l owns word quads
 // q = l, l + 32, ... (16-byte loads, coalesced 512 B per warp and row); for
@@ -29,7 +29,9 @@ namespace bwta {
 namespace {
 
 constexpr int GC_NT = 256;    // 8 warps per CTA
-constexpr int GC_CTAS = 2;    // CTAs per SM (<= 128 registers per thread)
+// CTAs per SM: 3 (<= 85 registers) for 1-2 small rows -- more warps in flight and an even
+// spread of the 4-row tasks -- and 2 (<= 128 registers) for 3-4 rows
+__host__ __device__ constexpr int gc_ctas(int ms) { return ms <= 2 ? 3 : 2; }
 
 struct GcParams {
     const uint32_t *l_sgn, *l_nz;  // large side (kernel rows): null plane = absent
@@ -86,12 +88,12 @@ __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x
 
 // LP / SP: large / small plane presence (bit 0 sgn, bit 1 nz); RW large rows per warp task
 template <int MS, int LP, int SP>
-__global__ void __launch_bounds__(GC_NT, GC_CTAS) cc_gemv_kernel(GcParams p) {
+__global__ void __launch_bounds__(GC_NT, gc_ctas(MS)) cc_gemv_kernel(GcParams p) {
     constexpr bool L_SGN = LP & 1, L_NZ = LP & 2, S_SGN = SP & 1, S_NZ = SP & 2;
     constexpr bool HOIST = !L_NZ;  // m = nz_small: popc(m) summed once per small row
     // rows per task: enough to reuse the small side's L1 loads, few enough for two iterations of
     // large-side loads in registers
-    constexpr int RW = (MS == 1 ? 8 : 4) / (L_NZ ? 2 : 1);
+    constexpr int RW = 4 / (L_NZ ? 2 : 1);
     constexpr int NV = RW * MS;
     pdl_launch_dependents();
     pdl_wait();
@@ -262,7 +264,8 @@ cudaError_t launch_matmul_gemv_cc(const MatmulArgs& a, cudaStream_t s) {
     }
     const int64_t warps = p.entries * ((p.L + 3) / 4);
     int64_t grid = (warps + GC_NT / 32 - 1) / (GC_NT / 32);
-    if (grid > int64_t(g_sms) * GC_CTAS) grid = int64_t(g_sms) * GC_CTAS;
+    const int ms = p.S == 1 ? 1 : (p.S == 2 ? 2 : 4);
+    if (grid > int64_t(g_sms) * gc_ctas(ms)) grid = int64_t(g_sms) * gc_ctas(ms);
     if (p.S == 1) return launch_l<1>(lp, sp, p, int(grid), s);
     if (p.S == 2) return launch_l<2>(lp, sp, p, int(grid), s);
     return launch_l<4>(lp, sp, p, int(grid), s);
