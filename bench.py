@@ -440,6 +440,33 @@ def decode_linear(B, dev, seed=505, shapes=((1, 8192, 28672), (16, 8192, 28672),
     return {"ops": ops, "inputs": {}, "output": None, "cfg": cfg, "oracle_sample": None}
 
 
+def decode_attn(B, dev, seed=606, shapes=((1, 32, 2048, 128), (8, 32, 2048, 128))):
+    """Fused decode attention (Tq = 1), one launch per call: LLaMA-7B heads,
+    a 2048-token context, batch 1 and 8; baseline = torch fp16 (cuBLAS QK^T, softmax, cuBLAS PV).
+    Bytes = the K and V^T bit planes + the query + the output."""
+    ops = []
+    for i, (b, h, tk, dh) in enumerate(shapes):
+        q = gen.activations((b, h, 1, dh), seed + 10 * i).to(dev)
+        k = gen.activations((b, h, tk, dh), seed + 10 * i + 1).to(dev)
+        v = gen.activations((b, h, tk, dh), seed + 10 * i + 2).to(dev)
+        sq, sk, sv = gen.act_scale(q), gen.act_scale(k), gen.act_scale(v)
+        alpha = float(np.float32(sq * sk / np.sqrt(dh)))
+        s_att = float(np.float32(2.0 / tk))
+        beta = float(np.float32(s_att * sv))
+        qp, kp = B.bwta_pack_act(q, sq), B.bwta_pack_act(k, sk)
+        vt = B.bwta_pack_act(v, sv, transpose=True)
+
+        def op(qp=qp, kp=kp, vt=vt, alpha=alpha, s_att=s_att, beta=beta):
+            B.bwta_attn_decode(qp, kp, vt, alpha, s_att, beta)
+        n = b * h
+        ops.append(Op(f"b{b}_h{h}_tk{tk}_d{dh}", "attn", op, 4 * n * tk * dh,
+                      n * (tk * dh / 4 + dh * tk / 4 + dh / 4 + 2 * dh),
+                      (lambda q=q, k=k, v=v, alpha=alpha: torch.softmax(
+                          (q @ k.transpose(-1, -2)).float() * alpha, -1).half() @ v)))
+    cfg = {"workload": "decode_attn: fused BWTA decode attention, 32 heads x 128, context 2048, batch 1 / 8"}
+    return {"ops": ops, "inputs": {}, "output": None, "cfg": cfg, "oracle_sample": None}
+
+
 def bert_linear(B, dev, seed=101):
     """configs[0]: single BWTA linear M=128 K=768 N=768."""
     return llama_prefill(B, dev, seed, M=128, K=768, Ns=(768,)) | {
@@ -447,7 +474,7 @@ def bert_linear(B, dev, seed=101):
 
 
 WORKLOADS = {"bert_layer": bert_layer, "llama_prefill": llama_prefill, "llama_attn": llama_attn,
-             "bert_linear": bert_linear, "decode_linear": decode_linear}
+             "bert_linear": bert_linear, "decode_linear": decode_linear, "decode_attn": decode_attn}
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) legs
@@ -710,7 +737,7 @@ def main():
     # -------- side measurements: configs[2] (headline target) and configs[3]
     extras = {}
     if not args.no_extras and args.workload == "bert_layer" and rank == 0:
-        for name in ("llama_prefill", "llama_attn", "decode_linear"):
+        for name in ("llama_prefill", "llama_attn", "decode_linear", "decode_attn"):
             Wx = WORKLOADS[name](B, dev)
             res = {}
             for op in Wx["ops"]:
@@ -718,7 +745,7 @@ def main():
                 r = {"us": t * 1e3}
                 if op.kind == "pack":
                     r["GB/s"] = op.bytes / (t / 1e3) / 1e9
-                elif name == "decode_linear":  # HBM-bound: bytes (pack input + weight stream + output)
+                elif name.startswith("decode"):  # HBM-bound: bytes (bit planes streamed + inputs + outputs)
                     r["GB/s"] = op.bytes / (t / 1e3) / 1e9
                     r["frac_hbm_peak"] = r["GB/s"] / pk["hbm_gbs"]
                 else:

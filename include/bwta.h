@@ -310,6 +310,33 @@ BWTA_API bwta_status_t bwta_attn_pv_pack(const uint32_t* p_sgn, const uint32_t* 
                            uint32_t* out_sgn, uint32_t* out_nz, int64_t out_ld_words,
                            const bwta_opts_t* opts, void* stream);
 
+/* ---- fused decode attention (one query row per entry) -------------------- */
+/*
+ * Per (batch b, head h), with one packed query row q (ternary; q_sgn/q_nz at
+ * b*q_bstride + h*q_hstride words), K planes [tk x ldk_words] (ternary, or binary
+ * with k_nz == NULL) and V^T planes [dh x ldv_words] (ternary, over tk):
+ *   s_j = fl32(float(q . k_j) * alpha)                        (R5)
+ *   p_j = softmax_j(s) in fp32, rounded to p_dt               (high-precision softmax)
+ *   b_j = [p_j >= s_att / 2] on the rounded value             (bool quantizer; R1-R2)
+ *   O[d] = round_{o_dt}(fl32(float(sum_j b_j v_jd) * beta))   (R5; I32: the raw dot)
+ * in one launch (SURVEY §8(f) N3 for Tq = 1): S, P and the P planes never touch
+ * memory.  O rows [dh] contiguous at b*o_bstride + h*o_hstride elements.  p_out
+ * (nullable) receives the P planes [entries x ldp_words] (b-major, then h) -- for
+ * tests.  1 <= tk <= 16384, dh <= 256.  The fp32 softmax is not bit-reproducible
+ * against another summation order: a bit of P may differ from an exact softmax
+ * only where p_j lies within rounding distance of s_att / 2.
+ */
+BWTA_API bwta_status_t bwta_attn_decode(const uint32_t* q_sgn, const uint32_t* q_nz,
+                           const uint32_t* k_sgn, const uint32_t* k_nz,
+                           const uint32_t* vt_sgn, const uint32_t* vt_nz,
+                           int64_t batch, int64_t heads, int64_t tk, int64_t dh,
+                           int64_t q_bstride, int64_t q_hstride,
+                           int64_t ldk_words, int64_t k_bstride, int64_t k_hstride,
+                           int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
+                           float alpha, float s_att, bwta_dtype_t p_dt, float beta,
+                           void* o, bwta_dtype_t o_dt, int64_t o_bstride, int64_t o_hstride,
+                           uint32_t* p_out, int64_t ldp_words, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,7 +21,7 @@ from . import _native as N
 from ._native import lib
 
 __all__ = ["Packed", "BwtaError", "bwta_ld_words", "bwta_pack_act", "bwta_pack_weight",
-           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "bwta_attn_pv_pack", "last_design", "lib"]
+           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "last_design", "lib"]
 
 
 class BwtaError(RuntimeError):
@@ -291,6 +291,35 @@ def bwta_attn_pv(p: Packed, vt: Packed, beta: float, out_dtype=torch.float16,
                           _stream(stream))
     _check(st, "bwta_attn_pv")
     return out
+
+
+def bwta_attn_decode(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: float, beta: float,
+                     out_dtype=torch.float16, p_dtype=torch.float16, return_p: bool = False, stream=None):
+    """Fused decode attention, one launch (Tq = 1):
+    O = beta * bool(round(softmax(alpha * ternary(q) (x) K^T), p_dtype) >= s_att / 2) (x) ternary(V).
+
+    q: Packed ternary [B, H, 1, ld] (one query row per head); k: Packed ternary or binary
+    [B, H, Tk, ld]; vt: Packed ternary [B, H, Dh, ld(Tk)] (bwta_pack_act(V, transpose=True)).
+    Returns O [B, H, 1, Dh] (and the P planes [B*H, ld(Tk)] with return_p)."""
+    qr, kr, vr = q.ref, k.ref, vt.ref
+    if q.kind != "ternary" or vt.kind != "ternary" or k.cols != q.cols or vt.cols != kr.shape[-2]:
+        raise ValueError("expects ternary q and V^T, K over the same head_dim, V^T over Tk")
+    if qr.dim() != 4 or qr.shape[-2] != 1:
+        raise ValueError("q must be Packed [B, H, 1, ld] (one query row per head)")
+    b, h, qbs, qhs = _batch_dims(qr)
+    _, _, kbs, khs = _batch_dims(kr)
+    _, _, vbs, vhs = _batch_dims(vr)
+    tk, dh = kr.shape[-2], vr.shape[-2]
+    out = torch.empty((b, h, 1, dh), dtype=out_dtype, device=qr.device)
+    ldp = bwta_ld_words(tk)
+    pout = torch.empty((b * h, ldp), dtype=torch.int32, device=qr.device) if return_p else None
+    k_nz = k.nz if k.kind == "ternary" else None
+    st = lib.bwta_attn_decode(_ptr(q.sgn), _ptr(q.nz), _ptr(k.sgn), _ptr(k_nz), _ptr(vt.sgn), _ptr(vt.nz), b, h, tk,
+                              dh, qbs, qhs, kr.stride(-2), kbs, khs, vr.stride(-2), vbs, vhs, ctypes.c_float(alpha),
+                              ctypes.c_float(s_att), _DT[p_dtype], ctypes.c_float(beta), _ptr(out), _DT[out_dtype],
+                              h * dh, dh, _ptr(pout), ldp if return_p else 0, _stream(stream))
+    _check(st, "bwta_attn_decode")
+    return (out, pout) if return_p else out
 
 
 def bwta_attn_pv_pack(p: Packed, vt: Packed, beta: float, out_scale: float, out_kind: str = "ternary",

@@ -137,6 +137,24 @@ struct MatmulArgs {
 
 cudaError_t launch_matmul_cc(const MatmulArgs& a, cudaStream_t s);
 
+// fused decode attention (attn_decode.cu): one query row per (batch, head) entry
+struct DecodeArgs {
+    const uint32_t *q_sgn, *q_nz;   // [entries][ldq words] (one row)
+    const uint32_t *k_sgn, *k_nz;   // [entries][tk][ldk]; k_nz null: binary K
+    const uint32_t *v_sgn, *v_nz;   // V^T [entries][dh][ldv]
+    int64_t nb, nh, tk, dh;
+    int64_t ldk, ldv;               // words
+    int64_t q_bs, q_hs, k_bs, k_hs, v_bs, v_hs;  // words
+    float alpha, p_t, beta;         // p_t: the bool threshold as a p_dt storage value (R2)
+    int p_dt;
+    void* o;
+    int o_dt;
+    int64_t o_bs, o_hs;             // elements; O rows [dh] contiguous
+    uint32_t* p_out;                // optional P planes [entries][p_ld]
+    int64_t p_ld, pw_ld;            // words; pw_ld = shared-memory words per warp
+};
+cudaError_t launch_attn_decode(const DecodeArgs& a, cudaStream_t s);
+
 // tcgen05 path (design (b)).  Returns cudaErrorNotSupported when the shape is
 // outside what the tcgen05 kernels handle (the dispatcher then uses design (a)).
 size_t matmul_tc_workspace(const MatmulArgs& a);

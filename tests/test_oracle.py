@@ -393,3 +393,47 @@ def test_dot_threads_deterministic():
     a = rng.integers(-1, 2, (37, 200)).astype(np.int8)
     b = rng.integers(-1, 2, (23, 200)).astype(np.int8)
     assert np.array_equal(oracle.dot(a, b, 1), oracle.dot(a, b, 7))
+
+
+# ---------------------------------------------- fused decode attention (N3) ----
+def test_attn_decode_uniform_scores_give_column_sums():
+    """alpha = 0: every score is 0, softmax is uniform 1/Tk; with s_att = 1/Tk every p
+    clears the threshold 1/(2 Tk), so O = beta * (column sums of V) -- a closed form."""
+    rng = np.random.default_rng(11)
+    bh, tk, dh = 3, 50, 64
+    qq = rng.integers(-1, 2, (bh, dh)).astype(np.int8)
+    qk = rng.integers(-1, 2, (bh, tk, dh)).astype(np.int8)
+    qv = rng.integers(-1, 2, (bh, tk, dh)).astype(np.int8)
+    beta = 0.125
+    o, pb, p = oracle.attn_decode(qq, qk, qv, 0.0, 1.0 / tk, "f16", beta, "f32")
+    assert np.allclose(p, 1.0 / tk) and pb.all()
+    assert np.array_equal(o, (qv.sum(axis=1).astype(np.float32) * np.float32(beta)).astype(np.float32))
+
+
+def test_attn_decode_dominant_key_selects_its_value():
+    """q = k_0 and every other key = -q: softmax is one-hot on key 0 (e^-80 elsewhere),
+    so P = e_0 and O = beta * v_0 exactly."""
+    rng = np.random.default_rng(12)
+    dh, tk = 64, 20
+    q = rng.integers(-1, 2, dh).astype(np.int8)
+    q[:40] = 1                                  # >= 40 non-zeros
+    qk = np.tile(-q, (tk, 1))
+    qk[0] = q
+    qv = rng.integers(-1, 2, (1, tk, dh)).astype(np.int8)
+    o, pb, _ = oracle.attn_decode(q[None], qk[None], qv, 1.0, 0.5, "f16", 1.0, "i32")
+    assert pb[0, 0] == 1 and pb[0, 1:].sum() == 0
+    assert np.array_equal(o[0], qv[0, 0].astype(np.int32))
+
+
+def test_attn_decode_key_permutation_invariance():
+    """Permuting the (key, value) pairs permutes P and leaves O unchanged."""
+    rng = np.random.default_rng(13)
+    bh, tk, dh = 2, 300, 128
+    qq = rng.integers(-1, 2, (bh, dh)).astype(np.int8)
+    qk = rng.integers(-1, 2, (bh, tk, dh)).astype(np.int8)
+    qv = rng.integers(-1, 2, (bh, tk, dh)).astype(np.int8)
+    perm = rng.permutation(tk)
+    o1, pb1, _ = oracle.attn_decode(qq, qk, qv, 0.09, 2.0 / tk, "f16", 0.01, "f16")
+    o2, pb2, _ = oracle.attn_decode(qq, qk[:, perm], qv[:, perm], 0.09, 2.0 / tk, "f16", 0.01, "f16")
+    assert np.array_equal(pb1[:, perm], pb2) and np.array_equal(o1, o2)
+    assert 0 < pb1.sum() < pb1.size

@@ -558,3 +558,51 @@ def test_attn_pv_pack_equals_pv_then_pack(B, kind, o_dtype):
         assert np.array_equal(words(got.nz), nz)
         if kind == "ternary":
             assert np.array_equal(words(got.sgn), sgn)
+
+
+# ---------------------------------------------------- fused decode attention ----
+@pytest.mark.parametrize("case", range(4))
+def test_attn_decode_parity(B, case):
+    """bwta_attn_decode (one launch) against the oracle's composition: P bits equal except
+    within rounding distance of the threshold (fp32 softmax vs the oracle's float64; none
+    expected at these sizes, counted); O equal to the oracle where no P bit differs, and
+    within one unit of the dot per differing bit otherwise."""
+    b, h, tk, dh, kbin, p_dt = [(2, 3, 1000, 128, False, torch.float16), (1, 4, 37, 64, False, torch.bfloat16),
+                                (2, 2, 4096, 128, True, torch.float16), (1, 2, 300, 96, False, torch.float32)][case]
+    seed = 7000 + 10 * case
+    q = gen.activations((b, h, 1, dh), seed)
+    k = gen.activations((b, h, tk, dh), seed + 1)
+    v = gen.activations((b, h, tk, dh), seed + 2)
+    sq, sk, sv = gen.act_scale(q), gen.act_scale(k), gen.act_scale(v)
+    alpha = float(np.float32(sq * sk / np.sqrt(dh)))
+    s_att = float(np.float32(2.0 / tk))
+    beta = float(np.float32(s_att * sv))
+    qp = B.bwta_pack_act(q.cuda(), sq, "ternary")
+    if kbin:
+        kb = B.bwta_pack_weight(k.reshape(-1, dh).cuda())
+        kp = type(qp)(kb.sgn.reshape(b, h, tk, -1), None, "binary", dh)
+    else:
+        kp = B.bwta_pack_act(k.cuda(), sk, "ternary")
+    vt = B.bwta_pack_act(v.cuda(), sv, "ternary", transpose=True)
+    pname = DT[p_dt]
+    o16, pbits = B.bwta_attn_decode(qp, kp, vt, alpha, s_att, beta, torch.float16, p_dt, return_p=True)
+    oi = B.bwta_attn_decode(qp, kp, vt, alpha, s_att, beta, torch.int32, p_dt)
+    oq = oracle.quantize_act(storage(q).reshape(b * h, dh), "f16", sq, "ternary")
+    if kbin:
+        ok = oracle.binarize_weight(storage(k).reshape(-1, dh), "f16").reshape(b * h, tk, dh)
+    else:
+        ok = oracle.quantize_act(storage(k).reshape(b * h, tk, dh), "f16", sk, "ternary")
+    ov = oracle.quantize_act(storage(v).reshape(b * h, tk, dh), "f16", sv, "ternary")
+    ref_i, pb, p64 = oracle.attn_decode(oq, ok, ov, alpha, s_att, pname, beta, "i32", threads=4)
+    ref_16, _, _ = oracle.attn_decode(oq, ok, ov, alpha, s_att, pname, beta, "f16", threads=4)
+    got_bits = oracle.unpack(None, words(pbits), "bool", tk).astype(np.int8)
+    diff = got_bits != pb
+    t = s_att / 2
+    assert np.all(np.abs(p64[diff] / t - 1.0) < 2.0 ** -8), "P differs away from the threshold"
+    flips = diff.sum(axis=1)
+    gi = oi.cpu().numpy().reshape(b * h, dh)
+    assert np.all(np.abs(gi - ref_i) <= flips[:, None])
+    g16 = out_storage(o16).reshape(b * h, dh)
+    same = flips == 0
+    assert np.array_equal(g16[same], ref_16[same])
+    assert pb.sum() > 0 and flips.sum() <= max(2, pb.size // 10000)
