@@ -171,3 +171,29 @@ def test_attn_pv_pack_validation(N):
     assert pvp(ldp=0) == 2
     assert pvp(o_nz=100) == 3               # 16-byte alignment
     assert pvp(b=0) == 0                    # empty problem
+
+
+def test_attn_decode_validation(N):
+    """bwta_attn_decode: host validation before any device work (no GPU here)."""
+    L = N.lib
+
+    def dec(**kw):
+        a = dict(qs=16, qn=32, ks=48, kn=64, vs=80, vn=96, b=1, h=2, tk=100, dh=64, ldk=4, ldv=4, alpha=0.1,
+                 s_att=0.02, p_dt=0, beta=0.1, o=112, o_dt=0, pout=None, ldp=0)
+        a.update(kw)
+        return L.bwta_attn_decode(a["qs"], a["qn"], a["ks"], a["kn"], a["vs"], a["vn"], a["b"], a["h"], a["tk"],
+                                  a["dh"], 0, 0, a["ldk"], 0, 0, a["ldv"], 0, 0, ctypes.c_float(a["alpha"]),
+                                  ctypes.c_float(a["s_att"]), a["p_dt"], ctypes.c_float(a["beta"]), a["o"],
+                                  a["o_dt"], 0, 0, a["pout"], a["ldp"], None)
+    assert dec() == 4                      # valid, but no sm_100 device here
+    assert dec(tk=0) == 2                  # softmax over an empty row
+    assert dec(dh=300) == 2                # head_dim <= 256
+    assert dec(tk=20000) == 2              # tk <= 16384
+    assert dec(ldv=0) == 2                 # < bwta_ld_words(tk)
+    assert dec(pout=128, ldp=0) == 2
+    assert dec(qs=None) == 1
+    assert dec(o=None) == 1
+    assert dec(s_att=0.0) == 1
+    assert dec(alpha=float("nan")) == 1
+    assert dec(p_dt=3) == 4                # P rounds to f16 / bf16 / f32
+    assert dec(b=0) == 0
