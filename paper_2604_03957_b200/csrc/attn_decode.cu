@@ -3,8 +3,10 @@
 //   p_j = softmax_j(s) in fp32, rounded to p_dt              (high-precision softmax)
 //   b_j = [round(p_j) >= s_att / 2]                          (bool quantizer; R1, R2)
 //   o_d = fl32(float(sum_j b_j v_jd) * beta)                 (Case 2; R5)
-// in ONE launch: no S, P or P-plane round trip through memory.  One CTA (8
-// warps) per (batch, head) entry.  The two products are the paper's bit-serial
+// in ONE launch: no S, P or P-plane round trip through memory.  One CTA of
+// 1024 threads per (batch, head) entry -- or a cluster of 2-8 CTAs splitting its
+// keys when there are few entries (their (max, sum) merged in rank order, their
+// partial PV dots summed by rank 0 through distributed shared memory).  The two products are the paper's bit-serial
 // identities on CUDA cores (R10): a decode query is a single row, far below a
 // tensor-core tile.
 //   pass 1: thread j-strided dots, online (max, sum of exp) per thread, merged
@@ -17,11 +19,23 @@
 #include <cuda_fp16.h>
 
 #include "bwta_internal.h"
+#include "sm100.cuh"
 
 namespace bwta {
 namespace {
 
-constexpr int AD_WARPS = 32;  // 1024 threads per entry: a decode batch has few (batch, head) entries
+constexpr int AD_WARPS = 32;  // 1024 threads per CTA
+constexpr int AD_CMAX = 8;    // CTAs per entry (a cluster) when there are few (batch, head) entries
+
+// cluster barrier with release / acquire semantics (the shared-memory data crosses it)
+__device__ __forceinline__ void cluster_sync_acqrel() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t ld_cluster_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
 constexpr int AD_QW = 8;  // head_dim <= 256
 
 __device__ __forceinline__ float round_to(int dt, float p) {
@@ -53,10 +67,18 @@ __device__ __forceinline__ int32_t qk_dot(const uint32_t (&qs)[AD_QW], const uin
 __global__ void __launch_bounds__(AD_WARPS * 32) attn_decode_kernel(DecodeArgs p) {
     pdl_launch_dependents();
     pdl_wait();
-    extern __shared__ uint32_t ad_pw[];  // the entry's P words [ld(tk)], then partial PV sums
+    extern __shared__ uint32_t ad_pw[];  // this CTA's P words, then partial PV sums
     __shared__ float red_m[AD_WARPS], red_z[AD_WARPS];
+    __shared__ float cta_mz[2];          // this CTA's (max, sum) -- read by the cluster
+    __shared__ int32_t cta_o[256];       // this CTA's partial O (head_dim <= 256) -- read by rank 0
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t e = blockIdx.x;
+    const int cs = p.cs;                 // CTAs per entry (cluster size)
+    const int rank = cs > 1 ? int(sm100::cluster_ctarank()) : 0;
+    const int64_t e = blockIdx.x / cs;
+    // this CTA's keys: whole words [w_lo, w_hi) of the P row
+    const int64_t nw = (p.tk + 31) / 32;
+    const int64_t w_lo = nw * rank / cs, w_hi = nw * (rank + 1) / cs;
+    const int64_t j_lo = 32 * w_lo, j_hi = 32 * w_hi < p.tk ? 32 * w_hi : p.tk;
     const int64_t eb = e / p.nh, eh = e % p.nh;
     const int qw = int((p.dh + 31) / 32);
     uint32_t qs[AD_QW], qn[AD_QW];
@@ -74,7 +96,7 @@ __global__ void __launch_bounds__(AD_WARPS * 32) attn_decode_kernel(DecodeArgs p
     constexpr int NT = AD_WARPS * 32;
     // pass 1: max and sum of exp, online per thread, merged across the CTA
     float mx = -INFINITY, z = 0.f;
-    for (int64_t j = tid; j < p.tk; j += NT) {
+    for (int64_t j = j_lo + tid; j < j_hi; j += NT) {
         const int32_t d = qk_dot(qs, qn, qw, kbase_s + j * p.ldk, kbase_n ? kbase_n + j * p.ldk : nullptr);
         const float s = __fmul_rn(float(d), p.alpha);
         if (s > mx) {
@@ -99,42 +121,63 @@ __global__ void __launch_bounds__(AD_WARPS * 32) attn_decode_kernel(DecodeArgs p
     mx = red_m[0];
     z = red_z[0];
     for (int w = 1; w < AD_WARPS; ++w) merge(mx, z, red_m[w], red_z[w]);  // same order in every thread
+    if (cs > 1) {  // merge the cluster's CTAs in rank order (identical in every CTA)
+        if (tid == 0) {
+            cta_mz[0] = mx;
+            cta_mz[1] = z;
+        }
+        cluster_sync_acqrel();
+        mx = __uint_as_float(ld_cluster_u32(sm100::mapa_smem(&cta_mz[0], 0)));
+        z = __uint_as_float(ld_cluster_u32(sm100::mapa_smem(&cta_mz[1], 0)));
+        for (int r = 1; r < cs; ++r)
+            merge(mx, z, __uint_as_float(ld_cluster_u32(sm100::mapa_smem(&cta_mz[0], r))),
+                  __uint_as_float(ld_cluster_u32(sm100::mapa_smem(&cta_mz[1], r))));
+    }
     // pass 2: P words (warp w, round i covers j = NT i + 32 w + lane -> word (NT / 32) i + w)
-    const int64_t nw = (p.tk + 31) / 32;
-    for (int64_t j0 = 0; j0 < p.tk; j0 += NT) {
+    const int64_t lw = w_hi - w_lo;  // this CTA's words; ad_pw[i] = P word w_lo + i
+    for (int64_t j0 = j_lo; j0 < j_hi; j0 += NT) {
         const int64_t j = j0 + tid;
         bool bit = false;
-        if (j < p.tk) {
+        if (j < j_hi) {
             const int32_t d = qk_dot(qs, qn, qw, kbase_s + j * p.ldk, kbase_n ? kbase_n + j * p.ldk : nullptr);
             const float s = __fmul_rn(float(d), p.alpha);
             const float pj = __fdiv_rn(expf(s - mx), z);
             bit = round_to(p.p_dt, pj) >= p.p_t;
         }
         const uint32_t word = __ballot_sync(0xffffffffu, bit);
-        const int64_t wi = (j0 + 32 * warp) / 32;
-        if (lane == 0 && wi < nw) ad_pw[wi] = word;
+        const int64_t wi = (j0 - j_lo + 32 * warp) / 32;
+        if (lane == 0 && wi < lw) ad_pw[wi] = word;
     }
-    for (int64_t wi = nw + tid; wi < p.pw_ld; wi += NT) ad_pw[wi] = 0u;
+    const int64_t lq = (lw + 3) / 4 + 1;  // local quads (+1: the slice may start mid-quad)
+    for (int64_t wi = lw + tid; wi < 4 * lq; wi += NT) ad_pw[wi] = 0u;
     __syncthreads();
     if (p.p_out) {
         uint32_t* po = p.p_out + e * p.p_ld;
-        for (int64_t wi = tid; wi < p.p_ld; wi += NT) po[wi] = wi < nw ? ad_pw[wi] : 0u;
+        for (int64_t wi = tid; wi < lw; wi += NT) po[w_lo + wi] = ad_pw[wi];
+        if (rank == cs - 1)
+            for (int64_t wi = nw + tid; wi < p.p_ld; wi += NT) po[wi] = 0u;
     }
     // PV: output d by NT / dh_groups threads, each a slice of the P words, partials through smem
-    int32_t* part = reinterpret_cast<int32_t*>(ad_pw + p.pw_ld);  // [NT]
+    int32_t* part = reinterpret_cast<int32_t*>(ad_pw + 4 * lq);  // [NT]
     const int dpad = int((p.dh + 31) / 32) * 32;                    // threads per slice group
     const int nslice = NT / dpad > 0 ? NT / dpad : 1;
     const int dd = tid % dpad, sl = tid / dpad;
     int32_t acc = 0;
     if (sl < nslice && dd < p.dh) {
-        // slice of whole word quads (rows are 16-byte aligned; P words past nw are 0 in smem)
-        const int64_t nq = p.pw_ld / 4, q0 = nq * sl / nslice, q1 = nq * (sl + 1) / nslice;
-        const uint4* vs = reinterpret_cast<const uint4*>(p.v_sgn + eb * p.v_bs + eh * p.v_hs + dd * p.ldv);
-        const uint4* vn = reinterpret_cast<const uint4*>(p.v_nz + eb * p.v_bs + eh * p.v_hs + dd * p.ldv);
-        const uint4* pq = reinterpret_cast<const uint4*>(ad_pw);
+        // V^T words [w_lo, w_hi) of row d, in word quads aligned to the V^T row (16-byte loads);
+        // the local P words are read at the matching (possibly unaligned) offsets
+        const int64_t a0 = w_lo & ~int64_t(3);                 // first aligned word
+        const int64_t nq = (w_hi - a0 + 3) / 4, q0 = nq * sl / nslice, q1 = nq * (sl + 1) / nslice;
+        const uint4* vs = reinterpret_cast<const uint4*>(p.v_sgn + eb * p.v_bs + eh * p.v_hs + dd * p.ldv + a0);
+        const uint4* vn = reinterpret_cast<const uint4*>(p.v_nz + eb * p.v_bs + eh * p.v_hs + dd * p.ldv + a0);
+        auto pword = [&](int64_t w) -> uint32_t {  // P word a0 + w (0 outside this CTA's range)
+            const int64_t g = a0 + w;
+            return (g >= w_lo && g < w_hi) ? ad_pw[g - w_lo] : 0u;
+        };
 #pragma unroll 4
         for (int64_t qi = q0; qi < q1; ++qi) {
-            const uint4 n4 = __ldg(vn + qi), s4 = __ldg(vs + qi), p4 = pq[qi];
+            const uint4 n4 = __ldg(vn + qi), s4 = __ldg(vs + qi);
+            const uint4 p4 = make_uint4(pword(4 * qi), pword(4 * qi + 1), pword(4 * qi + 2), pword(4 * qi + 3));
             const uint32_t m0 = p4.x & n4.x, m1 = p4.y & n4.y, m2 = p4.z & n4.z, m3 = p4.w & n4.w;
             acc += __popc(m0) + __popc(m1) + __popc(m2) + __popc(m3) -
                    2 * (__popc(m0 & s4.x) + __popc(m1 & s4.y) + __popc(m2 & s4.z) + __popc(m3 & s4.w));
@@ -142,9 +185,18 @@ __global__ void __launch_bounds__(AD_WARPS * 32) attn_decode_kernel(DecodeArgs p
     }
     part[tid] = acc;
     __syncthreads();
-    if (tid < p.dh) {
-        int32_t dot = 0;
+    int32_t dot = 0;
+    if (tid < p.dh)
         for (int s2 = 0; s2 < nslice; ++s2) dot += part[s2 * dpad + tid];
+    if (cs > 1) {  // rank 0 sums the cluster's partial dots (exact integers, any order)
+        if (tid < p.dh) cta_o[tid] = dot;
+        cluster_sync_acqrel();
+        if (rank == 0 && tid < p.dh)
+            for (int r = 1; r < cs; ++r) dot += int32_t(ld_cluster_u32(sm100::mapa_smem(&cta_o[tid], r)));
+        cluster_sync_acqrel();  // no CTA leaves while its shared memory may still be read
+        if (rank != 0) return;
+    }
+    if (tid < p.dh) {
         const int64_t off = eb * p.o_bs + eh * p.o_hs + tid;
         const float y = __fmul_rn(float(dot), p.beta);
         if (p.o_dt == DT_F16) reinterpret_cast<__half*>(p.o)[off] = __float2half_rn(y);
@@ -158,13 +210,19 @@ __global__ void __launch_bounds__(AD_WARPS * 32) attn_decode_kernel(DecodeArgs p
 
 cudaError_t launch_attn_decode(const DecodeArgs& a, cudaStream_t s) {
     const int64_t entries = a.nb * a.nh;
-    const int grid = int(entries);  // one CTA per (batch, head)
-    const size_t smem = sizeof(uint32_t) * (size_t(a.pw_ld) + AD_WARPS * 32);
+    // CTAs per entry: spread few entries over the SMs (cluster of up to 8), keeping >= 2 words each
+    int cs = 1;
+    while (cs < AD_CMAX && entries * cs * 2 <= 148 && (a.tk + 31) / 32 >= 2 * cs * 2) cs *= 2;
+    DecodeArgs b = a;
+    b.cs = cs;
+    const int grid = int(entries * cs);
+    const int64_t lw = ((a.tk + 31) / 32 + cs - 1) / cs;
+    const size_t smem = sizeof(uint32_t) * (size_t(4 * ((lw + 3) / 4 + 1)) + AD_WARPS * 32);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;
     }
-    return launch_pdl(attn_decode_kernel, dim3(grid), dim3(AD_WARPS * 32), smem, s, 1, a);
+    return launch_pdl(attn_decode_kernel, dim3(grid), dim3(AD_WARPS * 32), smem, s, cs, b);
 }
 
 }  // namespace bwta

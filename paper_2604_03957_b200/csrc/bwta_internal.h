@@ -151,7 +151,8 @@ struct DecodeArgs {
     int o_dt;
     int64_t o_bs, o_hs;             // elements; O rows [dh] contiguous
     uint32_t* p_out;                // optional P planes [entries][p_ld]
-    int64_t p_ld, pw_ld;            // words; pw_ld = shared-memory words per warp
+    int64_t p_ld, pw_ld;            // words; pw_ld = ld_words(tk)
+    int cs;                         // CTAs per entry (set by the launcher)
 };
 cudaError_t launch_attn_decode(const DecodeArgs& a, cudaStream_t s);
 
