@@ -433,6 +433,8 @@ def decode_linear(B, dev, seed=505, shapes=((1, 8192, 28672), (16, 8192, 28672),
         w16 = w.to(dev)
 
         def op_g(X=X, s_x=s_x, wp=wp, sw=sw, y=y):
+            # pack + GEMV (two launches): in a graph this beats bwta_gemm_x, whose every CTA
+            # re-quantizes the activation row (tools/decode_bench.py)
             B.bwta_gemm(B.bwta_pack_act(X, s_x), wp, sw, s_x, out=y)
         ops.append(Op(f"m{M}_k{K}_n{N}", "gemm", op_g, 2 * M * N * K, 2 * M * K + M * K / 4 + N * K / 8 + 2 * M * N,
                       (lambda X=X, w16=w16: torch.nn.functional.linear(X, w16))))

@@ -310,6 +310,20 @@ BWTA_API bwta_status_t bwta_attn_pv_pack(const uint32_t* p_sgn, const uint32_t* 
                            uint32_t* out_sgn, uint32_t* out_nz, int64_t out_ld_words,
                            const bwta_opts_t* opts, void* stream);
 
+/* ---- decode linear with the activation pack fused ------------------------ */
+/*
+ * Y = bwta_gemm(bwta_pack_act(x, a_scale, a_kind), W, w_scale, a_scale) in ONE launch for
+ * m <= 4 activation rows (decode): x [m x k] values (F16 | BF16 | F32, row stride ld_x
+ * elements) are quantized (R1-R3) into shared-memory planes by every CTA of a
+ * CUDA-core GEMV -- the paper's in-kernel bitpack -- then streamed against the
+ * binary weight planes [n x ldw_words].  Outputs and errors as bwta_gemm; m > 4 returns
+ * BWTA_ERR_UNSUPPORTED (pack + bwta_gemm there).
+ */
+BWTA_API bwta_status_t bwta_gemm_x(const void* x, bwta_dtype_t x_dt, int64_t m, int64_t ld_x, float a_scale,
+                                   bwta_kind_t a_kind, const uint32_t* w_sgn, int64_t n, int64_t ldw_words,
+                                   int64_t k, const float* w_scale, void* y, bwta_dtype_t y_dt, int64_t ld_y,
+                                   int y_transposed, void* stream);
+
 /* ---- fused decode attention (one query row per entry) -------------------- */
 /*
  * Per (batch b, head h), with one packed query row q (ternary; q_sgn/q_nz at

@@ -21,7 +21,7 @@ from . import _native as N
 from ._native import lib
 
 __all__ = ["Packed", "BwtaError", "bwta_ld_words", "bwta_pack_act", "bwta_pack_weight",
-           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "last_design", "lib"]
+           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "bwta_gemm_x", "last_design", "lib"]
 
 
 class BwtaError(RuntimeError):
@@ -213,6 +213,24 @@ def bwta_gemm(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: fl
                        w.sgn.stride(-2), k, _ptr(ws_scale), ctypes.c_float(a_scale), _ptr(out),
                        _DT[out.dtype], out.stride(0), int(y_transposed), _ptr(ws), wsb, o, _stream(stream))
     _check(st, "bwta_gemm")
+    return out
+
+
+def bwta_gemm_x(x: torch.Tensor, a_scale: float, w: Packed, w_scale: Optional[torch.Tensor], kind: str = "ternary",
+                out_dtype=torch.float16, y_transposed: bool = False, stream=None) -> torch.Tensor:
+    """bwta_gemm(bwta_pack_act(x, a_scale, kind), w, w_scale, a_scale) in one launch for <= 4
+    activation rows (decode): the pack runs inside the GEMV.  x [M, K] values."""
+    if kind not in ("ternary", "bool") or w.kind != "binary" or x.shape[-1] != w.cols or x.dim() != 2:
+        raise ValueError("bwta_gemm_x expects x [M, K] and binary weights of equal K")
+    if x.stride(-1) != 1:
+        x = x.contiguous()
+    m, k, n = x.shape[0], x.shape[1], w.sgn.shape[-2]
+    out = torch.empty((n, m) if y_transposed else (m, n), dtype=out_dtype, device=x.device)
+    ws_scale = None if w_scale is None else w_scale.to(device=x.device, dtype=torch.float32).contiguous()
+    st = lib.bwta_gemm_x(_ptr(x), _DT[x.dtype], m, x.stride(0), ctypes.c_float(a_scale), _KIND[kind], _ptr(w.sgn), n,
+                         w.sgn.stride(-2), k, _ptr(ws_scale), _ptr(out), _DT[out.dtype], out.stride(0),
+                         int(y_transposed), _stream(stream))
+    _check(st, "bwta_gemm_x")
     return out
 
 

@@ -20,7 +20,7 @@ EXPORTS = ("bwta_ld_words", "bwta_status_string", "bwta_last_cuda_error", "bwta_
            "bwta_version", "bwta_kernel_launches", "bwta_pack_act", "bwta_pack_act_batch", "bwta_pack_weight",
            "bwta_gemm_workspace_size", "bwta_gemm_pack",
            "bwta_gemm", "bwta_attn_qk_workspace_size", "bwta_attn_qk",
-           "bwta_attn_pv_workspace_size", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode")
+           "bwta_attn_pv_workspace_size", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "bwta_gemm_x")
 
 
 class Opts(ctypes.Structure):
@@ -78,6 +78,8 @@ def _declare(L):
                                f32, P, i32, i64, i64, i64, P, sz, OP, P]
     L.bwta_attn_pv_workspace_size.restype = sz
     L.bwta_attn_pv_workspace_size.argtypes = [i64, i64, i64, i64, OP]
+    L.bwta_gemm_x.restype = i32
+    L.bwta_gemm_x.argtypes = [P, i32, i64, i64, f32, i32, P, i64, i64, i64, P, P, i32, i64, i32, P]
     L.bwta_attn_decode.restype = i32
     L.bwta_attn_decode.argtypes = [P, P, P, P, P, P, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64,
                                    f32, f32, i32, f32, P, i32, i64, i64, P, i64, P]

@@ -546,6 +546,53 @@ size_t bwta_attn_pv_workspace_size(int64_t batch_heads, int64_t tq, int64_t tk, 
     return matmul_tc_supported(a) ? matmul_tc_workspace(a) : 0;
 }
 
+bwta_status_t bwta_gemm_x(const void* x, bwta_dtype_t x_dt, int64_t m, int64_t ld_x, float a_scale, bwta_kind_t a_kind,
+                          const uint32_t* w_sgn, int64_t n, int64_t ldw_words, int64_t k, const float* w_scale,
+                          void* y, bwta_dtype_t y_dt, int64_t ld_y, int y_transposed, void* stream) {
+    if (x_dt != BWTA_F16 && x_dt != BWTA_BF16 && x_dt != BWTA_F32) return BWTA_ERR_UNSUPPORTED;
+    if (a_kind != BWTA_TERNARY && a_kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
+    if (!valid_out_dt(y_dt)) return BWTA_ERR_UNSUPPORTED;
+    if (m < 0 || n < 0 || k < 0 || k > KMAX) return BWTA_ERR_SHAPE;
+    if (m > 4) return BWTA_ERR_UNSUPPORTED;  // decode sizes only (pack + bwta_gemm otherwise)
+    if (m == 0 || n == 0) return BWTA_OK;
+    if (x == nullptr || w_sgn == nullptr || y == nullptr) return BWTA_ERR_INVALID_VALUE;
+    if (!scale_ok_pos(a_scale)) return BWTA_ERR_INVALID_VALUE;
+    if (ld_x < k || ldw_words < ldw_of(k) || ld_y < (y_transposed ? m : n)) return BWTA_ERR_SHAPE;
+    if (ldw_words % 4 || !aligned16(w_sgn)) return BWTA_ERR_ALIGNMENT;
+    bwta_status_t st = check_device();
+    if (st != BWTA_OK) return st;
+    // R2 thresholds as values of the input type: +1 iff x >= tp, -1 iff x <= ntn
+    float tp, ntn;
+    if (x_dt == BWTA_F32) {
+        const Thresholds th = make_thresholds(DT_F32, a_scale);
+        tp = th.tpf;
+        ntn = th.ntnf;
+    } else {
+        const bool bf = x_dt == BWTA_BF16;
+        const double t = 0.5 * double(a_scale);
+        const uint16_t p1 = smallest_pattern(t, false, bf), p2 = smallest_pattern(t, true, bf);
+        tp = float(bf ? bf16_value(p1) : f16_value(p1));
+        ntn = -float(bf ? bf16_value(p2) : f16_value(p2));
+    }
+    MatmulArgs a{};
+    a.b_sgn = w_sgn;
+    a.M = m;
+    a.N = n;
+    a.K = k;
+    a.ldb = ldw_words;
+    a.nb = a.nh = 1;
+    a.y = y;
+    a.y_dt = y_dt;
+    a.ldy = ld_y;
+    a.y_trans = y_transposed ? 1 : 0;
+    a.col_scale = w_scale;
+    a.scalar = a_scale;
+    cudaError_t e = launch_gemv_cc_fused(x, x_dt, ld_x, tp, ntn, a_kind, a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_last_design = BWTA_DESIGN_CUDA_CORE;
+    return BWTA_OK;
+}
+
 bwta_status_t bwta_attn_decode(const uint32_t* q_sgn, const uint32_t* q_nz, const uint32_t* k_sgn,
                                const uint32_t* k_nz, const uint32_t* vt_sgn, const uint32_t* vt_nz, int64_t batch,
                                int64_t heads, int64_t tk, int64_t dh, int64_t q_bstride, int64_t q_hstride,

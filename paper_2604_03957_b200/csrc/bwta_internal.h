@@ -168,5 +168,7 @@ cudaError_t launch_matmul_gemv(const MatmulArgs& a, cudaStream_t s);
 // decode-sized products (smaller side <= 4 rows) on CUDA cores (gemv_cc.cu)
 bool matmul_gemv_cc_eligible(const MatmulArgs& a);
 cudaError_t launch_matmul_gemv_cc(const MatmulArgs& a, cudaStream_t s);
+cudaError_t launch_gemv_cc_fused(const void* x, int x_dt, int64_t ld_x, float tp, float ntn, int a_kind,
+                                 const MatmulArgs& a, cudaStream_t s);
 
 }  // namespace bwta

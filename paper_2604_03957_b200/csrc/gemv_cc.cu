@@ -47,6 +47,13 @@ struct GcParams {
     const float* scale;              // caller's per-N scale (large rows if scale_on_rows)
     int scale_on_rows;
     float scalar;
+    // fused activation pack (the paper's in-kernel bitpack): the small side given as
+    // values [S rows x K] (f16 / bf16 / f32, row stride ld_sx elements), quantized by every CTA
+    // into shared-memory planes before the main loop (q = +1 iff x >= s_tp, -1 iff x <= s_ntn; R1-R3)
+    const void* sx;
+    int sx_dt, s_kind;
+    int64_t ld_sx, K;
+    float s_tp, s_ntn;
 };
 
 __device__ __forceinline__ uint4 ldg_nc4(const uint32_t* p) {
@@ -87,7 +94,13 @@ __device__ __forceinline__ int32_t warp_reduce_many(int32_t (&v)[NV], int lane) 
 __host__ __device__ constexpr int ilog2(int x) { return x <= 1 ? 0 : 1 + ilog2(x / 2); }
 
 // LP / SP: large / small plane presence (bit 0 sgn, bit 1 nz); RW large rows per warp task
-template <int MS, int LP, int SP>
+__device__ __forceinline__ float sx_value(const GcParams& p, int64_t i) {
+    if (p.sx_dt == DT_F16) return __half2float(reinterpret_cast<const __half*>(p.sx)[i]);
+    if (p.sx_dt == DT_BF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p.sx)[i]);
+    return reinterpret_cast<const float*>(p.sx)[i];
+}
+
+template <int MS, int LP, int SP, bool SQ = false>
 __global__ void __launch_bounds__(GC_NT, gc_ctas(MS)) cc_gemv_kernel(GcParams p) {
     constexpr bool L_SGN = LP & 1, L_NZ = LP & 2, S_SGN = SP & 1, S_NZ = SP & 2;
     constexpr bool HOIST = !L_NZ;  // m = nz_small: popc(m) summed once per small row
@@ -103,6 +116,62 @@ __global__ void __launch_bounds__(GC_NT, gc_ctas(MS)) cc_gemv_kernel(GcParams p)
     const int64_t tasks_per_entry = (p.L + RW - 1) / RW;
     const int64_t total = p.entries * tasks_per_entry;
     const int nqi = (p.nq + 31) / 32;  // warp-uniform quad iterations
+    extern __shared__ uint4 gc_smem[];  // SQ: small-side planes [MS][4 nq] sgn, then nz
+    uint32_t* sp_sgn = reinterpret_cast<uint32_t*>(gc_smem);
+    uint32_t* sp_nz = sp_sgn + MS * 4 * p.nq;
+    if (SQ) {  // quantize + pack the small side once per CTA (single entry)
+        {   // first, start the HBM -> L2 stream of this warp's first task (it overlaps the pack)
+            const int64_t task = gw;
+            if (task < total) {
+                const int64_t r0 = task * RW;
+                for (int r = 0; r < RW; ++r)
+                    if (r0 + r < p.L)
+                        for (int q = lane; q < p.nq; q += 32)
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(p.l_sgn + (r0 + r) * p.ldl + 4 * q));
+            }
+        }
+        const int64_t ldw = 4 * int64_t(p.nq);
+        const int es = p.sx_dt == DT_F32 ? 4 : 2;
+        const bool vec = (reinterpret_cast<uintptr_t>(p.sx) % 16 == 0) && ((p.ld_sx * es) % 16 == 0);
+        for (int64_t idx = threadIdx.x; idx < MS * ldw; idx += GC_NT) {
+            const int m = int(idx / ldw);
+            const int64_t w = idx - m * ldw;
+            uint32_t pos = 0, neg = 0;
+            if (m < p.S && 32 * w < p.K) {
+                const int64_t base = m * p.ld_sx + 32 * w;
+                if (vec && es == 2 && 32 * w + 32 <= p.K) {  // 4 x 16-byte loads, 8 values each
+                    const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(p.sx) + base);
+                    uint4 v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) v[u] = __ldg(src + u);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t h[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const uint16_t bits = uint16_t(h[i >> 1] >> (16 * (i & 1)));
+                            const float x = p.sx_dt == DT_F16 ? __half2float(__ushort_as_half(bits))
+                                                              : __uint_as_float(uint32_t(bits) << 16);
+                            pos |= uint32_t(x >= p.s_tp) << (8 * u + i);
+                            neg |= uint32_t(x <= p.s_ntn) << (8 * u + i);
+                        }
+                    }
+                } else {
+                    for (int i = 0; i < 32; ++i) {
+                        const int64_t c = 32 * w + i;
+                        if (c < p.K) {
+                            const float x = sx_value(p, base + i);
+                            pos |= uint32_t(x >= p.s_tp) << i;
+                            neg |= uint32_t(x <= p.s_ntn) << i;
+                        }
+                    }
+                }
+            }
+            sp_nz[idx] = p.s_kind == K_TERNARY ? (pos | neg) : pos;
+            sp_sgn[idx] = p.s_kind == K_TERNARY ? neg : 0u;
+        }
+        __syncthreads();
+    }
     for (int64_t task = gw; task < total; task += nwarps) {
         const int64_t e = task / tasks_per_entry;
         const int64_t r0 = (task % tasks_per_entry) * RW;
@@ -145,9 +214,15 @@ __global__ void __launch_bounds__(GC_NT, gc_ctas(MS)) cc_gemv_kernel(GcParams p)
 #pragma unroll
             for (int m = 0; m < MS; ++m) {
                 const bool ok = qok && m < p.S;
-                const int64_t o = soff + int64_t(m < p.S ? m : 0) * p.lds + 4 * q;
-                ss[m] = S_SGN && ok ? ldg4(p.s_sgn + o) : make_uint4(0, 0, 0, 0);
-                sn[m] = !ok ? make_uint4(0, 0, 0, 0) : S_NZ ? ldg4(p.s_nz + o) : make_uint4(~0u, ~0u, ~0u, ~0u);
+                if (SQ) {
+                    const int64_t o = int64_t(m) * 4 * p.nq + 4 * q;
+                    ss[m] = ok ? *reinterpret_cast<const uint4*>(sp_sgn + o) : make_uint4(0, 0, 0, 0);
+                    sn[m] = ok ? *reinterpret_cast<const uint4*>(sp_nz + o) : make_uint4(0, 0, 0, 0);
+                } else {
+                    const int64_t o = soff + int64_t(m < p.S ? m : 0) * p.lds + 4 * q;
+                    ss[m] = S_SGN && ok ? ldg4(p.s_sgn + o) : make_uint4(0, 0, 0, 0);
+                    sn[m] = !ok ? make_uint4(0, 0, 0, 0) : S_NZ ? ldg4(p.s_nz + o) : make_uint4(~0u, ~0u, ~0u, ~0u);
+                }
             }
             if (HOIST) {
 #pragma unroll
@@ -213,7 +288,60 @@ cudaError_t launch_l(int lp, int sp, const GcParams& p, int grid, cudaStream_t s
     return launch_s<MS, 1>(sp, p, grid, s);
 }
 
+template <int MS>
+cudaError_t launch_sq(const GcParams& p, int grid, cudaStream_t s) {
+    const size_t smem = sizeof(uint32_t) * 2 * MS * 4 * size_t(p.nq);
+    auto k = p.s_kind == K_TERNARY ? cc_gemv_kernel<MS, 1, 3, true> : cc_gemv_kernel<MS, 1, 2, true>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        if (e != cudaSuccess) return e;
+    }
+    return launch_pdl(k, dim3(grid), dim3(GC_NT), smem, s, 1, p);
+}
+
 }  // namespace
+
+// Y = bwta_gemm(bwta_pack_act(x), W) for <= 4 activation rows with the pack fused (one launch):
+// x [m x k] values (row stride ld_x elements), binary W [n x ldw]; Y [m x n] (or Y^T).
+cudaError_t launch_gemv_cc_fused(const void* x, int x_dt, int64_t ld_x, float tp, float ntn, int a_kind,
+                                 const MatmulArgs& a, cudaStream_t s) {
+    GcParams p{};
+    p.l_sgn = a.b_sgn;
+    p.l_nz = nullptr;
+    p.L = a.N;
+    p.S = a.M;
+    p.ldl = a.ldb;
+    p.nh = 1;
+    p.entries = 1;
+    p.nq = int(((a.K + 31) / 32 + 3) / 4);
+    p.y = a.y;
+    p.y_dt = a.y_dt;
+    const int64_t si = a.y_trans ? 1 : a.ldy, sj = a.y_trans ? a.ldy : 1;
+    p.y_rs = sj;  // large side = the caller's N
+    p.y_cs = si;
+    p.scale = a.col_scale;
+    p.scale_on_rows = 1;
+    p.scalar = a.scalar;
+    p.sx = x;
+    p.sx_dt = x_dt;
+    p.s_kind = a_kind;
+    p.ld_sx = ld_x;
+    p.K = a.K;
+    p.s_tp = tp;
+    p.s_ntn = ntn;
+    if (g_sms == 0) {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) v = 148;
+        g_sms = v;
+    }
+    const int ms = p.S == 1 ? 1 : (p.S == 2 ? 2 : 4);
+    int64_t grid = (p.L + 3) / 4 / (GC_NT / 32) + 1;
+    if (grid > int64_t(g_sms) * gc_ctas(ms)) grid = int64_t(g_sms) * gc_ctas(ms);
+    if (ms == 1) return launch_sq<1>(p, int(grid), s);
+    if (ms == 2) return launch_sq<2>(p, int(grid), s);
+    return launch_sq<4>(p, int(grid), s);
+}
 
 bool matmul_gemv_cc_eligible(const MatmulArgs& a) {
     const int64_t small = a.M < a.N ? a.M : a.N;

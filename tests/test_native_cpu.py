@@ -197,3 +197,26 @@ def test_attn_decode_validation(N):
     assert dec(alpha=float("nan")) == 1
     assert dec(p_dt=3) == 4                # P rounds to f16 / bf16 / f32
     assert dec(b=0) == 0
+
+
+def test_gemm_x_validation(N):
+    """bwta_gemm_x: host validation before any device work (no GPU here)."""
+    L = N.lib
+
+    def gx(**kw):
+        a = dict(x=16, x_dt=0, m=1, ld_x=100, s=1.0, kind=2, w=48, n=8, ldw=4, k=100, ws=None, y=64, y_dt=0,
+                 ld_y=8, yt=0)
+        a.update(kw)
+        return L.bwta_gemm_x(a["x"], a["x_dt"], a["m"], a["ld_x"], ctypes.c_float(a["s"]), a["kind"], a["w"], a["n"],
+                             a["ldw"], a["k"], a["ws"], a["y"], a["y_dt"], a["ld_y"], a["yt"], None)
+    assert gx() == 4                        # valid, but no sm_100 device here
+    assert gx(m=5) == 4                     # decode sizes only
+    assert gx(kind=0) == 4
+    assert gx(x_dt=3) == 4
+    assert gx(x=None) == 1
+    assert gx(s=0.0) == 1
+    assert gx(ld_x=99) == 2
+    assert gx(ldw=0) == 2
+    assert gx(ld_y=7) == 2
+    assert gx(w=40) == 3
+    assert gx(m=0) == 0

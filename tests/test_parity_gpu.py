@@ -606,3 +606,26 @@ def test_attn_decode_parity(B, case):
     same = flips == 0
     assert np.array_equal(g16[same], ref_16[same])
     assert pb.sum() > 0 and flips.sum() <= max(2, pb.size // 10000)
+
+
+# ------------------------------------------- decode GEMM with the pack fused ----
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("kind", ["ternary", "bool"])
+def test_gemm_x_equals_pack_then_gemm(B, dtype, kind):
+    """bwta_gemm_x (the activation pack inside the GEMV) == bwta_gemm(bwta_pack_act(x)) bit-exactly
+    and == the oracle, incl. exact ties / +-0 / +-inf / NaN in x, ragged K, y transposed."""
+    for i, (m, n, k) in enumerate([(1, 300, 1000), (2, 777, 4100), (3, 1030, 513), (4, 65, 8192), (1, 5, 7)]):
+        seed = 8000 + 10 * i
+        s = tie_scale(dtype, seed)
+        x = inject_specials(gen.normal((m, k), seed, dtype), s, seed + 1)
+        w = gen.weights(n, k, seed + 2)
+        mu, s_w = gen.weight_stats(w)
+        wp = B.bwta_pack_weight(w.cuda(), mu=mu)
+        for yt in (False, True):
+            got = B.bwta_gemm_x(x.cuda(), s, wp, s_w.cuda(), kind, torch.float16, y_transposed=yt)
+            ref = B.bwta_gemm(B.bwta_pack_act(x.cuda(), s, kind), wp, s_w.cuda(), s, torch.float16, y_transposed=yt)
+            assert torch.equal(got.view(torch.int16), ref.view(torch.int16)), (m, n, k, yt)
+        gi = B.bwta_gemm_x(x.cuda(), s, wp, s_w.cuda(), kind, torch.int32)
+        qa = oracle.quantize_act(storage(x), DT[dtype], s, kind)
+        qw = oracle.binarize_weight(storage(w), "f16", mu=mu)
+        assert np.array_equal(gi.cpu().numpy(), oracle.dot(qa, qw, threads=4)), (m, n, k)

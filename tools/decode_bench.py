@@ -20,6 +20,8 @@ for (k, n) in [(4096, 4096), (4096, 11008), (11008, 4096), (5120, 13824), (8192,
         a = B.bwta_pack_act(x, s_a)
         y = torch.empty((m, n), dtype=torch.float16, device="cuda")
         t_sk = timeit(lambda: B.bwta_gemm(a, wp, s_w, s_a, out=y), flush=flush)
+        g_x = time_graph(lambda: B.bwta_gemm_x(x, s_a, wp, s_w)) if m <= 4 else float("nan")
+        g_px = time_graph(lambda: B.bwta_gemm(B.bwta_pack_act(x, s_a), wp, s_w, s_a, out=y))
         t_gen = timeit(lambda: B.bwta_gemm(a, wp, s_w, s_a, out=y, design="tcgen05"), flush=flush)
         xh = x.half()
         t_cub = timeit(lambda: torch.nn.functional.linear(xh, wh), flush=flush)
@@ -28,4 +30,5 @@ for (k, n) in [(4096, 4096), (4096, 11008), (11008, 4096), (5120, 13824), (8192,
         byt = n * k / 8 + m * k / 4 + 4 * n + 2 * m * n
         print(f"M={m:2d} K={k} N={n}: skinny {t_sk*1e3:6.2f}us ({byt/t_sk/1e6:5.0f} GB/s, {byt/(t_sk*1e-3)/hbm:.2f} HBM)"
               f" | tcgen05 {t_gen*1e3:6.2f}us | cuBLAS fp16 {t_cub*1e3:6.2f}us | x{t_cub/t_sk:5.1f} vs cuBLAS"
-              f" || graph (L2 warm): skinny {g_sk*1e3:6.2f}us cuBLAS {g_cub*1e3:6.2f}us", flush=True)
+              f" || graph (L2 warm): skinny {g_sk*1e3:6.2f}us pack+gemm {g_px*1e3:6.2f}us fused gemm_x {g_x*1e3:6.2f}us"
+              f" cuBLAS {g_cub*1e3:6.2f}us", flush=True)
