@@ -469,6 +469,38 @@ def decode_attn(B, dev, seed=606, shapes=((1, 32, 2048, 128), (8, 32, 2048, 128)
     return {"ops": ops, "inputs": {}, "output": None, "cfg": cfg, "oracle_sample": None}
 
 
+def nshard_gemm(B, dev, seed=707, M=2048, K=8192, N=28672):
+    """configs[4]: a LLaMA-70B-shaped BWTA linear (K 8192, N 28672, M 2048 tokens) N-sharded across
+    the ranks (paper_2604_03957_b200.dist): rank r packs its replica of the activations, computes
+    Y_r^T for its weight rows, and one NCCL all-gather (a copy at world 1) assembles Y^T.  Total
+    work is fixed: "scaling": "strong"."""
+    from paper_2604_03957_b200 import dist as D
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    X = gen.activations((M, K), seed).to(dev)
+    s_x = gen.act_scale(X)
+    w = gen.weights(N, K, seed + 1)                    # the same full weight on every rank
+    mu, s_w = gen.weight_stats(w)
+    st0, st1 = D.shard_bounds(N, world, rank)
+    wp = B.bwta_pack_weight(w[st0:st1].to(dev), mu=mu) if st1 > st0 else None
+    sw = s_w[st0:st1].to(dev)
+    st = {}
+
+    def op_pack():
+        st["xq"] = B.bwta_pack_act(X, s_x)
+
+    def op_gemm():
+        st["yt"] = D.gemm_nshard(st["xq"], wp, sw, s_x, N, world, rank)
+    op_pack()
+    ops = [Op("pack_x", "pack", op_pack, 0, 2 * M * K + M * K / 4),
+           Op("gemm_nshard_allgather", "gemm", op_gemm, 2 * M * (st1 - st0) * K,
+              M * K / 4 + (st1 - st0) * K / 8 + 2 * M * N)]
+    cfg = {"workload": f"nshard_gemm (configs[4]): K={K} N={N} M={M}, weight rows N-sharded over {world} rank(s), "
+                       "Y^T all-gathered (NCCL)", "tokens": M, "k": K, "n": N, "parallelism": f"N-shard x{world}"}
+    return {"ops": ops, "inputs": {"X": X}, "output": None, "cfg": cfg, "oracle_sample": None,
+            "scaling": "strong"}
+
+
 def bert_linear(B, dev, seed=101):
     """configs[0]: single BWTA linear M=128 K=768 N=768."""
     return llama_prefill(B, dev, seed, M=128, K=768, Ns=(768,)) | {
@@ -476,7 +508,8 @@ def bert_linear(B, dev, seed=101):
 
 
 WORKLOADS = {"bert_layer": bert_layer, "llama_prefill": llama_prefill, "llama_attn": llama_attn,
-             "bert_linear": bert_linear, "decode_linear": decode_linear, "decode_attn": decode_attn}
+             "bert_linear": bert_linear, "decode_linear": decode_linear, "decode_attn": decode_attn,
+             "nshard_gemm": nshard_gemm}
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) legs
@@ -780,7 +813,8 @@ def main():
         pack_gbs = {o.name: o.bytes / (per_op[o.name] / 1e3) / 1e9 for o in ops if o.kind == "pack"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": W.get("scaling", "weak"),
             "vs_baseline": None, "dtype": "fp4-e2m1 codes (tcgen05 kind::mxf4, f32 accumulate; fp16 in/out)",
             "data": "synthetic (seeded, recipe in DESIGN.md)",
             "config": W["cfg"] | {"parallelism": f"replicas x{world}" if world > 1 else "single GPU",

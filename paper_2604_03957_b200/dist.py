@@ -58,6 +58,8 @@ def gather_rows(local: torch.Tensor, n: int, world: int, group=None, align: int 
     """All-gather rank-major row blocks [n_r, ...] -> [n, ...].
 
     Each rank's block is padded to padded_shard() rows; one collective."""
+    if world == 1 and local.shape[0] == n:
+        return local  # nothing to gather
     per = padded_shard(n, world, align)
     if local.shape[0] > per:
         raise ValueError("local block larger than the padded shard")
