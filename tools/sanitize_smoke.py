@@ -28,5 +28,19 @@ g = B.bwta_pack_act_batch([(q, 1.6, "ternary", False), (v, 1.6, "ternary", True)
 for d in ("cuda_core", "tcgen05"):
     B.bwta_attn_qk(qp, kp, 0.1, design=d)
     B.bwta_attn_pv(pp, vt, 0.1, design=d)
+B.bwta_gemm_pack(a, wp, None, 1.0, 0.5, "bool")
+B.bwta_attn_pv_pack(pp, vt, 0.1, 0.5, "ternary")
+# decode paths: CUDA-core GEMV (M <= 4), skinny tcgen05 (M <= 32), fused pack GEMV, fused attention
+for m in (1, 3, 16):
+    xd = gen.activations((m, 1000), 7 + m).cuda()
+    wd = B.bwta_pack_weight(gen.weights(300, 1000, 8).cuda())
+    B.bwta_gemm(B.bwta_pack_act(xd, 1.6), wd, None, 1.0)
+    B.bwta_gemm(B.bwta_pack_act(xd, 1.6), wd, None, 1.0, y_transposed=True, out_dtype=torch.float32)
+    if m <= 4:
+        B.bwta_gemm_x(xd, 1.6, wd, None)
+q1 = B.bwta_pack_act(gen.activations((2, 3, 1, 64), 9).cuda(), 1.6)
+kd = B.bwta_pack_act(gen.activations((2, 3, 300, 64), 10).cuda(), 1.6)
+vd = B.bwta_pack_act(gen.activations((2, 3, 300, 64), 11).cuda(), 1.6, transpose=True)
+B.bwta_attn_decode(q1, kd, vd, 0.1, 2.0 / 300, 0.01, return_p=True)
 torch.cuda.synchronize()
 print("ok")
