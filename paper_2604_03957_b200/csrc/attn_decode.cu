@@ -11,7 +11,7 @@
 // tensor-core tile.
 //   pass 1: thread j-strided dots, online (max, sum of exp) per thread, merged
 //           across the warp (shuffles) and the CTA (fixed warp order);
-//   pass 2: the dots again, p_j = exp(s_j - max) / sum, round to p_dt, compare,
+//   pass 2: the scores (kept in shared memory), p_j = exp(s_j - max) / sum, round to p_dt, compare,
 //           __ballot_sync -> P word (32 consecutive j) in shared memory;
 //   PV:     thread (d, slice): popc over a slice of V^T row d's words against
 //           the P words; slices summed through shared memory.
@@ -96,9 +96,12 @@ __global__ void __launch_bounds__(AD_WARPS * 32) attn_decode_kernel(DecodeArgs p
     constexpr int NT = AD_WARPS * 32;
     // pass 1: max and sum of exp, online per thread, merged across the CTA
     float mx = -INFINITY, z = 0.f;
+    // this CTA's scores, kept for pass 2 (after the P words and the PV partials)
+    float* sc = reinterpret_cast<float*>(ad_pw + p.sc_off);
     for (int64_t j = j_lo + tid; j < j_hi; j += NT) {
         const int32_t d = qk_dot(qs, qn, qw, kbase_s + j * p.ldk, kbase_n ? kbase_n + j * p.ldk : nullptr);
         const float s = __fmul_rn(float(d), p.alpha);
+        sc[j - j_lo] = s;
         if (s > mx) {
             z = z * expf(mx - s) + 1.f;
             mx = s;
@@ -139,8 +142,7 @@ __global__ void __launch_bounds__(AD_WARPS * 32) attn_decode_kernel(DecodeArgs p
         const int64_t j = j0 + tid;
         bool bit = false;
         if (j < j_hi) {
-            const int32_t d = qk_dot(qs, qn, qw, kbase_s + j * p.ldk, kbase_n ? kbase_n + j * p.ldk : nullptr);
-            const float s = __fmul_rn(float(d), p.alpha);
+            const float s = sc[j - j_lo];  // written by this same thread in pass 1
             const float pj = __fdiv_rn(expf(s - mx), z);
             bit = round_to(p.p_dt, pj) >= p.p_t;
         }
@@ -217,7 +219,8 @@ cudaError_t launch_attn_decode(const DecodeArgs& a, cudaStream_t s) {
     b.cs = cs;
     const int grid = int(entries * cs);
     const int64_t lw = ((a.tk + 31) / 32 + cs - 1) / cs;
-    const size_t smem = sizeof(uint32_t) * (size_t(4 * ((lw + 3) / 4 + 1)) + AD_WARPS * 32);
+    b.sc_off = 4 * ((lw + 3) / 4 + 1) + AD_WARPS * 32;               // words: P words, PV partials, scores
+    const size_t smem = sizeof(uint32_t) * size_t(b.sc_off + 32 * lw);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e != cudaSuccess) return e;

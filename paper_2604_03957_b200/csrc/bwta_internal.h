@@ -153,6 +153,7 @@ struct DecodeArgs {
     uint32_t* p_out;                // optional P planes [entries][p_ld]
     int64_t p_ld, pw_ld;            // words; pw_ld = ld_words(tk)
     int cs;                         // CTAs per entry (set by the launcher)
+    int64_t sc_off;                 // shared-memory word offset of the kept scores (launcher)
 };
 cudaError_t launch_attn_decode(const DecodeArgs& a, cudaStream_t s);
 
