@@ -180,7 +180,7 @@ class Op:
 
 
 def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=3072, fuse_ffn=True,
-               qkv_packs="overlap_sep", fuse_ctx=True):
+               qkv_packs="overlap", fuse_ctx=True):
     """configs[1]: BERT-base layer, seq 128, batch 32 (M = 4096 tokens)."""
     M, D = batch * seq, hidden // heads
     g = lambda s: s + seed  # noqa: E731
