@@ -695,7 +695,7 @@ def main():
     # -------- roofline of the dominant KERNEL: the single-launch op with the largest time
     dom = max((o for o in ops if o.launches == 1), key=lambda o: per_op[o.name])
     t_dom = per_op[dom.name] / 1e3
-    if dom.kind == "pack":
+    if dom.kind == "pack" or args.workload.startswith("decode"):  # decode: the bit-plane stream bounds it
         roof = {"bound": "hbm", "achieved": dom.bytes / t_dom / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s"}
     else:
         roof = {"bound": "tensor", "achieved": dom.ops / t_dom / 1e12, "peak": tc_peak, "unit": "TOPS"}
