@@ -458,7 +458,9 @@ __device__ __forceinline__ void epi_tile_pack(const TcParams& p, uint32_t tacc, 
     }
 }
 
-template <int BN, int ES, int CG>
+// EO = 0: the kernel only ever runs the fp16/bf16 TMA-store epilogue (the common case; the other
+// variants are not compiled in, which shrinks the instruction footprint); EO = 1: every variant.
+template <int BN, int ES, int CG, int EO>
 __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& tmY, uint32_t tmem_base, uint8_t* sOut,
                                          float* sScale, uint64_t* tfull, uint64_t* tempty, int q, int h, int lane,
                                          int64_t tiles_per_entry, int64_t total, int rank, int64_t t0,
@@ -509,17 +511,17 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
         tc_fence_after();
         TRACE(5, tix, h == 0 && q == 0 && lane == 0);
         const uint32_t tacc = tmem_base + uint32_t(acc * BN);
-        if (p.pack_out) {
+        if (EO == 1 && p.pack_out) {
             epi_tile_pack<BN>(p, tacc, reinterpret_cast<uint8_t*>(cs), q, hh, lane, mrow0, nt,
                               int64_t(eb) * p.po_bs + int64_t(eh) * p.po_hs);
-        } else if (ok) {
+        } else if (EO == 0 || ok) {
             if (p.y_dt == DT_BF16)
                 epi_tile_fast<BN, true>(p, tmY, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix,
                                         nstore);
             else
                 epi_tile_fast<BN, false>(p, tmY, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix,
                                          nstore);
-        } else {
+        } else if constexpr (EO == 1) {
             epi_tile_generic<BN, ES>(p, tmY, tacc, stg, q, hh, lane, mrow0, nt, eb, eh);
         }
         tc_fence_before();
@@ -618,7 +620,7 @@ __device__ __forceinline__ uint64_t smem_desc_stage(uint32_t saddr) {
     return smem_desc_sw64(saddr);
 }
 
-template <int BN, int CG, int KS>
+template <int BN, int CG, int KS, int EO>
 __global__ void __launch_bounds__(NT, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
@@ -844,11 +846,11 @@ __global__ void __launch_bounds__(NT, 1)
     } else if (warp >= 4) {
         // ------------------------------ epilogue (warps 4-7 and 12-15) ------------------------------
         const int q = warp & 3, h = warp >= 12 ? 1 : 0;
-        if (p.y_dt == DT_F16 || p.y_dt == DT_BF16)
-            epilogue<BN, 2, CG>(p, tmY, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
+        if (EO == 0 || p.y_dt == DT_F16 || p.y_dt == DT_BF16)
+            epilogue<BN, 2, CG, EO>(p, tmY, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
                                 rank, t0, tstep);
         else
-            epilogue<BN, 4, CG>(p, tmY, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
+            if constexpr (EO == 1) epilogue<BN, 4, CG, EO>(p, tmY, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
                                 rank, t0, tstep);
     }
     TRACE(7, 0, warp == 4 && lane == 0);
@@ -977,11 +979,11 @@ TileChoice choose_tile(int64_t Mk, int64_t Nk, int64_t entries) {
     return best;
 }
 
-template <int BN, int CG, int KS>
+template <int BN, int CG, int KS, int EO>
 cudaError_t launch_ks(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUtensorMap& mb0, const CUtensorMap& mb1,
                       const CUtensorMap& my, const TcParams& p, cudaStream_t s) {
     using C = Cfg<BN, CG, KS>;
-    auto kern = tc_gemm_kernel<BN, CG, KS>;
+    auto kern = tc_gemm_kernel<BN, CG, KS, EO>;
     static bool attr_set = false;  // benign race: the same value may be set twice
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -997,8 +999,12 @@ cudaError_t launch_ks(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUte
 template <int BN, int CG>
 cudaError_t launch_cfg(int ks, const CUtensorMap& ma0, const CUtensorMap& ma1, const CUtensorMap& mb0,
                        const CUtensorMap& mb1, const CUtensorMap& my, const TcParams& p, cudaStream_t s) {
-    return ks == 128 ? launch_ks<BN, CG, 128>(ma0, ma1, mb0, mb1, my, p, s)
-                     : launch_ks<BN, CG, 256>(ma0, ma1, mb0, mb1, my, p, s);
+    const bool fast = !p.pack_out && p.use_tma_store && (p.y_dt == DT_F16 || p.y_dt == DT_BF16);
+    if (fast)
+        return ks == 128 ? launch_ks<BN, CG, 128, 0>(ma0, ma1, mb0, mb1, my, p, s)
+                         : launch_ks<BN, CG, 256, 0>(ma0, ma1, mb0, mb1, my, p, s);
+    return ks == 128 ? launch_ks<BN, CG, 128, 1>(ma0, ma1, mb0, mb1, my, p, s)
+                     : launch_ks<BN, CG, 256, 1>(ma0, ma1, mb0, mb1, my, p, s);
 }
 
 }  // namespace
