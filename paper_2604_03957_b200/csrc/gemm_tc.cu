@@ -459,7 +459,8 @@ __device__ __forceinline__ void epi_tile_pack(const TcParams& p, uint32_t tacc, 
 }
 
 // EO = 0: the kernel only ever runs the fp16/bf16 TMA-store epilogue (the common case; the other
-// variants are not compiled in, which shrinks the instruction footprint); EO = 1: every variant.
+// variants are not compiled in, which shrinks the instruction footprint); EO = 2: only the fused
+// next-layer pack; EO = 1: the generic epilogue (f32 / i32 outputs, layouts TMA cannot store).
 template <int BN, int ES, int CG, int EO>
 __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& tmY, uint32_t tmem_base, uint8_t* sOut,
                                          float* sScale, uint64_t* tfull, uint64_t* tempty, int q, int h, int lane,
@@ -511,10 +512,10 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
         tc_fence_after();
         TRACE(5, tix, h == 0 && q == 0 && lane == 0);
         const uint32_t tacc = tmem_base + uint32_t(acc * BN);
-        if (EO == 1 && p.pack_out) {
+        if (EO == 2) {
             epi_tile_pack<BN>(p, tacc, reinterpret_cast<uint8_t*>(cs), q, hh, lane, mrow0, nt,
                               int64_t(eb) * p.po_bs + int64_t(eh) * p.po_hs);
-        } else if (EO == 0 || ok) {
+        } else if (EO == 0 || (EO == 1 && ok)) {
             if (p.y_dt == DT_BF16)
                 epi_tile_fast<BN, true>(p, tmY, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix,
                                         nstore);
@@ -846,7 +847,7 @@ __global__ void __launch_bounds__(NT, 1)
     } else if (warp >= 4) {
         // ------------------------------ epilogue (warps 4-7 and 12-15) ------------------------------
         const int q = warp & 3, h = warp >= 12 ? 1 : 0;
-        if (EO == 0 || p.y_dt == DT_F16 || p.y_dt == DT_BF16)
+        if (EO != 1 || p.y_dt == DT_F16 || p.y_dt == DT_BF16)
             epilogue<BN, 2, CG, EO>(p, tmY, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
                                 rank, t0, tstep);
         else
@@ -1003,6 +1004,9 @@ cudaError_t launch_cfg(int ks, const CUtensorMap& ma0, const CUtensorMap& ma1, c
     if (fast)
         return ks == 128 ? launch_ks<BN, CG, 128, 0>(ma0, ma1, mb0, mb1, my, p, s)
                          : launch_ks<BN, CG, 256, 0>(ma0, ma1, mb0, mb1, my, p, s);
+    if (p.pack_out)
+        return ks == 128 ? launch_ks<BN, CG, 128, 2>(ma0, ma1, mb0, mb1, my, p, s)
+                         : launch_ks<BN, CG, 256, 2>(ma0, ma1, mb0, mb1, my, p, s);
     return ks == 128 ? launch_ks<BN, CG, 128, 1>(ma0, ma1, mb0, mb1, my, p, s)
                      : launch_ks<BN, CG, 256, 1>(ma0, ma1, mb0, mb1, my, p, s);
 }
