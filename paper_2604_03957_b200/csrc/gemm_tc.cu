@@ -621,7 +621,9 @@ __device__ __forceinline__ uint64_t smem_desc_stage(uint32_t saddr) {
     return smem_desc_sw64(saddr);
 }
 
-template <int BN, int CG, int KS, int EO>
+// KK = 0: operand kinds read from the parameters; KK = 1 + 3 * a_kind + b_kind: fixed at compile
+// time (the common BWTA combinations), so the other unpack variants are not compiled in
+template <int BN, int CG, int KS, int EO, int KK = 0>
 __global__ void __launch_bounds__(NT, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
@@ -653,7 +655,8 @@ __global__ void __launch_bounds__(NT, 1)
     const int lane = threadIdx.x & 31;
     const int rank = CG == 2 ? int(cluster_ctarank()) : 0;
     const bool leader = rank == 0;
-    const int a_planes = nplanes_of(p.a_kind), b_planes = nplanes_of(p.b_kind);
+    const int a_kind_ = KK ? (KK - 1) / 3 : p.a_kind, b_kind_ = KK ? (KK - 1) % 3 : p.b_kind;
+    const int a_planes = nplanes_of(a_kind_), b_planes = nplanes_of(b_kind_);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA0);
@@ -805,7 +808,7 @@ __global__ void __launch_bounds__(NT, 1)
         // ------------------------------ unpack (8-11: B rows, 16-19: A rows) ------------------------------
         const bool is_a = warp >= 16;
         const int ut = threadIdx.x - (is_a ? 512 : 256);  // 0..127
-        const int kind = is_a ? p.a_kind : p.b_kind;
+        const int kind = is_a ? a_kind_ : b_kind_;
         const int rows = is_a ? BM : C::BNC;
         const int plane_bytes = (is_a ? BM : C::BNC) * WPS * 4;
         const uint32_t bready_addr0 = CG == 2 ? mapa_smem(&bready[0], 0) : 0u;
@@ -980,11 +983,11 @@ TileChoice choose_tile(int64_t Mk, int64_t Nk, int64_t entries) {
     return best;
 }
 
-template <int BN, int CG, int KS, int EO>
+template <int BN, int CG, int KS, int EO, int KK = 0>
 cudaError_t launch_ks(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUtensorMap& mb0, const CUtensorMap& mb1,
                       const CUtensorMap& my, const TcParams& p, cudaStream_t s) {
     using C = Cfg<BN, CG, KS>;
-    auto kern = tc_gemm_kernel<BN, CG, KS, EO>;
+    auto kern = tc_gemm_kernel<BN, CG, KS, EO, KK>;
     static bool attr_set = false;  // benign race: the same value may be set twice
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -1001,12 +1004,30 @@ template <int BN, int CG>
 cudaError_t launch_cfg(int ks, const CUtensorMap& ma0, const CUtensorMap& ma1, const CUtensorMap& mb0,
                        const CUtensorMap& mb1, const CUtensorMap& my, const TcParams& p, cudaStream_t s) {
     const bool fast = !p.pack_out && p.use_tma_store && (p.y_dt == DT_F16 || p.y_dt == DT_BF16);
-    if (fast)
+    // the heavy GEMM tiles (BN = 192, 256-K stages) get kinds fixed at compile time for the BWTA
+    // linear's combinations: activations (ternary / bool) x binary weights, and the swapped pack
+    const int kk = 1 + 3 * p.a_kind + p.b_kind;
+    const bool spec = ks == 256 &&
+                      (kk == 1 + 3 * B_TERNARY + B_BINARY || kk == 1 + 3 * B_BOOL + B_BINARY ||
+                       kk == 1 + 3 * B_BINARY + B_TERNARY);
+    if (fast) {
+        if constexpr (BN == 192) if (spec) {
+            if (kk == 1 + 3 * B_TERNARY + B_BINARY) return launch_ks<BN, CG, 256, 0, 1 + 3 * B_TERNARY + B_BINARY>(ma0, ma1, mb0, mb1, my, p, s);
+            if (kk == 1 + 3 * B_BOOL + B_BINARY) return launch_ks<BN, CG, 256, 0, 1 + 3 * B_BOOL + B_BINARY>(ma0, ma1, mb0, mb1, my, p, s);
+            return launch_ks<BN, CG, 256, 0, 1 + 3 * B_BINARY + B_TERNARY>(ma0, ma1, mb0, mb1, my, p, s);
+        }
         return ks == 128 ? launch_ks<BN, CG, 128, 0>(ma0, ma1, mb0, mb1, my, p, s)
                          : launch_ks<BN, CG, 256, 0>(ma0, ma1, mb0, mb1, my, p, s);
-    if (p.pack_out)
+    }
+    if (p.pack_out) {
+        if constexpr (BN == 192) if (spec) {
+            if (kk == 1 + 3 * B_TERNARY + B_BINARY) return launch_ks<BN, CG, 256, 2, 1 + 3 * B_TERNARY + B_BINARY>(ma0, ma1, mb0, mb1, my, p, s);
+            if (kk == 1 + 3 * B_BOOL + B_BINARY) return launch_ks<BN, CG, 256, 2, 1 + 3 * B_BOOL + B_BINARY>(ma0, ma1, mb0, mb1, my, p, s);
+            return launch_ks<BN, CG, 256, 2, 1 + 3 * B_BINARY + B_TERNARY>(ma0, ma1, mb0, mb1, my, p, s);
+        }
         return ks == 128 ? launch_ks<BN, CG, 128, 2>(ma0, ma1, mb0, mb1, my, p, s)
                          : launch_ks<BN, CG, 256, 2>(ma0, ma1, mb0, mb1, my, p, s);
+    }
     return ks == 128 ? launch_ks<BN, CG, 128, 1>(ma0, ma1, mb0, mb1, my, p, s)
                      : launch_ks<BN, CG, 256, 1>(ma0, ma1, mb0, mb1, my, p, s);
 }
