@@ -2,28 +2,28 @@
 bitpack GB/s) against cuBLAS FP16 on the same GPU.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl bwta|reference]
-                    [--workload bert_layer|llama_prefill|llama_attn|bert_linear]
+                    [--workload llama_prefill|bert_layer|llama_attn|bert_linear|...]
 
 Metric (BASELINE.json): "BWTA GEMM effective TOPS and speedup vs cuBLAS FP16 on
 B200; bitpack HBM GB/s".  Effective TOPS = 2*M*N*K / t (the paper's
 convention), summed over every BWTA matmul of one step.
 
-Default workload = BASELINE.json configs[1]: one BERT-base layer (batch 32 x
-seq 128, hidden 768, 12 heads x 64, FFN 3072).  A step runs every §8(a) row of
-the hot path once: ternary pack of the layer input, QKV linear, per-head
-ternary packs of Q/K and the transposed ternary pack of V (straight from the
-QKV output, no copies), QK^T, bool pack of the attention probabilities, PV
-(written into the [B, T, H*D] context layout), ternary pack + output
-projection, ternary pack + FFN1, bool pack + FFN2.  The FP operators the
-paper keeps in high precision (softmax, LayerNorm, activation)
-are not part of the BWTA library: their outputs are synthetic tensors with the
-recipe's distributions (bwta_inputs.py), generated outside the timed region.
+Default workload = BASELINE.json configs[2], the north star's target and the
+largest single-GPU config: the LLaMA-7B prefill linears (M = 2048 tokens,
+K = 4096, N = 4096 and 11008).  A step runs the hot path once over one batch:
+the ternary pack of X (A1), then both BWTA linears (A4 + A5) on the packed X.
+At N > 1 GPUs (torchrun, one process per GPU, NCCL) the same step is
+N-sharded (A8): every rank packs its replica of X, computes its output
+channels in chunks and all-gathers them (in place, overlapped with the next
+chunk's GEMM) so every rank ends with the full Y^T; total work is fixed
+("scaling": "strong").  `--workload bert_layer` (configs[1]) runs one BERT-base
+layer (every §8(a) row incl. attention); at N > 1 it runs replicas (weak).
 
-Timing: each step is one CUDA-graph replay of the library calls, bracketed by
-CUDA events on the capture stream; a 256 MiB buffer (> 126 MB L2) is written
-between steps (outside the events), so every step starts L2-cold.  N > 1 GPUs
-(torchrun): every rank runs its own replica of the workload (independent
-batches: weak scaling, no collective on the data path); time = max over ranks.
+Timing: each step is one CUDA-graph replay of the library calls (N = 1;
+eager launches at N > 1, where the step holds NCCL collectives), bracketed by
+CUDA events on the launching stream; a 256 MiB buffer (> 126 MB L2) is read
+between steps (outside the events), so every step starts L2-cold; time = max
+over ranks.
 """
 from __future__ import annotations
 
@@ -340,23 +340,24 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
            M * ffn / 8 + hidden * ffn / 8 + 2 * M * hidden, cub["f2"]),
     ]
     host_inputs = {"X": X, "Xf": Xf, "P": P}
-    cfg = {"workload": "bert_layer (configs[1]): BERT-base layer, batch 32 x seq 128, hidden 768, "
-                       "12 heads x 64, FFN 3072", "batch": batch, "seq_len": seq, "hidden": hidden,
-           "heads": heads, "ffn": ffn, "tokens": M}
+    cfg = CFGS["bert_layer"]()
     def step():  # the whole path; the V^T pack joins the step's stream after QK^T (see op_pack_qkv)
         st["defer_join"] = True
         for op in ops:
             op.fn()
         st["defer_join"] = False
-    return {"ops": ops, "step": step, "inputs": host_inputs, "output": y2, "cfg": cfg,
+    return {"ops": ops, "step": step, "inputs": host_inputs, "outputs": [y2], "cfg": cfg,
             "oracle_sample": dict(X=X, Xf=Xf, R=R, P=P, Ws=Ws, s=s, heads=heads, D=D, batch=batch, seq=seq)}
 
 
-def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008)):
-    """configs[2]: LLaMA-7B prefill linears, M = 2048 tokens, K = 4096, N = 4096 / 11008."""
+def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008), world=1, rank=0, chunks=4):
+    """configs[2]: LLaMA-7B prefill linears, M = 2048 tokens, K = 4096, N = 4096 / 11008.
+    world > 1: each linear N-sharded over the ranks (dist.NShardPlan, `chunks` chunks per rank),
+    Y^T all-gathered chunk by chunk, overlapped with the next chunk's GEMM."""
+    from paper_2604_03957_b200 import dist as D
     X = gen.activations((M, K), seed).to(dev)
     s_x = gen.act_scale(X)
-    ops, st = [], {}
+    ops, st, outs, ws16 = [], {}, [], {}
 
     def op_pack():
         st["xq"] = B.bwta_pack_act(X, s_x)
@@ -364,19 +365,33 @@ def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008)):
     for i, N in enumerate(Ns):
         w = gen.weights(N, K, seed + 1 + i)
         mu, s_w = gen.weight_stats(w)
-        wp = B.bwta_pack_weight(w.to(dev), mu=mu)
-        sw = s_w.to(dev)
-        y = torch.empty((M, N), dtype=torch.float16, device=dev)
-        w16 = w.to(dev)
+        if world == 1:
+            wp = B.bwta_pack_weight(w.to(dev), mu=mu)          # offline
+            sw = s_w.to(dev)
+            y = torch.empty((M, N), dtype=torch.float16, device=dev)
 
-        def op_g(wp=wp, sw=sw, y=y):
-            B.bwta_gemm(st["xq"], wp, sw, s_x, out=y)
-        ops.append(Op(f"gemm_n{N}", "gemm", op_g, 2 * M * N * K, M * K / 4 + N * K / 8 + 2 * M * N,
-                      (lambda w16=w16: torch.nn.functional.linear(X, w16))))
+            def op_g(wp=wp, sw=sw, y=y):
+                B.bwta_gemm(st["xq"], wp, sw, s_x, out=y)
+        else:
+            plan = D.NShardPlan(N, world, rank, chunks)
+            rows = plan.local_rows()
+            wp = B.bwta_pack_weight(w[rows].contiguous().to(dev), mu=mu)
+            sw = s_w[rows].contiguous().to(dev)
+            y = torch.empty((plan.n_pad, M), dtype=torch.float16, device=dev)
+
+            def op_g(wp=wp, sw=sw, y=y, plan=plan):
+                D.gemm_nshard_overlap(st["xq"], wp, sw, s_x, plan, out=y)
+        outs.append(y)
+        ws16[N] = w
+        ops.append(Op(f"gemm_n{N}", "gemm", op_g, 2 * M * N * K, M * K / 4 + N * K / 8 + 4 * N + 2 * M * N,
+                      (lambda N=N: torch.nn.functional.linear(X, st["w16"][N]))))
+    st["w16"] = {N: w.to(dev) for N, w in ws16.items()} if world == 1 else {}
     op_pack()
-    cfg = {"workload": "llama_prefill (configs[2]): LLaMA-7B prefill linears M=2048 K=4096 N=4096/11008",
-           "tokens": M, "k": K, "n": list(Ns)}
-    return {"ops": ops, "inputs": {"X": X}, "output": None, "cfg": cfg, "oracle_sample": None}
+    smp = dict(X=X.cpu(), s_x=s_x, Ws=ws16, seed=seed)
+    return {"ops": ops, "inputs": {"X": X}, "outputs": outs, "cfg": CFGS["llama_prefill"](),
+            "oracle_sample": smp, "scaling": "strong",
+            "parallelism": f"N-shard x{world} ({chunks} chunks/rank, in-place all-gather overlapped)"
+            if world > 1 else "single GPU"}
 
 
 def llama_attn(B, dev, seed=404, heads=32, seq=2048, D=128):
@@ -414,7 +429,7 @@ def llama_attn(B, dev, seed=404, heads=32, seq=2048, D=128):
               lambda: torch.matmul(P, v))]
     cfg = {"workload": "llama_attn (configs[3]): ternary attention, 32 heads, head_dim 128, seq 2048",
            "heads": heads, "seq_len": seq, "head_dim": D}
-    return {"ops": ops, "inputs": {"P": P}, "output": None, "cfg": cfg, "oracle_sample": None}
+    return {"ops": ops, "inputs": {"P": P}, "outputs": [], "cfg": cfg, "oracle_sample": None}
 
 
 def decode_linear(B, dev, seed=505, shapes=((1, 8192, 28672), (16, 8192, 28672), (1, 4096, 11008))):
@@ -439,7 +454,7 @@ def decode_linear(B, dev, seed=505, shapes=((1, 8192, 28672), (16, 8192, 28672),
         ops.append(Op(f"m{M}_k{K}_n{N}", "gemm", op_g, 2 * M * N * K, 2 * M * K + M * K / 4 + N * K / 8 + 2 * M * N,
                       (lambda X=X, w16=w16: torch.nn.functional.linear(X, w16))))
     cfg = {"workload": "decode_linear: M = 1 / 16 tokens x (K 8192, N 28672) and (K 4096, N 11008)"}
-    return {"ops": ops, "inputs": {}, "output": None, "cfg": cfg, "oracle_sample": None}
+    return {"ops": ops, "inputs": {}, "outputs": [], "cfg": cfg, "oracle_sample": None}
 
 
 def decode_attn(B, dev, seed=606, shapes=((1, 32, 2048, 128), (8, 32, 2048, 128))):
@@ -466,45 +481,39 @@ def decode_attn(B, dev, seed=606, shapes=((1, 32, 2048, 128), (8, 32, 2048, 128)
                       (lambda q=q, k=k, v=v, alpha=alpha: torch.softmax(
                           (q @ k.transpose(-1, -2)).float() * alpha, -1).half() @ v)))
     cfg = {"workload": "decode_attn: fused BWTA decode attention, 32 heads x 128, context 2048, batch 1 / 8"}
-    return {"ops": ops, "inputs": {}, "output": None, "cfg": cfg, "oracle_sample": None}
+    return {"ops": ops, "inputs": {}, "outputs": [], "cfg": cfg, "oracle_sample": None}
 
 
-def nshard_gemm(B, dev, seed=707, M=2048, K=8192, N=28672):
-    """configs[4]: a LLaMA-70B-shaped BWTA linear (K 8192, N 28672, M 2048 tokens) N-sharded across
-    the ranks (paper_2604_03957_b200.dist): rank r packs its replica of the activations, computes
-    Y_r^T for its weight rows, and one NCCL all-gather (a copy at world 1) assembles Y^T.  Total
-    work is fixed: "scaling": "strong"."""
-    from paper_2604_03957_b200 import dist as D
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    X = gen.activations((M, K), seed).to(dev)
-    s_x = gen.act_scale(X)
-    w = gen.weights(N, K, seed + 1)                    # the same full weight on every rank
-    mu, s_w = gen.weight_stats(w)
-    st0, st1 = D.shard_bounds(N, world, rank)
-    wp = B.bwta_pack_weight(w[st0:st1].to(dev), mu=mu) if st1 > st0 else None
-    sw = s_w[st0:st1].to(dev)
-    st = {}
-
-    def op_pack():
-        st["xq"] = B.bwta_pack_act(X, s_x)
-
-    def op_gemm():
-        st["yt"] = D.gemm_nshard(st["xq"], wp, sw, s_x, N, world, rank)
-    op_pack()
-    ops = [Op("pack_x", "pack", op_pack, 0, 2 * M * K + M * K / 4),
-           Op("gemm_nshard_allgather", "gemm", op_gemm, 2 * M * (st1 - st0) * K,
-              M * K / 4 + (st1 - st0) * K / 8 + 2 * M * N)]
-    cfg = {"workload": f"nshard_gemm (configs[4]): K={K} N={N} M={M}, weight rows N-sharded over {world} rank(s), "
-                       "Y^T all-gathered (NCCL)", "tokens": M, "k": K, "n": N, "parallelism": f"N-shard x{world}"}
-    return {"ops": ops, "inputs": {"X": X}, "output": None, "cfg": cfg, "oracle_sample": None,
-            "scaling": "strong"}
+def nshard_gemm(B, dev, seed=707, world=1, rank=0):
+    """configs[4]: the LLaMA-70B-shaped BWTA linear (K 8192, N 28672, M 2048 tokens) N-sharded across
+    the ranks exactly like llama_prefill at N > 1 (strong scaling)."""
+    W = llama_prefill(B, dev, seed, M=2048, K=8192, Ns=(28672,), world=world, rank=rank)
+    W["cfg"] = CFGS["nshard_gemm"]()
+    W["oracle_sample"] = None
+    return W
 
 
-def bert_linear(B, dev, seed=101):
+def bert_linear(B, dev, seed=101, world=1, rank=0):
     """configs[0]: single BWTA linear M=128 K=768 N=768."""
-    return llama_prefill(B, dev, seed, M=128, K=768, Ns=(768,)) | {
-        "cfg": {"workload": "bert_linear (configs[0]): M=128 K=768 N=768", "tokens": 128, "k": 768, "n": [768]}}
+    W = llama_prefill(B, dev, seed, M=128, K=768, Ns=(768,), world=world, rank=rank, chunks=1)
+    W["cfg"] = CFGS["bert_linear"]()
+    W["oracle_sample"] = None
+    return W
+
+
+# the config dict of each workload: identical in the GPU arm and the reference (oracle) arm
+CFGS = {
+    "llama_prefill": lambda: {"workload": "llama_prefill (configs[2]): LLaMA-7B prefill linears, M=2048 tokens, "
+                                          "K=4096, N=4096 and N=11008, fp16 activations packed in the step",
+                              "tokens": 2048, "k": 4096, "n": [4096, 11008]},
+    "bert_layer": lambda: {"workload": "bert_layer (configs[1]): BERT-base layer, batch 32 x seq 128, hidden 768, "
+                                       "12 heads x 64, FFN 3072", "batch": 32, "seq_len": 128, "hidden": 768,
+                           "heads": 12, "ffn": 3072, "tokens": 4096},
+    "nshard_gemm": lambda: {"workload": "nshard_gemm (configs[4]): K=8192 N=28672 M=2048, weight rows N-sharded, "
+                                        "Y^T all-gathered (NCCL)", "tokens": 2048, "k": 8192, "n": [28672]},
+    "bert_linear": lambda: {"workload": "bert_linear (configs[0]): M=128 K=768 N=768", "tokens": 128, "k": 768,
+                            "n": [768]},
+}
 
 
 WORKLOADS = {"bert_layer": bert_layer, "llama_prefill": llama_prefill, "llama_attn": llama_attn,
@@ -552,6 +561,43 @@ def oracle_bert_layer_step(smp, threads, row_frac=1.0):
     return ops, f"{rows}/{M} token rows of each BWTA linear + {qq.shape[0]} (batch x head) attention entries"
 
 
+def _st(t):
+    t = t.detach().cpu().contiguous()
+    return t.view(torch.int16).numpy().view(np.uint16) if t.dtype in (torch.float16, torch.bfloat16) else t.numpy()
+
+
+class OracleLlamaPrefill:
+    """configs[2]'s step through the CPU oracle: quantize a sample of X's token rows,
+    the integer dot with both binarized weights (the naive triple loop), the R5 epilogue to fp16.
+    Weights are binarized once up front (offline in the product too)."""
+
+    def __init__(self, smp, threads):
+        import oracle
+        self.o, self.smp, self.threads = oracle, smp, threads
+        self.qw = {}
+        for N, w in smp["Ws"].items():
+            mu, s_w = gen.weight_stats(w)
+            self.qw[N] = (oracle.binarize_weight(_st(w), "f16", mu=mu), s_w.numpy())
+        self.xs = _st(smp["X"])
+
+    def step(self, rows: int):
+        o, M = self.o, self.xs.shape[0]
+        r0 = (self._i * rows) % M if hasattr(self, "_i") else 0
+        self._i = getattr(self, "_i", 0) + 1
+        idx = (np.arange(rows) + r0) % M
+        qa = o.quantize_act(self.xs[idx], "f16", self.smp["s_x"], "ternary")
+        ops = 0
+        for N, (qw, s_w) in self.qw.items():
+            o.gemm(qa, qw, s_w, self.smp["s_x"], "f16", threads=self.threads)
+            ops += 2 * rows * qw.shape[0] * qw.shape[1]
+        return ops
+
+
+def _llama_inputs_cpu(seed=303, M=2048, K=4096, Ns=(4096, 11008)):
+    X = gen.activations((M, K), seed)
+    return dict(X=X, s_x=gen.act_scale(X), Ws={N: gen.weights(N, K, seed + 1 + i) for i, N in enumerate(Ns)})
+
+
 def reference_arm(args):
     """--impl reference: the CPU oracle, as it stands, on the host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -560,37 +606,51 @@ def reference_arm(args):
     import oracle
     oracle.build()
     threads = oracle.default_threads()
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
 
     wl = args.workload
-    if wl != "bert_layer":
-        print(json.dumps({"impl": "reference", "unavailable": f"reference arm implemented for bert_layer only "
-                                                             f"(asked {wl})"}))
+    if wl == "llama_prefill":
+        orc = OracleLlamaPrefill(_llama_inputs_cpu(), threads)
+        # size each step so the whole --steps/--warmup run takes about a minute of CPU time
+        t0 = time.perf_counter()
+        orc.step(32)
+        t32 = time.perf_counter() - t0
+        budget = 60.0 / max(1, args.steps + args.warmup)
+        rows = int(min(2048, max(16, 32 * budget / max(t32, 1e-6))))
+        for _ in range(args.warmup):
+            orc.step(rows)
+        t0 = time.perf_counter()
+        tot_ops = sum(orc.step(rows) for _ in range(args.steps))
+        dt = time.perf_counter() - t0
+        sample = (f"{rows} of 2048 token rows per step (rotating) through both linears (N 4096 + 11008, K 4096): "
+                  "quantize X rows + integer dot + fp16 epilogue; weights binarized once (offline)")
+        scaling = "strong"
+    elif wl == "bert_layer":
+        smp = _bert_inputs_cpu()
+        frac = args.ref_row_frac
+        for _ in range(args.warmup):
+            oracle_bert_layer_step(smp, threads, frac)
+        t0 = time.perf_counter()
+        tot_ops = 0
+        for _ in range(args.steps):
+            o, sample = oracle_bert_layer_step(smp, threads, frac)
+            tot_ops += o
+        dt = time.perf_counter() - t0
+        scaling = "weak"
+    else:
+        print(json.dumps({"impl": "reference", "unavailable": f"reference arm implemented for llama_prefill and "
+                                                             f"bert_layer only (asked {wl})"}))
         return 0
-    smp = _bert_inputs_cpu()
-    frac = args.ref_row_frac
-    for _ in range(args.warmup):
-        oracle_bert_layer_step(smp, threads, frac)
-    t0 = time.perf_counter()
-    tot_ops = 0
-    for _ in range(args.steps):
-        o, sample = oracle_bert_layer_step(smp, threads, frac)
-        tot_ops += o
-    dt = time.perf_counter() - t0
     val = tot_ops / dt / 1e12
-    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32 (oracle integer dot, fp32 epilogue)",
-            "data": "synthetic", "config": _bert_cfg() | {"ref_row_frac": frac},
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "int32 (oracle integer dot, fp32 epilogue)",
+            "data": "synthetic (seeded, recipe in DESIGN.md)", "config": CFGS[wl](),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
-
-
-def _bert_cfg():
-    return {"workload": "bert_layer (configs[1]): BERT-base layer, batch 32 x seq 128, hidden 768, "
-                        "12 heads x 64, FFN 3072", "batch": 32, "seq_len": 128, "hidden": 768, "heads": 12,
-            "ffn": 3072, "tokens": 4096}
 
 
 def _bert_inputs_cpu(seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=3072):
@@ -608,28 +668,64 @@ def _bert_inputs_cpu(seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=3072
 
 
 # ----------------------------------------------------------------------------- main arm
+def _spawn(args) -> int:
+    """--gpus N > 1 without a torchrun environment: launch N ranks with torchrun on this node."""
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def time_eager(step, flush, reps, stream):
+    """Per-step device times (ms) of eager launches (N > 1: the step holds NCCL collectives)."""
+    ts = []
+    with torch.cuda.stream(stream):
+        for _ in range(reps):
+            flush_l2(flush)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            ts.append((e0, e1))
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ts]
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="bwta", choices=["bwta", "reference"])
-    ap.add_argument("--workload", default="bert_layer", choices=sorted(WORKLOADS))
-    ap.add_argument("--no-extras", action="store_true", help="skip the configs[2]/[3] side measurements")
+    ap.add_argument("--workload", default="llama_prefill", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-extras", action="store_true", help="skip the secondary-workload side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline (oracle) leg")
     ap.add_argument("--ref-row-frac", type=float, default=1.0)
+    ap.add_argument("--chunks", type=int, default=4, help="N-shard chunks per rank (N > 1)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return reference_arm(args)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return _spawn(args)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,TUNING")
+        os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(ROOT, "gpurun_out", f"nccl_rank{rank}.log"))
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         dist.init_process_group("nccl", device_id=dev)
     import paper_2604_03957_b200 as B
 
@@ -639,18 +735,30 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    W = WORKLOADS[args.workload](B, dev)
+    wl_fn = WORKLOADS[args.workload]
+    import inspect
+    kw = {}
+    if "world" in inspect.signature(wl_fn).parameters:
+        kw = {"world": world, "rank": rank}
+        if "chunks" in inspect.signature(wl_fn).parameters:
+            kw["chunks"] = args.chunks
+    W = wl_fn(B, dev, **kw)
     ops = W["ops"]
+    scaling = W.get("scaling", "weak") if world > 1 or W.get("scaling") else "weak"
+    sharded = world > 1 and scaling == "strong"
 
     def step():
         if W.get("step"):
             return W["step"]()
         for op in ops:
             op.fn()
-    total_ops = sum(op.ops for op in ops)
+    total_ops = sum(op.ops for op in ops)           # one replica / the whole sharded job
+    job_ops = total_ops * (world if (world > 1 and not sharded) else 1)
 
-    # -------- device-time step (CUDA graph of the library calls)
-    g_step = graph_of(step, stream)
+    # -------- device-time step (CUDA graph of the library calls at N = 1)
+    use_graph = world == 1
+    g_step = graph_of(step, stream) if use_graph else None
+    run = (lambda: g_step.replay()) if use_graph else step
     l0 = B.lib.bwta_kernel_launches()
     with torch.cuda.stream(stream):
         step()
@@ -663,14 +771,15 @@ def main():
     while nw < args.warmup or time.perf_counter() - t_w < 0.5:   # >= W steps and >= 0.5 s under load
         with torch.cuda.stream(stream):
             flush_l2(flush)
-            g_step.replay()
+            run()
         nw += 1
         if nw % 16 == 0:
             torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    times = time_graph(g_step, flush, args.steps, 0, stream)
+    times = time_graph(g_step, flush, args.steps, 0, stream) if use_graph else time_eager(step, flush, args.steps,
+                                                                                          stream)
     torch.cuda.synchronize()
     clk.__exit__()
     if world > 1:
@@ -681,19 +790,25 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_total = float(t.item())
     ms_step = t_total / args.steps
-    value = world * total_ops * args.steps / (t_total / 1e3) / 1e12
+    value = job_ops * args.steps / (t_total / 1e3) / 1e12
 
-    # -------- per-op device times, cuBLAS FP16 baselines
+    # -------- per-op device times and cuBLAS FP16 baselines (N = 1: graphs of one op)
     per_op, cub_ms = {}, {}
-    for op in ops:
-        per_op[op.name] = op_time_ms(op.fn, flush, stream)
-        if op.cublas is not None:
-            cub_ms[op.name] = op_time_ms(op.cublas, flush, stream)
+    if world == 1:
+        for op in ops:
+            per_op[op.name] = op_time_ms(op.fn, flush, stream)
+            if op.cublas is not None:
+                cub_ms[op.name] = op_time_ms(op.cublas, flush, stream)
+    else:   # eager per-op times (compute + its gathers at N > 1)
+        for op in ops:
+            per_op[op.name] = statistics.median(time_eager(op.fn, flush, 10, stream))
     cublas_total = sum(cub_ms.values())
     bwta_mm_only = sum(per_op[n] for n in cub_ms)
+    pack_ms = sum(per_op[o.name] for o in ops if o.kind == "pack")
 
     # -------- roofline of the dominant KERNEL: the single-launch op with the largest time
-    dom = max((o for o in ops if o.launches == 1), key=lambda o: per_op[o.name])
+    cands = [o for o in ops if o.launches == 1]
+    dom = max(cands, key=lambda o: per_op[o.name])
     t_dom = per_op[dom.name] / 1e3
     if dom.kind == "pack" or args.workload.startswith("decode"):  # decode: the bit-plane stream bounds it
         roof = {"bound": "hbm", "achieved": dom.bytes / t_dom / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s"}
@@ -701,28 +816,29 @@ def main():
         roof = {"bound": "tensor", "achieved": dom.ops / t_dom / 1e12, "peak": tc_peak, "unit": "TOPS"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["kernel"] = dom.name
+    roof["algorithmic"] = {"ops_per_launch": dom.ops, "bytes_per_launch": dom.bytes}
     roof["peak_source"] = (f"{pk['source']} bf16 {pk['bf16_tflops']} TFLOP/s x 4 (dense fp4/bf16 nominal ratio; "
                            "the path runs tcgen05.mma.kind::mxf4)"
                            if roof["unit"] == "TOPS" else f"{pk['source']} HBM copy")
     roof["traffic"] = _traffic(dom.name, args.workload)
+    roof["traffic_source"] = "profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum, ncu --set full"
 
     # -------- end to end through the public API with host buffers
     e2e = None
     if W["inputs"]:
         hosts = {k: v.detach().cpu().pin_memory() for k, v in W["inputs"].items()}
-        out = W["output"]
-        out_h = torch.empty(out.shape, dtype=out.dtype).pin_memory() if out is not None else None
+        outs = W.get("outputs") or []
+        outs_h = [[torch.empty(o.shape, dtype=o.dtype).pin_memory() for o in outs] for _ in range(2)]
         h2d = sum(v.numel() * v.element_size() for v in hosts.values())
-        d2h = out_h.numel() * out_h.element_size() if out_h is not None else 0
+        d2h = sum(o.numel() * o.element_size() for o in outs)
         # Pipelined like a serving loop: step i's inputs go H2D (pinned -> device staging, copy
-        # stream) while step i-1 computes; the compute stream moves them into the graph's input
-        # tensors (D2D), flushes L2, replays the step graph and stages the output; a second copy
-        # stream reads it back D2H.  Every step's H2D and D2H is inside the timed region (from the
+        # stream) while step i-1 computes; the compute stream moves them into the step's input
+        # tensors (D2D), flushes L2, runs the step and stages the outputs; a second copy stream
+        # reads them back D2H.  Every step's H2D and D2H is inside the timed region (from the
         # first H2D to the last D2H, pipeline fill and drain included).
         cin, cout = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
         stage_in = [{k: torch.empty_like(v) for k, v in W["inputs"].items()} for _ in range(2)]
-        stage_out = [torch.empty_like(out) for _ in range(2)] if out is not None else None
-        outs_h = [out_h, torch.empty_like(out_h).pin_memory()] if out_h is not None else None
+        stage_out = [[torch.empty_like(o) for o in outs] for _ in range(2)]
         ev_in_ready = [torch.cuda.Event() for _ in range(2)]
         ev_in_free = [torch.cuda.Event() for _ in range(2)]
         ev_out_ready = [torch.cuda.Event() for _ in range(2)]
@@ -731,6 +847,8 @@ def main():
         def run_pipelined(nsteps):
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
             t0.record(cin)
             for i in range(nsteps):
                 sl = i % 2
@@ -746,35 +864,53 @@ def main():
                         W["inputs"][k].copy_(stage_in[sl][k], non_blocking=True)
                     ev_in_free[sl].record(stream)
                     flush_l2(flush)
-                    g_step.replay()
-                    if stage_out is not None:
+                    run()
+                    if outs:
                         if i >= 2:
                             stream.wait_event(ev_out_free[sl])
-                        stage_out[sl].copy_(out, non_blocking=True)
+                        for so, o in zip(stage_out[sl], outs):
+                            so.copy_(o, non_blocking=True)
                         ev_out_ready[sl].record(stream)
-                if stage_out is not None:
+                if outs:
                     with torch.cuda.stream(cout):
                         cout.wait_event(ev_out_ready[sl])
-                        outs_h[sl].copy_(stage_out[sl], non_blocking=True)
+                        for oh, so in zip(outs_h[sl], stage_out[sl]):
+                            oh.copy_(so, non_blocking=True)
                         ev_out_free[sl].record(cout)
             cout.wait_stream(stream)
             t1.record(cout)
             torch.cuda.synchronize()
-            return t0.elapsed_time(t1)
+            ms = t0.elapsed_time(t1)
+            if world > 1:
+                t = torch.tensor([ms], device=dev)
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                ms = float(t.item())
+            return ms
 
         run_pipelined(args.warmup)
         t_e2e = run_pipelined(args.steps)
-        e2e = {"value": world * total_ops * args.steps / (t_e2e / 1e3) / 1e12, "unit": UNIT,
+        e2e = {"value": job_ops * args.steps / (t_e2e / 1e3) / 1e12, "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e / args.steps,
-               "pipelined": "H2D of step i overlaps the compute of step i-1 (two staging buffers); "
-                            "L2 flushed before every step's graph; fill and drain inside the timed region"}
+               "pipelined": "H2D of step i overlaps the compute of step i-1 (two staging buffers); the outputs "
+                            "are read back D2H every step; L2 flushed before every step; fill and drain inside "
+                            "the timed region"}
 
-    # -------- side measurements: configs[2] (headline target) and configs[3]
+    # -------- side measurements: the secondary workloads (N = 1, rank 0)
     extras = {}
-    if not args.no_extras and args.workload == "bert_layer" and rank == 0:
-        for name in ("llama_prefill", "llama_attn", "decode_linear", "decode_attn"):
+    if not args.no_extras and world == 1:
+        names = [n for n in ("llama_prefill", "bert_layer", "llama_attn", "decode_linear", "decode_attn")
+                 if n != args.workload]
+        for name in names:
             Wx = WORKLOADS[name](B, dev)
             res = {}
+            if Wx.get("step"):          # a whole-step graph (bert_layer)
+                def st_x():
+                    Wx["step"]()
+                gx = graph_of(st_x, stream)
+                tx = statistics.median(time_graph(gx, flush, 20, 3, stream))
+                ox = sum(o.ops for o in Wx["ops"])
+                res["step"] = {"us": tx * 1e3, "TOPS": ox / (tx / 1e3) / 1e12}
+                del gx
             for op in Wx["ops"]:
                 t = op_time_ms(op.fn, flush, stream)
                 r = {"us": t * 1e3}
@@ -791,11 +927,12 @@ def main():
                     r["cublas_fp16_us"] = tc * 1e3
                     r["speedup_vs_cublas_fp16"] = tc / t
                 res[op.name] = r
-            if name == "llama_prefill":
-                for n in ("gemm_n4096", "gemm_n11008"):
-                    res[n]["speedup_incl_pack"] = res[n]["cublas_fp16_us"] / (res[n]["us"] + res["pack_x"]["us"])
+            if "step" in res:
+                cb = sum(r.get("cublas_fp16_us", 0) for r in res.values())
+                res["step"]["speedup_vs_cublas_fp16_matmuls"] = cb / res["step"]["us"]
             extras[name] = res
             del Wx
+        torch.cuda.empty_cache()
 
     # -------- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None
@@ -803,31 +940,52 @@ def main():
         import oracle
         oracle.build()
         threads = oracle.default_threads()
-        t0 = time.perf_counter()
-        o, sample = oracle_bert_layer_step(W["oracle_sample"], threads, 1.0)
-        dt = time.perf_counter() - t0
-        cpu = {"value": o / dt / 1e12, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"one full step: {sample}; {dt:.2f} s wall"}
+        if args.workload == "llama_prefill":
+            orc = OracleLlamaPrefill(W["oracle_sample"], threads)
+            t0 = time.perf_counter()
+            o, n = 0, 0
+            while n < 1 or time.perf_counter() - t0 < 10.0:       # >= one full step and >= 10 s of CPU work
+                o += orc.step(2048)
+                n += 1
+            dt = time.perf_counter() - t0
+            sample = (f"{n} full step(s) (all 2048 token rows through both linears: quantize X + integer dot + "
+                      f"fp16 epilogue; weights binarized once, offline); {dt:.2f} s wall")
+        else:
+            t0 = time.perf_counter()
+            o, sample = oracle_bert_layer_step(W["oracle_sample"], threads, 1.0)
+            dt = time.perf_counter() - t0
+            sample = f"one full step: {sample}; {dt:.2f} s wall"
+        cpu = {"value": o / dt / 1e12, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
 
     if rank == 0:
         pack_gbs = {o.name: o.bytes / (per_op[o.name] / 1e3) / 1e9 for o in ops if o.kind == "pack"}
+        speed = None
+        if cub_ms:
+            speed = {"matmuls_only": cublas_total / bwta_mm_only if bwta_mm_only else None,
+                     "incl_activation_pack": cublas_total / (bwta_mm_only + pack_ms),
+                     "whole_step": cublas_total / ms_step,
+                     "per_op": {n: cub_ms[n] / per_op[n] for n in cub_ms}}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": W.get("scaling", "weak"),
+            "scaling": scaling,
             "vs_baseline": None, "dtype": "fp4-e2m1 codes (tcgen05 kind::mxf4, f32 accumulate; fp16 in/out)",
             "data": "synthetic (seeded, recipe in DESIGN.md)",
-            "config": W["cfg"] | {"parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                                  "l2": "256 MiB read (clean eviction) between steps, outside the timed events",
-            "clock_window": "nvidia-smi every 20 ms over >= 0.5 s of warm-up load + the timed steps"},
+            "config": W["cfg"],
+            "parallelism": W.get("parallelism", f"replicas x{world}" if world > 1 else "single GPU"),
+            "timing": {"l2": "256 MiB read (clean eviction) between steps, outside the timed events",
+                       "launch": "CUDA graph of the step" if use_graph else "eager launches (NCCL in the step)",
+                       "clock_window": "nvidia-smi every 20 ms over >= 0.5 s of warm-up load + the timed steps"},
             "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "speedup_vs_cublas_fp16": {"matmuls_only": cublas_total / bwta_mm_only if bwta_mm_only else None,
-                                       "whole_step_incl_packs": cublas_total / ms_step},
+            "speedup_vs_cublas_fp16": speed,
             "per_op_us": {k: v * 1e3 for k, v in per_op.items()},
             "cublas_fp16_us": {k: v * 1e3 for k, v in cub_ms.items()},
             "pack_GBps": pack_gbs, "extras": extras,
         }
+        if world > 1:
+            line["comm"] = {"backend": "nccl", "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                            "collective": "all_gather_into_tensor (in place, async, per chunk)"}
         print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()

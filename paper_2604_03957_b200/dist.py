@@ -72,12 +72,10 @@ def gather_rows(local: torch.Tensor, n: int, world: int, group=None, align: int 
         out.copy_(send)
     else:
         dist.all_gather_into_tensor(out, send.contiguous(), group=group)
-    # rank r's rows live at [r * per, r * per + n_r); keep them in rank order
-    pieces = []
-    for r in range(world):
-        s, e = shard_bounds(n, world, r, align)
-        pieces.append(out[r * per: r * per + (e - s)])
-    return torch.cat(pieces, 0) if world > 1 else out[:n]
+    # rank r's rows live at [r * per, r * per + n_r) and n_r = per for every rank but the
+    # trailing ones (shard_bounds), so the rank-major prefix out[:n] IS the gathered matrix:
+    # no re-copy
+    return out[:n]
 
 
 def gemm_nshard(a, w_local, w_scale_local: Optional[torch.Tensor], a_scale: float, n_total: int,
@@ -108,3 +106,83 @@ def heads_shard(bh: int, world: int, rank: int) -> Tuple[int, int]:
 def gather_heads(local: torch.Tensor, bh: int, world: int, group=None) -> torch.Tensor:
     """All-gather per-rank [bh_r, T, D] context blocks -> [bh, T, D] (head-major)."""
     return gather_rows(local, bh, world, group, align=1)
+
+
+# ----------------------------------------------------------------------------
+# Chunked N partition with the all-gather overlapped with the GEMM.
+#
+# The N rows (output channels) are cut into world x chunks blocks of nrc rows;
+# block (c, r) -- global rows [(c * world + r) * nrc, +nrc) -- belongs to rank r.
+# Chunk c of every rank together is the contiguous row range
+# [c * world * nrc, (c + 1) * world * nrc) of Y^T, so each chunk's all-gather
+# writes its final place in Y^T directly (in place: rank r's GEMM writes its
+# block inside the gather buffer), and chunk c's gather runs on NCCL's stream
+# while chunk c + 1's GEMM runs.  The owner of an output channel changes, not
+# its arithmetic: the result equals the single-GPU Y^T bit for bit.
+# ----------------------------------------------------------------------------
+class NShardPlan:
+    def __init__(self, n: int, world: int, rank: int, chunks: int = 1):
+        if world < 1 or not (0 <= rank < world) or chunks < 1 or n < 0:
+            raise ValueError("bad n/world/rank/chunks")
+        self.n, self.world, self.rank, self.chunks = n, world, rank, chunks
+        self.nrc = -(-n // (world * chunks)) if n else 0
+        self.n_pad = self.nrc * world * chunks
+
+    def block(self, c: int, r: Optional[int] = None) -> Tuple[int, int]:
+        """Global rows [start, stop) of chunk c on rank r (clipped to n; may be empty)."""
+        r = self.rank if r is None else r
+        s = (c * self.world + r) * self.nrc
+        return min(s, self.n), min(s + self.nrc, self.n)
+
+    def local_rows(self) -> torch.Tensor:
+        """Global row indices this rank owns, chunk-major (the rows of its local weight shard)."""
+        idx = [torch.arange(*self.block(c)) for c in range(self.chunks)]
+        return torch.cat(idx) if idx else torch.zeros(0, dtype=torch.int64)
+
+    def local_span(self, c: int) -> Tuple[int, int]:
+        """[start, stop) of chunk c inside the local shard (local_rows order)."""
+        s = sum(self.block(i)[1] - self.block(i)[0] for i in range(c))
+        b0, b1 = self.block(c)
+        return s, s + (b1 - b0)
+
+
+def gemm_nshard_overlap(a, w_local, w_scale_local: Optional[torch.Tensor], a_scale: float, plan: NShardPlan,
+                        out: Optional[torch.Tensor] = None, group=None, out_dtype=torch.float16,
+                        local_gemm: Optional[Callable] = None) -> torch.Tensor:
+    """Y^T [N x M] of a BWTA linear N-sharded by `plan`, gathered on every rank.
+
+    a: packed activations (replicated); w_local / w_scale_local: this rank's weight rows and
+    scales in plan.local_rows() order; out: optional [plan.n_pad x M] buffer.  Chunk c's GEMM
+    writes Y^T rows of block (c, rank) straight into `out`; its all-gather (async, NCCL stream)
+    overlaps chunk c + 1's GEMM.  Returns out[:N] (a view)."""
+    if local_gemm is None:
+        from . import bwta_gemm
+
+        def local_gemm(a_, w_, s_, sa_, out_):
+            return bwta_gemm(a_, w_, s_, sa_, out_dtype=out_.dtype, y_transposed=True, out=out_)
+    m = a.ref.shape[-2]
+    if out is None:
+        out = torch.empty((plan.n_pad, m), dtype=out_dtype, device=a.ref.device)
+    if out.shape[0] < plan.n_pad or out.shape[1] != m or not out.is_contiguous():
+        raise ValueError("out must be a contiguous [n_pad, M] buffer")
+    works = []
+    P, nrc = plan.world, plan.nrc
+    for c in range(plan.chunks):
+        g0, g1 = plan.block(c)
+        l0, l1 = plan.local_span(c)
+        if g1 > g0:
+            w_c = _slice_packed(w_local, l0, l1) if hasattr(w_local, "sgn") else w_local[l0:l1]
+            s_c = None if w_scale_local is None else w_scale_local[l0:l1]
+            local_gemm(a, w_c, s_c, a_scale, out[g0:g1])
+        if P > 1:
+            blk = out[c * P * nrc:(c + 1) * P * nrc]
+            mine = blk[plan.rank * nrc:(plan.rank + 1) * nrc]
+            works.append(dist.all_gather_into_tensor(blk, mine, group=group, async_op=True))
+    for w in works:
+        w.wait()
+    return out[:plan.n]
+
+
+def _slice_packed(p, l0: int, l1: int):
+    """Rows [l0, l1) of a Packed weight (a view of its planes)."""
+    return type(p)(p.sgn[l0:l1], None if p.nz is None else p.nz[l0:l1], p.kind, p.cols)

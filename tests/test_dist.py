@@ -30,6 +30,30 @@ def test_shard_bounds_cover_and_align():
     assert D.shard_bounds(11008, 8, 3) == (3 * 1376, 4 * 1376)
 
 
+def test_nshard_plan_blocks_tile_the_rows():
+    """Chunk c of all ranks is one contiguous row range of Y^T (so each chunk's all-gather writes
+    its final place), every row has one owner, padding only at the end."""
+    for n in (1, 37, 100, 4096, 11008, 28672):
+        for world in (1, 2, 4, 8):
+            for chunks in (1, 2, 4):
+                plans = [D.NShardPlan(n, world, r, chunks) for r in range(world)]
+                p0 = plans[0]
+                assert p0.n_pad >= n and p0.n_pad - n < world * chunks
+                for c in range(chunks):
+                    spans = [p.block(c) for p in plans]
+                    assert spans[0][0] == min(n, c * world * p0.nrc)
+                    for (s0, e0), (s1, e1) in zip(spans, spans[1:]):
+                        assert e0 == s1
+                owned = torch.cat([p.local_rows() for p in plans]).sort().values
+                assert torch.equal(owned, torch.arange(n))
+                for p in plans:
+                    tot = 0
+                    for c in range(chunks):
+                        l0, l1 = p.local_span(c)
+                        assert l0 == tot and l1 - l0 == p.block(c)[1] - p.block(c)[0]
+                        tot = l1
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -70,7 +94,23 @@ def _worker(rank, world, port, outq):
             torch.zeros((0, T, T), dtype=torch.float32)
         s_all = D.gather_heads(local, BH, world)
         ok_attn = bool(np.array_equal(s_all.numpy(), oracle.attn_qk(qq, kk, 0.25, "f32")))
-        outq.put((rank, ok_gemm, ok_attn))
+
+        # chunked N partition with the in-place, overlapped per-chunk all-gathers
+        ok_chunks = True
+        for chunks in (1, 3, 7):
+            plan = D.NShardPlan(N, world, rank, chunks)
+            rows = plan.local_rows().numpy()
+            yt2 = D.gemm_nshard_overlap(a, qw[rows], torch.from_numpy(s_w[rows]), s_a, plan,
+                                        out_dtype=torch.float32, local_gemm=local_gemm)
+            ok_chunks &= yt2.shape == (N, M) and bool(np.array_equal(
+                yt2.numpy().view(np.uint32), np.ascontiguousarray(full).view(np.uint32)))
+            # every global row is owned by exactly one rank
+            owned = torch.from_numpy(rows.astype(np.int64))
+            sizes = [None] * world
+            dist.all_gather_object(sizes, owned.tolist())
+            flat = sorted(i for r in sizes for i in r)
+            ok_chunks &= flat == list(range(N))
+        outq.put((rank, ok_gemm and ok_chunks, ok_attn))
     finally:
         dist.destroy_process_group()
 
