@@ -97,7 +97,7 @@ typedef enum { BWTA_BINARY = 0, BWTA_BOOL = 1, BWTA_TERNARY = 2 } bwta_kind_t;
 typedef enum {
     BWTA_DESIGN_AUTO = 0,      /* pick per shape */
     BWTA_DESIGN_CUDA_CORE = 1, /* design (a): LOP3 + POPC bit-serial on CUDA cores */
-    BWTA_DESIGN_TCGEN05 = 2    /* design (b): unpack to int8 + tcgen05.mma.kind::i8 */
+    BWTA_DESIGN_TCGEN05 = 2    /* design (b): unpack to E2M1 codes + tcgen05.mma.kind::mxf4 (FP32 acc, exact) */
 } bwta_design_t;
 
 /* Options for the matmul entry points; NULL = all defaults (zero-initialised). */

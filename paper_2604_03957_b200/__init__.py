@@ -99,6 +99,22 @@ def _batch_dims(t: torch.Tensor):
     raise ValueError("expected a 2-, 3- or 4-D tensor")
 
 
+def _check_out(out: torch.Tensor, shape: tuple, device, what: str):
+    """A caller-supplied output must have the result's shape, a supported dtype, live on the
+    operands' device and have unit stride along its last dimension (the C ABI receives only the
+    pointer and the leading strides; a wrong `out` would be written out of bounds)."""
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError(f"{what}: out has shape {tuple(out.shape)}, expected {tuple(shape)}")
+    if out.dtype not in _DT:
+        raise ValueError(f"{what}: unsupported out dtype {out.dtype}")
+    if out.device != torch.device(device):
+        raise ValueError(f"{what}: out is on {out.device}, operands on {device}")
+    if out.dim() and out.shape[-1] > 1 and out.stride(-1) != 1:
+        raise ValueError(f"{what}: out must have unit stride in its last dimension")
+    if out.dim() >= 2 and out.shape[-2] > 1 and out.stride(-2) < out.shape[-1]:
+        raise ValueError(f"{what}: out rows overlap (row stride < row length)")
+
+
 _WS: dict = {}
 
 
@@ -206,6 +222,8 @@ def bwta_gemm(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: fl
     dev = ar.device
     if out is None:
         out = torch.empty((n, m) if y_transposed else (m, n), dtype=out_dtype, device=dev)
+    else:
+        _check_out(out, (n, m) if y_transposed else (m, n), dev, "bwta_gemm")
     o = _opts(design, tile)
     ws, wsb = _workspace(lib.bwta_gemm_workspace_size(m, n, k, o), dev)
     ws_scale = None if w_scale is None else w_scale.to(device=dev, dtype=torch.float32).contiguous()
@@ -273,6 +291,8 @@ def bwta_attn_qk(q: Packed, k: Packed, alpha: float, out_dtype=torch.float16,
         raise ValueError("Q and K must have the same head dim")
     if out is None:
         out = torch.empty(tuple(qr.shape[:-2]) + (tq, tk), dtype=out_dtype, device=qr.device)
+    else:
+        _check_out(out, tuple(qr.shape[:-2]) + (tq, tk), qr.device, "bwta_attn_qk")
     _, _, obs, ohs = _batch_dims(out)
     o = _opts(design, tile)
     ws, wsb = _workspace(lib.bwta_attn_qk_workspace_size(b * h, tq, tk, dh, o), qr.device)
@@ -299,6 +319,8 @@ def bwta_attn_pv(p: Packed, vt: Packed, beta: float, out_dtype=torch.float16,
         raise ValueError("V^T must be ternary planes over the same Tk as P")
     if out is None:
         out = torch.empty(tuple(pr.shape[:-2]) + (tq, dh), dtype=out_dtype, device=pr.device)
+    else:
+        _check_out(out, tuple(pr.shape[:-2]) + (tq, dh), pr.device, "bwta_attn_pv")
     _, _, obs, ohs = _batch_dims(out)
     o = _opts(design, tile)
     ws, wsb = _workspace(lib.bwta_attn_pv_workspace_size(b * h, tq, tk, dh, o), pr.device)

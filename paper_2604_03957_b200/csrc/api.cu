@@ -15,7 +15,25 @@ using namespace bwta;
 
 namespace bwta {
 std::atomic<uint64_t> g_launches{0};
+
+namespace {
+std::atomic<int> g_dev_sms[64];
 }
+int device_sms() {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 148;
+    }
+    if (dev >= 0 && dev < 64 && (v = g_dev_sms[dev].load(std::memory_order_relaxed)) > 0) return v;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+        cudaGetLastError();
+        v = 148;
+    }
+    if (dev >= 0 && dev < 64) g_dev_sms[dev].store(v, std::memory_order_relaxed);
+    return v;
+}
+}  // namespace bwta
 
 namespace {
 
@@ -141,16 +159,22 @@ const bwta_opts_t* opts_or_default(const bwta_opts_t* o) {
     return o ? o : &d;
 }
 
-// Run a matmul description with the requested design.
-bwta_status_t run_matmul(const MatmulArgs& a0, void* ws, size_t ws_bytes, const bwta_opts_t* opts,
-                         cudaStream_t s) {
-    opts = opts_or_default(opts);
+// Every entry point taking bwta_opts_t validates it here, before anything is enqueued.
+bwta_status_t check_opts(const bwta_opts_t* opts) {
     if (opts->design < 0 || opts->design > 2) return BWTA_ERR_INVALID_VALUE;
     for (int r : opts->reserved)
         if (r != 0) return BWTA_ERR_INVALID_VALUE;
     if (!(opts->tile_n == 0 || opts->tile_n == 64 || opts->tile_n == 128 || opts->tile_n == 192) ||
         opts->cta_group < 0 || opts->cta_group > 2)
         return BWTA_ERR_INVALID_VALUE;
+    return BWTA_OK;
+}
+
+// Run a matmul description with the requested design.
+bwta_status_t run_matmul(const MatmulArgs& a0, void* ws, size_t ws_bytes, const bwta_opts_t* opts,
+                         cudaStream_t s) {
+    opts = opts_or_default(opts);
+    if (bwta_status_t st = check_opts(opts); st != BWTA_OK) return st;
     MatmulArgs a = a0;
     a.tile_n = opts->tile_n;
     a.cta_group = opts->cta_group;
@@ -416,6 +440,7 @@ bwta_status_t bwta_gemm_pack(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_k
         !aligned16(w_sgn) || !aligned16(out_nz) || (out_sgn && !aligned16(out_sgn)))
         return BWTA_ERR_ALIGNMENT;
     const bwta_opts_t* o = opts_or_default(opts);
+    if (bwta_status_t so = check_opts(o); so != BWTA_OK) return so;
     if (o->design == BWTA_DESIGN_CUDA_CORE) return BWTA_ERR_UNSUPPORTED;  // fused pack: design (b) only
     bwta_status_t st = check_device();
     if (st != BWTA_OK) return st;
@@ -441,6 +466,8 @@ bwta_status_t bwta_gemm_pack(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_k
     const bool bf = y_dt == BWTA_BF16;
     a.po_tp = rounding_threshold(smallest_pattern(t, false, bf), bf);
     a.po_tn = rounding_threshold(smallest_pattern(t, true, bf), bf);
+    a.tile_n = o->tile_n;
+    a.cta_group = o->cta_group;
     if (!matmul_tc_supported(a)) return BWTA_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
     if (out_ld_words * 32 > n) {
@@ -449,11 +476,8 @@ bwta_status_t bwta_gemm_pack(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_k
         if (e == cudaSuccess && out_sgn)
             e = cudaMemsetAsync(out_sgn, 0, sizeof(uint32_t) * size_t(m) * size_t(out_ld_words), s);
         if (e != cudaSuccess) return cuda_fail(e);
+        count_launch(out_sgn ? 2 : 1);
     }
-    a.tile_n = o->tile_n;
-    a.cta_group = o->cta_group;
-    for (int r : o->reserved)
-        if (r != 0) return BWTA_ERR_INVALID_VALUE;
     cudaError_t e = launch_matmul_tc(a, nullptr, 0, s);
     if (e != cudaSuccess) return cuda_fail(e);
     g_last_design = BWTA_DESIGN_TCGEN05;
@@ -615,6 +639,12 @@ bwta_status_t bwta_attn_decode(const uint32_t* q_sgn, const uint32_t* q_nz, cons
     if (q_bstride < 0 || q_hstride < 0 || k_bstride < 0 || k_hstride < 0 || v_bstride < 0 || v_hstride < 0 ||
         o_bstride < 0 || o_hstride < 0)
         return BWTA_ERR_SHAPE;
+    // every plane is read with 16-byte vector loads (attn_decode.cu)
+    if (ldk_words % 4 || ldv_words % 4 || q_bstride % 4 || q_hstride % 4 || k_bstride % 4 || k_hstride % 4 ||
+        v_bstride % 4 || v_hstride % 4 || (p_out && ldp_words % 4) || !aligned16(q_sgn) || !aligned16(q_nz) ||
+        !aligned16(k_sgn) || (k_nz && !aligned16(k_nz)) || !aligned16(vt_sgn) || !aligned16(vt_nz) ||
+        (p_out && !aligned16(p_out)))
+        return BWTA_ERR_ALIGNMENT;
     st = check_device();
     if (st != BWTA_OK) return st;
     DecodeArgs a{};
@@ -683,9 +713,8 @@ bwta_status_t bwta_attn_pv_pack(const uint32_t* p_sgn, const uint32_t* p_nz, con
         !aligned16(vt_nz) || !aligned16(out_nz) || (out_sgn && !aligned16(out_sgn)))
         return BWTA_ERR_ALIGNMENT;
     const bwta_opts_t* o = opts_or_default(opts);
+    if (bwta_status_t so = check_opts(o); so != BWTA_OK) return so;
     if (o->design == BWTA_DESIGN_CUDA_CORE) return BWTA_ERR_UNSUPPORTED;  // fused pack: design (b) only
-    for (int r : o->reserved)
-        if (r != 0) return BWTA_ERR_INVALID_VALUE;
     st = check_device();
     if (st != BWTA_OK) return st;
     MatmulArgs a{};

@@ -50,6 +50,22 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
+// Per-device state.  One process may drive several GPUs: the SM count and every
+// kernel's shared-memory opt-in are cached per device ordinal (lock-free atomics),
+// not per process.
+int device_sms();  // SM count of the current device (cached per device)
+template <typename Kern>
+inline cudaError_t ensure_smem_optin(Kern kernel, int bytes, std::atomic<uint64_t>& done_mask) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = (dev >= 0 && dev < 64) ? (uint64_t(1) << dev) : 0;
+    if (bit && (done_mask.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess && bit) done_mask.fetch_or(bit, std::memory_order_release);
+    return e;
+}
+
 enum Dt { DT_F16 = 0, DT_BF16 = 1, DT_F32 = 2, DT_I32 = 3 };
 enum Kind { K_BINARY = 0, K_BOOL = 1, K_TERNARY = 2 };
 

@@ -2,26 +2,30 @@
 //
 // sm_100a has no binary (b1) MMA (the paper's mma.sync b1 is
 // emulated there through IMMA + MOVM), so the codes {-1, 0, +1} are fed to
-// tcgen05.mma.kind::i8 (s8 x s8 -> s32, exact for |dot| <= 2^24).  The dot
-// product is the same integer the paper's Case 1/2/3 instruction sequences
-// compute; the epilogue applies c = fl32(scale[n] * scalar)
-// (w_scale * a_scale, or alpha / beta) exactly as design (a).
+// tcgen05.mma.kind::mxf4.block_scale as the E2M1 values 0xA / 0x0 / 0x2 with
+// every UE8M0 block scale = 1.0: each product is exact and every partial sum
+// is an integer of magnitude <= K <= 2^24, so the FP32 accumulator holds the
+// integer dot exactly (DESIGN R12; tests/test_parity_gpu_large.py drives
+// |dot| up to K = 2^24 - 32).  The dot is the same integer the paper's
+// Case 1/2/3 instruction sequences compute; the epilogue applies
+// c = fl32(scale[n] * scalar) (w_scale * a_scale, or alpha / beta) exactly as
+// design (a).
 //
 // Operand roles.  The kernel computes D[i][j] = sum_k A[i][k] * B[j][k] with
-// BOTH operands read as packed bit planes by TMA (box 4 words x rows: 2 bits
-// per ternary element, 1 per bool/binary) and unpacked to int8 codes in
-// shared memory by 8 unpack warps, straight into the UMMA 128B-swizzled
-// K-major layout.  No int8 copy of either operand touches L2 or HBM: the
-// L2 -> SM traffic is the bit planes only (measured on B200: an int8 operand
-// image streamed by TMA capped the mainloop at ~740 cycles per 128-K stage,
-// ~24 B/clk/SM of L2 reads, against the 512-cycle tensor floor).  The
-// caller's A (M side) and W (N side) swap roles when M > N; the epilogue then
-// stores D^T (Y[m][n] = D[n][m]).
+// BOTH operands read as packed bit planes by TMA (box WPS words x rows: 2 bits
+// per ternary element, 1 per bool/binary) and unpacked to E2M1 codes by 8
+// unpack warps: kernel-B's into the UMMA 128B-swizzled K-major shared-memory
+// layout, kernel-A's (256-K stages) into TMEM, where the MMA reads A.  No
+// code image of either operand touches L2 or HBM: the L2 -> SM traffic is the
+// bit planes only (measured on B200: an int8 operand image streamed by TMA
+// capped the mainloop at ~740 cycles per 128-K stage against the 512-cycle
+// int8 tensor floor).  The caller's A (M side) and W (N side) swap roles when
+// that tiles the grid better; the epilogue then stores D^T (Y[m][n] = D[n][m]).
 //
 // CTA (one per SM, persistent over tiles of 128 x BN, or 256 x BN for a CTA
 // pair), 20 warps:
 //   warp 0     TMA producer: A and B bit-plane slices into a STAGES ring
-//   warp 1     MMA issuer: 4 x tcgen05.mma (128 x BN x 32) per 128-K stage,
+//   warp 1     MMA issuer: KS/64 x tcgen05.mma (128|256 x BN x 64) per stage,
 //              accumulators double-buffered in TMEM (2 x BN columns)
 //   warp 2     TMEM allocator
 //   warps 4-7, 12-15  epilogue (two warps per TMEM lane quarter, alternate
@@ -913,16 +917,7 @@ bool encode(CUtensorMap* m, CUtensorMapDataType dt, int rank, void* base, const 
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int num_sms() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) v = 148;
-        n = v;
-    }
-    return n;
-}
+int num_sms() { return device_sms(); }
 
 int64_t kw4_of(int64_t K) { return ((K + 31) / 32 + 3) / 4 * 4; }
 
@@ -988,12 +983,8 @@ cudaError_t launch_ks(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUte
                       const CUtensorMap& my, const TcParams& p, cudaStream_t s) {
     using C = Cfg<BN, CG, KS>;
     auto kern = tc_gemm_kernel<BN, CG, KS, EO, KK>;
-    static bool attr_set = false;  // benign race: the same value may be set twice
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> optin{0};  // per device
+    if (cudaError_t e = ensure_smem_optin(kern, C::SMEM, optin); e != cudaSuccess) return e;
     const int64_t tiles = p.entries * int64_t(p.m_tiles) * p.n_tiles;
     const int64_t slots = num_sms() / CG;
     const int grid = int((tiles < slots ? tiles : slots) * CG);

@@ -273,7 +273,6 @@ __global__ void __launch_bounds__(GC_NT, gc_ctas(MS)) cc_gemv_kernel(GcParams p)
     }
 }
 
-int g_sms = 0;
 
 template <int MS, int LP>
 cudaError_t launch_s(int sp, const GcParams& p, int grid, cudaStream_t s) {
@@ -329,12 +328,7 @@ cudaError_t launch_gemv_cc_fused(const void* x, int x_dt, int64_t ld_x, float tp
     p.K = a.K;
     p.s_tp = tp;
     p.s_ntn = ntn;
-    if (g_sms == 0) {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) v = 148;
-        g_sms = v;
-    }
+    const int g_sms = device_sms();
     const int ms = p.S == 1 ? 1 : (p.S == 2 ? 2 : 4);
     int64_t grid = (p.L + 3) / 4 / (GC_NT / 32) + 1;
     if (grid > int64_t(g_sms) * gc_ctas(ms)) grid = int64_t(g_sms) * gc_ctas(ms);
@@ -384,12 +378,7 @@ cudaError_t launch_matmul_gemv_cc(const MatmulArgs& a, cudaStream_t s) {
     p.scale_on_rows = swap ? 1 : 0;
     p.scalar = a.scalar;
     const int lp = (p.l_sgn ? 1 : 0) | (p.l_nz ? 2 : 0), sp = (p.s_sgn ? 1 : 0) | (p.s_nz ? 2 : 0);
-    if (g_sms == 0) {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) v = 148;
-        g_sms = v;
-    }
+    const int g_sms = device_sms();
     const int64_t warps = p.entries * ((p.L + 3) / 4);
     int64_t grid = (warps + GC_NT / 32 - 1) / (GC_NT / 32);
     const int ms = p.S == 1 ? 1 : (p.S == 2 ? 2 : 4);

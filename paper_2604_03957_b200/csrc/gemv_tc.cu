@@ -375,12 +375,8 @@ cudaError_t launch_gemv(const CUtensorMap& a0, const CUtensorMap& a1, const CUte
     p.ring = ring;
     const int smem = fixed + ring * stage;
     auto kern = tc_gemv_kernel<NB>;
-    static bool attr_set = false;  // benign race: the same value may be set twice
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, GV_SMEM_MAX);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> optin{0};  // per device
+    if (cudaError_t e = ensure_smem_optin(kern, GV_SMEM_MAX, optin); e != cudaSuccess) return e;
     const int64_t total = p.entries * p.tiles_per_entry;
     const int grid = int(total < num_sms() ? total : num_sms());
     return launch_pdl(kern, dim3(grid), dim3(GV_NT), size_t(smem), s, 1, a0, a1, b0, b1, p);

@@ -410,16 +410,7 @@ cudaError_t launch_group_rows(const PackGroup& g, int kind, bool vec, int blocks
                : launch_pdl(pack_group_rows_kernel<T, K_TERNARY, false>, blocks, 256, 0, s, 1, g);
 }
 
-int num_sms_pack() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) v = 148;
-        n = v;
-    }
-    return n;
-}
+int num_sms_pack() { return device_sms(); }
 
 // One resident wave (2 x 256-thread blocks per SM, <= 128 registers); warps loop with prefetch.
 int grid_for(int64_t warp_items) {

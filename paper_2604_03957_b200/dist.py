@@ -174,7 +174,7 @@ def gemm_nshard_overlap(a, w_local, w_scale_local: Optional[torch.Tensor], a_sca
             w_c = _slice_packed(w_local, l0, l1) if hasattr(w_local, "sgn") else w_local[l0:l1]
             s_c = None if w_scale_local is None else w_scale_local[l0:l1]
             local_gemm(a, w_c, s_c, a_scale, out[g0:g1])
-        if P > 1:
+        if P > 1 or group is not None:   # (an explicit 1-rank group still runs the collective)
             blk = out[c * P * nrc:(c + 1) * P * nrc]
             mine = blk[plan.rank * nrc:(plan.rank + 1) * nrc]
             works.append(dist.all_gather_into_tensor(blk, mine, group=group, async_op=True))

@@ -197,6 +197,41 @@ def test_attn_decode_validation(N):
     assert dec(alpha=float("nan")) == 1
     assert dec(p_dt=3) == 4                # P rounds to f16 / bf16 / f32
     assert dec(b=0) == 0
+    # every plane is read with 16-byte vector loads: ld % 4 and 16-byte pointers
+    assert dec(ldk=5) == 3
+    assert dec(ldv=5) == 3
+    assert dec(ks=20) == 3
+    assert dec(qn=36) == 3
+    assert dec(vs=84) == 3
+    assert dec(kn=None) == 4               # binary K is valid
+    assert dec(pout=132, ldp=4) == 3
+
+
+def test_fused_pack_entry_points_validate_opts(N):
+    """bwta_gemm_pack / bwta_attn_pv_pack reject bad tile overrides and designs on the host,
+    before the padding memsets or any launch (a tile_n of 256 would otherwise launch a kernel
+    whose TMA boxes and stages disagree)."""
+    L = N.lib
+
+    def opts(design=0, tile_n=0, cg=0):
+        o = N.Opts()
+        o.design, o.tile_n, o.cta_group = design, tile_n, cg
+        return ctypes.byref(o)
+
+    def gp(o):
+        return L.bwta_gemm_pack(16, 32, 2, 8, 4, 48, 8, 4, 100, None, ctypes.c_float(1.0), 0, ctypes.c_float(1.0),
+                                2, 64, 80, 4, o, None)
+
+    def pvp(o):
+        return L.bwta_attn_pv_pack(None, 32, 48, 64, 1, 2, 4, 100, 64, 4, 0, 0, 4, 0, 0, ctypes.c_float(0.1), 0,
+                                   ctypes.c_float(1.0), 2, 80, 96, 4, o, None)
+    for f in (gp, pvp):
+        assert f(None) == 4                 # valid, but no sm_100 device here
+        assert f(opts(tile_n=128, cg=2)) == 4
+        for bad in (opts(tile_n=256), opts(tile_n=32), opts(tile_n=96), opts(cg=3), opts(cg=-1), opts(design=3),
+                    opts(design=-1)):
+            assert f(bad) == 1
+        assert f(opts(design=1)) == 4       # fused pack: design (b) only
 
 
 def test_gemm_x_validation(N):
