@@ -821,7 +821,10 @@ def main():
                            "the path runs tcgen05.mma.kind::mxf4)"
                            if roof["unit"] == "TOPS" else f"{pk['source']} HBM copy")
     roof["traffic"] = _traffic(dom.name, args.workload)
-    roof["traffic_source"] = "profiles/ncu_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum, ncu --set full"
+    roof["traffic_l2"] = _traffic(dom.name, args.workload + "_lts_bytes")
+    roof["traffic_source"] = ("profiles/ncu_traffic.json (ncu --set full, one launch): traffic = dram__bytes_read.sum + "
+                              "dram__bytes_write.sum (the output write stays in L2 during the launch, so it is "
+                              "undercounted); traffic_l2 = lts__t_sectors_srcunit_tex x 32 B")
 
     # -------- end to end through the public API with host buffers
     e2e = None

@@ -41,6 +41,7 @@
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "bwta_internal.h"
@@ -67,6 +68,27 @@ constexpr int OUT_BUF = 4096;
 constexpr int OUT_NBUF = 2;  // staging buffers per epilogue warp (fast path: store k overlaps the staging of k + 1)
 
 using namespace tc;
+
+// barrier wait of the tile kernel; trace builds can switch the wait flavour (BWTA_DBG bits 5-6)
+__device__ __forceinline__ void kwait(uint64_t* bar, uint32_t parity, int dbg) {
+#ifdef BWTA_TRACE
+    const int mode = (dbg >> 5) & 3;
+    if (mode == 1) {
+        mbar_wait(bar, parity);  // the hinted wait
+        return;
+    }
+    if (mode == 2) {
+        while (!mbar_test_wait(bar, parity)) {
+        }
+        return;
+    }
+#endif
+    (void)dbg;
+    // no suspend-time hint: measured 11 % faster per stage than the hinted wait on the C3 GEMM
+    // (the hinted wait's wake-up latency sits on every barrier hand-off)
+    while (!mbar_try_wait_nh(bar, parity)) {
+    }
+}
 
 extern __shared__ __align__(16) uint8_t smem_raw[];  // dynamic shared memory of tc_gemm_kernel
 
@@ -113,6 +135,7 @@ struct TcParams {
     int64_t po_ld;
     int64_t po_bs, po_hs;  // words between the planes of consecutive batch / head entries
     float po_tp, po_tn;
+    int dbg;  // BWTA_TRACE builds only (tools/trace_gemm.py): 1 skip unpack math, 2 skip MMAs, 4 skip TMA, 8 skip A unpack, 16 skip B unpack
 };
 
 __host__ __device__ constexpr int nplanes_of(int kind) { return kind == B_TERNARY ? 2 : 1; }
@@ -142,10 +165,12 @@ struct Cfg {
     // a_tmem mode: SA stages of kernel-A codes (32 columns = 256 K each) after the scale factors
     static constexpr int A_COL = 2 * BN + 16;
     static constexpr int SA_FIT = (512 - A_COL) / 32;
-    static constexpr int SA = SA_FIT > 4 ? 4 : SA_FIT;
+    static constexpr int SA0 = SA_FIT > 8 ? 8 : SA_FIT;
+    static constexpr int SA = SA0 > STAGES ? STAGES : SA0;
     static constexpr int TMEM_COLS = 512;
     static_assert(SF_COL + 16 <= TMEM_COLS, "accumulators + scale factors exceed TMEM");
     static_assert(STAGES >= 2, "pipeline too shallow");
+    static_assert(KS != 256 || SA <= STAGES, "the A code ring is released through empty[]");
     static_assert(BNC % 8 == 0, "swizzle atoms are 8 rows");
     static_assert(A_BYTES % 1024 == 0 && B_BYTES % 1024 == 0 && OUT_BYTES % 1024 == 0 && SCALE_BYTES % 128 == 0 &&
                       ABITS % 128 == 0 && BBITS % 128 == 0,
@@ -512,7 +537,7 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
             }
             __syncwarp();
         }
-        mbar_wait(&tfull[acc], acc_phase);
+        kwait(&tfull[acc], acc_phase, p.dbg);
         tc_fence_after();
         TRACE(5, tix, h == 0 && q == 0 && lane == 0);
         const uint32_t tacc = tmem_base + uint32_t(acc * BN);
@@ -571,6 +596,52 @@ __device__ __forceinline__ void unpack_row(uint32_t p0addr, uint32_t p1addr, uin
     }
 }
 
+// items [i0, rows * WPS/4) step `step` of one operand slice: item i = word quad i / rows of
+// row i % rows (16 bytes per plane -> 4 x 16 bytes of codes); warp-uniform kind
+template <int KIND, int KS>
+__device__ __forceinline__ void unpack_quad(uint32_t p0addr, uint32_t p1addr, uint32_t rowaddr, int r, int h) {
+    const int sw = KS == 256 ? (r & 7) : ((r >> 1) & 3);
+    const uint4 w0 = lds128(p0addr + 16 * h);
+    uint4 w1 = make_uint4(0, 0, 0, 0);
+    if (KIND == B_TERNARY) w1 = lds128(p1addr + 16 * h);
+    uint32_t x0[4] = {w0.x, w0.y, w0.z, w0.w};
+    const uint32_t x1[4] = {w1.x, w1.y, w1.z, w1.w};
+    if (KIND == B_TERNARY) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) x0[g] &= x1[g];  // canonical sgn (subset of nz)
+    }
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = unpack_word<KIND>(x0[g], x1[g], j);
+        sts128(rowaddr + (((4 * h + g) ^ sw) << 4), o[0], o[1], o[2], o[3]);
+    }
+}
+template <int KS>
+__device__ __forceinline__ void unpack_quads(int kind, uint32_t bits, int plane_bytes, uint32_t dst, int i0, int rows,
+                                             int step) {
+    constexpr int RB = Stage<KS>::WPS * 4;  // bit bytes per row per plane
+    constexpr int ROWB = Stage<KS>::ROWB;
+    const int items = rows * (Stage<KS>::WPS / 4);
+    if (kind == B_TERNARY) {
+        for (int i = i0; i < items; i += step) {
+            const int r = i % rows, h = i / rows;
+            unpack_quad<B_TERNARY, KS>(bits + r * RB, bits + plane_bytes + r * RB, dst + r * ROWB, r, h);
+        }
+    } else if (kind == B_BOOL) {
+        for (int i = i0; i < items; i += step) {
+            const int r = i % rows, h = i / rows;
+            unpack_quad<B_BOOL, KS>(bits + r * RB, 0, dst + r * ROWB, r, h);
+        }
+    } else {
+        for (int i = i0; i < items; i += step) {
+            const int r = i % rows, h = i / rows;
+            unpack_quad<B_BINARY, KS>(bits + r * RB, 0, dst + r * ROWB, r, h);
+        }
+    }
+}
+
 // rows [r0, rows) step `step` of one operand slice (warp-uniform kind)
 template <int KS>
 __device__ __forceinline__ void unpack_rows(int kind, uint32_t bits, int plane_bytes, uint32_t dst, int r0, int rows,
@@ -590,7 +661,7 @@ __device__ __forceinline__ void unpack_rows(int kind, uint32_t bits, int plane_b
 // One 256-K operand row (8 words per plane) -> 32 TMEM columns (code word 4g + j
 // in column 4g + j: the same K order as the shared-memory layout's 16-byte chunks).
 template <int KIND>
-__device__ __forceinline__ void unpack_row_tmem_k(uint32_t p0, uint32_t p1, uint32_t taddr) {
+__device__ __forceinline__ void unpack_row_tmem_k(uint32_t p0, uint32_t p1, uint32_t (&v)[32]) {
     uint32_t x0[8], x1[8];
     {
         const uint4 a = lds128(p0), b = lds128(p0 + 16);
@@ -605,17 +676,16 @@ __device__ __forceinline__ void unpack_row_tmem_k(uint32_t p0, uint32_t p1, uint
 #pragma unroll
         for (int g = 0; g < 8; ++g) x1[g] = 0;
     }
-    uint32_t v[32];
 #pragma unroll
     for (int g = 0; g < 8; ++g)
 #pragma unroll
         for (int j = 0; j < 4; ++j) v[4 * g + j] = unpack_word<KIND>(x0[g], x1[g], j);
-    tmem_st_32x32b_x32(taddr, v);
 }
-__device__ __forceinline__ void unpack_row_tmem(int kind, uint32_t p0, uint32_t p1, uint32_t taddr) {
-    if (kind == B_TERNARY) unpack_row_tmem_k<B_TERNARY>(p0, p1, taddr);
-    else if (kind == B_BOOL) unpack_row_tmem_k<B_BOOL>(p0, p1, taddr);
-    else unpack_row_tmem_k<B_BINARY>(p0, p1, taddr);
+// the codes of one 256-K kernel-A row in registers (stored to TMEM by the caller, one stage later)
+__device__ __forceinline__ void unpack_row_regs(int kind, uint32_t p0, uint32_t p1, uint32_t (&v)[32]) {
+    if (kind == B_TERNARY) unpack_row_tmem_k<B_TERNARY>(p0, p1, v);
+    else if (kind == B_BOOL) unpack_row_tmem_k<B_BOOL>(p0, p1, v);
+    else unpack_row_tmem_k<B_BINARY>(p0, p1, v);
 }
 
 // UMMA shared-memory descriptor of a K-major operand tile for the stage layout
@@ -649,8 +719,7 @@ __global__ void __launch_bounds__(NT, 1)
     uint64_t* empty = bready + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
-    uint64_t* aempty = tempty + 2;  // a_tmem mode: A code stage consumed (MMA commit)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 4);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 #ifdef BWTA_TRACE
     for (int i = threadIdx.x; i < TRACE_EV * TRACE_N; i += blockDim.x) reinterpret_cast<unsigned long long*>(smem_raw)[i] = 0;
 #endif
@@ -670,15 +739,12 @@ __global__ void __launch_bounds__(NT, 1)
         if (p.use_tma_store) tma_prefetch_desc(&tmY);
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&bready[s], 8 * CG);  // A and B unpack warps of every CTA of the pair
+            mbar_init(&bready[s], 10 * CG);  // 4 A + 6 B unpack warps of every CTA of the pair
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 8 * CG);  // epilogue warps of every CTA of the pair
-        }
-        for (int a = 0; a < 4; ++a) {
-            mbar_init(&aempty[a], 1);
         }
         fence_barrier_init();
     }
@@ -727,9 +793,20 @@ __global__ void __launch_bounds__(NT, 1)
             const int arow = mt * BM * CG + rank * BM;
             const int brow = nt * BN + rank * C::BNC;
             for (int kb = 0; kb < p.num_kb; ++kb) {
-                mbar_wait(&empty[stage], phase ^ 1);
+                kwait(&empty[stage], phase ^ 1, p.dbg);
                 TRACE(1, it, lane == 0);
                 ++it;
+#ifdef BWTA_TRACE
+                if (p.dbg & 4) {
+                    if (lane == 0) mbar_arrive(&full[stage]);
+                    __syncwarp();
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                    continue;
+                }
+#endif
                 if (lane == 0) {
                     mbar_arrive_expect_tx(&full[stage], tx);
                     uint8_t* ab = sABits + stage * C::ABITS;
@@ -759,15 +836,22 @@ __global__ void __launch_bounds__(NT, 1)
             int it = 0;
             int sa = 0;  // a_tmem mode: A code stage
             for (int64_t t = t0; t < total; t += tstep) {
-                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                kwait(&tempty[acc], acc_phase ^ 1, p.dbg);
                 tc_fence_after();
                 const uint32_t d = tmem_base + uint32_t(acc * BN);
                 for (int kb = 0; kb < p.num_kb; ++kb) {
-                    mbar_wait(&bready[stage], phase);
+                    kwait(&bready[stage], phase, p.dbg);
                     tc_fence_after();
                     TRACE(4, it, lane == 0);
                     ++it;
-                    if (lane == 0) {
+                    bool skip_mma = false;
+#ifdef BWTA_TRACE
+                    skip_mma = (p.dbg & 2) != 0;
+#endif
+                    if (lane == 0 && skip_mma) {
+                        if (CG == 1) tc_commit(&empty[stage]);
+                        else tc_commit2_mc(&empty[stage], 0x3);
+                    } else if (lane == 0) {
                         const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
                         if (KS == 256 && p.a_tmem) {
                             const uint32_t a0 = tmem_base + uint32_t(C::A_COL + sa * 32);
@@ -777,8 +861,8 @@ __global__ void __launch_bounds__(NT, 1)
                                 if (CG == 1) mma_mxf4_ts(d, a0 + 8 * k, bd, idesc, sfa, sfb, (kb | k) != 0);
                                 else mma_mxf4_ts_cg2(d, a0 + 8 * k, bd, idesc, sfa, sfb, (kb | k) != 0);
                             }
-                            if (CG == 1) tc_commit(&aempty[sa]);
-                            else tc_commit2_mc(&aempty[sa], 0x3);
+                            // (the A code stage is released by the same commit as the bit/B stage:
+                            // the A unpack warps wait on empty[] of the stage SA back)
                         } else {
                             const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
 #pragma unroll
@@ -808,37 +892,91 @@ __global__ void __launch_bounds__(NT, 1)
                 if (acc == 0) acc_phase ^= 1;
             }
         }
-    } else if ((warp >= 8 && warp < 12) || warp >= 16) {
-        // ------------------------------ unpack (8-11: B rows, 16-19: A rows) ------------------------------
+    } else if (warp >= 16 && KS == 256 && p.a_tmem) {
+        // ------------------------------ unpack kernel-A rows into TMEM (warps 16-19) ------------------------------
+        // Software-pipelined: the codes of stage it are computed while the TMEM store of stage it - 1
+        // drains; then stage it - 1 is signalled (wait::st, bready) and stage it stored.  Thread ut owns
+        // kernel-A row ut = TMEM lane ut (warp w: lane quarter w & 3); A code stage it % SA.
+        const int ut = threadIdx.x - 512;
+        const int kind = a_kind_;
+        const int plane_bytes = BM * WPS * 4;
+        const uint32_t bready_addr0 = CG == 2 ? mapa_smem(&bready[0], 0) : 0u;
+        int stage = 0, prev = -1;
+        uint32_t phase = 0;
+        int it = 0;
+        uint32_t v[32];
+        for (int64_t t = t0; t < total; t += tstep) {
+            for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
+                kwait(&full[stage], phase, p.dbg);
+                TRACE(10, it, ut == 0);
+                const uint32_t bits = smem_u32(sABits + stage * C::ABITS);
+#ifdef BWTA_TRACE
+                if (!(p.dbg & 9))
+#endif
+                unpack_row_regs(kind, bits + ut * 32, bits + plane_bytes + ut * 32, v);
+                if (prev >= 0) {  // stage it - 1 is in TMEM: signal it
+                    tmem_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (CG == 1) mbar_arrive(&bready[prev]);
+                        else mbar_arrive_cluster(bready_addr0 + prev * 8);
+                    }
+                }
+                // A code stage sa was last read by the MMAs of stage it - SA, whose commit completes
+                // use (it - SA) / STAGES of empty[(it - SA) % STAGES] (one commit per stage frees both
+                // rings; SA <= STAGES, so that barrier cannot run a phase ahead)
+                const int sa = it % C::SA;
+                if (it >= C::SA) {
+                    const int pit = it - C::SA;
+                    kwait(&empty[pit % C::STAGES], uint32_t((pit / C::STAGES) & 1), p.dbg);
+                }
+                tc_fence_after();
+                tmem_st_32x32b_x32(tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(C::A_COL + sa * 32), v);
+                TRACE(11, it, ut == 0);
+                prev = stage;
+                if (++stage == C::STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        if (prev >= 0) {
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (CG == 1) mbar_arrive(&bready[prev]);
+                else mbar_arrive_cluster(bready_addr0 + prev * 8);
+            }
+        }
+    } else if (warp >= 16 || (warp >= 8 && warp < 12) || warp == 2 || warp == 3) {
+        // ------------------------------ unpack into shared memory ------------------------------
+        // kernel-B: warps 2, 3, 8-11 (192 threads) over (row, 16-byte word quad) items;
+        // kernel-A (128-K stages only): warps 16-19, one row per thread
         const bool is_a = warp >= 16;
-        const int ut = threadIdx.x - (is_a ? 512 : 256);  // 0..127
+        const int ut = is_a ? threadIdx.x - 512 : (warp < 4 ? (warp - 2) * 32 + lane : 64 + (warp - 8) * 32 + lane);
         const int kind = is_a ? a_kind_ : b_kind_;
         const int rows = is_a ? BM : C::BNC;
-        const int plane_bytes = (is_a ? BM : C::BNC) * WPS * 4;
+        const int plane_bytes = rows * WPS * 4;
         const uint32_t bready_addr0 = CG == 2 ? mapa_smem(&bready[0], 0) : 0u;
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
-        const bool a_tm = KS == 256 && is_a && p.a_tmem;
         for (int64_t t = t0; t < total; t += tstep) {
             for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
-                mbar_wait(&full[stage], phase);
+                kwait(&full[stage], phase, p.dbg);
                 TRACE(is_a ? 10 : 2, it, ut == 0);
                 const uint32_t bits = is_a ? smem_u32(sABits + stage * C::ABITS) : smem_u32(sBBits + stage * C::BBITS);
-                if (a_tm) {
-                    // kernel-A row ut -> TMEM lane ut (warp w owns lane quarter w & 3), A code stage it % SA
-                    const int sa = it % C::SA;
-                    mbar_wait(&aempty[sa], ((it / C::SA) & 1) ^ 1);
-                    tc_fence_after();
-                    const uint32_t ta = tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(C::A_COL + sa * 32);
-                    unpack_row_tmem(kind, bits + ut * 32, bits + plane_bytes + ut * 32, ta);
-                    tmem_wait_st();
-                    tc_fence_before();
-                } else {
-                    const uint32_t dst = is_a ? smem_u32(sA + stage * C::A_BYTES) : smem_u32(sB + stage * C::B_BYTES);
-                    unpack_rows<KS>(kind, bits, plane_bytes, dst, ut, rows, 128);
-                    fence_proxy_async_smem();
+                const uint32_t dst = is_a ? smem_u32(sA + stage * C::A_BYTES) : smem_u32(sB + stage * C::B_BYTES);
+#ifdef BWTA_TRACE
+                if (!(p.dbg & (is_a ? 9 : 17)))
+#endif
+                {
+                    if (is_a) unpack_rows<KS>(kind, bits, plane_bytes, dst, ut, rows, 128);
+                    else unpack_quads<KS>(kind, bits, plane_bytes, dst, ut, rows, 192);
                 }
+                fence_proxy_async_smem();
                 __syncwarp();
                 TRACE(is_a ? 11 : 3, it, ut == 0);
                 if (lane == 0) {
@@ -1149,6 +1287,9 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     // kernel-A codes go to TMEM (no shared-memory round trip for the 128-row operand) for 256-K
     // stages; measured 2-7 % faster than the shared-memory A path (tools/ab_atmem.py)
     p.a_tmem = ks == 256 ? 1 : 0;
+#ifdef BWTA_TRACE
+    if (const char* dbg = getenv("BWTA_DBG")) p.dbg = atoi(dbg);
+#endif
         if (!ok) my = ma0;  // unused
     }
     if (cg == 2) {

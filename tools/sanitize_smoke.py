@@ -29,6 +29,14 @@ for d in ("cuda_core", "tcgen05"):
     B.bwta_attn_qk(qp, kp, 0.1, design=d)
     B.bwta_attn_pv(pp, vt, 0.1, design=d)
 B.bwta_gemm_pack(a, wp, None, 1.0, 0.5, "bool")
+# the lean grouped row pack (Q + K of the BERT step) and the kind-specialised BN = 192 CTA-pair tiles
+B.bwta_pack_act_batch([(q, 1.6, "ternary", False), (k, 1.3, "ternary", False)])
+x2 = gen.activations((300, 517), 12).cuda()
+w2 = B.bwta_pack_weight(gen.weights(400, 517, 13).cuda())
+for kind in ("ternary", "bool"):
+    a2 = B.bwta_pack_act(torch.relu(x2) if kind == "bool" else x2, 1.6, kind)
+    B.bwta_gemm(a2, w2, None, 1.0, tile=(192, 2))
+    B.bwta_gemm_pack(a2, w2, None, 1.0, 0.5, "ternary", tile=(192, 2))
 B.bwta_attn_pv_pack(pp, vt, 0.1, 0.5, "ternary")
 # decode paths: CUDA-core GEMV (M <= 4), skinny tcgen05 (M <= 32), fused pack GEMV, fused attention
 for m in (1, 3, 16):

@@ -31,7 +31,8 @@ else:
     a = B.bwta_pack_act(x, 1.6, kind=kind)
     wp = B.bwta_pack_weight(w)
     y = torch.empty((m, n), dtype=torch.float16, device="cuda")
-    run = lambda: B.bwta_gemm(a, wp, None, 1.0, out=y, design="tcgen05")
+    tile = tuple(int(v) for v in os.environ["BWTA_TILE"].split(",")) if os.environ.get("BWTA_TILE") else None
+    run = lambda: B.bwta_gemm(a, wp, None, 1.0, out=y, design="tcgen05", tile=tile)
 buf = np.zeros((2, 16, 64), np.uint64)
 f = B.lib.bwta_trace_fetch
 for it in range(3):
