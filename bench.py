@@ -419,6 +419,10 @@ def llama_attn(B, dev, seed=404, heads=32, seq=2048, D=128):
 
     def op_pv():
         B.bwta_attn_pv(st["pp"], st["vt"], beta, out=O)
+
+    def op_fused():   # QK^T -> fp32 softmax -> bool P -> PV in one launch (N3); S and P stay on chip
+        B.bwta_attn_prefill(st["qp"], st["kp"], st["vt"], alpha, s_att, beta, out=O2)
+    O2 = torch.empty((1, heads, seq, D), dtype=torch.float16, device=q.device)
     op_pack_qkv(); op_pack_p()  # noqa: E702
     n = heads * seq * D
     ops = [Op("pack_qkv", "pack", op_pack_qkv, 0, 3 * (2 * n + n / 4)),
@@ -426,10 +430,19 @@ def llama_attn(B, dev, seed=404, heads=32, seq=2048, D=128):
               lambda: torch.matmul(q, k.transpose(-1, -2))),
            Op("pack_p", "pack", op_pack_p, 0, 2 * heads * seq * seq + heads * seq * seq / 8),
            Op("attn_pv", "pv", op_pv, 2 * heads * seq * seq * D, heads * seq * seq / 8 + n / 4 + 2 * n,
-              lambda: torch.matmul(P, v))]
-    cfg = {"workload": "llama_attn (configs[3]): ternary attention, 32 heads, head_dim 128, seq 2048",
+              lambda: torch.matmul(P, v)),
+           # the fused op does both products (4 T^2 D ops); baseline: torch fp16 QK^T, fp32 softmax, PV
+           Op("attn_prefill_fused", "attn", op_fused, 4 * heads * seq * seq * D, 2 * n / 4 + n / 4 + 2 * n,
+              lambda: torch.matmul(torch.softmax(torch.matmul(q, k.transpose(-1, -2)).float() * alpha, -1).half(), v))]
+    cfg = {"workload": "llama_attn (configs[3]): ternary attention, 32 heads, head_dim 128, seq 2048 (step: Q/K/V^T "
+                       "packs + the fused prefill attention; the unfused ops are timed alongside)",
            "heads": heads, "seq_len": seq, "head_dim": D}
-    return {"ops": ops, "inputs": {"P": P}, "outputs": [], "cfg": cfg, "oracle_sample": None}
+
+    def step():
+        op_pack_qkv()
+        op_fused()
+    return {"ops": ops, "inputs": {}, "outputs": [O2], "cfg": cfg, "oracle_sample": None, "step": step,
+            "step_ops": ["pack_qkv", "attn_prefill_fused"]}
 
 
 def decode_linear(B, dev, seed=505, shapes=((1, 8192, 28672), (16, 8192, 28672), (1, 4096, 11008))):
@@ -752,7 +765,8 @@ def main():
             return W["step"]()
         for op in ops:
             op.fn()
-    total_ops = sum(op.ops for op in ops)           # one replica / the whole sharded job
+    step_ops = W.get("step_ops")
+    total_ops = sum(op.ops for op in ops if step_ops is None or op.name in step_ops)  # one replica / sharded job
     job_ops = total_ops * (world if (world > 1 and not sharded) else 1)
 
     # -------- device-time step (CUDA graph of the library calls at N = 1)

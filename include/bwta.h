@@ -324,6 +324,36 @@ BWTA_API bwta_status_t bwta_gemm_x(const void* x, bwta_dtype_t x_dt, int64_t m, 
                                    int64_t k, const float* w_scale, void* y, bwta_dtype_t y_dt, int64_t ld_y,
                                    int y_transposed, void* stream);
 
+/* ---- fused prefill attention (tensor cores) ------------------------------ */
+/*
+ * The whole BWTA attention of a layer in ONE launch: per (batch b,
+ * head h), with Q planes [tq x ldq_words] (ternary), K planes [tk x ldk_words] (ternary,
+ * or binary with k_nz == NULL) and V^T planes [dh x ldv_words] (ternary, over tk, from
+ * bwta_pack_act(V, transpose=1)):
+ *   s_ij = fl32(float(q_i . k_j) * alpha)                     (R5)
+ *   p_ij = softmax_j(s_i) in fp32, rounded to p_dt            (high-precision softmax)
+ *   b_ij = [p_ij >= s_att / 2] on the rounded value           (bool quantizer; R1-R2)
+ *   O_id = round_{o_dt}(fl32(float(sum_j b_ij v_jd) * beta))  (R5; I32: the raw dot)
+ * S, P and the P planes never touch memory (QK^T and PV on tcgen05, the softmax in
+ * registers).  Entry (b, h) of Q/K/V^T at b*X_bstride + h*X_hstride words;
+ * O rows [dh] at b*o_bstride + h*o_hstride + i*ld_o elements.  p_out (nullable) receives the
+ * P planes [batch*heads][tq][ldp_words] (tests; zeroed by a memset on `stream` first).
+ * 1 <= dh <= 128 (BWTA_ERR_UNSUPPORTED above), tk >= 1, tk <= 2^24.  Alignment: every
+ * plane pointer 16-byte aligned, every ld / stride a multiple of 4 words (TMA).  As for
+ * bwta_attn_decode, a bit of P may differ from an exact softmax only where p_ij lies
+ * within rounding distance of s_att / 2 (R13).
+ */
+BWTA_API bwta_status_t bwta_attn_prefill(const uint32_t* q_sgn, const uint32_t* q_nz,
+                           const uint32_t* k_sgn, const uint32_t* k_nz,
+                           const uint32_t* vt_sgn, const uint32_t* vt_nz,
+                           int64_t batch, int64_t heads, int64_t tq, int64_t tk, int64_t dh,
+                           int64_t ldq_words, int64_t q_bstride, int64_t q_hstride,
+                           int64_t ldk_words, int64_t k_bstride, int64_t k_hstride,
+                           int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
+                           float alpha, float s_att, bwta_dtype_t p_dt, float beta,
+                           void* o, bwta_dtype_t o_dt, int64_t ld_o, int64_t o_bstride, int64_t o_hstride,
+                           uint32_t* p_out, int64_t ldp_words, void* stream);
+
 /* ---- fused decode attention (one query row per entry) -------------------- */
 /*
  * Per (batch b, head h), with one packed query row q (ternary; q_sgn/q_nz at

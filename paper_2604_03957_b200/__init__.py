@@ -21,7 +21,7 @@ from . import _native as N
 from ._native import lib
 
 __all__ = ["Packed", "BwtaError", "bwta_ld_words", "bwta_pack_act", "bwta_pack_weight",
-           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "bwta_gemm_x", "last_design", "lib"]
+           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "bwta_attn_prefill", "bwta_gemm_x", "last_design", "lib"]
 
 
 class BwtaError(RuntimeError):
@@ -359,6 +359,43 @@ def bwta_attn_decode(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: floa
                               ctypes.c_float(s_att), _DT[p_dtype], ctypes.c_float(beta), _ptr(out), _DT[out_dtype],
                               h * dh, dh, _ptr(pout), ldp if return_p else 0, _stream(stream))
     _check(st, "bwta_attn_decode")
+    return (out, pout) if return_p else out
+
+
+def bwta_attn_prefill(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: float, beta: float,
+                      out_dtype=torch.float16, p_dtype=torch.float16, return_p: bool = False,
+                      out: Optional[torch.Tensor] = None, stream=None):
+    """Fused prefill attention, one launch:
+    O = beta * bool(round(softmax(alpha * ternary(Q) (x) K^T), p_dtype) >= s_att / 2) (x) ternary(V).
+
+    q: Packed ternary [B, H, Tq, ld] (or [B, Tq, ld] / [Tq, ld]); k: Packed ternary or binary
+    [.., Tk, ld] over the same head_dim (<= 128); vt: Packed ternary [.., Dh, ld(Tk)]
+    (bwta_pack_act(V, transpose=True)).  Returns O [.., Tq, Dh] (and the P planes
+    [entries, Tq, ld(Tk)] with return_p)."""
+    qr, kr, vr = q.ref, k.ref, vt.ref
+    if q.kind != "ternary" or vt.kind != "ternary" or k.cols != q.cols or vt.cols != kr.shape[-2]:
+        raise ValueError("expects ternary Q and V^T, K over the same head_dim, V^T over Tk")
+    b, h, qbs, qhs = _batch_dims(qr)
+    _, _, kbs, khs = _batch_dims(kr)
+    _, _, vbs, vhs = _batch_dims(vr)
+    tq, tk, dh = qr.shape[-2], kr.shape[-2], vr.shape[-2]
+    if dh != q.cols:
+        raise ValueError("V^T rows must equal the head_dim")
+    shape = tuple(qr.shape[:-2]) + (tq, dh)
+    if out is None:
+        out = torch.empty(shape, dtype=out_dtype, device=qr.device)
+    else:
+        _check_out(out, shape, qr.device, "bwta_attn_prefill")
+    _, _, obs, ohs = _batch_dims(out)
+    ldp = bwta_ld_words(tk)
+    pout = torch.empty((b * h, tq, ldp), dtype=torch.int32, device=qr.device) if return_p else None
+    k_nz = k.nz if k.kind == "ternary" else None
+    st = lib.bwta_attn_prefill(_ptr(q.sgn), _ptr(q.nz), _ptr(k.sgn), _ptr(k_nz), _ptr(vt.sgn), _ptr(vt.nz), b, h,
+                               tq, tk, dh, qr.stride(-2), qbs, qhs, kr.stride(-2), kbs, khs, vr.stride(-2), vbs, vhs,
+                               ctypes.c_float(alpha), ctypes.c_float(s_att), _DT[p_dtype], ctypes.c_float(beta),
+                               _ptr(out), _DT[out.dtype], out.stride(-2), obs, ohs, _ptr(pout),
+                               ldp if return_p else 0, _stream(stream))
+    _check(st, "bwta_attn_prefill")
     return (out, pout) if return_p else out
 
 

@@ -689,6 +689,93 @@ bwta_status_t bwta_attn_decode(const uint32_t* q_sgn, const uint32_t* q_nz, cons
     return BWTA_OK;
 }
 
+bwta_status_t bwta_attn_prefill(const uint32_t* q_sgn, const uint32_t* q_nz, const uint32_t* k_sgn,
+                                const uint32_t* k_nz, const uint32_t* vt_sgn, const uint32_t* vt_nz, int64_t batch,
+                                int64_t heads, int64_t tq, int64_t tk, int64_t dh, int64_t ldq_words,
+                                int64_t q_bstride, int64_t q_hstride, int64_t ldk_words, int64_t k_bstride,
+                                int64_t k_hstride, int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
+                                float alpha, float s_att, bwta_dtype_t p_dt, float beta, void* o, bwta_dtype_t o_dt,
+                                int64_t ld_o, int64_t o_bstride, int64_t o_hstride, uint32_t* p_out,
+                                int64_t ldp_words, void* stream) {
+    if (!valid_out_dt(o_dt) || (p_dt != BWTA_F16 && p_dt != BWTA_BF16 && p_dt != BWTA_F32))
+        return BWTA_ERR_UNSUPPORTED;
+    bwta_status_t st = check_batch(batch, heads);
+    if (st != BWTA_OK) return st;
+    if (tq < 0 || tk < 0 || dh < 0 || tk > KMAX || tq > (int64_t(1) << 31)) return BWTA_ERR_SHAPE;
+    if (dh > 128) return BWTA_ERR_UNSUPPORTED;  // one 128-element tensor-core stage per Q/K row
+    if (batch == 0 || tq == 0 || dh == 0) return BWTA_OK;
+    if (tk == 0) return BWTA_ERR_SHAPE;  // softmax over an empty row
+    if (q_sgn == nullptr || q_nz == nullptr || k_sgn == nullptr || vt_sgn == nullptr || vt_nz == nullptr ||
+        o == nullptr)
+        return BWTA_ERR_INVALID_VALUE;
+    if (!std::isfinite(alpha) || !std::isfinite(beta) || !scale_ok_pos(s_att)) return BWTA_ERR_INVALID_VALUE;
+    if (ldq_words < ldw_of(dh) || ldk_words < ldw_of(dh) || ldv_words < ldw_of(tk) || ld_o < dh ||
+        (p_out && ldp_words < ldw_of(tk)))
+        return BWTA_ERR_SHAPE;
+    if (q_bstride < 0 || q_hstride < 0 || k_bstride < 0 || k_hstride < 0 || v_bstride < 0 || v_hstride < 0 ||
+        o_bstride < 0 || o_hstride < 0)
+        return BWTA_ERR_SHAPE;
+    // every plane is read by TMA: 16-byte aligned bases and row / batch / head strides
+    if (ldq_words % 4 || ldk_words % 4 || ldv_words % 4 || q_bstride % 4 || q_hstride % 4 || k_bstride % 4 ||
+        k_hstride % 4 || v_bstride % 4 || v_hstride % 4 || !aligned16(q_sgn) || !aligned16(q_nz) ||
+        !aligned16(k_sgn) || (k_nz && !aligned16(k_nz)) || !aligned16(vt_sgn) || !aligned16(vt_nz) ||
+        (p_out && (ldp_words % 4 || !aligned16(p_out))))
+        return BWTA_ERR_ALIGNMENT;
+    st = check_device();
+    if (st != BWTA_OK) return st;
+    AttnPrefillArgs a{};
+    a.q_sgn = q_sgn;
+    a.q_nz = q_nz;
+    a.k_sgn = k_sgn;
+    a.k_nz = k_nz;
+    a.v_sgn = vt_sgn;
+    a.v_nz = vt_nz;
+    a.nb = batch;
+    a.nh = heads;
+    a.tq = tq;
+    a.tk = tk;
+    a.dh = dh;
+    a.ldq = ldq_words;
+    a.ldk = ldk_words;
+    a.ldv = ldv_words;
+    a.q_bs = q_bstride;
+    a.q_hs = q_hstride;
+    a.k_bs = k_bstride;
+    a.k_hs = k_hstride;
+    a.v_bs = v_bstride;
+    a.v_hs = v_hstride;
+    a.alpha = alpha;
+    a.beta = beta;
+    a.p_dt = p_dt;
+    const double t = 0.5 * double(s_att);  // exact
+    if (p_dt == BWTA_F32) {
+        a.p_t = float(t);                  // exact (halving a normal float)
+    } else {
+        const bool bf = p_dt == BWTA_BF16;
+        const uint16_t tp = smallest_pattern(t, false, bf);  // smallest storage value >= s/2 (R2)
+        a.p_t = float(bf ? bf16_value(tp) : f16_value(tp));
+    }
+    a.o = o;
+    a.o_dt = o_dt;
+    a.ld_o = ld_o;
+    a.o_bs = o_bstride;
+    a.o_hs = o_hstride;
+    a.p_out = p_out;
+    a.p_ld = ldp_words;
+    if (!attn_prefill_supported(a)) return BWTA_ERR_UNSUPPORTED;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (p_out) {  // the kernel writes the data words of P; padding words stay zero
+        cudaError_t e = cudaMemsetAsync(p_out, 0, sizeof(uint32_t) * size_t(batch * heads) * size_t(tq) *
+                                                        size_t(ldp_words), s);
+        if (e != cudaSuccess) return cuda_fail(e);
+        count_launch();
+    }
+    cudaError_t e = launch_attn_prefill(a, s);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_last_design = BWTA_DESIGN_TCGEN05;
+    return BWTA_OK;
+}
+
 bwta_status_t bwta_attn_pv_pack(const uint32_t* p_sgn, const uint32_t* p_nz, const uint32_t* vt_sgn,
                                 const uint32_t* vt_nz, int64_t batch, int64_t heads, int64_t tq, int64_t tk, int64_t dh,
                                 int64_t ldp_words, int64_t p_bstride, int64_t p_hstride, int64_t ldv_words,

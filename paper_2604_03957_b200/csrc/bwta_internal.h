@@ -173,6 +173,25 @@ struct DecodeArgs {
 };
 cudaError_t launch_attn_decode(const DecodeArgs& a, cudaStream_t s);
 
+// fused prefill attention on tcgen05 (attn_prefill.cu): Q tiles of 128 rows per (batch, head)
+struct AttnPrefillArgs {
+    const uint32_t *q_sgn, *q_nz;   // [entries][tq][ldq]
+    const uint32_t *k_sgn, *k_nz;   // [entries][tk][ldk]; k_nz null: binary K
+    const uint32_t *v_sgn, *v_nz;   // V^T [entries][dh][ldv]
+    int64_t nb, nh, tq, tk, dh;
+    int64_t ldq, ldk, ldv;          // words
+    int64_t q_bs, q_hs, k_bs, k_hs, v_bs, v_hs;  // words
+    float alpha, p_t, beta;         // p_t: the bool threshold as a p_dt storage value (R2)
+    int p_dt;
+    void* o;
+    int o_dt;
+    int64_t ld_o, o_bs, o_hs;       // elements
+    uint32_t* p_out;                // optional P planes [entries][tq][p_ld]
+    int64_t p_ld;
+};
+bool attn_prefill_supported(const AttnPrefillArgs& a);
+cudaError_t launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t s);
+
 // tcgen05 path (design (b)).  Returns cudaErrorNotSupported when the shape is
 // outside what the tcgen05 kernels handle (the dispatcher then uses design (a)).
 size_t matmul_tc_workspace(const MatmulArgs& a);
