@@ -138,12 +138,14 @@ BWTA_API uint64_t bwta_kernel_launches(void);
  *
  * x      : [batch*heads] matrices of [rows x cols], dtype x_dt (F16 | BF16 | F32),
  *          row stride ld_x >= cols elements; entry e at x + b*x_bstride + h*x_hstride.
- * scale  : s_A > 0, finite (host value).  kind: BWTA_TERNARY or BWTA_BOOL.
+ * scale  : s_A > 0, finite (host value).  kind: BWTA_TERNARY, BWTA_BOOL, or BWTA_BINARY
+ *          (W1A1 activations: q = sign(x) of Eq. sign P:903-908 -- +1 iff x >= 0,
+ *          so -0.0 -> +1 and NaN -> -1 (R4); the scale does not enter the quantizer).
  * transpose = 0 : pack along cols -> planes [rows x ld_words], ld_words >= bwta_ld_words(cols)
  * transpose = 1 : pack along rows (the planes of X^T, used for V^T in PV)
  *                 -> planes [cols x ld_words], ld_words >= bwta_ld_words(rows)
- * sgn    : TERNARY: output sign plane; BOOL: must be NULL.
- * nz     : output non-zero plane (required).
+ * sgn    : TERNARY / BINARY: output sign plane; BOOL: must be NULL.
+ * nz     : TERNARY / BOOL: output non-zero plane; BINARY: must be NULL (every element is +-1).
  *          Plane entry e at plane + b*p_bstride + h*p_hstride (words).
  * row_nnz: nullable; int32 [batch*heads*out_rows], contiguous, = number of
  *          non-zero quantized values per packed row (out_rows = rows, or cols
@@ -201,8 +203,10 @@ BWTA_API bwta_status_t bwta_pack_weight(const void* w, bwta_dtype_t w_dt, int64_
 /*
  * Y[m][n] = fl32(float(dot[m][n]) * fl32(w_scale[n] * a_scale)),
  * dot[m][n] = sum_k qa[m][k] * qw[n][k].
- * A      : activations, a_kind = TERNARY (a_sgn, a_nz) or BOOL (a_sgn NULL, a_nz),
- *          planes [m x lda_words] (lda_words >= bwta_ld_words(k)).
+ * A      : activations, a_kind = TERNARY (a_sgn, a_nz), BOOL (a_sgn NULL, a_nz) or BINARY
+ *          (a_sgn, a_nz NULL: the W1A1 "Binary Linear"), planes [m x lda_words]
+ *          (lda_words >= bwta_ld_words(k)).  With binary A every kernel multiplies its own K
+ *          padding as (+1)(+1) and subtracts that count from the dot before the epilogue.
  * W      : weight sign plane [n x ldw_words] (ldw_words >= bwta_ld_words(k)).
  * w_scale: nullable device float [n] (NULL -> 1).  a_scale: host float.
  * y      : y_transposed = 0: Y [m x n] with row stride ld_y >= n;
@@ -270,7 +274,8 @@ BWTA_API bwta_status_t bwta_attn_qk(const uint32_t* q_sgn, const uint32_t* q_nz,
  * O_e[i][d] = fl32(float(sum_j p[i][j] v[j][d]) * beta)
  * P planes [tq x ldp_words]: bool (p_sgn == NULL, p_nz) or ternary.
  * V is given TRANSPOSED: planes [dh x ldv_words] over the tk axis, as
- * produced by bwta_pack_act(transpose = 1) of V [tk x dh]; ternary (vt_sgn, vt_nz).
+ * produced by bwta_pack_act(transpose = 1) of V [tk x dh]; ternary (vt_sgn, vt_nz) or binary
+ * (vt_sgn, vt_nz NULL: the "Binary A x V" of P:553; P's nz plane masks the key padding).
  * O [tq x dh] per entry, row stride ld_o, dtype o_dt.
  */
 BWTA_API size_t bwta_attn_pv_workspace_size(int64_t batch_heads, int64_t tq, int64_t tk, int64_t dh,

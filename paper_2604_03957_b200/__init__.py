@@ -142,8 +142,8 @@ def _pack_desc(x: torch.Tensor, scale: float, kind: str, transpose: bool, row_nn
     ldw = bwta_ld_words(plen)
     lead = tuple(x.shape[:-2])
     shape = lead + (out_rows, ldw)
-    nz = torch.empty(shape, dtype=torch.int32, device=x.device)
-    sgn = torch.empty(shape, dtype=torch.int32, device=x.device) if kind == "ternary" else None
+    nz = torch.empty(shape, dtype=torch.int32, device=x.device) if kind != "binary" else None
+    sgn = torch.empty(shape, dtype=torch.int32, device=x.device) if kind != "bool" else None
     rn = torch.empty(lead + (out_rows,), dtype=torch.int32, device=x.device) if row_nnz else None
     pbs = h * out_rows * ldw if x.dim() == 4 else out_rows * ldw
     phs = out_rows * ldw if x.dim() == 4 else 0
@@ -156,7 +156,9 @@ def _pack_desc(x: torch.Tensor, scale: float, kind: str, transpose: bool, row_nn
 
 def bwta_pack_act(x: torch.Tensor, scale: float, kind: str = "ternary", transpose: bool = False,
                   row_nnz: bool = False, stream=None) -> Packed:
-    """Quantize and bit-pack activations.
+    """Quantize and bit-pack activations.  kind: "ternary" (sgn + nz planes), "bool"
+    (nz), or "binary" (sgn only: sign(x) of Eq. sign, P:903-908 -- W1A1 activations; `scale` is
+    then only the epilogue's s_A).
 
     x: CUDA tensor (f16/bf16/f32) [rows, cols], [B, rows, cols] or
     [B, H, rows, cols] (any batch/head/row strides, unit column stride).
@@ -215,8 +217,8 @@ def bwta_gemm(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: fl
 
     a: Packed activations [M, lda] (ternary or bool); w: Packed weights [N, ldw].
     Returns Y [M, N] (or Y^T [N, M] if y_transposed)."""
-    if a.kind not in ("ternary", "bool") or w.kind != "binary" or a.cols != w.cols:
-        raise ValueError("bwta_gemm expects ternary/bool activations and binary weights of equal K")
+    if a.kind not in ("ternary", "bool", "binary") or w.kind != "binary" or a.cols != w.cols:
+        raise ValueError("bwta_gemm expects ternary/bool/binary activations and binary weights of equal K")
     ar = a.ref
     m, n, k = ar.shape[-2], w.sgn.shape[-2], a.cols
     dev = ar.device
@@ -315,8 +317,8 @@ def bwta_attn_pv(p: Packed, vt: Packed, beta: float, out_dtype=torch.float16,
     b, h, pbs, phs = _batch_dims(pr)
     _, _, vbs, vhs = _batch_dims(vr)
     tq, dh, tk = pr.shape[-2], vr.shape[-2], p.cols
-    if vt.cols != tk or vt.kind != "ternary":
-        raise ValueError("V^T must be ternary planes over the same Tk as P")
+    if vt.cols != tk or vt.kind not in ("ternary", "binary") or p.kind not in ("bool", "ternary"):
+        raise ValueError("V^T must be ternary or binary planes over the same Tk as P (bool or ternary)")
     if out is None:
         out = torch.empty(tuple(pr.shape[:-2]) + (tq, dh), dtype=out_dtype, device=pr.device)
     else:

@@ -249,16 +249,19 @@ bwta_status_t prepare_pack(const bwta_pack_desc_t& d, PackArgs& a, bool& empty) 
     uint32_t* nz = d.nz;
     const int64_t ld_words = d.ld_words, p_bstride = d.p_bstride, p_hstride = d.p_hstride;
     if (x_dt != BWTA_F16 && x_dt != BWTA_BF16 && x_dt != BWTA_F32) return BWTA_ERR_UNSUPPORTED;
-    if (kind != BWTA_TERNARY && kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
+    if (kind != BWTA_TERNARY && kind != BWTA_BOOL && kind != BWTA_BINARY) return BWTA_ERR_UNSUPPORTED;
     if (!scale_ok_pos(scale)) return BWTA_ERR_INVALID_VALUE;
     if (transpose != 0 && transpose != 1) return BWTA_ERR_INVALID_VALUE;
     if (batch < 0 || heads < 1 || rows < 0 || cols < 0) return BWTA_ERR_SHAPE;
-    if (x == nullptr || nz == nullptr) return BWTA_ERR_INVALID_VALUE;
-    if ((kind == BWTA_TERNARY) != (sgn != nullptr)) return BWTA_ERR_INVALID_VALUE;
+    if (x == nullptr) return BWTA_ERR_INVALID_VALUE;
+    // planes: TERNARY sgn + nz, BOOL nz only, BINARY (W1A1 activations, sign(x)) sgn only
+    if ((kind != BWTA_BOOL) != (sgn != nullptr) || (kind != BWTA_BINARY) != (nz != nullptr))
+        return BWTA_ERR_INVALID_VALUE;
+    if (kind == BWTA_BINARY && d.row_nnz) return BWTA_ERR_INVALID_VALUE;  // every element is non-zero
     const int64_t packed_len = transpose ? rows : cols;
     if (ld_x < cols || ld_words < ldw_of(packed_len)) return BWTA_ERR_SHAPE;
     if (x_bstride < 0 || x_hstride < 0 || p_bstride < 0 || p_hstride < 0) return BWTA_ERR_SHAPE;
-    if (ld_words % 4 || p_bstride % 4 || p_hstride % 4 || !aligned16(nz) || (sgn && !aligned16(sgn)))
+    if (ld_words % 4 || p_bstride % 4 || p_hstride % 4 || (nz && !aligned16(nz)) || (sgn && !aligned16(sgn)))
         return BWTA_ERR_ALIGNMENT;
     // No packed rows at all -> nothing to write.  (Packed rows whose length
     // is 0 are all padding and are still written as zero words.)
@@ -273,9 +276,10 @@ bwta_status_t prepare_pack(const bwta_pack_desc_t& d, PackArgs& a, bool& empty) 
     a.ld_x = ld_x;
     a.x_bs = x_bstride;
     a.x_hs = x_hstride;
-    a.kind = kind;
+    a.kind = kind;  // BWTA_* and K_* share the numbering; K_BINARY with mu = 0 is sign(x) (Eq. sign, R4)
     a.sgn = sgn;
     a.nz = nz;
+    a.mu = nullptr;
     a.ldw = ld_words;
     a.p_bs = p_bstride;
     a.p_hs = p_hstride;
@@ -384,18 +388,20 @@ bwta_status_t bwta_gemm(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t
                         const uint32_t* w_sgn, int64_t n, int64_t ldw_words, int64_t k, const float* w_scale,
                         float a_scale, void* y, bwta_dtype_t y_dt, int64_t ld_y, int y_transposed, void* workspace,
                         size_t workspace_bytes, const bwta_opts_t* opts, void* stream) {
-    if (a_kind != BWTA_TERNARY && a_kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
+    if (a_kind != BWTA_TERNARY && a_kind != BWTA_BOOL && a_kind != BWTA_BINARY) return BWTA_ERR_UNSUPPORTED;
     if (!valid_out_dt(y_dt)) return BWTA_ERR_UNSUPPORTED;
     if (m < 0 || n < 0 || k < 0 || k > KMAX) return BWTA_ERR_SHAPE;
     if (m == 0 || n == 0) return BWTA_OK;  // empty product: nothing to read or write
-    if (a_nz == nullptr || w_sgn == nullptr || y == nullptr) return BWTA_ERR_INVALID_VALUE;
-    if ((a_kind == BWTA_TERNARY) != (a_sgn != nullptr)) return BWTA_ERR_INVALID_VALUE;
+    if (w_sgn == nullptr || y == nullptr) return BWTA_ERR_INVALID_VALUE;
+    if ((a_kind != BWTA_BOOL) != (a_sgn != nullptr) || (a_kind != BWTA_BINARY) != (a_nz != nullptr))
+        return BWTA_ERR_INVALID_VALUE;
     if (!std::isfinite(a_scale)) return BWTA_ERR_INVALID_VALUE;
     if (y_transposed != 0 && y_transposed != 1) return BWTA_ERR_INVALID_VALUE;
     const int64_t need = ldw_of(k);
     if (lda_words < need || ldw_words < need) return BWTA_ERR_SHAPE;
     if (ld_y < (y_transposed ? m : n)) return BWTA_ERR_SHAPE;
-    if (lda_words % 4 || ldw_words % 4 || !aligned16(a_nz) || (a_sgn && !aligned16(a_sgn)) || !aligned16(w_sgn))
+    if (lda_words % 4 || ldw_words % 4 || (a_nz && !aligned16(a_nz)) || (a_sgn && !aligned16(a_sgn)) ||
+        !aligned16(w_sgn))
         return BWTA_ERR_ALIGNMENT;
     bwta_status_t st = check_device();
     if (st != BWTA_OK) return st;
@@ -862,14 +868,15 @@ bwta_status_t bwta_attn_pv(const uint32_t* p_sgn, const uint32_t* p_nz, const ui
     if (st != BWTA_OK) return st;
     if (tq < 0 || tk < 0 || dh < 0 || tk > KMAX) return BWTA_ERR_SHAPE;
     if (batch == 0 || tq == 0 || dh == 0) return BWTA_OK;
-    if (p_nz == nullptr || vt_sgn == nullptr || vt_nz == nullptr || o == nullptr) return BWTA_ERR_INVALID_VALUE;
+    // vt_nz == NULL: binary V (Binary A x V); P's nz plane masks the key padding
+    if (p_nz == nullptr || vt_sgn == nullptr || o == nullptr) return BWTA_ERR_INVALID_VALUE;
     if (!std::isfinite(beta)) return BWTA_ERR_INVALID_VALUE;
     const int64_t need = ldw_of(tk);
     if (ldp_words < need || ldv_words < need || ld_o < dh) return BWTA_ERR_SHAPE;
     if (p_bstride < 0 || p_hstride < 0 || v_bstride < 0 || v_hstride < 0 || o_bstride < 0 || o_hstride < 0)
         return BWTA_ERR_SHAPE;
     if (ldp_words % 4 || ldv_words % 4 || p_bstride % 4 || p_hstride % 4 || v_bstride % 4 || v_hstride % 4 ||
-        !aligned16(p_nz) || (p_sgn && !aligned16(p_sgn)) || !aligned16(vt_sgn) || !aligned16(vt_nz))
+        !aligned16(p_nz) || (p_sgn && !aligned16(p_sgn)) || !aligned16(vt_sgn) || (vt_nz && !aligned16(vt_nz)))
         return BWTA_ERR_ALIGNMENT;
     st = check_device();
     if (st != BWTA_OK) return st;

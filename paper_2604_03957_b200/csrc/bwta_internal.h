@@ -140,6 +140,9 @@ struct MatmulArgs {
     const float* col_scale;   // [N] or null
     float scalar;
     int tile_n = 0, cta_group = 0;  // design (b) tile overrides (0 = auto)
+    // Both operands binary (W1A1, no nz plane on either side): every kernel multiplies its own K
+    // padding (zero sign bits = +1 x +1) and subtracts that count from the dot in its epilogue
+    // (dot_bias = K - K_processed, exact integer arithmetic).
     // fused next-layer pack (bwta_gemm_pack): instead of writing Y, quantize
     // round(Y to y_dt) with the next layer's thresholds and write its planes
     int pack_out = 0;

@@ -37,7 +37,9 @@ __device__ __forceinline__ void store_out(void* y, int dt, int64_t idx, int32_t 
     else reinterpret_cast<float*>(y)[idx] = v;
 }
 
-template <bool A_SGN, bool B_NZ>
+// A_NZ = false: binary A (W1A1 activations, sgn plane only): its nz words are all-ones over the
+// kw4 words the kernel reads, and the epilogue removes the (+1)(+1) products of the padding
+template <bool A_SGN, bool B_NZ, bool A_NZ = true>
 __global__ void __launch_bounds__(NT) matmul_cc_kernel(MatmulArgs p) {
     __shared__ __align__(16) uint32_t sAs[2][KW][BM + PAD];
     __shared__ __align__(16) uint32_t sAn[2][KW][BM + PAD];
@@ -52,7 +54,7 @@ __global__ void __launch_bounds__(NT) matmul_cc_kernel(MatmulArgs p) {
     const int64_t i0 = int64_t(blockIdx.y) * BM, j0 = int64_t(blockIdx.x) * BN;
     const int64_t eb = e / p.nh, eh = e % p.nh;
     const uint32_t* As = A_SGN ? p.a_sgn + eb * p.a_bs + eh * p.a_hs : nullptr;
-    const uint32_t* An = p.a_nz + eb * p.a_bs + eh * p.a_hs;
+    const uint32_t* An = A_NZ ? p.a_nz + eb * p.a_bs + eh * p.a_hs : nullptr;
     const uint32_t* Bs = p.b_sgn + eb * p.b_bs + eh * p.b_hs;
     const uint32_t* Bn = B_NZ ? p.b_nz + eb * p.b_bs + eh * p.b_hs : nullptr;
     const int64_t kw = (p.K + 31) / 32;
@@ -67,7 +69,8 @@ __global__ void __launch_bounds__(NT) matmul_cc_kernel(MatmulArgs p) {
         const bool wok = w < kw4;
         const int64_t ia = i0 + lr, jb = j0 + lr;
         const uint4 z = make_uint4(0, 0, 0, 0);
-        ra_n = (wok && ia < p.M) ? *reinterpret_cast<const uint4*>(An + ia * p.lda + w) : z;
+        if (A_NZ) ra_n = (wok && ia < p.M) ? *reinterpret_cast<const uint4*>(An + ia * p.lda + w) : z;
+        else ra_n = (wok && ia < p.M) ? make_uint4(~0u, ~0u, ~0u, ~0u) : z;
         if (A_SGN) ra_s = (wok && ia < p.M) ? *reinterpret_cast<const uint4*>(As + ia * p.lda + w) : z;
         rb_s = (wok && jb < p.N) ? *reinterpret_cast<const uint4*>(Bs + jb * p.ldb + w) : z;
         if (B_NZ) rb_n = (wok && jb < p.N) ? *reinterpret_cast<const uint4*>(Bn + jb * p.ldb + w) : z;
@@ -168,7 +171,8 @@ __global__ void __launch_bounds__(NT) matmul_cc_kernel(MatmulArgs p) {
         for (int i = 0; i < TM; ++i) {
             const int64_t gi = i0 + ty * TM + i;
             if (gi >= p.M) continue;
-            const int32_t d = B_NZ ? acc2[i][j] - 2 * acc[i][j] : base[i] - 2 * acc[i][j];
+            int32_t d = B_NZ ? acc2[i][j] - 2 * acc[i][j] : base[i] - 2 * acc[i][j];
+            if (!A_NZ && !B_NZ) d -= int32_t(32 * kw4 - p.K);  // W1A1: the K padding counted as +1
             const int64_t idx = ybase + (p.y_trans ? gj * p.ldy + gi : gi * p.ldy + gj);
             store_out(Y, p.y_dt, idx, d, c);
         }
@@ -181,6 +185,10 @@ cudaError_t launch_matmul_cc(const MatmulArgs& a, cudaStream_t s) {
     if (a.M == 0 || a.N == 0 || a.nb * a.nh == 0) return cudaSuccess;
     dim3 grid(unsigned((a.N + BN - 1) / BN), unsigned((a.M + BM - 1) / BM), unsigned(a.nb * a.nh));
     const bool asg = a.a_sgn != nullptr, bnz = a.b_nz != nullptr;
+    if (!a.a_nz) {  // binary A (W1A1)
+        if (bnz) return launch_pdl(matmul_cc_kernel<true, true, false>, grid, NT, 0, s, 1, a);
+        return launch_pdl(matmul_cc_kernel<true, false, false>, grid, NT, 0, s, 1, a);
+    }
     if (asg && bnz) return launch_pdl(matmul_cc_kernel<true, true>, grid, NT, 0, s, 1, a);
     if (asg) return launch_pdl(matmul_cc_kernel<true, false>, grid, NT, 0, s, 1, a);
     if (bnz) return launch_pdl(matmul_cc_kernel<false, true>, grid, NT, 0, s, 1, a);

@@ -127,6 +127,7 @@ struct TcParams {
     int64_t po_ld;
     int64_t po_bs, po_hs;  // words between the planes of consecutive batch / head entries
     float po_tp, po_tn;
+    float dot_bias;  // W1A1: K - K_processed (both operands binary; the generic epilogue adds it)
     int dbg;  // BWTA_TRACE builds only (tools/trace_gemm.py): 1 skip unpack math, 2 skip MMAs, 4 skip TMA, 8 skip A unpack, 16 skip B unpack
 };
 
@@ -226,6 +227,10 @@ __device__ __forceinline__ void epi_tile_generic(const TcParams& p, const CUtens
             uint32_t v[32];
             tmem_ld_32x32b_x32(tacc + (uint32_t(q * 32) << 16) + uint32_t(c0 + 32 * u), v);
             tmem_wait_ld();
+            if (p.dot_bias != 0.f) {  // W1A1: remove the +1 x +1 products of the K padding (exact)
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__fadd_rn(__uint_as_float(v[j]), p.dot_bias));
+            }
             const int64_t nl = n0 + 32 * u + lane;
             const float cl = col_scaled ? __fmul_rn(__ldg(p.scale + (nl < p.N ? nl : 0)), p.scalar) : crow;
             float f[32];
@@ -490,7 +495,7 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
     uint8_t* stg = sOut + (h * 4 + q) * OUT_NBUF * OUT_BUF;
     int nstore = 0;  // fast path: chunks stored by this warp (selects the staging buffer)
     float* cs = sScale + (h * 4 + q) * Cfg<BN, CG>::SCALE_COLS;
-    const bool fast_ok = ES == 2 && p.use_tma_store;
+    const bool fast_ok = ES == 2 && p.use_tma_store && p.dot_bias == 0.f;
     const bool col_scaled = !p.scale_on_rows && p.scale;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -1079,7 +1084,7 @@ cudaError_t launch_ks(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUte
 template <int BN, int CG>
 cudaError_t launch_cfg(int ks, const CUtensorMap& ma0, const CUtensorMap& ma1, const CUtensorMap& mb0,
                        const CUtensorMap& mb1, const CUtensorMap& my, const TcParams& p, cudaStream_t s) {
-    const bool fast = !p.pack_out && p.use_tma_store && (p.y_dt == DT_F16 || p.y_dt == DT_BF16);
+    const bool fast = !p.pack_out && p.use_tma_store && (p.y_dt == DT_F16 || p.y_dt == DT_BF16) && p.dot_bias == 0.f;
     // the heavy GEMM tiles (BN = 192, 256-K stages) get kinds fixed at compile time for the BWTA
     // linear's combinations: activations (ternary / bool) x binary weights, and the swapped pack
     const int kk = 1 + 3 * p.a_kind + p.b_kind;
@@ -1186,6 +1191,9 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     p.M = pl.Mk;
     p.N = pl.Nk;
     p.num_kb = int((kw4 + wps - 1) / wps);
+    // W1A1 (both operands binary): the num_kb * ks K positions the kernel multiplies include the
+    // zero-bit padding, each contributing (+1)(+1) -- subtract them in the epilogue
+    if (!pl.a_nz && !pl.b_nz) p.dot_bias = float(a.K - int64_t(p.num_kb) * ks);
     p.entries = entries;
     p.nh = a.nh;
     p.m_tiles = int((pl.Mk + BM * cg - 1) / (BM * cg));

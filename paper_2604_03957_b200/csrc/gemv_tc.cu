@@ -63,6 +63,7 @@ constexpr int GV_TMEM_COLS = 512;
 constexpr int GV_SMEM_MAX = 200 * 1024;
 
 struct GvParams {
+    float dot_bias;  // W1A1 (both operands binary): K - K_processed, added to every dot
     int64_t M, N;  // kernel-A rows / kernel-B rows (N <= NB) per entry
     int num_kb;
     int64_t nh, entries;
@@ -346,7 +347,8 @@ __global__ void __launch_bounds__(GV_NT, 1)
                 for (int j = 0; j < NB; ++j) {
                     if (j < ncol) {
                         const float cj = p.scale && !p.scale_on_rows ? __fmul_rn(__ldg(p.scale + j), p.scalar) : crow;
-                        store_out(p, eoff + r * p.y_rs + j * p.y_cs, __fmul_rn(__uint_as_float(v[j]), cj), v[j]);
+                        const uint32_t vj = __float_as_uint(__fadd_rn(__uint_as_float(v[j]), p.dot_bias));
+                        store_out(p, eoff + r * p.y_rs + j * p.y_cs, __fmul_rn(__uint_as_float(vj), cj), vj);
                     }
                 }
             }
@@ -420,6 +422,7 @@ cudaError_t launch_matmul_gemv(const MatmulArgs& a, cudaStream_t s) {
     p.M = Mk;
     p.N = Nk;
     p.num_kb = int((kw4_of(a.K) + GV_WPS - 1) / GV_WPS);
+    if (!ka_nz && !kb_nz) p.dot_bias = float(a.K - int64_t(p.num_kb) * GV_WPS * 32);  // W1A1 padding
     p.nh = a.nh;
     p.entries = a.nb * a.nh;
     p.tiles_per_entry = int((Mk + GV_BM - 1) / GV_BM);

@@ -313,24 +313,33 @@ __device__ __forceinline__ void pack_cols_body(const PackArgs& p, unsigned vb, u
 #pragma unroll
             for (int g = 0; g < GL; ++g) {
                 uint32_t pos = 0, neg = 0;
+                if (KIND == K_BINARY) {
+                    // sign (Eq. sign; R4): -1 unless x >= 0 (NaN -> -1, -0.0 -> +1); rows past
+                    // the end were loaded as +0 and columns past the end are dropped by the caller
+                    const int64_t r = (int64_t(gq) * G + g0 + g) * 32 + lane;
 #pragma unroll
-                for (int q = 0; q < NV; ++q) {
-                    uint32_t pb, nb;
-                    chunk_bits<T>(v[g][q], p.th, pb, nb);
-                    pos |= pb << (q * E);
-                    neg |= nb << (q * E);
+                    for (int q = 0; q < NV; ++q) neg |= chunk_lt_mu<T>(v[g][q], 0.f) << (q * E);
+                    if (r >= p.rows) neg = 0u;  // padding bits are 0 (R8)
+                } else {
+#pragma unroll
+                    for (int q = 0; q < NV; ++q) {
+                        uint32_t pb, nb;
+                        chunk_bits<T>(v[g][q], p.th, pb, nb);
+                        pos |= pb << (q * E);
+                        neg |= nb << (q * E);
+                    }
                 }
-                nzw[g0 + g] = transpose32(KIND == K_BOOL ? pos : (pos | neg), lane);
-                sgw[g0 + g] = (KIND == K_TERNARY) ? transpose32(neg, lane) : 0u;
+                nzw[g0 + g] = KIND == K_BINARY ? 0u : transpose32(KIND == K_BOOL ? pos : (pos | neg), lane);
+                sgw[g0 + g] = (KIND != K_BOOL) ? transpose32(neg, lane) : 0u;
             }
         }
         const int64_t col = int64_t(tc) * 32 + lane;
         if (col < p.cols) {
             const int64_t poff = int64_t(e / nh) * p.p_bs + int64_t(e % nh) * p.p_hs + col * p.ldw + int64_t(gq) * G;
-            *reinterpret_cast<uint4*>(p.nz + poff) = make_uint4(nzw[0], nzw[1], nzw[2], nzw[3]);
-            if (KIND == K_TERNARY)
+            if (KIND != K_BINARY) *reinterpret_cast<uint4*>(p.nz + poff) = make_uint4(nzw[0], nzw[1], nzw[2], nzw[3]);
+            if (KIND != K_BOOL)
                 *reinterpret_cast<uint4*>(p.sgn + poff) = make_uint4(sgw[0], sgw[1], sgw[2], sgw[3]);
-            if (p.row_nnz) {
+            if (KIND != K_BINARY && p.row_nnz) {
                 const int c = __popc(nzw[0]) + __popc(nzw[1]) + __popc(nzw[2]) + __popc(nzw[3]);
                 if (c) atomicAdd(p.row_nnz + int64_t(e) * p.cols + col, c);
             }
@@ -365,7 +374,7 @@ struct PackGroup {
 
 template <typename T, int KIND, bool VEC>
 __device__ __forceinline__ void group_body(const PackArgs& p, int transpose, unsigned vb, unsigned vg) {
-    if (transpose) pack_cols_body<T, KIND == K_BINARY ? K_TERNARY : KIND, VEC, uint32_t>(p, vb, vg);
+    if (transpose) pack_cols_body<T, KIND, VEC, uint32_t>(p, vb, vg);
     else pack_rows_body<T, KIND, VEC, uint32_t>(p, vb, vg);
 }
 
@@ -443,6 +452,7 @@ cudaError_t cols_dispatch(const PackArgs& a, cudaStream_t s, int grid) {
         else err = launch_pdl(pack_cols_kernel<T, KIND, false, IDX>, grid, 256, 0, s, 1, a);         \
     } while (0)
     if (a.kind == K_BOOL) BWTA_COLS(K_BOOL);
+    else if (a.kind == K_BINARY) BWTA_COLS(K_BINARY);
     else BWTA_COLS(K_TERNARY);
 #undef BWTA_COLS
     return err;

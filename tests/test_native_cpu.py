@@ -76,7 +76,7 @@ def test_pack_act_validation(N):
     assert _pack(L, nz=None) == 1
     assert _pack(L, kind=1) == 1            # BOOL must not get a sgn plane
     assert _pack(L, sgn=None) == 1          # TERNARY needs one
-    assert _pack(L, kind=0) == 4            # BINARY is the weight pack, not pack_act
+    assert _pack(L, kind=0) == 1            # BINARY (W1A1 sign) has a sgn plane only, no nz
     assert _pack(L, x_dt=3) == 4            # I32 input unsupported
     assert _pack(L, rows=-1) == 2
     assert _pack(L, heads=0) == 2
@@ -104,7 +104,7 @@ def test_gemm_and_attention_validation(N):
     assert gemm(lda=5, k=100) == 3 or gemm(lda=5, k=100) == 2
     assert gemm(a_sgn=None) == 1
     assert gemm(kind=1) == 1                 # BOOL activations have no sgn plane
-    assert gemm(kind=0) == 4
+    assert gemm(kind=0) == 1                 # BINARY activations have no nz plane
     assert gemm(y=None) == 1
     assert gemm(y_dt=7) == 4
     assert gemm(ld_y=3) == 2
@@ -124,7 +124,9 @@ def test_gemm_and_attention_validation(N):
     assert L.bwta_attn_pv(None, 32, 48, 64, 1, 1, 4, 100, 64, 4, 0, 0, 4, 0, 0, ctypes.c_float(0.1), 80, 0,
                           64, 0, 0, None, 0, None, None) == 4
     assert L.bwta_attn_pv(None, 32, 48, None, 1, 1, 4, 100, 64, 4, 0, 0, 4, 0, 0, ctypes.c_float(0.1), 80, 0,
-                          64, 0, 0, None, 0, None, None) == 1
+                          64, 0, 0, None, 0, None, None) == 4   # binary V^T (vt_nz NULL): valid
+    assert L.bwta_attn_pv(None, 32, None, 64, 1, 1, 4, 100, 64, 4, 0, 0, 4, 0, 0, ctypes.c_float(0.1), 80, 0,
+                          64, 0, 0, None, 0, None, None) == 1   # V^T always has a sign plane
     assert L.bwta_attn_pv(None, 32, 48, 64, 1, 1, 4, 100, 64, 4, 0, 0, 4, 0, 0, ctypes.c_float(0.1), 80, 0,
                           63, 0, 0, None, 0, None, None) == 2
 
