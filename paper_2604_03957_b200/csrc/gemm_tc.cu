@@ -128,7 +128,7 @@ struct TcParams {
     int64_t po_bs, po_hs;  // words between the planes of consecutive batch / head entries
     float po_tp, po_tn;
     float dot_bias;  // W1A1: K - K_processed (both operands binary; the generic epilogue adds it)
-    int dbg;  // BWTA_TRACE builds only (tools/trace_gemm.py): 1 skip unpack math, 2 skip MMAs, 4 skip TMA, 8 skip A unpack, 16 skip B unpack
+    int dbg;  // BWTA_TRACE builds only (tools/trace_gemm.py): 1 skip unpack math, 2 skip MMAs, 4 skip TMA, 8 skip A unpack, 16 skip B unpack, 32/64 wait flavour, 128 skip the B-code proxy fence
 };
 
 __host__ __device__ constexpr int nplanes_of(int kind) { return kind == B_TERNARY ? 2 : 1; }
@@ -928,6 +928,9 @@ __global__ void __launch_bounds__(NT, 1)
                     if (is_a) unpack_rows<KS>(kind, bits, plane_bytes, dst, ut, rows, 128);
                     else unpack_quads<KS>(kind, bits, plane_bytes, dst, ut, rows, 192);
                 }
+#ifdef BWTA_TRACE
+                if (!(p.dbg & 128))
+#endif
                 fence_proxy_async_smem();
                 __syncwarp();
                 TRACE(is_a ? 11 : 3, it, ut == 0);

@@ -13,6 +13,41 @@ __device__ __forceinline__ void waitb(uint64_t* b, uint32_t ph, int hint) {
     else { while (!mbar_try_wait_nh(b, ph)) {} }
 }
 
+// issue rate of the MMA thread: commits alone, or n MMAs (M=128, N, K=64 mxf4, A from smem or TMEM) + 1 commit
+__global__ void issue_kern(int iters, int nmma, int N, int ts, long long* out) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t X;
+    __shared__ uint32_t tslot;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 40000 / 4 - 16; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+    fence_proxy_async_smem();
+    if (threadIdx.x == 0) { mbar_init(&X, 1); fence_barrier_init(); }
+    if (warp == 0) tmem_alloc(&tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tb = tslot;
+    if (warp == 0 && lane == 0) {
+        const uint32_t idesc = idesc_mxf4(128, N);
+        long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+            for (int k = 0; k < nmma; ++k) {
+                if (ts) mma_mxf4_ts(tb, tb + 256 + 8 * k, smem_desc_sw128(smem_u32(sm + 16384) + 32 * k), idesc, tb + 480, tb + 488, 1);
+                else mma_mxf4(tb, smem_desc_sw128(smem_u32(sm) + 32 * k), smem_desc_sw128(smem_u32(sm + 16384) + 32 * k), idesc, tb + 480, tb + 488, 1);
+            }
+            tc_commit(&X);
+        }
+        long long t1 = clock64();
+        mbar_wait(&X, (iters - 1) & 1);
+        long long t2 = clock64();
+        out[0] = (t1 - t0) / iters;
+        out[1] = (t2 - t0) / iters;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) { tc_fence_after(); tmem_dealloc(tslot, 512); }
+}
+
 __global__ void kern(int iters, int mode, int hint, long long* out) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint64_t X, Y;
@@ -69,5 +104,18 @@ int main() {
             printf("%-26s %s try_wait: %lld cycles per round trip (%s)\n", names[mode], hint ? "hinted  " : "unhinted", h,
                    cudaGetErrorString(cudaGetLastError()));
         }
+    long long* d2;
+    cudaMalloc(&d2, 16);
+    cudaFuncSetAttribute(issue_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 50000);
+    for (int ts = 0; ts < 2; ++ts)
+        for (int nmma : {0, 1, 2, 4})
+            for (int N : {128, 192, 256}) {
+                if (nmma == 0 && (N != 128 || ts)) continue;
+                issue_kern<<<1, 64, 50000>>>(2000, nmma, N, ts, d2);
+                long long h[2];
+                cudaMemcpy(h, d2, 16, cudaMemcpyDeviceToHost);
+                printf("issue: %d x MMA(128x%dx64, A %s) + commit: issue %lld cyc/iter, completion %lld cyc/iter (%s)\n",
+                       nmma, N, ts ? "TMEM" : "smem", h[0], h[1], cudaGetErrorString(cudaGetLastError()));
+            }
     return 0;
 }
