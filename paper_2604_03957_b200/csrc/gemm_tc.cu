@@ -745,6 +745,9 @@ __global__ void __launch_bounds__(NT, 1)
             const int arow = mt * BM * CG + rank * BM;
             const int brow = nt * BN + rank * C::BNC;
             for (int kb = 0; kb < p.num_kb; ++kb) {
+#ifdef BWTA_TRACE
+                if (!(p.dbg & 1024))
+#endif
                 kwait(&empty[stage], phase ^ 1, p.dbg);
                 TRACE(1, it, lane == 0);
                 ++it;
@@ -792,6 +795,9 @@ __global__ void __launch_bounds__(NT, 1)
                 tc_fence_after();
                 const uint32_t d = tmem_base + uint32_t(acc * BN);
                 for (int kb = 0; kb < p.num_kb; ++kb) {
+#ifdef BWTA_TRACE
+                    if (!(p.dbg & 256))
+#endif
                     kwait(&bready[stage], phase, p.dbg);
                     tc_fence_after();
                     TRACE(4, it, lane == 0);
@@ -879,7 +885,11 @@ __global__ void __launch_bounds__(NT, 1)
                 // use (it - SA) / STAGES of empty[(it - SA) % STAGES] (one commit per stage frees both
                 // rings; SA <= STAGES, so that barrier cannot run a phase ahead)
                 const int sa = it % C::SA;
-                if (it >= C::SA) {
+                if (it >= C::SA
+#ifdef BWTA_TRACE
+                    && !(p.dbg & 512)
+#endif
+                ) {
                     const int pit = it - C::SA;
                     kwait(&empty[pit % C::STAGES], uint32_t((pit / C::STAGES) & 1), p.dbg);
                 }
