@@ -174,9 +174,10 @@ def op_time_ms(fn, flush, stream, reps=20, trials=5):
 
 # ----------------------------------------------------------------------------- workloads
 class Op:
-    def __init__(self, name, kind, fn, ops=0, bytes_=0, cublas=None, launches=1):
+    def __init__(self, name, kind, fn, ops=0, bytes_=0, cublas=None, launches=1, alts=None):
         self.name, self.kind, self.fn, self.ops, self.bytes, self.cublas = name, kind, fn, ops, bytes_, cublas
         self.launches = launches  # library kernels per call
+        self.alts = alts or {}    # the same op through other designs (timed alongside, not in the step)
 
 
 def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=3072, fuse_ffn=True,
@@ -392,7 +393,14 @@ def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008), world=1, r
 
             def op_g(wp=wp, sw=sw, y=y):
                 B.bwta_gemm(st["xq"], wp, sw, s_x, out=y)
+
+            def op_b1(wp=wp, sw=sw, y=y):  # prior art: the paper's mma.sync b1 design on this GPU
+                B.bwta_gemm(st["xq"], wp, sw, s_x, out=y, design="mma_b1")
+
+            def op_cc(wp=wp, sw=sw, y=y):  # design (a): LOP3 + POPC on CUDA cores
+                B.bwta_gemm(st["xq"], wp, sw, s_x, out=y, design="cuda_core")
         else:
+            op_b1 = op_cc = None
             plan = D.NShardPlan(N, world, rank, chunks)
             rows = plan.local_rows()
             wp = B.bwta_pack_weight(w[rows].contiguous().to(dev), mu=mu)
@@ -404,7 +412,8 @@ def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008), world=1, r
         outs.append(y)
         ws16[N] = w
         ops.append(Op(f"gemm_n{N}", "gemm", op_g, 2 * M * N * K, M * K / 4 + N * K / 8 + 4 * N + 2 * M * N,
-                      (lambda N=N: torch.nn.functional.linear(X, st["w16"][N]))))
+                      (lambda N=N: torch.nn.functional.linear(X, st["w16"][N])),
+                      alts={"design_a_cuda_core": op_cc, "prior_art_mma_b1": op_b1} if op_b1 else None))
     st["w16"] = {N: w.to(dev) for N, w in ws16.items()} if world == 1 else {}
     op_pack()
     smp = dict(X=X.cpu(), s_x=s_x, Ws=ws16, seed=seed)
@@ -836,6 +845,11 @@ def main():
     else:   # eager per-op times (compute + its gathers at N > 1)
         for op in ops:
             per_op[op.name] = statistics.median(time_eager(op.fn, flush, 10, stream))
+    alt_ms = {}
+    if world == 1:
+        for op in ops:
+            for an, fn in op.alts.items():
+                alt_ms.setdefault(op.name, {})[an] = op_time_ms(fn, flush, stream, reps=5, trials=3)
     cublas_total = sum(cub_ms.values())
     bwta_mm_only = sum(per_op[n] for n in cub_ms)
     pack_ms = sum(per_op[o.name] for o in ops if o.kind == "pack")
@@ -1018,6 +1032,7 @@ def main():
             "speedup_vs_cublas_fp16": speed,
             "per_op_us": {k: v * 1e3 for k, v in per_op.items()},
             "cublas_fp16_us": {k: v * 1e3 for k, v in cub_ms.items()},
+            "other_designs_us": {k: {a: t * 1e3 for a, t in v.items()} for k, v in alt_ms.items()},
             "pack_GBps": pack_gbs, "extras": extras,
         }
         if world > 1:

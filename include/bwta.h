@@ -97,7 +97,9 @@ typedef enum { BWTA_BINARY = 0, BWTA_BOOL = 1, BWTA_TERNARY = 2 } bwta_kind_t;
 typedef enum {
     BWTA_DESIGN_AUTO = 0,      /* pick per shape */
     BWTA_DESIGN_CUDA_CORE = 1, /* design (a): LOP3 + POPC bit-serial on CUDA cores */
-    BWTA_DESIGN_TCGEN05 = 2    /* design (b): unpack to E2M1 codes + tcgen05.mma.kind::mxf4 (FP32 acc, exact) */
+    BWTA_DESIGN_TCGEN05 = 2,   /* design (b): unpack to E2M1 codes + tcgen05.mma.kind::mxf4 (FP32 acc, exact) */
+    BWTA_DESIGN_MMA_B1 = 3     /* prior art: the paper's warp-level mma.sync b1 AND-popcount design (
+                                  ptxas emulates it on sm_100a with MOVM + IMMA); selectable, never AUTO */
 } bwta_design_t;
 
 /* Options for the matmul entry points; NULL = all defaults (zero-initialised). */

@@ -41,7 +41,7 @@ def _check(st: int, where: str):
 _DT = {torch.float16: N.F16, torch.bfloat16: N.BF16, torch.float32: N.F32, torch.int32: N.I32}
 _KIND = {"binary": N.BINARY, "bool": N.BOOL, "ternary": N.TERNARY}
 _DESIGN = {"auto": N.DESIGN_AUTO, "cuda_core": N.DESIGN_CUDA_CORE, "cc": N.DESIGN_CUDA_CORE,
-           "tcgen05": N.DESIGN_TCGEN05, "tc": N.DESIGN_TCGEN05}
+           "tcgen05": N.DESIGN_TCGEN05, "tc": N.DESIGN_TCGEN05, "mma_b1": N.DESIGN_MMA_B1}
 
 
 def bwta_ld_words(cols: int) -> int:
@@ -49,7 +49,7 @@ def bwta_ld_words(cols: int) -> int:
 
 
 def last_design() -> str:
-    return {0: "none", 1: "cuda_core", 2: "tcgen05"}[lib.bwta_last_design()]
+    return {0: "none", 1: "cuda_core", 2: "tcgen05", 3: "mma_b1"}[lib.bwta_last_design()]
 
 
 @dataclass

@@ -14,7 +14,7 @@ STATUS = {0: "BWTA_OK", 1: "BWTA_ERR_INVALID_VALUE", 2: "BWTA_ERR_SHAPE", 3: "BW
           4: "BWTA_ERR_UNSUPPORTED", 5: "BWTA_ERR_CUDA", 6: "BWTA_ERR_WORKSPACE"}
 F16, BF16, F32, I32 = 0, 1, 2, 3
 BINARY, BOOL, TERNARY = 0, 1, 2
-DESIGN_AUTO, DESIGN_CUDA_CORE, DESIGN_TCGEN05 = 0, 1, 2
+DESIGN_AUTO, DESIGN_CUDA_CORE, DESIGN_TCGEN05, DESIGN_MMA_B1 = 0, 1, 2, 3
 
 EXPORTS = ("bwta_ld_words", "bwta_status_string", "bwta_last_cuda_error", "bwta_last_design",
            "bwta_version", "bwta_kernel_launches", "bwta_pack_act", "bwta_pack_act_batch", "bwta_pack_weight",

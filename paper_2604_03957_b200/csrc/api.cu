@@ -161,7 +161,7 @@ const bwta_opts_t* opts_or_default(const bwta_opts_t* o) {
 
 // Every entry point taking bwta_opts_t validates it here, before anything is enqueued.
 bwta_status_t check_opts(const bwta_opts_t* opts) {
-    if (opts->design < 0 || opts->design > 2) return BWTA_ERR_INVALID_VALUE;
+    if (opts->design < 0 || opts->design > 3) return BWTA_ERR_INVALID_VALUE;
     for (int r : opts->reserved)
         if (r != 0) return BWTA_ERR_INVALID_VALUE;
     if (!(opts->tile_n == 0 || opts->tile_n == 64 || opts->tile_n == 128 || opts->tile_n == 192) ||
@@ -178,6 +178,12 @@ bwta_status_t run_matmul(const MatmulArgs& a0, void* ws, size_t ws_bytes, const 
     MatmulArgs a = a0;
     a.tile_n = opts->tile_n;
     a.cta_group = opts->cta_group;
+    if (opts->design == BWTA_DESIGN_MMA_B1) {  // prior art: the paper's mma.sync b1 design (never AUTO)
+        cudaError_t e = launch_matmul_b1(a, s);
+        if (e != cudaSuccess) return cuda_fail(e);
+        g_last_design = BWTA_DESIGN_MMA_B1;
+        return BWTA_OK;
+    }
     // decode-sized products (<= 4 rows on one side): the CUDA-core GEMV (design (a)
     // family) streams the large side at HBM rate; AUTO prefers it unless a tile
     // shape was forced
@@ -447,7 +453,8 @@ bwta_status_t bwta_gemm_pack(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_k
         return BWTA_ERR_ALIGNMENT;
     const bwta_opts_t* o = opts_or_default(opts);
     if (bwta_status_t so = check_opts(o); so != BWTA_OK) return so;
-    if (o->design == BWTA_DESIGN_CUDA_CORE) return BWTA_ERR_UNSUPPORTED;  // fused pack: design (b) only
+    if (o->design == BWTA_DESIGN_CUDA_CORE || o->design == BWTA_DESIGN_MMA_B1)
+        return BWTA_ERR_UNSUPPORTED;  // fused pack: design (b) only
     bwta_status_t st = check_device();
     if (st != BWTA_OK) return st;
     MatmulArgs a{};
@@ -807,7 +814,8 @@ bwta_status_t bwta_attn_pv_pack(const uint32_t* p_sgn, const uint32_t* p_nz, con
         return BWTA_ERR_ALIGNMENT;
     const bwta_opts_t* o = opts_or_default(opts);
     if (bwta_status_t so = check_opts(o); so != BWTA_OK) return so;
-    if (o->design == BWTA_DESIGN_CUDA_CORE) return BWTA_ERR_UNSUPPORTED;  // fused pack: design (b) only
+    if (o->design == BWTA_DESIGN_CUDA_CORE || o->design == BWTA_DESIGN_MMA_B1)
+        return BWTA_ERR_UNSUPPORTED;  // fused pack: design (b) only
     st = check_device();
     if (st != BWTA_OK) return st;
     MatmulArgs a{};

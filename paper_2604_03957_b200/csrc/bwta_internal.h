@@ -155,6 +155,8 @@ struct MatmulArgs {
 };
 
 cudaError_t launch_matmul_cc(const MatmulArgs& a, cudaStream_t s);
+// the paper's own design (legacy mma.sync b1 AND-popcount; prior art measured on B200, gemm_b1.cu)
+cudaError_t launch_matmul_b1(const MatmulArgs& a, cudaStream_t s);
 
 // fused decode attention (attn_decode.cu): one query row per (batch, head) entry
 struct DecodeArgs {

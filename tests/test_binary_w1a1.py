@@ -66,7 +66,7 @@ def test_gemm_w1a1_parity(B, case):
     d = oracle.dot(qa, qw, threads=oracle.default_threads())
     assert np.all(np.abs(d) <= k) and np.all((d - k) % 2 == 0)  # +-1 x +-1: dot = k - 2 (#disagree)
     for kw in (dict(), dict(design="tcgen05"), dict(tile=(64, 1)), dict(tile=(192, 2)), dict(tile=(128, 2)),
-               dict(design="cuda_core")):
+               dict(design="cuda_core"), dict(design="mma_b1")):
         yi = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.int32, **kw)
         assert np.array_equal(yi.cpu().numpy(), d), (m, n, k, kw)
         y = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=torch.float16, **kw)

@@ -194,7 +194,7 @@ def _gemm_case(B, m, n, k, seed, a_kind="ternary"):
     return a, wp, s_a, s_w, qa, qw
 
 
-@pytest.mark.parametrize("design", ["cuda_core", "tcgen05"])
+@pytest.mark.parametrize("design", ["cuda_core", "tcgen05", "mma_b1"])
 def test_gemm_parity(B, design):
     for i, (m, n, k) in enumerate(GEMM_SHAPES):
         for a_kind in ("ternary", "bool"):
@@ -312,7 +312,7 @@ def test_gemm_exhaustive_k6(B):
         a = Bm.Packed(torch.from_numpy(sa.view(np.int32)).cuda(), torch.from_numpy(na.view(np.int32)).cuda(),
                       "ternary", K)
         w = Bm.Packed(torch.from_numpy(sw.view(np.int32)).cuda(), None, "binary", K)
-        for design in ("cuda_core", "tcgen05"):
+        for design in ("cuda_core", "tcgen05", "mma_b1"):
             y = B.bwta_gemm(a, w, None, 1.0, out_dtype=torch.int32, design=design)
             assert np.array_equal(y.cpu().numpy(), oracle.dot(qa, qw)), (off, design)
 
@@ -335,7 +335,7 @@ def test_gemm_k_zero_and_empty(B):
 ATT = [(1, 1, 1, 1, 64), (2, 3, 37, 41, 64), (1, 2, 128, 128, 128), (2, 2, 130, 129, 33), (1, 1, 256, 300, 128)]
 
 
-@pytest.mark.parametrize("design", ["cuda_core", "tcgen05"])
+@pytest.mark.parametrize("design", ["cuda_core", "tcgen05", "mma_b1"])
 def test_attention_parity(B, design):
     for i, (b, h, tq, tk, dh) in enumerate(ATT):
         seed = 3000 + 10 * i
