@@ -440,7 +440,8 @@ SKINNY = [(1, 300, 1000, "ternary"), (5, 1000, 777, "bool"), (16, 1000, 2048, "t
           (17, 517, 300, "bool"), (32, 129, 3000, "ternary"), (2000, 9, 333, "ternary"),
           (3000, 32, 1000, "bool"), (1, 1, 40, "ternary"), (24, 4100, 96, "ternary"),
           (2, 777, 4100, "bool"), (3, 1030, 513, "ternary"), (4, 65, 8192, "ternary"), (1000, 3, 260, "bool"),
-          (700, 1, 129, "ternary")]
+          (700, 1, 129, "ternary"), (1, 4100, 16384, "ternary"), (4, 333, 16384, "bool"), (2, 1000, 16385, "ternary"),
+          (3, 4097, 4096, "ternary")]
 
 
 @pytest.mark.parametrize("case", range(len(SKINNY)))
