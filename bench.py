@@ -274,6 +274,11 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
             torch.cuda.current_stream().wait_stream(side)
         B.bwta_attn_prefill(st["qp"], st["kp"], st["vt"], s["alpha"], s["att"], s["beta"], out=ctx_v)
 
+    def op_attn_pack():  # ... with the O-projection's input pack fused into its epilogue (no ctx write)
+        if st.pop("vt_pending", False):
+            torch.cuda.current_stream().wait_stream(side)
+        st["cq"] = B.bwta_attn_prefill_pack(st["qp"], st["kp"], st["vt"], s["alpha"], s["att"], s["beta"], s["ctx"])
+
     def op_o():
         B.bwta_gemm(st["cq"], packed["o"], wsc["o"], s["ctx"], out=y_o)
 
@@ -327,7 +332,11 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
            M * hidden / 4 + 3 * hidden * hidden / 8 + 2 * M * 3 * hidden, cub["qkv"]),
         Op("pack_qkv", "pack", op_pack_qkv, 0, 3 * pk(M * hidden, 2), launches=2),
     ]
-    if fused_attn:   # the real softmax runs inside the fused kernel: no P stand-in, no S/P in memory
+    if fused_attn and fuse_ctx:  # real softmax inside; no P stand-in, no S/P/context in memory
+        ops += [Op("attn_prefill_pack", "attn", op_attn_pack, 2 * mm(batch * heads * seq, seq, D),
+                   2 * batch * heads * seq * D / 4 + batch * heads * D * seq / 4 + M * hidden / 4, cub["attn"],
+                   launches=1)]
+    elif fused_attn:
         ops += [Op("attn_prefill", "attn", op_attn, 2 * mm(batch * heads * seq, seq, D),
                    2 * batch * heads * seq * D / 4 + batch * heads * D * seq / 4 + 2 * M * hidden, cub["attn"]),
                 Op("pack_ctx", "pack", op_pack_ctx, 0, pk(M * hidden, 2))]

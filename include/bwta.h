@@ -361,6 +361,25 @@ BWTA_API bwta_status_t bwta_attn_prefill(const uint32_t* q_sgn, const uint32_t* 
                            void* o, bwta_dtype_t o_dt, int64_t ld_o, int64_t o_bstride, int64_t o_hstride,
                            uint32_t* p_out, int64_t ldp_words, void* stream);
 
+/*
+ * bwta_attn_prefill with the next layer's activation pack fused into its epilogue (SURVEY
+ * §8(f) N2): instead of O, the planes of the [batch*tq, heads*dh] attention context
+ * (round_{o_dt}(O), o_dt F16 | BF16) quantized with out_scale / out_kind (TERNARY | BOOL),
+ * exactly as bwta_pack_act would quantize the stored context: row b*tq + t, head h owning words
+ * [h dh/32, (h+1) dh/32) (dh % 32 == 0), out_ld_words >= bwta_ld_words(heads*dh) (padding words
+ * zeroed by a memset on `stream`).  Other arguments and errors as bwta_attn_prefill.
+ */
+BWTA_API bwta_status_t bwta_attn_prefill_pack(const uint32_t* q_sgn, const uint32_t* q_nz,
+                           const uint32_t* k_sgn, const uint32_t* k_nz,
+                           const uint32_t* vt_sgn, const uint32_t* vt_nz,
+                           int64_t batch, int64_t heads, int64_t tq, int64_t tk, int64_t dh,
+                           int64_t ldq_words, int64_t q_bstride, int64_t q_hstride,
+                           int64_t ldk_words, int64_t k_bstride, int64_t k_hstride,
+                           int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
+                           float alpha, float s_att, bwta_dtype_t p_dt, float beta,
+                           bwta_dtype_t o_dt, float out_scale, bwta_kind_t out_kind,
+                           uint32_t* out_sgn, uint32_t* out_nz, int64_t out_ld_words, void* stream);
+
 /* ---- fused decode attention (one query row per entry) -------------------- */
 /*
  * Per (batch b, head h), with one packed query row q (ternary; q_sgn/q_nz at

@@ -21,7 +21,7 @@ from . import _native as N
 from ._native import lib
 
 __all__ = ["Packed", "BwtaError", "bwta_ld_words", "bwta_pack_act", "bwta_pack_weight",
-           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "bwta_attn_prefill", "bwta_gemm_x", "last_design", "lib"]
+           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "bwta_attn_prefill", "bwta_attn_prefill_pack", "bwta_gemm_x", "last_design", "lib"]
 
 
 class BwtaError(RuntimeError):
@@ -399,6 +399,34 @@ def bwta_attn_prefill(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: flo
                                ldp if return_p else 0, _stream(stream))
     _check(st, "bwta_attn_prefill")
     return (out, pout) if return_p else out
+
+
+def bwta_attn_prefill_pack(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: float, beta: float,
+                           out_scale: float, out_kind: str = "ternary", o_dtype=torch.float16,
+                           p_dtype=torch.float16, stream=None) -> Packed:
+    """bwta_pack_act(C, out_scale, out_kind) of the attention context C[b*Tq + t, h*Dh + d] =
+    round_{o_dtype}(O_{b,h}[t][d]) of bwta_attn_prefill, the pack fused into its epilogue (O is
+    never written): the O-projection's input planes [B*Tq, ld(H*Dh)].  Dh % 32 == 0."""
+    qr, kr, vr = q.ref, k.ref, vt.ref
+    if out_kind not in ("ternary", "bool"):
+        raise ValueError("out_kind must be 'ternary' or 'bool'")
+    if q.kind != "ternary" or vt.kind != "ternary" or k.cols != q.cols or vt.cols != kr.shape[-2]:
+        raise ValueError("expects ternary Q and V^T, K over the same head_dim, V^T over Tk")
+    b, h, qbs, qhs = _batch_dims(qr)
+    _, _, kbs, khs = _batch_dims(kr)
+    _, _, vbs, vhs = _batch_dims(vr)
+    tq, tk, dh = qr.shape[-2], kr.shape[-2], vr.shape[-2]
+    ldo = bwta_ld_words(h * dh)
+    nz = torch.empty((b * tq, ldo), dtype=torch.int32, device=qr.device)
+    sgn = torch.empty((b * tq, ldo), dtype=torch.int32, device=qr.device) if out_kind == "ternary" else None
+    k_nz = k.nz if k.kind == "ternary" else None
+    st = lib.bwta_attn_prefill_pack(_ptr(q.sgn), _ptr(q.nz), _ptr(k.sgn), _ptr(k_nz), _ptr(vt.sgn), _ptr(vt.nz), b, h,
+                                    tq, tk, dh, qr.stride(-2), qbs, qhs, kr.stride(-2), kbs, khs, vr.stride(-2), vbs,
+                                    vhs, ctypes.c_float(alpha), ctypes.c_float(s_att), _DT[p_dtype],
+                                    ctypes.c_float(beta), _DT[o_dtype], ctypes.c_float(out_scale), _KIND[out_kind],
+                                    _ptr(sgn), _ptr(nz), ldo, _stream(stream))
+    _check(st, "bwta_attn_prefill_pack")
+    return Packed(sgn, nz, out_kind, h * dh)
 
 
 def bwta_attn_pv_pack(p: Packed, vt: Packed, beta: float, out_scale: float, out_kind: str = "ternary",

@@ -702,14 +702,24 @@ bwta_status_t bwta_attn_decode(const uint32_t* q_sgn, const uint32_t* q_nz, cons
     return BWTA_OK;
 }
 
-bwta_status_t bwta_attn_prefill(const uint32_t* q_sgn, const uint32_t* q_nz, const uint32_t* k_sgn,
+}  // extern "C"
+
+namespace {
+// bwta_attn_prefill (pack = 0: O) and bwta_attn_prefill_pack (pack = 1: the context planes)
+bwta_status_t attn_prefill_impl(const uint32_t* q_sgn, const uint32_t* q_nz, const uint32_t* k_sgn,
                                 const uint32_t* k_nz, const uint32_t* vt_sgn, const uint32_t* vt_nz, int64_t batch,
                                 int64_t heads, int64_t tq, int64_t tk, int64_t dh, int64_t ldq_words,
                                 int64_t q_bstride, int64_t q_hstride, int64_t ldk_words, int64_t k_bstride,
                                 int64_t k_hstride, int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
                                 float alpha, float s_att, bwta_dtype_t p_dt, float beta, void* o, bwta_dtype_t o_dt,
                                 int64_t ld_o, int64_t o_bstride, int64_t o_hstride, uint32_t* p_out,
-                                int64_t ldp_words, void* stream) {
+                                int64_t ldp_words, int pack, float out_scale, bwta_kind_t out_kind,
+                                uint32_t* out_sgn, uint32_t* out_nz, int64_t out_ld_words, void* stream) {
+    if (pack) {
+        if (o_dt != BWTA_F16 && o_dt != BWTA_BF16) return BWTA_ERR_UNSUPPORTED;  // the rounding being packed
+        if (out_kind != BWTA_TERNARY && out_kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
+        if (dh % 32) return BWTA_ERR_UNSUPPORTED;  // a head must own whole words of the context row
+    }
     if (!valid_out_dt(o_dt) || (p_dt != BWTA_F16 && p_dt != BWTA_BF16 && p_dt != BWTA_F32))
         return BWTA_ERR_UNSUPPORTED;
     bwta_status_t st = check_batch(batch, heads);
@@ -719,11 +729,12 @@ bwta_status_t bwta_attn_prefill(const uint32_t* q_sgn, const uint32_t* q_nz, con
     if (batch == 0 || tq == 0 || dh == 0) return BWTA_OK;
     if (tk == 0) return BWTA_ERR_SHAPE;  // softmax over an empty row
     if (q_sgn == nullptr || q_nz == nullptr || k_sgn == nullptr || vt_sgn == nullptr || vt_nz == nullptr ||
-        o == nullptr)
+        (!pack && o == nullptr) || (pack && (out_nz == nullptr || (out_kind == BWTA_TERNARY) != (out_sgn != nullptr))))
         return BWTA_ERR_INVALID_VALUE;
+    if (pack && !scale_ok_pos(out_scale)) return BWTA_ERR_INVALID_VALUE;
     if (!std::isfinite(alpha) || !std::isfinite(beta) || !scale_ok_pos(s_att)) return BWTA_ERR_INVALID_VALUE;
-    if (ldq_words < ldw_of(dh) || ldk_words < ldw_of(dh) || ldv_words < ldw_of(tk) || ld_o < dh ||
-        (p_out && ldp_words < ldw_of(tk)))
+    if (ldq_words < ldw_of(dh) || ldk_words < ldw_of(dh) || ldv_words < ldw_of(tk) || (!pack && ld_o < dh) ||
+        (p_out && ldp_words < ldw_of(tk)) || (pack && out_ld_words < ldw_of(heads * dh)))
         return BWTA_ERR_SHAPE;
     if (q_bstride < 0 || q_hstride < 0 || k_bstride < 0 || k_hstride < 0 || v_bstride < 0 || v_hstride < 0 ||
         o_bstride < 0 || o_hstride < 0)
@@ -732,7 +743,8 @@ bwta_status_t bwta_attn_prefill(const uint32_t* q_sgn, const uint32_t* q_nz, con
     if (ldq_words % 4 || ldk_words % 4 || ldv_words % 4 || q_bstride % 4 || q_hstride % 4 || k_bstride % 4 ||
         k_hstride % 4 || v_bstride % 4 || v_hstride % 4 || !aligned16(q_sgn) || !aligned16(q_nz) ||
         !aligned16(k_sgn) || (k_nz && !aligned16(k_nz)) || !aligned16(vt_sgn) || !aligned16(vt_nz) ||
-        (p_out && (ldp_words % 4 || !aligned16(p_out))))
+        (p_out && (ldp_words % 4 || !aligned16(p_out))) ||
+        (pack && (out_ld_words % 4 || !aligned16(out_nz) || (out_sgn && !aligned16(out_sgn)))))
         return BWTA_ERR_ALIGNMENT;
     st = check_device();
     if (st != BWTA_OK) return st;
@@ -775,8 +787,26 @@ bwta_status_t bwta_attn_prefill(const uint32_t* q_sgn, const uint32_t* q_nz, con
     a.o_hs = o_hstride;
     a.p_out = p_out;
     a.p_ld = ldp_words;
+    if (pack) {
+        a.pack_out = 1;
+        a.po_kind = out_kind;
+        a.po_sgn = out_sgn;
+        a.po_nz = out_nz;
+        a.po_ld = out_ld_words;
+        const double tt = 0.5 * double(out_scale);  // exact
+        const bool bf = o_dt == BWTA_BF16;
+        a.po_tp = rounding_threshold(smallest_pattern(tt, false, bf), bf);
+        a.po_tn = rounding_threshold(smallest_pattern(tt, true, bf), bf);
+    }
     if (!attn_prefill_supported(a)) return BWTA_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
+    if (pack && out_ld_words * 32 > heads * dh) {  // padding words of the context rows: no head writes them
+        const size_t bytes = sizeof(uint32_t) * size_t(batch) * size_t(tq) * size_t(out_ld_words);
+        cudaError_t e = cudaMemsetAsync(out_nz, 0, bytes, s);
+        if (e == cudaSuccess && out_sgn) e = cudaMemsetAsync(out_sgn, 0, bytes, s);
+        if (e != cudaSuccess) return cuda_fail(e);
+        count_launch(out_sgn ? 2 : 1);
+    }
     if (p_out) {  // the kernel writes the data words of P; padding words stay zero
         cudaError_t e = cudaMemsetAsync(p_out, 0, sizeof(uint32_t) * size_t(batch * heads) * size_t(tq) *
                                                         size_t(ldp_words), s);
@@ -787,6 +817,37 @@ bwta_status_t bwta_attn_prefill(const uint32_t* q_sgn, const uint32_t* q_nz, con
     if (e != cudaSuccess) return cuda_fail(e);
     g_last_design = BWTA_DESIGN_TCGEN05;
     return BWTA_OK;
+}
+}  // namespace
+
+extern "C" {
+
+bwta_status_t bwta_attn_prefill(const uint32_t* q_sgn, const uint32_t* q_nz, const uint32_t* k_sgn,
+                                const uint32_t* k_nz, const uint32_t* vt_sgn, const uint32_t* vt_nz, int64_t batch,
+                                int64_t heads, int64_t tq, int64_t tk, int64_t dh, int64_t ldq_words,
+                                int64_t q_bstride, int64_t q_hstride, int64_t ldk_words, int64_t k_bstride,
+                                int64_t k_hstride, int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
+                                float alpha, float s_att, bwta_dtype_t p_dt, float beta, void* o, bwta_dtype_t o_dt,
+                                int64_t ld_o, int64_t o_bstride, int64_t o_hstride, uint32_t* p_out,
+                                int64_t ldp_words, void* stream) {
+    return attn_prefill_impl(q_sgn, q_nz, k_sgn, k_nz, vt_sgn, vt_nz, batch, heads, tq, tk, dh, ldq_words, q_bstride,
+                             q_hstride, ldk_words, k_bstride, k_hstride, ldv_words, v_bstride, v_hstride, alpha, s_att,
+                             p_dt, beta, o, o_dt, ld_o, o_bstride, o_hstride, p_out, ldp_words, 0, 0.f, BWTA_TERNARY,
+                             nullptr, nullptr, 0, stream);
+}
+
+bwta_status_t bwta_attn_prefill_pack(const uint32_t* q_sgn, const uint32_t* q_nz, const uint32_t* k_sgn,
+                                     const uint32_t* k_nz, const uint32_t* vt_sgn, const uint32_t* vt_nz, int64_t batch,
+                                     int64_t heads, int64_t tq, int64_t tk, int64_t dh, int64_t ldq_words,
+                                     int64_t q_bstride, int64_t q_hstride, int64_t ldk_words, int64_t k_bstride,
+                                     int64_t k_hstride, int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
+                                     float alpha, float s_att, bwta_dtype_t p_dt, float beta, bwta_dtype_t o_dt,
+                                     float out_scale, bwta_kind_t out_kind, uint32_t* out_sgn, uint32_t* out_nz,
+                                     int64_t out_ld_words, void* stream) {
+    return attn_prefill_impl(q_sgn, q_nz, k_sgn, k_nz, vt_sgn, vt_nz, batch, heads, tq, tk, dh, ldq_words, q_bstride,
+                             q_hstride, ldk_words, k_bstride, k_hstride, ldv_words, v_bstride, v_hstride, alpha, s_att,
+                             p_dt, beta, nullptr, o_dt, 0, 0, 0, nullptr, 0, 1, out_scale, out_kind, out_sgn, out_nz,
+                             out_ld_words, stream);
 }
 
 bwta_status_t bwta_attn_pv_pack(const uint32_t* p_sgn, const uint32_t* p_nz, const uint32_t* vt_sgn,

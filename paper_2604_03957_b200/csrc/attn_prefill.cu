@@ -94,6 +94,13 @@ struct ApParams {
     int dbg;  // BWTA_TRACE builds only: 1 skip pass-1 math, 2 skip pass-2 math, 4 skip MMAs, 8 skip unpack, 16 spin on S
     uint32_t* p_out;           // optional P planes [entries][tq][p_ld] (zeroed by the host)
     int64_t p_ld;
+    // fused next-layer pack of the context (N2): instead of O, the planes of the [B*Tq, H*Dh]
+    // context rows, head h owning words [h Dh/32, (h+1) Dh/32) of row b*Tq + t (Dh % 32 == 0);
+    // +1 iff fl32(dot * beta) >= po_tp, -1 iff <= -po_tn (the o_dt rounding boundaries, R2)
+    int pack_out, po_kind;
+    uint32_t *po_sgn, *po_nz;
+    int64_t po_ld;
+    float po_tp, po_tn;
 };
 
 __device__ __forceinline__ float round_to(int dt, float p) {
@@ -516,6 +523,25 @@ __global__ void __launch_bounds__(AP_NT, 1)
             tc_fence_after();
             const bool rok = qrow < p.tq;
             const int64_t obase = int64_t(eb) * p.o_bs + int64_t(eh) * p.o_hs + qrow * p.ld_o;
+            if (p.pack_out) {  // 32-column chunks -> one word per plane per thread
+                for (int c0 = 32 * h; c0 < p.dh; c0 += 32 * AP_NH) {
+                    uint32_t o[32];
+                    tmem_ld_32x32b_x32(lane_base + uint32_t(TM_O + c0), o);
+                    tmem_wait_ld();
+                    uint32_t pos = 0, neg = 0;
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        const float y = __fmul_rn(__uint_as_float(o[c]), p.beta);  // R5
+                        pos |= uint32_t(y >= p.po_tp) << c;
+                        neg |= uint32_t(y <= -p.po_tn) << c;
+                    }
+                    if (rok) {
+                        const int64_t off = (int64_t(eb) * p.tq + qrow) * p.po_ld + (int64_t(eh) * p.dh + c0) / 32;
+                        p.po_nz[off] = p.po_kind == K_TERNARY ? (pos | neg) : pos;
+                        if (p.po_kind == K_TERNARY) p.po_sgn[off] = neg;
+                    }
+                }
+            } else
             for (int c0 = 16 * h; c0 < p.dhp; c0 += 16 * AP_NH) {
                 uint32_t o[16];
                 tmem_ld_32x32b_x16(lane_base + uint32_t(TM_O + c0), o);
@@ -597,6 +623,13 @@ cudaError_t launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t s) {
     p.o_hs = a.o_hs;
     p.p_out = a.p_out;
     p.p_ld = a.p_ld;
+    p.pack_out = a.pack_out;
+    p.po_kind = a.po_kind;
+    p.po_sgn = a.po_sgn;
+    p.po_nz = a.po_nz;
+    p.po_ld = a.po_ld;
+    p.po_tp = a.po_tp;
+    p.po_tn = a.po_tn;
     p.vec_o = (a.o_dt == DT_F16 || a.o_dt == DT_BF16) && (reinterpret_cast<uintptr_t>(a.o) & 15) == 0 &&
               a.ld_o % 8 == 0 && a.o_bs % 8 == 0 && a.o_hs % 8 == 0;
     CUtensorMap qs, qn, ks, kn, vs, vn;

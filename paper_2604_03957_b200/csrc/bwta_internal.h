@@ -193,6 +193,10 @@ struct AttnPrefillArgs {
     int64_t ld_o, o_bs, o_hs;       // elements
     uint32_t* p_out;                // optional P planes [entries][tq][p_ld]
     int64_t p_ld;
+    int pack_out = 0, po_kind = 0;  // fused pack of the [nb*tq, nh*dh] context (dh % 32 == 0)
+    uint32_t *po_sgn = nullptr, *po_nz = nullptr;
+    int64_t po_ld = 0;
+    float po_tp = 0.f, po_tn = 0.f;
 };
 bool attn_prefill_supported(const AttnPrefillArgs& a);
 cudaError_t launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t s);

@@ -102,6 +102,32 @@ def test_attn_prefill_strided_heads_and_out_view(B):
     assert torch.equal(ctx_v.contiguous().view(torch.int16), ref.view(torch.int16))
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["ternary", "bool"])
+@pytest.mark.parametrize("o_dtype", [torch.float16, torch.bfloat16])
+def test_attn_prefill_pack_equals_prefill_then_pack(B, kind, o_dtype):
+    """bwta_attn_prefill_pack == bwta_pack_act(context of bwta_attn_prefill) bit-exactly (the
+    fused epilogue rounds to o_dtype exactly like the stored context), ragged Tq / Tk, Dh 32-128."""
+    for i, (b, h, tq, tk, dh) in enumerate([(2, 3, 37, 41, 64), (1, 2, 130, 300, 128), (4, 12, 128, 128, 64),
+                                            (1, 5, 200, 129, 32)]):
+        seed = 9700 + 10 * i
+        q, k, v = (gen.activations((b, h, t, dh), seed + j) for j, t in enumerate((tq, tk, tk)))
+        sq, sk, sv = gen.act_scale(q), gen.act_scale(k), gen.act_scale(v)
+        alpha = float(np.float32(sq * sk / np.sqrt(dh)))
+        s_att = float(np.float32(2.0 / tk))
+        beta = float(np.float32(s_att * sv))
+        qp, kp = B.bwta_pack_act(q.cuda(), sq), B.bwta_pack_act(k.cuda(), sk)
+        vt = B.bwta_pack_act(v.cuda(), sv, "ternary", transpose=True)
+        o = B.bwta_attn_prefill(qp, kp, vt, alpha, s_att, beta, out_dtype=o_dtype)
+        ctx = o.transpose(1, 2).reshape(b * tq, h * dh).contiguous()
+        s_ctx = gen.act_scale(ctx) or 1.0
+        ref = B.bwta_pack_act(ctx, s_ctx, kind)
+        got = B.bwta_attn_prefill_pack(qp, kp, vt, alpha, s_att, beta, s_ctx, kind, o_dtype=o_dtype)
+        assert torch.equal(got.nz, ref.nz), (b, h, tq, tk, dh)
+        if kind == "ternary":
+            assert torch.equal(got.sgn, ref.sgn), (b, h, tq, tk, dh)
+
+
 def test_attn_prefill_validation():
     """Host validation before any device work (no GPU here)."""
     from paper_2604_03957_b200 import _native as N
@@ -131,3 +157,21 @@ def test_attn_prefill_validation():
     assert pf(p_dt=3) == 4
     assert pf(kn=None) == 4              # binary K is valid
     assert pf(b=0) == 0 and pf(tq=0) == 0
+
+    def pfp(**kw):
+        a = dict(qs=16, qn=32, ks=48, kn=64, vs=80, vn=96, b=1, h=2, tq=10, tk=100, dh=64, o_dt=0, s_o=1.0, kind=2,
+                 os_=112, on=128, ldo=4)
+        a.update(kw)
+        return L.bwta_attn_prefill_pack(a["qs"], a["qn"], a["ks"], a["kn"], a["vs"], a["vn"], a["b"], a["h"], a["tq"],
+                                        100, a["dh"], 4, 0, 0, 4, 0, 0, 4, 0, 0, ctypes.c_float(0.1),
+                                        ctypes.c_float(0.02), 0, ctypes.c_float(0.1), a["o_dt"], ctypes.c_float(a["s_o"]),
+                                        a["kind"], a["os_"], a["on"], a["ldo"], None)
+    assert pfp() == 4                    # valid, but no sm_100 device here
+    assert pfp(dh=48) == 4               # a head must own whole words of the context row
+    assert pfp(o_dt=2) == 4              # the pack rounds to f16 / bf16
+    assert pfp(kind=0) == 4
+    assert pfp(on=None) == 1
+    assert pfp(kind=1) == 1              # bool output has no sgn plane
+    assert pfp(s_o=0.0) == 1
+    assert pfp(ldo=0) == 2
+    assert pfp(on=132) == 3

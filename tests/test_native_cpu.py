@@ -230,10 +230,11 @@ def test_fused_pack_entry_points_validate_opts(N):
     for f in (gp, pvp):
         assert f(None) == 4                 # valid, but no sm_100 device here
         assert f(opts(tile_n=128, cg=2)) == 4
-        for bad in (opts(tile_n=256), opts(tile_n=32), opts(tile_n=96), opts(cg=3), opts(cg=-1), opts(design=3),
+        for bad in (opts(tile_n=256), opts(tile_n=32), opts(tile_n=96), opts(cg=3), opts(cg=-1), opts(design=4),
                     opts(design=-1)):
             assert f(bad) == 1
         assert f(opts(design=1)) == 4       # fused pack: design (b) only
+        assert f(opts(design=3)) == 4       # (nor the mma.sync b1 prior art)
 
 
 def test_gemm_x_validation(N):
