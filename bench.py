@@ -181,7 +181,7 @@ class Op:
 
 
 def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=3072, fuse_ffn=True,
-               qkv_packs="overlap", fuse_ctx=True, fused_attn=True):
+               qkv_packs="overlap", fuse_ctx=True, fused_attn=True, fuse_qkv=True):
     """configs[1]: BERT-base layer, seq 128, batch 32 (M = 4096 tokens)."""
     M, D = batch * seq, hidden // heads
     g = lambda s: s + seed  # noqa: E731
@@ -225,6 +225,10 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
 
     def op_qkv():
         B.bwta_gemm(st["xq"], packed["qkv"], wsc["qkv"], s["x"], out=qkv)
+
+    def op_qkv_pack():  # QKV projection emitting the per-head Q / K / V^T planes (N2; Y never written)
+        st["qp"], st["kp"], st["vt"] = B.bwta_gemm_pack_qkv(st["xq"], packed["qkv"], wsc["qkv"], s["x"], batch, seq,
+                                                            heads, D, (s["q"], s["k"], s["v"]))
 
     def op_pack_qkv():  # the per-head Q, K and V^T packs (one launch by default)
         qa, ka, va = ((heads_view(qkv, 0), s["q"], "ternary", False), (heads_view(qkv, 1), s["k"], "ternary", False),
@@ -326,12 +330,14 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
     }
     mm = lambda m, n, k: 2 * m * n * k  # noqa: E731
     pk = lambda n_el, planes: 2 * n_el + n_el * planes / 8  # noqa: E731  fp16 in + planes out
-    ops = [
-        Op("pack_x", "pack", op_pack_x, 0, pk(M * hidden, 2)),
-        Op("gemm_qkv", "gemm", op_qkv, mm(M, 3 * hidden, hidden),
-           M * hidden / 4 + 3 * hidden * hidden / 8 + 2 * M * 3 * hidden, cub["qkv"]),
-        Op("pack_qkv", "pack", op_pack_qkv, 0, 3 * pk(M * hidden, 2), launches=2),
-    ]
+    ops = [Op("pack_x", "pack", op_pack_x, 0, pk(M * hidden, 2))]
+    if fuse_qkv:
+        ops += [Op("gemm_qkv_pack", "gemm", op_qkv_pack, mm(M, 3 * hidden, hidden),
+                   M * hidden / 4 + 3 * hidden * hidden / 8 + 3 * M * hidden / 4, cub["qkv"])]
+    else:
+        ops += [Op("gemm_qkv", "gemm", op_qkv, mm(M, 3 * hidden, hidden),
+                   M * hidden / 4 + 3 * hidden * hidden / 8 + 2 * M * 3 * hidden, cub["qkv"]),
+                Op("pack_qkv", "pack", op_pack_qkv, 0, 3 * pk(M * hidden, 2), launches=2)]
     if fused_attn and fuse_ctx:  # real softmax inside; no P stand-in, no S/P/context in memory
         ops += [Op("attn_prefill_pack", "attn", op_attn_pack, 2 * mm(batch * heads * seq, seq, D),
                    2 * batch * heads * seq * D / 4 + batch * heads * D * seq / 4 + M * hidden / 4, cub["attn"],

@@ -250,6 +250,27 @@ BWTA_API bwta_status_t bwta_gemm_pack(const uint32_t* a_sgn, const uint32_t* a_n
                                       uint32_t* out_sgn, uint32_t* out_nz, int64_t out_ld_words,
                                       const bwta_opts_t* opts, void* stream);
 
+/* ---- QKV projection with the per-head Q / K / V^T packs fused ---- */
+/*
+ * Y = bwta_gemm(A, W, w_scale, a_scale) rounded to y_dt (F16 | BF16) with Y = [Q | K | V] (n =
+ * 3*heads*head_dim columns, the rows the m = batch*seq tokens), written only as the next operands'
+ * planes, exactly as bwta_pack_act would pack the stored per-head views (R1-R3):
+ *   Q, K planes [batch][heads][seq][ldq/ldk_words] (packed along head_dim, scale out_scale[0/1]),
+ *   V^T planes  [batch][heads][head_dim][ldv_words] (packed along the tokens, out_scale[2]) --
+ * the inputs of bwta_attn_qk / bwta_attn_pv / bwta_attn_prefill.  out_kind TERNARY | BOOL for all
+ * three; padding words are zeroed by the kernel.  head_dim % 32 == 0 and seq % 32 == 0 (whole
+ * words per head and per 32 tokens), design (b) only.  Other arguments and errors as bwta_gemm_pack.
+ */
+BWTA_API bwta_status_t bwta_gemm_pack_qkv(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t a_kind,
+                                          int64_t m, int64_t lda_words, const uint32_t* w_sgn, int64_t n,
+                                          int64_t ldw_words, int64_t k, const float* w_scale, float a_scale,
+                                          bwta_dtype_t y_dt, int64_t batch, int64_t seq, int64_t heads,
+                                          int64_t head_dim, const float* out_scale /* host [3] */,
+                                          bwta_kind_t out_kind, uint32_t* q_sgn, uint32_t* q_nz, int64_t ldq_words,
+                                          uint32_t* k_sgn, uint32_t* k_nz, int64_t ldk_words,
+                                          uint32_t* vt_sgn, uint32_t* vt_nz, int64_t ldv_words,
+                                          const bwta_opts_t* opts, void* stream);
+
 /* ---- attention QK^T (Case 3) -------------------------------------------- */
 /*
  * S_e[i][j] = fl32(float(sum_d q[i][d] k[j][d]) * alpha)

@@ -21,7 +21,7 @@ from . import _native as N
 from ._native import lib
 
 __all__ = ["Packed", "BwtaError", "bwta_ld_words", "bwta_pack_act", "bwta_pack_weight",
-           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "bwta_attn_prefill", "bwta_attn_prefill_pack", "bwta_gemm_x", "last_design", "lib"]
+           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "bwta_attn_prefill", "bwta_attn_prefill_pack", "bwta_gemm_pack_qkv", "bwta_gemm_x", "last_design", "lib"]
 
 
 class BwtaError(RuntimeError):
@@ -277,6 +277,39 @@ def bwta_gemm_pack(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scal
                             _opts(design, tile), _stream(stream))
     _check(st, "bwta_gemm_pack")
     return Packed(sgn, nz, out_kind, n)
+
+
+def bwta_gemm_pack_qkv(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: float, batch: int,
+                       seq: int, heads: int, head_dim: int, out_scales, out_kind: str = "ternary",
+                       y_dtype=torch.float16, design: str = "auto", stream=None, tile=None):
+    """The QKV projection with the per-head packs fused (Y = [Q | K | V] never written): returns
+    (Q, K, V^T) Packed planes [B, H, T, ld(D)], [B, H, T, ld(D)], [B, H, D, ld(T)] -- what
+    bwta_pack_act of the per-head views (V transposed) of the stored Y would give."""
+    if a.kind not in ("ternary", "bool") or w.kind != "binary" or a.cols != w.cols:
+        raise ValueError("bwta_gemm_pack_qkv expects ternary/bool activations and binary weights of equal K")
+    if out_kind not in ("ternary", "bool"):
+        raise ValueError("out_kind must be 'ternary' or 'bool'")
+    ar = a.ref
+    m, n, k = ar.shape[-2], w.sgn.shape[-2], a.cols
+    dev = ar.device
+    ldd, ldt = bwta_ld_words(head_dim), bwta_ld_words(seq)
+
+    def planes(shape):
+        nz = torch.empty(shape, dtype=torch.int32, device=dev)
+        sg = torch.empty(shape, dtype=torch.int32, device=dev) if out_kind == "ternary" else None
+        return sg, nz
+    qs, qn = planes((batch, heads, seq, ldd))
+    ks, kn = planes((batch, heads, seq, ldd))
+    vs, vn = planes((batch, heads, head_dim, ldt))
+    sc = (ctypes.c_float * 3)(*[float(x) for x in out_scales])
+    ws_scale = None if w_scale is None else w_scale.to(device=dev, dtype=torch.float32).contiguous()
+    st = lib.bwta_gemm_pack_qkv(_ptr(a.sgn), _ptr(a.nz), _KIND[a.kind], m, ar.stride(-2), _ptr(w.sgn), n,
+                                w.sgn.stride(-2), k, _ptr(ws_scale), ctypes.c_float(a_scale), _DT[y_dtype], batch, seq,
+                                heads, head_dim, ctypes.cast(sc, ctypes.c_void_p), _KIND[out_kind], _ptr(qs), _ptr(qn),
+                                ldd, _ptr(ks), _ptr(kn), ldd, _ptr(vs), _ptr(vn), ldt, _opts(design, tile),
+                                _stream(stream))
+    _check(st, "bwta_gemm_pack_qkv")
+    return (Packed(qs, qn, out_kind, head_dim), Packed(ks, kn, out_kind, head_dim), Packed(vs, vn, out_kind, seq))
 
 
 def bwta_attn_qk(q: Packed, k: Packed, alpha: float, out_dtype=torch.float16,

@@ -497,6 +497,83 @@ bwta_status_t bwta_gemm_pack(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_k
     return BWTA_OK;
 }
 
+bwta_status_t bwta_gemm_pack_qkv(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t a_kind, int64_t m,
+                                 int64_t lda_words, const uint32_t* w_sgn, int64_t n, int64_t ldw_words, int64_t k,
+                                 const float* w_scale, float a_scale, bwta_dtype_t y_dt, int64_t batch, int64_t seq,
+                                 int64_t heads, int64_t head_dim, const float* out_scale, bwta_kind_t out_kind,
+                                 uint32_t* q_sgn, uint32_t* q_nz, int64_t ldq_words, uint32_t* k_sgn, uint32_t* k_nz,
+                                 int64_t ldk_words, uint32_t* vt_sgn, uint32_t* vt_nz, int64_t ldv_words,
+                                 const bwta_opts_t* opts, void* stream) {
+    if (a_kind != BWTA_TERNARY && a_kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
+    if (out_kind != BWTA_TERNARY && out_kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
+    if (y_dt != BWTA_F16 && y_dt != BWTA_BF16) return BWTA_ERR_UNSUPPORTED;
+    if (m < 0 || n < 0 || k < 0 || k > KMAX || batch < 0 || seq < 0 || heads < 1 || head_dim < 1) return BWTA_ERR_SHAPE;
+    if (m != batch * seq || n != 3 * heads * head_dim) return BWTA_ERR_SHAPE;
+    if (m == 0) return BWTA_OK;
+    if (head_dim % 32 || seq % 32) return BWTA_ERR_UNSUPPORTED;  // whole words per head / per 32 tokens
+    if (a_nz == nullptr || w_sgn == nullptr || out_scale == nullptr || q_nz == nullptr || k_nz == nullptr ||
+        vt_nz == nullptr)
+        return BWTA_ERR_INVALID_VALUE;
+    if ((a_kind == BWTA_TERNARY) != (a_sgn != nullptr)) return BWTA_ERR_INVALID_VALUE;
+    const bool tern = out_kind == BWTA_TERNARY;
+    if (tern != (q_sgn != nullptr) || tern != (k_sgn != nullptr) || tern != (vt_sgn != nullptr))
+        return BWTA_ERR_INVALID_VALUE;
+    if (!std::isfinite(a_scale)) return BWTA_ERR_INVALID_VALUE;
+    for (int r = 0; r < 3; ++r)
+        if (!scale_ok_pos(out_scale[r])) return BWTA_ERR_INVALID_VALUE;
+    const int64_t need = ldw_of(k);
+    if (lda_words < need || ldw_words < need || ldq_words < ldw_of(head_dim) || ldk_words < ldw_of(head_dim) ||
+        ldv_words < ldw_of(seq))
+        return BWTA_ERR_SHAPE;
+    auto al = [](const void* q) { return q == nullptr || aligned16(q); };
+    if (lda_words % 4 || ldw_words % 4 || ldq_words % 4 || ldk_words % 4 || ldv_words % 4 || !al(a_nz) || !al(a_sgn) ||
+        !al(w_sgn) || !al(q_sgn) || !al(q_nz) || !al(k_sgn) || !al(k_nz) || !al(vt_sgn) || !al(vt_nz))
+        return BWTA_ERR_ALIGNMENT;
+    const bwta_opts_t* o = opts_or_default(opts);
+    if (bwta_status_t so = check_opts(o); so != BWTA_OK) return so;
+    if (o->design == BWTA_DESIGN_CUDA_CORE || o->design == BWTA_DESIGN_MMA_B1) return BWTA_ERR_UNSUPPORTED;
+    bwta_status_t st = check_device();
+    if (st != BWTA_OK) return st;
+    MatmulArgs a{};
+    a.a_sgn = a_sgn;
+    a.a_nz = a_nz;
+    a.b_sgn = w_sgn;
+    a.M = m;
+    a.N = n;
+    a.K = k;
+    a.lda = lda_words;
+    a.ldb = ldw_words;
+    a.nb = a.nh = 1;
+    a.y_dt = y_dt;
+    a.col_scale = w_scale;
+    a.scalar = a_scale;
+    a.pack_out = 1;
+    a.po_kind = out_kind;
+    a.po_heads = 1;
+    a.ph_T = seq;
+    a.ph_H = heads;
+    a.ph_D = head_dim;
+    uint32_t* sg[3] = {q_sgn, k_sgn, vt_sgn};
+    uint32_t* nzp[3] = {q_nz, k_nz, vt_nz};
+    const int64_t lds[3] = {ldq_words, ldk_words, ldv_words};
+    const bool bf = y_dt == BWTA_BF16;
+    for (int r = 0; r < 3; ++r) {
+        a.ph_sgn[r] = sg[r];
+        a.ph_nz[r] = nzp[r];
+        a.ph_ld[r] = lds[r];
+        const double t = 0.5 * double(out_scale[r]);  // exact
+        a.ph_tp[r] = rounding_threshold(smallest_pattern(t, false, bf), bf);
+        a.ph_tn[r] = rounding_threshold(smallest_pattern(t, true, bf), bf);
+    }
+    a.tile_n = o->tile_n;
+    a.cta_group = o->cta_group;
+    if (!matmul_tc_supported(a) || matmul_gemv_eligible(a)) return BWTA_ERR_UNSUPPORTED;
+    cudaError_t e = launch_matmul_tc(a, nullptr, 0, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_last_design = BWTA_DESIGN_TCGEN05;
+    return BWTA_OK;
+}
+
 size_t bwta_attn_qk_workspace_size(int64_t batch_heads, int64_t tq, int64_t tk, int64_t dh, const bwta_opts_t* opts) {
     opts = opts_or_default(opts);
     if (batch_heads <= 0 || tq <= 0 || tk <= 0 || dh < 0 || opts->design == BWTA_DESIGN_CUDA_CORE) return 0;

@@ -152,6 +152,15 @@ struct MatmulArgs {
     int64_t po_ld = 0;        // words per packed row (rows = the M rows of Y)
     int64_t po_bs = 0, po_hs = 0;  // words between the planes of consecutive batch / head entries
     float po_tp = 0.f, po_tn = 0.f;  // +1 iff y >= po_tp; -1 iff y <= -po_tn (exact storage values)
+    // head-split multi-output pack (bwta_gemm_pack_qkv): the columns of Y = [Q | K | V] (each H*D
+    // wide) go to per-head planes: Q, K [B, H, T, ld] along D (region 0, 1), V^T [B, H, D, ld(T)]
+    // along the tokens (region 2); the rows of Y are the B*T tokens
+    int po_heads = 0;
+    int64_t ph_T = 0, ph_H = 0, ph_D = 0;
+    uint32_t* ph_sgn[3] = {nullptr, nullptr, nullptr};
+    uint32_t* ph_nz[3] = {nullptr, nullptr, nullptr};
+    int64_t ph_ld[3] = {0, 0, 0};
+    float ph_tp[3] = {0.f, 0.f, 0.f}, ph_tn[3] = {0.f, 0.f, 0.f};
 };
 
 cudaError_t launch_matmul_cc(const MatmulArgs& a, cudaStream_t s);

@@ -127,6 +127,13 @@ struct TcParams {
     int64_t po_ld;
     int64_t po_bs, po_hs;  // words between the planes of consecutive batch / head entries
     float po_tp, po_tn;
+    // head-split Q / K / V^T pack (MatmulArgs::po_heads); kernel rows = tokens (never swapped)
+    int po_heads;
+    int64_t ph_T, ph_H, ph_D;
+    uint32_t* ph_sgn[3];
+    uint32_t* ph_nz[3];
+    int64_t ph_ld[3];
+    float ph_tp[3], ph_tn[3];
     float dot_bias;  // W1A1: K - K_processed (both operands binary; the generic epilogue adds it)
     int dbg;  // BWTA_TRACE builds only (tools/trace_gemm.py): 1 skip unpack math, 2 skip MMAs, 4 skip TMA, 8 skip A unpack, 16 skip B unpack, 32/64 wait flavour, 128 skip the B-code proxy fence
 };
@@ -430,7 +437,61 @@ __device__ __forceinline__ void epi_tile_pack(const TcParams& p, uint32_t tacc, 
             const int64_t nl = n0 + lane;
             cl = __fmul_rn(__ldg(p.scale + (nl < p.N ? nl : 0)), p.scalar);
         }
-        if (!p.out_trans) {
+        if (p.po_heads) {
+            // chunk of Q / K / V (warp-uniform: H*D and D are multiples of 32); thread = token row
+            const int64_t HD = p.ph_H * p.ph_D;
+            const int reg = int(n0 / HD);
+            const int64_t nl = n0 - reg * HD, hh = nl / p.ph_D, dcol = nl - hh * p.ph_D;
+            const float tp = p.ph_tp[reg], tn = p.ph_tn[reg];
+            uint32_t* psg = p.ph_sgn[reg];
+            uint32_t* pnz = p.ph_nz[reg];
+            if (reg < 2) {  // Q / K: the thread's 32 columns are 32 consecutive head dims of its token
+                uint32_t pos = 0, neg = 0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float c = col_scaled ? __shfl_sync(0xffffffffu, cl, j) : crow;
+                    const float y = scaled(v[j], c);
+                    pos |= uint32_t(y >= tp) << j;
+                    neg |= uint32_t(y <= -tn) << j;
+                }
+                if (rok) {
+                    const int64_t b = row / p.ph_T, t = row - b * p.ph_T;
+                    const int64_t off = ((b * p.ph_H + hh) * p.ph_T + t) * p.ph_ld[reg] + dcol / 32;
+                    pnz[off] = ternary ? (pos | neg) : pos;
+                    if (ternary) psg[off] = neg;
+                    if (dcol + 32 == p.ph_D)  // the row's last data word: zero its padding words (R8)
+                        for (int64_t w = 1; w < p.ph_ld[reg] - dcol / 32; ++w) {
+                            pnz[off + w] = 0u;
+                            if (ternary) psg[off + w] = 0u;
+                        }
+                }
+            } else {        // V^T: the warp's 32 lanes are 32 consecutive tokens of one sequence
+                uint32_t* sc = reinterpret_cast<uint32_t*>(scratch);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float c = col_scaled ? __shfl_sync(0xffffffffu, cl, j) : crow;
+                    const float y = scaled(v[j], c);
+                    sc[j] = __ballot_sync(0xffffffffu, rok && y >= tp);
+                    if (ternary) sc[32 + j] = __ballot_sync(0xffffffffu, rok && y <= -tn);
+                }
+                __syncwarp();
+                const uint32_t my_pos = sc[lane];
+                const uint32_t my_neg = ternary ? sc[32 + lane] : 0u;
+                __syncwarp();
+                const int64_t m0 = mrow0 + q * 32;
+                if (m0 < p.M) {
+                    const int64_t b = m0 / p.ph_T, t0 = m0 - b * p.ph_T;
+                    const int64_t off = ((b * p.ph_H + hh) * p.ph_D + dcol + lane) * p.ph_ld[2] + t0 / 32;
+                    pnz[off] = ternary ? (my_pos | my_neg) : my_pos;
+                    if (ternary) psg[off] = my_neg;
+                    if (t0 + 32 == p.ph_T)  // the row's last data word: zero its padding words (R8)
+                        for (int64_t w = 1; w < p.ph_ld[2] - t0 / 32; ++w) {
+                            pnz[off + w] = 0u;
+                            if (ternary) psg[off + w] = 0u;
+                        }
+                }
+            }
+        } else if (!p.out_trans) {
             // this thread's 32 columns are 32 consecutive elements of its output row
             uint32_t pos = 0, neg = 0;
 #pragma unroll
@@ -1175,7 +1236,7 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     // measured 5-11 % faster on the BERT GEMMs, tools/ab_swap.py); the fused pack swaps when M > N
     // (its ballot path with integer thresholds is 1.4x faster than the register-word path)
     const bool tie = !(t_ns.cost < t_sw.cost - 1e-9) && !(t_sw.cost < t_ns.cost - 1e-9);
-    const bool swap = t_sw.cost < t_ns.cost - 1e-9 || (tie && a.pack_out && a.M > a.N);
+    const bool swap = !a.po_heads && (t_sw.cost < t_ns.cost - 1e-9 || (tie && a.pack_out && a.M > a.N));
     const Plan pl = make_plan(a, swap);
     TileChoice tc = swap ? t_sw : t_ns;
     if (a.tile_n) tc.bn = a.tile_n;
@@ -1231,6 +1292,17 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     p.po_hs = a.po_hs;
     p.po_tp = a.po_tp;
     p.po_tn = a.po_tn;
+    p.po_heads = a.po_heads;
+    p.ph_T = a.ph_T;
+    p.ph_H = a.ph_H;
+    p.ph_D = a.ph_D;
+    for (int r = 0; r < 3; ++r) {
+        p.ph_sgn[r] = a.ph_sgn[r];
+        p.ph_nz[r] = a.ph_nz[r];
+        p.ph_ld[r] = a.ph_ld[r];
+        p.ph_tp[r] = a.ph_tp[r];
+        p.ph_tn[r] = a.ph_tn[r];
+    }
     // output tensor map (TMA store) when the layout allows it
     {
         const int es = (a.y_dt == DT_F16 || a.y_dt == DT_BF16) ? 2 : 4;

@@ -630,3 +630,31 @@ def test_gemm_x_equals_pack_then_gemm(B, dtype, kind):
         qa = oracle.quantize_act(storage(x), DT[dtype], s, kind)
         qw = oracle.binarize_weight(storage(w), "f16", mu=mu)
         assert np.array_equal(gi.cpu().numpy(), oracle.dot(qa, qw, threads=4)), (m, n, k)
+
+
+# ------------------------------------------- QKV projection with the head-split packs fused ----
+@pytest.mark.parametrize("kind", ["ternary", "bool"])
+@pytest.mark.parametrize("y_dt", [torch.float16, torch.bfloat16])
+def test_gemm_pack_qkv_equals_gemm_then_head_packs(B, kind, y_dt):
+    """bwta_gemm_pack_qkv == bwta_pack_act of the per-head Q / K views and the transposed V view of
+    the stored Y (bit-exact, incl. padding words), and == the oracle's quantization of its Y."""
+    for i, (bsz, t, h, d, tile) in enumerate([(2, 64, 3, 64, None), (4, 128, 12, 64, None), (3, 96, 2, 96, None),
+                                              (2, 160, 4, 32, (64, 1)), (1, 256, 2, 128, (192, 2))]):
+        m, n, k = bsz * t, 3 * h * d, 300 + 37 * i
+        a, wp, s_a, s_w, qa, qw = _gemm_case(B, m, n, k, 9800 + i)
+        y = B.bwta_gemm(a, wp, s_w.cuda(), s_a, out_dtype=y_dt)
+        views = [y[:, j * h * d:(j + 1) * h * d].reshape(bsz, t, h, d).transpose(1, 2) for j in range(3)]
+        sc = [gen.act_scale(v) or 1.0 for v in views]
+        got = B.bwta_gemm_pack_qkv(a, wp, s_w.cuda(), s_a, bsz, t, h, d, sc, kind, y_dt, tile=tile)
+        for j, (g, v) in enumerate(zip(got, views)):
+            ref = B.bwta_pack_act(v, sc[j], kind, transpose=(j == 2))
+            assert torch.equal(g.nz, ref.nz), (i, j)
+            if kind == "ternary":
+                assert torch.equal(g.sgn, ref.sgn), (i, j)
+        # oracle: Y from the oracle's dot + R5 epilogue, quantized per head with the oracle's pack
+        name = DT[y_dt]
+        yo = oracle.epilogue_linear(oracle.dot(qa, qw, threads=oracle.default_threads()), s_w.numpy(), s_a, name)
+        for j in range(3):
+            vj = np.ascontiguousarray(yo[:, j * h * d:(j + 1) * h * d].reshape(bsz, t, h, d).transpose(0, 2, 1, 3))
+            sg, nz, _ = oracle.pack_act(vj.reshape(bsz * h, t, d), name, sc[j], kind, transpose=(j == 2))
+            assert np.array_equal(words(got[j].nz).reshape(nz.shape), nz), (i, j, "oracle")
