@@ -386,7 +386,7 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
             "oracle_sample": dict(X=X, Xf=Xf, R=R, P=P, Ws=Ws, s=s, heads=heads, D=D, batch=batch, seq=seq)}
 
 
-def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008), world=1, rank=0, chunks=4):
+def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008), world=1, rank=0, chunks=2, group=None):
     """configs[2]: LLaMA-7B prefill linears, M = 2048 tokens, K = 4096, N = 4096 / 11008.
     world > 1: each linear N-sharded over the ranks (dist.NShardPlan, `chunks` chunks per rank),
     Y^T all-gathered chunk by chunk, overlapped with the next chunk's GEMM."""
@@ -401,7 +401,7 @@ def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008), world=1, r
     for i, N in enumerate(Ns):
         w = gen.weights(N, K, seed + 1 + i)
         mu, s_w = gen.weight_stats(w)
-        if world == 1:
+        if world == 1 and group is None:
             wp = B.bwta_pack_weight(w.to(dev), mu=mu)          # offline
             sw = s_w.to(dev)
             y = torch.empty((M, N), dtype=torch.float16, device=dev)
@@ -423,19 +423,20 @@ def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008), world=1, r
             y = torch.empty((plan.n_pad, M), dtype=torch.float16, device=dev)
 
             def op_g(wp=wp, sw=sw, y=y, plan=plan):
-                D.gemm_nshard_overlap(st["xq"], wp, sw, s_x, plan, out=y)
+                D.gemm_nshard_overlap(st["xq"], wp, sw, s_x, plan, out=y, group=group)
         outs.append(y)
         ws16[N] = w
         ops.append(Op(f"gemm_n{N}", "gemm", op_g, 2 * M * N * K, M * K / 4 + N * K / 8 + 4 * N + 2 * M * N,
-                      (lambda N=N: torch.nn.functional.linear(X, st["w16"][N])),
+                      (lambda N=N: torch.nn.functional.linear(X, st["w16"][N])) if world == 1 and group is None
+                      else None,
                       alts={"design_a_cuda_core": op_cc, "prior_art_mma_b1": op_b1} if op_b1 else None))
-    st["w16"] = {N: w.to(dev) for N, w in ws16.items()} if world == 1 else {}
+    st["w16"] = {N: w.to(dev) for N, w in ws16.items()} if world == 1 and group is None else {}
     op_pack()
     smp = dict(X=X.cpu(), s_x=s_x, Ws=ws16, seed=seed)
     return {"ops": ops, "inputs": {"X": X}, "outputs": outs, "cfg": CFGS["llama_prefill"](),
             "oracle_sample": smp, "scaling": "strong",
             "parallelism": f"N-shard x{world} ({chunks} chunks/rank, in-place all-gather overlapped)"
-            if world > 1 else "single GPU"}
+            if (world > 1 or group is not None) else "single GPU"}
 
 
 def llama_attn(B, dev, seed=404, heads=32, seq=2048, D=128):
@@ -762,7 +763,9 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip the secondary-workload side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline (oracle) leg")
     ap.add_argument("--ref-row-frac", type=float, default=1.0)
-    ap.add_argument("--chunks", type=int, default=4, help="N-shard chunks per rank (N > 1)")
+    ap.add_argument("--chunks", type=int, default=2, help="N-shard chunks per rank (N > 1 or --nshard)")
+    ap.add_argument("--nshard", action="store_true",
+                    help="run the N-sharded path with its NCCL all-gathers even at N = 1 (a 1-rank communicator)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -777,13 +780,28 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.nshard:
         import torch.distributed as dist
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,TUNING")
         os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(ROOT, "gpurun_out", f"nccl_rank{rank}.log"))
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-        dist.init_process_group("nccl", device_id=dev)
+        if "MASTER_ADDR" not in os.environ:  # --nshard at N = 1 without torchrun
+            import socket
+            so = socket.socket()
+            so.bind(("127.0.0.1", 0))
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(so.getsockname()[1]), RANK="0", WORLD_SIZE="1")
+            so.close()
+        # NCCL prints its version on stdout at communicator creation: keep stdout for the JSON line
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=dev)
+            dist.barrier()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     import paper_2604_03957_b200 as B
 
     pk = peaks()
@@ -797,12 +815,14 @@ def main():
     kw = {}
     if "world" in inspect.signature(wl_fn).parameters:
         kw = {"world": world, "rank": rank}
+        if args.nshard and "group" in inspect.signature(wl_fn).parameters:
+            kw["group"] = torch.distributed.group.WORLD
         if "chunks" in inspect.signature(wl_fn).parameters:
             kw["chunks"] = args.chunks
     W = wl_fn(B, dev, **kw)
     ops = W["ops"]
     scaling = W.get("scaling", "weak") if world > 1 or W.get("scaling") else "weak"
-    sharded = world > 1 and scaling == "strong"
+    sharded = (world > 1 or args.nshard) and scaling == "strong"
 
     def step():
         if W.get("step"):
@@ -814,8 +834,15 @@ def main():
     job_ops = total_ops * (world if (world > 1 and not sharded) else 1)
 
     # -------- device-time step (CUDA graph of the library calls at N = 1)
-    use_graph = world == 1
-    g_step = graph_of(step, stream) if use_graph else None
+    # the step (incl. the NCCL all-gathers of the sharded path) is captured into a CUDA graph;
+    # eager launches only if the capture fails (the host would otherwise bound the sharded step)
+    use_graph = True
+    try:
+        g_step = graph_of(step, stream)
+    except Exception as exc:  # pragma: no cover
+        print(f"bench: CUDA-graph capture failed ({exc!r}); eager launches", file=sys.stderr)
+        torch.cuda.synchronize()
+        use_graph, g_step = False, None
     run = (lambda: g_step.replay()) if use_graph else step
     l0 = B.lib.bwta_kernel_launches()
     with torch.cuda.stream(stream):
@@ -852,7 +879,7 @@ def main():
 
     # -------- per-op device times and cuBLAS FP16 baselines (N = 1: graphs of one op)
     per_op, cub_ms = {}, {}
-    if world == 1:
+    if use_graph:
         for op in ops:
             per_op[op.name] = op_time_ms(op.fn, flush, stream)
             if op.cublas is not None:
@@ -1050,11 +1077,11 @@ def main():
             "other_designs_us": {k: {a: t * 1e3 for a, t in v.items()} for k, v in alt_ms.items()},
             "pack_GBps": pack_gbs, "extras": extras,
         }
-        if world > 1:
+        if world > 1 or args.nshard:
             line["comm"] = {"backend": "nccl", "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
                             "collective": "all_gather_into_tensor (in place, async, per chunk)"}
         print(json.dumps(line))
-    if world > 1:
+    if world > 1 or args.nshard:
         torch.distributed.destroy_process_group()
     return 0
 

@@ -52,3 +52,18 @@ vd = B.bwta_pack_act(gen.activations((2, 3, 300, 64), 11).cuda(), 1.6, transpose
 B.bwta_attn_decode(q1, kd, vd, 0.1, 2.0 / 300, 0.01, return_p=True)
 torch.cuda.synchronize()
 print("ok")
+# round-2 entry points: fused prefill attention (+ context pack), QKV head-split pack, W1A1, b1 prior art
+qp2 = B.bwta_pack_act(gen.activations((2, 3, 130, 64), 20).cuda(), 1.6)
+kp2 = B.bwta_pack_act(gen.activations((2, 3, 150, 64), 21).cuda(), 1.6)
+vt2 = B.bwta_pack_act(gen.activations((2, 3, 150, 64), 22).cuda(), 1.6, transpose=True)
+B.bwta_attn_prefill(qp2, kp2, vt2, 0.1, 2.0 / 150, 0.01, return_p=True)
+B.bwta_attn_prefill_pack(qp2, kp2, vt2, 0.1, 2.0 / 150, 0.01, 0.5)
+xq = B.bwta_pack_act(gen.activations((128, 300), 23).cuda(), 1.6)
+wq = B.bwta_pack_weight(gen.weights(3 * 2 * 64, 300, 24).cuda())
+B.bwta_gemm_pack_qkv(xq, wq, None, 1.0, 2, 64, 2, 64, (0.5, 0.5, 0.5))
+ab = B.bwta_pack_act(x, 1.6, "binary")
+for d in ("auto", "cuda_core", "mma_b1"):
+    B.bwta_gemm(ab, wp, None, 1.0, design=d)
+B.bwta_attn_pv(pp, B.bwta_pack_act(v, 1.0, "binary", transpose=True), 0.1)
+torch.cuda.synchronize()
+print("ok2")
