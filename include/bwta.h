@@ -366,6 +366,9 @@ BWTA_API bwta_status_t bwta_gemm_x(const void* x, bwta_dtype_t x_dt, int64_t m, 
  * registers).  Entry (b, h) of Q/K/V^T at b*X_bstride + h*X_hstride words;
  * O rows [dh] at b*o_bstride + h*o_hstride + i*ld_o elements.  p_out (nullable) receives the
  * P planes [batch*heads][tq][ldp_words] (tests; zeroed by a memset on `stream` first).
+ * alpha_heads / beta_heads (nullable, device float [heads]): per-head alpha / beta replacing
+ * alpha / beta for head h (the per-head scales of SURVEY §8(f) N4; a negative alpha_heads[h]
+ * negates that head's scores).
  * 1 <= dh <= 128 (BWTA_ERR_UNSUPPORTED above), tk >= 1, tk <= 2^24.  Alignment: every
  * plane pointer 16-byte aligned, every ld / stride a multiple of 4 words (TMA).  As for
  * bwta_attn_decode, a bit of P may differ from an exact softmax only where p_ij lies
@@ -379,6 +382,7 @@ BWTA_API bwta_status_t bwta_attn_prefill(const uint32_t* q_sgn, const uint32_t* 
                            int64_t ldk_words, int64_t k_bstride, int64_t k_hstride,
                            int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
                            float alpha, float s_att, bwta_dtype_t p_dt, float beta,
+                           const float* alpha_heads, const float* beta_heads,
                            void* o, bwta_dtype_t o_dt, int64_t ld_o, int64_t o_bstride, int64_t o_hstride,
                            uint32_t* p_out, int64_t ldp_words, void* stream);
 
@@ -398,6 +402,7 @@ BWTA_API bwta_status_t bwta_attn_prefill_pack(const uint32_t* q_sgn, const uint3
                            int64_t ldk_words, int64_t k_bstride, int64_t k_hstride,
                            int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
                            float alpha, float s_att, bwta_dtype_t p_dt, float beta,
+                           const float* alpha_heads, const float* beta_heads,
                            bwta_dtype_t o_dt, float out_scale, bwta_kind_t out_kind,
                            uint32_t* out_sgn, uint32_t* out_nz, int64_t out_ld_words, void* stream);
 
@@ -424,7 +429,7 @@ BWTA_API bwta_status_t bwta_attn_decode(const uint32_t* q_sgn, const uint32_t* q
                            int64_t q_bstride, int64_t q_hstride,
                            int64_t ldk_words, int64_t k_bstride, int64_t k_hstride,
                            int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
-                           float alpha, float s_att, bwta_dtype_t p_dt, float beta,
+                           float alpha, float s_att, bwta_dtype_t p_dt, float beta, const float* alpha_heads, const float* beta_heads,
                            void* o, bwta_dtype_t o_dt, int64_t o_bstride, int64_t o_hstride,
                            uint32_t* p_out, int64_t ldp_words, void* stream);
 

@@ -368,8 +368,19 @@ def bwta_attn_pv(p: Packed, vt: Packed, beta: float, out_dtype=torch.float16,
     return out
 
 
+def _heads_vec(v, heads: int, dev):
+    """Optional per-head scale vector -> a contiguous float32 device tensor [heads] (or None)."""
+    if v is None:
+        return None
+    t = torch.as_tensor(v, dtype=torch.float32, device=dev).reshape(-1).contiguous()
+    if t.numel() != heads:
+        raise ValueError(f"expected {heads} per-head scales, got {t.numel()}")
+    return t
+
+
 def bwta_attn_decode(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: float, beta: float,
-                     out_dtype=torch.float16, p_dtype=torch.float16, return_p: bool = False, stream=None):
+                     out_dtype=torch.float16, p_dtype=torch.float16, return_p: bool = False, stream=None,
+                     alpha_heads=None, beta_heads=None):
     """Fused decode attention, one launch (Tq = 1):
     O = beta * bool(round(softmax(alpha * ternary(q) (x) K^T), p_dtype) >= s_att / 2) (x) ternary(V).
 
@@ -389,9 +400,11 @@ def bwta_attn_decode(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: floa
     ldp = bwta_ld_words(tk)
     pout = torch.empty((b * h, ldp), dtype=torch.int32, device=qr.device) if return_p else None
     k_nz = k.nz if k.kind == "ternary" else None
+    ah, bh_ = _heads_vec(alpha_heads, h, qr.device), _heads_vec(beta_heads, h, qr.device)
     st = lib.bwta_attn_decode(_ptr(q.sgn), _ptr(q.nz), _ptr(k.sgn), _ptr(k_nz), _ptr(vt.sgn), _ptr(vt.nz), b, h, tk,
                               dh, qbs, qhs, kr.stride(-2), kbs, khs, vr.stride(-2), vbs, vhs, ctypes.c_float(alpha),
-                              ctypes.c_float(s_att), _DT[p_dtype], ctypes.c_float(beta), _ptr(out), _DT[out_dtype],
+                              ctypes.c_float(s_att), _DT[p_dtype], ctypes.c_float(beta), _ptr(ah), _ptr(bh_), _ptr(out),
+                              _DT[out_dtype],
                               h * dh, dh, _ptr(pout), ldp if return_p else 0, _stream(stream))
     _check(st, "bwta_attn_decode")
     return (out, pout) if return_p else out
@@ -399,7 +412,7 @@ def bwta_attn_decode(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: floa
 
 def bwta_attn_prefill(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: float, beta: float,
                       out_dtype=torch.float16, p_dtype=torch.float16, return_p: bool = False,
-                      out: Optional[torch.Tensor] = None, stream=None):
+                      out: Optional[torch.Tensor] = None, stream=None, alpha_heads=None, beta_heads=None):
     """Fused prefill attention, one launch:
     O = beta * bool(round(softmax(alpha * ternary(Q) (x) K^T), p_dtype) >= s_att / 2) (x) ternary(V).
 
@@ -425,10 +438,11 @@ def bwta_attn_prefill(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: flo
     ldp = bwta_ld_words(tk)
     pout = torch.empty((b * h, tq, ldp), dtype=torch.int32, device=qr.device) if return_p else None
     k_nz = k.nz if k.kind == "ternary" else None
+    ah, bh_ = _heads_vec(alpha_heads, h, qr.device), _heads_vec(beta_heads, h, qr.device)
     st = lib.bwta_attn_prefill(_ptr(q.sgn), _ptr(q.nz), _ptr(k.sgn), _ptr(k_nz), _ptr(vt.sgn), _ptr(vt.nz), b, h,
                                tq, tk, dh, qr.stride(-2), qbs, qhs, kr.stride(-2), kbs, khs, vr.stride(-2), vbs, vhs,
                                ctypes.c_float(alpha), ctypes.c_float(s_att), _DT[p_dtype], ctypes.c_float(beta),
-                               _ptr(out), _DT[out.dtype], out.stride(-2), obs, ohs, _ptr(pout),
+                               _ptr(ah), _ptr(bh_), _ptr(out), _DT[out.dtype], out.stride(-2), obs, ohs, _ptr(pout),
                                ldp if return_p else 0, _stream(stream))
     _check(st, "bwta_attn_prefill")
     return (out, pout) if return_p else out
@@ -436,7 +450,7 @@ def bwta_attn_prefill(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: flo
 
 def bwta_attn_prefill_pack(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: float, beta: float,
                            out_scale: float, out_kind: str = "ternary", o_dtype=torch.float16,
-                           p_dtype=torch.float16, stream=None) -> Packed:
+                           p_dtype=torch.float16, stream=None, alpha_heads=None, beta_heads=None) -> Packed:
     """bwta_pack_act(C, out_scale, out_kind) of the attention context C[b*Tq + t, h*Dh + d] =
     round_{o_dtype}(O_{b,h}[t][d]) of bwta_attn_prefill, the pack fused into its epilogue (O is
     never written): the O-projection's input planes [B*Tq, ld(H*Dh)].  Dh % 32 == 0."""
@@ -453,10 +467,11 @@ def bwta_attn_prefill_pack(q: Packed, k: Packed, vt: Packed, alpha: float, s_att
     nz = torch.empty((b * tq, ldo), dtype=torch.int32, device=qr.device)
     sgn = torch.empty((b * tq, ldo), dtype=torch.int32, device=qr.device) if out_kind == "ternary" else None
     k_nz = k.nz if k.kind == "ternary" else None
+    ah, bh_ = _heads_vec(alpha_heads, h, qr.device), _heads_vec(beta_heads, h, qr.device)
     st = lib.bwta_attn_prefill_pack(_ptr(q.sgn), _ptr(q.nz), _ptr(k.sgn), _ptr(k_nz), _ptr(vt.sgn), _ptr(vt.nz), b, h,
                                     tq, tk, dh, qr.stride(-2), qbs, qhs, kr.stride(-2), kbs, khs, vr.stride(-2), vbs,
                                     vhs, ctypes.c_float(alpha), ctypes.c_float(s_att), _DT[p_dtype],
-                                    ctypes.c_float(beta), _DT[o_dtype], ctypes.c_float(out_scale), _KIND[out_kind],
+                                    ctypes.c_float(beta), _ptr(ah), _ptr(bh_), _DT[o_dtype], ctypes.c_float(out_scale), _KIND[out_kind],
                                     _ptr(sgn), _ptr(nz), ldo, _stream(stream))
     _check(st, "bwta_attn_prefill_pack")
     return Packed(sgn, nz, out_kind, h * dh)

@@ -83,16 +83,16 @@ def _declare(L):
     L.bwta_gemm_x.argtypes = [P, i32, i64, i64, f32, i32, P, i64, i64, i64, P, P, i32, i64, i32, P]
     L.bwta_attn_decode.restype = i32
     L.bwta_attn_decode.argtypes = [P, P, P, P, P, P, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64,
-                                   f32, f32, i32, f32, P, i32, i64, i64, P, i64, P]
+                                   f32, f32, i32, f32, P, P, P, i32, i64, i64, P, i64, P]
     L.bwta_attn_prefill.restype = i32
-    L.bwta_attn_prefill.argtypes = [P, P, P, P, P, P] + [i64] * 14 + [f32, f32, i32, f32, P, i32, i64, i64, i64, P,
-                                                                      i64, P]
+    L.bwta_attn_prefill.argtypes = [P, P, P, P, P, P] + [i64] * 14 + [f32, f32, i32, f32, P, P, P, i32, i64, i64, i64,
+                                                                      P, i64, P]
     L.bwta_gemm_pack_qkv.restype = i32
     L.bwta_gemm_pack_qkv.argtypes = [P, P, i32, i64, i64, P, i64, i64, i64, P, f32, i32, i64, i64, i64, i64, P, i32,
                                      P, P, i64, P, P, i64, P, P, i64, OP, P]
     L.bwta_attn_prefill_pack.restype = i32
-    L.bwta_attn_prefill_pack.argtypes = [P, P, P, P, P, P] + [i64] * 14 + [f32, f32, i32, f32, i32, f32, i32, P, P,
-                                                                           i64, P]
+    L.bwta_attn_prefill_pack.argtypes = [P, P, P, P, P, P] + [i64] * 14 + [f32, f32, i32, f32, P, P, i32, f32, i32, P,
+                                                                           P, i64, P]
     L.bwta_attn_pv_pack.restype = i32
     L.bwta_attn_pv_pack.argtypes = [P, P, P, P, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64,
                                     f32, i32, f32, i32, P, P, i64, P, P]

@@ -712,8 +712,9 @@ bwta_status_t bwta_attn_decode(const uint32_t* q_sgn, const uint32_t* q_nz, cons
                                int64_t heads, int64_t tk, int64_t dh, int64_t q_bstride, int64_t q_hstride,
                                int64_t ldk_words, int64_t k_bstride, int64_t k_hstride, int64_t ldv_words,
                                int64_t v_bstride, int64_t v_hstride, float alpha, float s_att, bwta_dtype_t p_dt,
-                               float beta, void* o, bwta_dtype_t o_dt, int64_t o_bstride, int64_t o_hstride,
-                               uint32_t* p_out, int64_t ldp_words, void* stream) {
+                               float beta, const float* alpha_heads, const float* beta_heads, void* o,
+                               bwta_dtype_t o_dt, int64_t o_bstride, int64_t o_hstride, uint32_t* p_out,
+                               int64_t ldp_words, void* stream) {
     if (!valid_out_dt(o_dt) || (p_dt != BWTA_F16 && p_dt != BWTA_BF16 && p_dt != BWTA_F32))
         return BWTA_ERR_UNSUPPORTED;
     bwta_status_t st = check_batch(batch, heads);
@@ -758,6 +759,8 @@ bwta_status_t bwta_attn_decode(const uint32_t* q_sgn, const uint32_t* q_nz, cons
     a.v_hs = v_hstride;
     a.alpha = alpha;
     a.beta = beta;
+    a.alpha_h = alpha_heads;
+    a.beta_h = beta_heads;
     a.p_dt = p_dt;
     const double t = 0.5 * double(s_att);  // exact
     if (p_dt == BWTA_F32) {
@@ -788,7 +791,8 @@ bwta_status_t attn_prefill_impl(const uint32_t* q_sgn, const uint32_t* q_nz, con
                                 int64_t heads, int64_t tq, int64_t tk, int64_t dh, int64_t ldq_words,
                                 int64_t q_bstride, int64_t q_hstride, int64_t ldk_words, int64_t k_bstride,
                                 int64_t k_hstride, int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
-                                float alpha, float s_att, bwta_dtype_t p_dt, float beta, void* o, bwta_dtype_t o_dt,
+                                float alpha, float s_att, bwta_dtype_t p_dt, float beta, const float* alpha_heads,
+                                const float* beta_heads, void* o, bwta_dtype_t o_dt,
                                 int64_t ld_o, int64_t o_bstride, int64_t o_hstride, uint32_t* p_out,
                                 int64_t ldp_words, int pack, float out_scale, bwta_kind_t out_kind,
                                 uint32_t* out_sgn, uint32_t* out_nz, int64_t out_ld_words, void* stream) {
@@ -848,6 +852,8 @@ bwta_status_t attn_prefill_impl(const uint32_t* q_sgn, const uint32_t* q_nz, con
     a.v_hs = v_hstride;
     a.alpha = alpha;
     a.beta = beta;
+    a.alpha_h = alpha_heads;
+    a.beta_h = beta_heads;
     a.p_dt = p_dt;
     const double t = 0.5 * double(s_att);  // exact
     if (p_dt == BWTA_F32) {
@@ -904,13 +910,14 @@ bwta_status_t bwta_attn_prefill(const uint32_t* q_sgn, const uint32_t* q_nz, con
                                 int64_t heads, int64_t tq, int64_t tk, int64_t dh, int64_t ldq_words,
                                 int64_t q_bstride, int64_t q_hstride, int64_t ldk_words, int64_t k_bstride,
                                 int64_t k_hstride, int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
-                                float alpha, float s_att, bwta_dtype_t p_dt, float beta, void* o, bwta_dtype_t o_dt,
+                                float alpha, float s_att, bwta_dtype_t p_dt, float beta, const float* alpha_heads,
+                                const float* beta_heads, void* o, bwta_dtype_t o_dt,
                                 int64_t ld_o, int64_t o_bstride, int64_t o_hstride, uint32_t* p_out,
                                 int64_t ldp_words, void* stream) {
     return attn_prefill_impl(q_sgn, q_nz, k_sgn, k_nz, vt_sgn, vt_nz, batch, heads, tq, tk, dh, ldq_words, q_bstride,
                              q_hstride, ldk_words, k_bstride, k_hstride, ldv_words, v_bstride, v_hstride, alpha, s_att,
-                             p_dt, beta, o, o_dt, ld_o, o_bstride, o_hstride, p_out, ldp_words, 0, 0.f, BWTA_TERNARY,
-                             nullptr, nullptr, 0, stream);
+                             p_dt, beta, alpha_heads, beta_heads, o, o_dt, ld_o, o_bstride, o_hstride, p_out,
+                             ldp_words, 0, 0.f, BWTA_TERNARY, nullptr, nullptr, 0, stream);
 }
 
 bwta_status_t bwta_attn_prefill_pack(const uint32_t* q_sgn, const uint32_t* q_nz, const uint32_t* k_sgn,
@@ -918,13 +925,14 @@ bwta_status_t bwta_attn_prefill_pack(const uint32_t* q_sgn, const uint32_t* q_nz
                                      int64_t heads, int64_t tq, int64_t tk, int64_t dh, int64_t ldq_words,
                                      int64_t q_bstride, int64_t q_hstride, int64_t ldk_words, int64_t k_bstride,
                                      int64_t k_hstride, int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
-                                     float alpha, float s_att, bwta_dtype_t p_dt, float beta, bwta_dtype_t o_dt,
+                                     float alpha, float s_att, bwta_dtype_t p_dt, float beta,
+                                     const float* alpha_heads, const float* beta_heads, bwta_dtype_t o_dt,
                                      float out_scale, bwta_kind_t out_kind, uint32_t* out_sgn, uint32_t* out_nz,
                                      int64_t out_ld_words, void* stream) {
     return attn_prefill_impl(q_sgn, q_nz, k_sgn, k_nz, vt_sgn, vt_nz, batch, heads, tq, tk, dh, ldq_words, q_bstride,
                              q_hstride, ldk_words, k_bstride, k_hstride, ldv_words, v_bstride, v_hstride, alpha, s_att,
-                             p_dt, beta, nullptr, o_dt, 0, 0, 0, nullptr, 0, 1, out_scale, out_kind, out_sgn, out_nz,
-                             out_ld_words, stream);
+                             p_dt, beta, alpha_heads, beta_heads, nullptr, o_dt, 0, 0, 0, nullptr, 0, 1, out_scale,
+                             out_kind, out_sgn, out_nz, out_ld_words, stream);
 }
 
 bwta_status_t bwta_attn_pv_pack(const uint32_t* p_sgn, const uint32_t* p_nz, const uint32_t* vt_sgn,

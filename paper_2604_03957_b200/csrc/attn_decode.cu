@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(AD_WARPS * 32) attn_decode_kernel(DecodeArgs p
     const int64_t w_lo = nw * rank / cs, w_hi = nw * (rank + 1) / cs;
     const int64_t j_lo = 32 * w_lo, j_hi = 32 * w_hi < p.tk ? 32 * w_hi : p.tk;
     const int64_t eb = e / p.nh, eh = e % p.nh;
+    const float alpha = p.alpha_h ? __ldg(p.alpha_h + eh) : p.alpha;  // per-head alpha (nullable)
     const int qw = int((p.dh + 31) / 32);
     uint32_t qs[AD_QW], qn[AD_QW];
     const uint32_t* q0 = p.q_nz + eb * p.q_bs + eh * p.q_hs;
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(AD_WARPS * 32) attn_decode_kernel(DecodeArgs p
     float* sc = reinterpret_cast<float*>(ad_pw + p.sc_off);
     for (int64_t j = j_lo + tid; j < j_hi; j += NT) {
         const int32_t d = qk_dot(qs, qn, qw, kbase_s + j * p.ldk, kbase_n ? kbase_n + j * p.ldk : nullptr);
-        const float s = __fmul_rn(float(d), p.alpha);
+        const float s = __fmul_rn(float(d), alpha);
         sc[j - j_lo] = s;
         if (s > mx) {
             z = z * expf(mx - s) + 1.f;
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(AD_WARPS * 32) attn_decode_kernel(DecodeArgs p
     }
     if (tid < p.dh) {
         const int64_t off = eb * p.o_bs + eh * p.o_hs + tid;
-        const float y = __fmul_rn(float(dot), p.beta);
+        const float y = __fmul_rn(float(dot), p.beta_h ? __ldg(p.beta_h + eh) : p.beta);
         if (p.o_dt == DT_F16) reinterpret_cast<__half*>(p.o)[off] = __float2half_rn(y);
         else if (p.o_dt == DT_BF16) reinterpret_cast<__nv_bfloat16*>(p.o)[off] = __float2bfloat16_rn(y);
         else if (p.o_dt == DT_F32) reinterpret_cast<float*>(p.o)[off] = y;

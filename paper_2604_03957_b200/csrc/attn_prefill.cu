@@ -71,7 +71,7 @@ constexpr int VCH_BLK = VCH_W / 4;                 // key blocks per V^T chunk
 constexpr int VCH_B = 2 * AP_DH * VCH_W * 4;       // both planes, <= 32 KB
 constexpr int P_CODES = AP_BQ * CODE_ROW;         // 8 KB per P buffer
 constexpr int SMEM_AP = 1024 + 2 * Q_CODES + AP_S * STAGE_B + AP_VS * V_CODES + 2 * VCH_B + 2 * P_CODES +
-                        2 * Q_BITS + 4 * 512 /*table*/ + 2 * AP_NH * AP_BQ * 4 * 2 /*merge*/ + 512 /*barriers*/;
+                        2 * Q_BITS + 4 * 1024 /*tables*/ + 2 * AP_NH * AP_BQ * 4 * 2 /*merge*/ + 512 /*barriers*/;
 static_assert(SMEM_AP <= 227 * 1024, "shared memory");
 constexpr int TM_S = 0, TM_O = 256, TM_SF = 384;  // TMEM columns: S[0], S[1], O, scale factors
 
@@ -83,6 +83,8 @@ struct ApParams {
     int k_kind;            // B_TERNARY or B_BINARY
     int neg;               // alpha < 0: Q codes negated
     float alpha;           // |alpha|
+    const float* alpha_h;  // per-head alpha [nh] (nullable; signed: negative heads negate their Q codes)
+    const float* beta_h;   // per-head beta [nh] (nullable)
     float p_t;             // bool threshold as a p_dt storage value (R2)
     int p_dt;
     float beta;
@@ -139,8 +141,8 @@ __device__ __forceinline__ void unpack_q_row(uint32_t sgn_addr, uint32_t nz_addr
 }
 
 // bit(d): R13's expression for an integer dot d (|alpha|-scaled, the row's s_max and z)
-__device__ __forceinline__ bool p_bit(const ApParams& p, int d, float mx, float z) {
-    const float s = __fmul_rn(float(d), p.alpha);
+__device__ __forceinline__ bool p_bit(const ApParams& p, float alpha, int d, float mx, float z) {
+    const float s = __fmul_rn(float(d), alpha);
     return round_to(p.p_dt, __fdiv_rn(expf(__fsub_rn(s, mx)), z)) >= p.p_t;
 }
 
@@ -158,7 +160,8 @@ __global__ void __launch_bounds__(AP_NT, 1)
     uint8_t* sP = sV + 2 * VCH_B;                       // 2 P code buffers
     uint8_t* sQb = sP + 2 * P_CODES;                    // 2 x Q bits (sgn plane, nz plane)
     float* tbl = reinterpret_cast<float*>(sQb + 2 * Q_BITS);     // exp(|alpha| (i - 2 Dh_max)), 2 KB
-    float* mrg = tbl + 512;                                       // [2 parity][AP_NH slices][128 rows][R, z]
+    // (per-head alphas: tbl[0..512) and tbl[512..1024) alternate between items)
+    float* mrg = tbl + 1024;                                      // [2 parity][AP_NH slices][128 rows][R, z]
     uint64_t* bars = reinterpret_cast<uint64_t*>(mrg + 2 * AP_NH * AP_BQ * 2);
     uint64_t* k_full = bars;
     uint64_t* k_ready = k_full + AP_S;
@@ -351,8 +354,9 @@ __global__ void __launch_bounds__(AP_NT, 1)
             const int qb = ic & 1;
             wait_bar(&q_full[qb], uint32_t((ic >> 1) & 1));
             const uint32_t qbits = smem_u32(sQb + qb * Q_BITS);
+            const bool negq = p.alpha_h ? (__ldg(p.alpha_h + (t / p.q_tiles) % p.nh) < 0.f) : p.neg != 0;
             unpack_q_row(qbits + ut * 16, qbits + AP_BQ * 16 + ut * 16, smem_u32(sQ + qb * Q_CODES) + ut * CODE_ROW, ut,
-                         p.neg != 0);
+                         negq);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&q_ready[qb]);
@@ -393,12 +397,22 @@ __global__ void __launch_bounds__(AP_NT, 1)
         const int r = 32 * q + lane;                       // query row within the tile = TMEM lane
         const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16);
         const float MAGIC = 12582912.f;                    // 1.5 * 2^23: float_as_int(x + MAGIC) = 0x4B400000 + x
-        const uint32_t tbl_s = smem_u32(tbl);
         int sg = 0, pg = 0, ic = 0;
         for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++ic) {
             const int64_t e = t / p.q_tiles;
             const int64_t qrow = int64_t(t % p.q_tiles) * AP_BQ + r;
             const int eb = int(e / p.nh), eh = int(e % p.nh);
+            float alpha = p.alpha, beta = p.beta;
+            uint32_t tbl_s = smem_u32(tbl);
+            if (p.alpha_h) {  // this head's |alpha|: its own exp table (double-buffered by item parity)
+                alpha = fabsf(__ldg(p.alpha_h + eh));
+                float* tb = tbl + 512 * (ic & 1);
+                for (int i = threadIdx.x - 256; i < AP_TBL; i += 32 * AP_SMW)
+                    tb[i] = expf(__fmul_rn(float(i - 2 * AP_DH), alpha));
+                named_bar(5, 32 * AP_SMW);  // every softmax warp sees the table before using it
+                tbl_s = smem_u32(tb);
+            }
+            if (p.beta_h) beta = __ldg(p.beta_h + eh);
             // ---- pass 1: R = running max of the integer dots (|alpha|-signed), z = sum exp(|alpha| (d - R))
             float R = -INFINITY, z = 0.f;
             for (int j = 0; j < nblk; ++j, ++sg) {
@@ -465,11 +479,11 @@ __global__ void __launch_bounds__(AP_NT, 1)
                 if (Rh != -INFINITY) zt += zh * lds_f32(tbl_s + 4 * (int(Rh - Rm) + 2 * AP_DH));
             }
             // ---- the row's integer threshold: bit(d) <=> d >= dthr (binary search over [-Dh, Rm + 1])
-            const float mx = __fmul_rn(Rm, p.alpha);
+            const float mx = __fmul_rn(Rm, alpha);
             int lo = -p.dh, hi = int(Rm) + 1;
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;  // floor for negatives too
-                if (p_bit(p, mid, mx, zt)) hi = mid;
+                if (p_bit(p, alpha, mid, mx, zt)) hi = mid;
                 else lo = mid + 1;
             }
             const float dthr = float(lo);
@@ -531,7 +545,7 @@ __global__ void __launch_bounds__(AP_NT, 1)
                     uint32_t pos = 0, neg = 0;
 #pragma unroll
                     for (int c = 0; c < 32; ++c) {
-                        const float y = __fmul_rn(__uint_as_float(o[c]), p.beta);  // R5
+                        const float y = __fmul_rn(__uint_as_float(o[c]), beta);  // R5
                         pos |= uint32_t(y >= p.po_tp) << c;
                         neg |= uint32_t(y <= -p.po_tn) << c;
                     }
@@ -551,8 +565,8 @@ __global__ void __launch_bounds__(AP_NT, 1)
                         uint32_t w[8];
 #pragma unroll
                         for (int c = 0; c < 8; ++c) {
-                            const float y0 = __fmul_rn(__uint_as_float(o[2 * c]), p.beta);
-                            const float y1 = __fmul_rn(__uint_as_float(o[2 * c + 1]), p.beta);
+                            const float y0 = __fmul_rn(__uint_as_float(o[2 * c]), beta);
+                            const float y1 = __fmul_rn(__uint_as_float(o[2 * c + 1]), beta);
                             if (p.o_dt == DT_F16) {
                                 __half2 hv = __halves2half2(__float2half_rn(y0), __float2half_rn(y1));
                                 w[c] = *reinterpret_cast<uint32_t*>(&hv);
@@ -569,7 +583,7 @@ __global__ void __launch_bounds__(AP_NT, 1)
                         for (int c = 0; c < 16; ++c) {
                             if (c0 + c < p.dh) {
                                 const float acc = __uint_as_float(o[c]);
-                                const float y = __fmul_rn(acc, p.beta);
+                                const float y = __fmul_rn(acc, beta);
                                 const int64_t off = obase + c0 + c;
                                 if (p.o_dt == DT_F16) reinterpret_cast<__half*>(p.o)[off] = __float2half_rn(y);
                                 else if (p.o_dt == DT_BF16) reinterpret_cast<__nv_bfloat16*>(p.o)[off] = __float2bfloat16_rn(y);
@@ -616,6 +630,8 @@ cudaError_t launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t s) {
     p.p_t = a.p_t;
     p.p_dt = a.p_dt;
     p.beta = a.beta;
+    p.alpha_h = a.alpha_h;
+    p.beta_h = a.beta_h;
     p.o = a.o;
     p.o_dt = a.o_dt;
     p.ld_o = a.ld_o;

@@ -176,6 +176,7 @@ struct DecodeArgs {
     int64_t ldk, ldv;               // words
     int64_t q_bs, q_hs, k_bs, k_hs, v_bs, v_hs;  // words
     float alpha, p_t, beta;         // p_t: the bool threshold as a p_dt storage value (R2)
+    const float *alpha_h, *beta_h;  // per-head alpha / beta [nh] (nullable)
     int p_dt;
     void* o;
     int o_dt;
@@ -196,6 +197,7 @@ struct AttnPrefillArgs {
     int64_t ldq, ldk, ldv;          // words
     int64_t q_bs, q_hs, k_bs, k_hs, v_bs, v_hs;  // words
     float alpha, p_t, beta;         // p_t: the bool threshold as a p_dt storage value (R2)
+    const float *alpha_h = nullptr, *beta_h = nullptr;  // per-head alpha / beta [nh] (nullable)
     int p_dt;
     void* o;
     int o_dt;

@@ -140,7 +140,8 @@ def test_attn_prefill_validation():
         return L.bwta_attn_prefill(a["qs"], a["qn"], a["ks"], a["kn"], a["vs"], a["vn"], a["b"], a["h"], a["tq"],
                                    a["tk"], a["dh"], a["ldq"], 0, 0, a["ldk"], 0, 0, a["ldv"], 0, 0,
                                    ctypes.c_float(a["alpha"]), ctypes.c_float(a["s_att"]), a["p_dt"],
-                                   ctypes.c_float(a["beta"]), a["o"], a["o_dt"], a["ld_o"], 0, 0, a["pout"], a["ldp"],
+                                   ctypes.c_float(a["beta"]), None, None, a["o"], a["o_dt"], a["ld_o"], 0, 0, a["pout"],
+                                   a["ldp"],
                                    None)
     assert pf() == 4                     # valid, but no sm_100 device here
     assert pf(dh=129) == 4               # one 128-element tensor-core stage per row
@@ -164,7 +165,8 @@ def test_attn_prefill_validation():
         a.update(kw)
         return L.bwta_attn_prefill_pack(a["qs"], a["qn"], a["ks"], a["kn"], a["vs"], a["vn"], a["b"], a["h"], a["tq"],
                                         100, a["dh"], 4, 0, 0, 4, 0, 0, 4, 0, 0, ctypes.c_float(0.1),
-                                        ctypes.c_float(0.02), 0, ctypes.c_float(0.1), a["o_dt"], ctypes.c_float(a["s_o"]),
+                                        ctypes.c_float(0.02), 0, ctypes.c_float(0.1), None, None, a["o_dt"],
+                                        ctypes.c_float(a["s_o"]),
                                         a["kind"], a["os_"], a["on"], a["ldo"], None)
     assert pfp() == 4                    # valid, but no sm_100 device here
     assert pfp(dh=48) == 4               # a head must own whole words of the context row
@@ -175,3 +177,35 @@ def test_attn_prefill_validation():
     assert pfp(s_o=0.0) == 1
     assert pfp(ldo=0) == 2
     assert pfp(on=132) == 3
+
+
+@pytest.mark.gpu
+def test_attn_per_head_scales(B):
+    """Per-head alpha / beta: one call with alpha_heads / beta_heads equals the
+    per-head calls with the scalar alpha_h / beta_h bit for bit (prefill, prefill + context pack,
+    decode), including a head with a negative alpha."""
+    b, h, tq, tk, dh = 2, 4, 130, 300, 64
+    q, k, v = (gen.activations((b, h, t, dh), 9900 + j) for j, t in enumerate((tq, tk, tk)))
+    qp, kp = B.bwta_pack_act(q.cuda(), 1.3), B.bwta_pack_act(k.cuda(), 1.2)
+    vt = B.bwta_pack_act(v.cuda(), 1.1, "ternary", transpose=True)
+    s_att = float(np.float32(2.0 / tk))
+    ah = [0.11, -0.07, 0.23, 0.05]
+    bh = [0.01, 0.02, 0.015, 0.03]
+    o = B.bwta_attn_prefill(qp, kp, vt, 1.0, s_att, 1.0, alpha_heads=ah, beta_heads=bh)
+    for hh in range(h):
+        sub = lambda P: type(P)(None if P.sgn is None else P.sgn[:, hh:hh + 1], P.nz[:, hh:hh + 1], P.kind, P.cols)
+        ref = B.bwta_attn_prefill(sub(qp), sub(kp), sub(vt), ah[hh], s_att, bh[hh])
+        assert torch.equal(o[:, hh:hh + 1].view(torch.int16), ref.view(torch.int16)), hh
+    # decode (one query row per head)
+    q1 = B.bwta_pack_act(gen.activations((b, h, 1, dh), 9950).cuda(), 1.3)
+    od = B.bwta_attn_decode(q1, kp, vt, 1.0, s_att, 1.0, alpha_heads=ah, beta_heads=bh)
+    for hh in range(h):
+        sub = lambda P: type(P)(None if P.sgn is None else P.sgn[:, hh:hh + 1], P.nz[:, hh:hh + 1], P.kind, P.cols)
+        ref = B.bwta_attn_decode(sub(q1), sub(kp), sub(vt), ah[hh], s_att, bh[hh])
+        assert torch.equal(od[:, hh:hh + 1].view(torch.int16), ref.view(torch.int16)), hh
+    # the fused context pack with per-head scales == pack of the per-head-scaled context
+    ctx = o.transpose(1, 2).reshape(b * tq, h * dh).contiguous()
+    s_ctx = gen.act_scale(ctx) or 1.0
+    got = B.bwta_attn_prefill_pack(qp, kp, vt, 1.0, s_att, 1.0, s_ctx, alpha_heads=ah, beta_heads=bh)
+    ref = B.bwta_pack_act(ctx, s_ctx)
+    assert torch.equal(got.nz, ref.nz) and torch.equal(got.sgn, ref.sgn)

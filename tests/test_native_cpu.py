@@ -185,7 +185,7 @@ def test_attn_decode_validation(N):
         a.update(kw)
         return L.bwta_attn_decode(a["qs"], a["qn"], a["ks"], a["kn"], a["vs"], a["vn"], a["b"], a["h"], a["tk"],
                                   a["dh"], 0, 0, a["ldk"], 0, 0, a["ldv"], 0, 0, ctypes.c_float(a["alpha"]),
-                                  ctypes.c_float(a["s_att"]), a["p_dt"], ctypes.c_float(a["beta"]), a["o"],
+                                  ctypes.c_float(a["s_att"]), a["p_dt"], ctypes.c_float(a["beta"]), None, None, a["o"],
                                   a["o_dt"], 0, 0, a["pout"], a["ldp"], None)
     assert dec() == 4                      # valid, but no sm_100 device here
     assert dec(tk=0) == 2                  # softmax over an empty row
