@@ -647,25 +647,29 @@ __device__ __forceinline__ void unpack_quad(uint32_t p0addr, uint32_t p1addr, ui
         sts128(rowaddr + (((4 * h + g) ^ sw) << 4), o[0], o[1], o[2], o[3]);
     }
 }
-template <int KS>
-__device__ __forceinline__ void unpack_quads(int kind, uint32_t bits, int plane_bytes, uint32_t dst, int i0, int rows,
-                                             int step) {
+template <int KS, int ROWS, int STEP>
+__device__ __forceinline__ void unpack_quads(int kind, uint32_t bits, uint32_t dst, int i0) {
+    // ROWS / STEP compile-time: the item -> (row, quad) split is a multiply-shift, not a division
     constexpr int RB = Stage<KS>::WPS * 4;  // bit bytes per row per plane
     constexpr int ROWB = Stage<KS>::ROWB;
-    const int items = rows * (Stage<KS>::WPS / 4);
+    constexpr int ITEMS = ROWS * (Stage<KS>::WPS / 4);
+    constexpr int PB = ROWS * RB;           // plane bytes
     if (kind == B_TERNARY) {
-        for (int i = i0; i < items; i += step) {
-            const int r = i % rows, h = i / rows;
-            unpack_quad<B_TERNARY, KS>(bits + r * RB, bits + plane_bytes + r * RB, dst + r * ROWB, r, h);
+#pragma unroll
+        for (int i = i0; i < ITEMS; i += STEP) {
+            const int r = i % ROWS, h = i / ROWS;
+            unpack_quad<B_TERNARY, KS>(bits + r * RB, bits + PB + r * RB, dst + r * ROWB, r, h);
         }
     } else if (kind == B_BOOL) {
-        for (int i = i0; i < items; i += step) {
-            const int r = i % rows, h = i / rows;
+#pragma unroll
+        for (int i = i0; i < ITEMS; i += STEP) {
+            const int r = i % ROWS, h = i / ROWS;
             unpack_quad<B_BOOL, KS>(bits + r * RB, 0, dst + r * ROWB, r, h);
         }
     } else {
-        for (int i = i0; i < items; i += step) {
-            const int r = i % rows, h = i / rows;
+#pragma unroll
+        for (int i = i0; i < ITEMS; i += STEP) {
+            const int r = i % ROWS, h = i / ROWS;
             unpack_quad<B_BINARY, KS>(bits + r * RB, 0, dst + r * ROWB, r, h);
         }
     }
@@ -997,7 +1001,7 @@ __global__ void __launch_bounds__(NT, 1)
 #endif
                 {
                     if (is_a) unpack_rows<KS>(kind, bits, plane_bytes, dst, ut, rows, 128);
-                    else unpack_quads<KS>(kind, bits, plane_bytes, dst, ut, rows, 192);
+                    else unpack_quads<KS, C::BNC, 192>(kind, bits, dst, ut);
                 }
 #ifdef BWTA_TRACE
                 if (!(p.dbg & 128))
