@@ -229,6 +229,54 @@ BWTA_API bwta_status_t bwta_gemm(const uint32_t* a_sgn, const uint32_t* a_nz, bw
                         void* workspace, size_t workspace_bytes,
                         const bwta_opts_t* opts, void* stream);
 
+/* ---- N-sharded BWTA linear with the all-gather fused into the epilogue ---- */
+/*
+ * The north star's multi-GPU linear: rank r of `world` GPUs holds the weight rows of its N-shard
+ * and computes its block of Y^T; with the NCCL all-gather as the baseline, here the GEMM's epilogue
+ * itself stores every output tile both to y and to the same position of each peer's buffer
+ * y_peers[0 .. n_peers) (device pointers valid in this process: peer GPUs' memory mapped with
+ * bwta_ipc_open, reached over NVLink / NVSwitch), so the gather overlaps the math tile by tile
+ * and no collective is launched.  Arguments and result as bwta_gemm (one shard: w_sgn / n / w_scale
+ * are the local rows, y the local block inside the full Y^T, y_peers the same block in the peers'
+ * Y^T), restricted to what the tile kernel's 16-bit TMA-store epilogue covers: y_dt F16 | BF16,
+ * y and every y_peers[i] 16-byte aligned, ld_y % 8 == 0, design AUTO | TCGEN05, not W1A1 (binary
+ * A with binary W), and a shape that takes the tile kernel (both m and n > 32) -- anything else
+ * returns BWTA_ERR_UNSUPPORTED with nothing enqueued (gather those with a collective).
+ * 0 <= n_peers <= 7.  The stores are complete when the kernel is; bwta_peer_barrier, enqueued after
+ * it on every rank, makes all ranks' stores visible to the work that follows.  The caller keeps
+ * the buffers alive and does not overwrite a buffer a peer may still be reading (double-buffer Y^T
+ * across steps, or barrier before the GEMM too).
+ */
+BWTA_API bwta_status_t bwta_gemm_peers(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t a_kind,
+                                       int64_t m, int64_t lda_words,
+                                       const uint32_t* w_sgn, int64_t n, int64_t ldw_words, int64_t k,
+                                       const float* w_scale, float a_scale,
+                                       void* y, bwta_dtype_t y_dt, int64_t ld_y, int y_transposed,
+                                       void* const* y_peers, int n_peers,
+                                       const bwta_opts_t* opts, void* stream);
+
+/*
+ * Cross-GPU barrier over flag arrays in device memory: flags[r] (host array of `world` device
+ * pointers, valid in this process) is rank r's array of `world` uint32 slots, zero-initialised
+ * before the first use.  One tiny kernel on `stream`: for every rank t it performs a system-scope
+ * release store flags[t][rank] = epoch after a system-scope fence (so every store of the work
+ * enqueued before it on this stream -- e.g. bwta_gemm_peers' peer stores -- is visible to rank t),
+ * then waits with acquire loads until flags[rank][t] >= epoch for every t.  epoch >= 1 and grows by
+ * one per barrier (the same sequence on every rank).  1 <= world <= 8, 0 <= rank < world.  A rank
+ * that never arrives traps the kernel after 30 s (sticky CUDA error) instead of hanging.
+ */
+BWTA_API bwta_status_t bwta_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch,
+                                         void* stream);
+
+/* CUDA IPC for the peer mappings: the handle (BWTA_IPC_HANDLE_BYTES bytes, host memory) of the
+ * allocation holding device pointer ptr and ptr's byte offset in it; another process opens it with
+ * bwta_ipc_open (-> a device pointer to the same bytes) and unmaps it with bwta_ipc_close(ptr,
+ * offset).  One open per allocation per process. */
+#define BWTA_IPC_HANDLE_BYTES 64
+BWTA_API bwta_status_t bwta_ipc_handle(const void* ptr, void* handle, int64_t* offset);
+BWTA_API bwta_status_t bwta_ipc_open(const void* handle, int64_t offset, void** ptr);
+BWTA_API bwta_status_t bwta_ipc_close(void* ptr, int64_t offset);
+
 /* ---- BWTA linear with the next layer's pack fused into the epilogue ------ */
 /*
  * out = bwta_pack_act(Y, y_dt, out_scale, out_kind), Y = bwta_gemm(...) in

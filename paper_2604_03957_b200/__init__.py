@@ -21,7 +21,8 @@ from . import _native as N
 from ._native import lib
 
 __all__ = ["Packed", "BwtaError", "bwta_ld_words", "bwta_pack_act", "bwta_pack_weight",
-           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "bwta_attn_prefill", "bwta_attn_prefill_pack", "bwta_gemm_pack_qkv", "bwta_gemm_x", "last_design", "lib"]
+           "bwta_pack_act_batch", "bwta_gemm", "bwta_gemm_pack", "bwta_attn_qk", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "bwta_attn_prefill", "bwta_attn_prefill_pack", "bwta_gemm_pack_qkv", "bwta_gemm_x", "bwta_gemm_peers", "bwta_peer_barrier",
+           "ipc_handle", "ipc_open", "ipc_close", "last_design", "lib"]
 
 
 class BwtaError(RuntimeError):
@@ -234,6 +235,57 @@ def bwta_gemm(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: fl
                        _DT[out.dtype], out.stride(0), int(y_transposed), _ptr(ws), wsb, o, _stream(stream))
     _check(st, "bwta_gemm")
     return out
+
+
+def bwta_gemm_peers(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: float, y_ptr: int, ld_y: int,
+                    peer_ptrs, out_dtype=torch.float16, y_transposed: bool = True, design: str = "auto",
+                    stream=None, tile=None) -> None:
+    """bwta_gemm of one N-shard whose epilogue also stores every output tile into each peer's buffer
+    (the fused all-gather, include/bwta.h bwta_gemm_peers).  y_ptr / peer_ptrs are device addresses
+    (ints) of this shard's block in this GPU's / the peers' Y^T (row stride ld_y elements); the
+    buffers are the caller's (paper_2604_03957_b200.dist.PeerAllGather owns them)."""
+    if a.kind not in ("ternary", "bool", "binary") or w.kind != "binary" or a.cols != w.cols:
+        raise ValueError("bwta_gemm_peers expects ternary/bool/binary activations and binary weights of equal K")
+    if out_dtype not in (torch.float16, torch.bfloat16):
+        raise ValueError("bwta_gemm_peers stores f16 / bf16")
+    ar = a.ref
+    m, n, k = ar.shape[-2], w.sgn.shape[-2], a.cols
+    peers = list(peer_ptrs)
+    arr = (ctypes.c_void_p * max(1, len(peers)))(*[ctypes.c_void_p(int(q)) for q in peers])
+    ws_scale = None if w_scale is None else w_scale.to(device=ar.device, dtype=torch.float32).contiguous()
+    st = lib.bwta_gemm_peers(_ptr(a.sgn), _ptr(a.nz), _KIND[a.kind], m, ar.stride(-2), _ptr(w.sgn), n,
+                             w.sgn.stride(-2), k, _ptr(ws_scale), ctypes.c_float(a_scale), ctypes.c_void_p(int(y_ptr)),
+                             _DT[out_dtype], int(ld_y), int(y_transposed), arr, len(peers), _opts(design, tile),
+                             _stream(stream))
+    _check(st, "bwta_gemm_peers")
+
+
+def bwta_peer_barrier(flag_ptrs, rank: int, epoch: int, stream=None) -> None:
+    """Cross-GPU barrier (include/bwta.h bwta_peer_barrier): flag_ptrs[r] = device address of rank r's
+    uint32 flag array as mapped in this process."""
+    arr = (ctypes.c_void_p * len(flag_ptrs))(*[ctypes.c_void_p(int(q)) for q in flag_ptrs])
+    _check(lib.bwta_peer_barrier(arr, len(flag_ptrs), int(rank), ctypes.c_uint32(epoch), _stream(stream)),
+           "bwta_peer_barrier")
+
+
+def ipc_handle(t: torch.Tensor):
+    """(handle bytes, byte offset) of the allocation holding t's storage (CUDA IPC)."""
+    h = (ctypes.c_char * N.IPC_HANDLE_BYTES)()
+    off = ctypes.c_int64(0)
+    _check(lib.bwta_ipc_handle(ctypes.c_void_p(t.data_ptr()), h, ctypes.byref(off)), "bwta_ipc_handle")
+    return bytes(h.raw), int(off.value)
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    """Map another process's allocation (ipc_handle) into this one; returns the device address."""
+    h = (ctypes.c_char * N.IPC_HANDLE_BYTES).from_buffer_copy(handle)
+    ptr = ctypes.c_void_p(0)
+    _check(lib.bwta_ipc_open(h, int(offset), ctypes.byref(ptr)), "bwta_ipc_open")
+    return int(ptr.value)
+
+
+def ipc_close(ptr: int, offset: int) -> None:
+    _check(lib.bwta_ipc_close(ctypes.c_void_p(int(ptr)), int(offset)), "bwta_ipc_close")
 
 
 def bwta_gemm_x(x: torch.Tensor, a_scale: float, w: Packed, w_scale: Optional[torch.Tensor], kind: str = "ternary",

@@ -21,7 +21,9 @@ EXPORTS = ("bwta_ld_words", "bwta_status_string", "bwta_last_cuda_error", "bwta_
            "bwta_gemm_workspace_size", "bwta_gemm_pack",
            "bwta_gemm", "bwta_attn_qk_workspace_size", "bwta_attn_qk",
            "bwta_attn_pv_workspace_size", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "bwta_gemm_x",
-           "bwta_attn_prefill", "bwta_attn_prefill_pack", "bwta_gemm_pack_qkv")
+           "bwta_attn_prefill", "bwta_attn_prefill_pack", "bwta_gemm_pack_qkv", "bwta_gemm_peers",
+           "bwta_peer_barrier", "bwta_ipc_handle", "bwta_ipc_open", "bwta_ipc_close")
+IPC_HANDLE_BYTES = 64
 
 
 class Opts(ctypes.Structure):
@@ -96,6 +98,17 @@ def _declare(L):
     L.bwta_attn_pv_pack.restype = i32
     L.bwta_attn_pv_pack.argtypes = [P, P, P, P, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64,
                                     f32, i32, f32, i32, P, P, i64, P, P]
+    L.bwta_gemm_peers.restype = i32
+    L.bwta_gemm_peers.argtypes = [P, P, i32, i64, i64, P, i64, i64, i64, P, f32, P, i32, i64, i32,
+                                  P, i32, OP, P]
+    L.bwta_peer_barrier.restype = i32
+    L.bwta_peer_barrier.argtypes = [P, i32, i32, ctypes.c_uint32, P]
+    L.bwta_ipc_handle.restype = i32
+    L.bwta_ipc_handle.argtypes = [P, P, ctypes.POINTER(i64)]
+    L.bwta_ipc_open.restype = i32
+    L.bwta_ipc_open.argtypes = [P, i64, ctypes.POINTER(P)]
+    L.bwta_ipc_close.restype = i32
+    L.bwta_ipc_close.argtypes = [P, i64]
     L.bwta_attn_pv.restype = i32
     L.bwta_attn_pv.argtypes = [P, P, P, P, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64, i64,
                                f32, P, i32, i64, i64, i64, P, sz, OP, P]

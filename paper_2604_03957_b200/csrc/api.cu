@@ -432,6 +432,120 @@ bwta_status_t bwta_gemm(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t
     return run_matmul(a, workspace, workspace_bytes, opts, (cudaStream_t)stream);
 }
 
+bwta_status_t bwta_gemm_peers(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t a_kind, int64_t m,
+                              int64_t lda_words, const uint32_t* w_sgn, int64_t n, int64_t ldw_words, int64_t k,
+                              const float* w_scale, float a_scale, void* y, bwta_dtype_t y_dt, int64_t ld_y,
+                              int y_transposed, void* const* y_peers, int n_peers, const bwta_opts_t* opts,
+                              void* stream) {
+    if (n_peers < 0 || n_peers > MAX_PEERS || (n_peers > 0 && y_peers == nullptr)) return BWTA_ERR_INVALID_VALUE;
+    if (y_dt != BWTA_F16 && y_dt != BWTA_BF16) return BWTA_ERR_UNSUPPORTED;
+    const bwta_opts_t* o = opts_or_default(opts);
+    if (bwta_status_t st = check_opts(o); st != BWTA_OK) return st;
+    if (o->design != BWTA_DESIGN_AUTO && o->design != BWTA_DESIGN_TCGEN05) return BWTA_ERR_UNSUPPORTED;
+    for (int i = 0; i < n_peers; ++i) {
+        if (y_peers[i] == nullptr) return BWTA_ERR_INVALID_VALUE;
+        if (!aligned16(y_peers[i])) return BWTA_ERR_ALIGNMENT;
+    }
+    if (a_kind != BWTA_TERNARY && a_kind != BWTA_BOOL && a_kind != BWTA_BINARY) return BWTA_ERR_UNSUPPORTED;
+    if (m < 0 || n < 0 || k < 0 || k > KMAX) return BWTA_ERR_SHAPE;
+    if (m == 0 || n == 0) return BWTA_OK;
+    if (w_sgn == nullptr || y == nullptr) return BWTA_ERR_INVALID_VALUE;
+    if ((a_kind != BWTA_BOOL) != (a_sgn != nullptr) || (a_kind != BWTA_BINARY) != (a_nz != nullptr))
+        return BWTA_ERR_INVALID_VALUE;
+    if (!std::isfinite(a_scale)) return BWTA_ERR_INVALID_VALUE;
+    if (y_transposed != 0 && y_transposed != 1) return BWTA_ERR_INVALID_VALUE;
+    const int64_t need = ldw_of(k);
+    if (lda_words < need || ldw_words < need) return BWTA_ERR_SHAPE;
+    if (ld_y < (y_transposed ? m : n)) return BWTA_ERR_SHAPE;
+    if (lda_words % 4 || ldw_words % 4 || (a_nz && !aligned16(a_nz)) || (a_sgn && !aligned16(a_sgn)) ||
+        !aligned16(w_sgn) || !aligned16(y) || ld_y % 8)
+        return BWTA_ERR_ALIGNMENT;
+    bwta_status_t st = check_device();
+    if (st != BWTA_OK) return st;
+    MatmulArgs a{};
+    a.a_sgn = a_sgn;
+    a.a_nz = a_nz;
+    a.b_sgn = w_sgn;
+    a.M = m;
+    a.N = n;
+    a.K = k;
+    a.lda = lda_words;
+    a.ldb = ldw_words;
+    a.nb = a.nh = 1;
+    a.y = y;
+    a.y_dt = y_dt;
+    a.ldy = ld_y;
+    a.y_trans = y_transposed;
+    a.col_scale = w_scale;
+    a.scalar = a_scale;
+    a.tile_n = o->tile_n;
+    a.cta_group = o->cta_group;
+    a.n_peers = n_peers;
+    for (int i = 0; i < n_peers; ++i) a.y_peers[i] = y_peers[i];
+    // only the tile kernel's 16-bit TMA-store epilogue stores to peers: skinny (GEMV) shapes and W1A1
+    // take other epilogues -> the caller gathers those with a collective
+    if (!matmul_tc_peers_ok(a)) return BWTA_ERR_UNSUPPORTED;
+    cudaError_t e = launch_matmul_tc(a, nullptr, 0, (cudaStream_t)stream);
+    if (e == cudaErrorNotSupported) return BWTA_ERR_UNSUPPORTED;
+    if (e != cudaSuccess) return cuda_fail(e);
+    g_last_design = BWTA_DESIGN_TCGEN05;
+    return BWTA_OK;
+}
+
+bwta_status_t bwta_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch, void* stream) {
+    if (flags == nullptr || world < 1 || world > MAX_PEERS + 1 || rank < 0 || rank >= world || epoch == 0)
+        return BWTA_ERR_INVALID_VALUE;
+    for (int r = 0; r < world; ++r) {
+        if (flags[r] == nullptr) return BWTA_ERR_INVALID_VALUE;
+        if (reinterpret_cast<uintptr_t>(flags[r]) % 4) return BWTA_ERR_ALIGNMENT;
+    }
+    bwta_status_t st = check_device();
+    if (st != BWTA_OK) return st;
+    cudaError_t e = launch_peer_barrier(flags, world, rank, epoch, (cudaStream_t)stream);
+    return e == cudaSuccess ? BWTA_OK : cuda_fail(e);
+}
+
+bwta_status_t bwta_ipc_handle(const void* ptr, void* handle, int64_t* offset) {
+    if (ptr == nullptr || handle == nullptr || offset == nullptr) return BWTA_ERR_INVALID_VALUE;
+    static_assert(sizeof(cudaIpcMemHandle_t) == BWTA_IPC_HANDLE_BYTES, "IPC handle size");
+    using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);  // cuMemGetAddressRange_v2
+    static GetRange get_range = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<GetRange>(fn);
+    }();
+    if (get_range == nullptr) return BWTA_ERR_UNSUPPORTED;
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, reinterpret_cast<unsigned long long>(ptr)) != 0) return BWTA_ERR_INVALID_VALUE;
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+    if (e != cudaSuccess) return cuda_fail(e);
+    std::memcpy(handle, &h, sizeof(h));
+    *offset = int64_t(reinterpret_cast<unsigned long long>(ptr) - base);
+    return BWTA_OK;
+}
+
+bwta_status_t bwta_ipc_open(const void* handle, int64_t offset, void** ptr) {
+    if (handle == nullptr || ptr == nullptr || offset < 0) return BWTA_ERR_INVALID_VALUE;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e);
+    *ptr = static_cast<char*>(base) + offset;
+    return BWTA_OK;
+}
+
+bwta_status_t bwta_ipc_close(void* ptr, int64_t offset) {
+    if (ptr == nullptr || offset < 0) return BWTA_ERR_INVALID_VALUE;
+    cudaError_t e = cudaIpcCloseMemHandle(static_cast<char*>(ptr) - offset);
+    return e == cudaSuccess ? BWTA_OK : cuda_fail(e);
+}
+
 bwta_status_t bwta_gemm_pack(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t a_kind, int64_t m,
                              int64_t lda_words, const uint32_t* w_sgn, int64_t n, int64_t ldw_words, int64_t k,
                              const float* w_scale, float a_scale, bwta_dtype_t y_dt, float out_scale,

@@ -113,6 +113,7 @@ struct PackArgs {
 cudaError_t launch_pack_rows(const PackArgs& a, cudaStream_t s);
 cudaError_t launch_pack_cols(const PackArgs& a, cudaStream_t s);
 constexpr int PACK_GROUP_MAX = 4;
+constexpr int MAX_PEERS = 7;  // bwta_gemm_peers: up to 8 GPUs of one NVSwitch node
 // several activation packs in one launch (falls back to one launch each)
 cudaError_t launch_pack_group(const PackArgs* a, const int* transpose, int n, cudaStream_t s);
 
@@ -161,6 +162,10 @@ struct MatmulArgs {
     uint32_t* ph_nz[3] = {nullptr, nullptr, nullptr};
     int64_t ph_ld[3] = {0, 0, 0};
     float ph_tp[3] = {0.f, 0.f, 0.f}, ph_tn[3] = {0.f, 0.f, 0.f};
+    // fused all-gather (bwta_gemm_peers): the epilogue also TMA-stores every output tile to the
+    // same position of each of these n_peers buffers (peer GPUs' Y, mapped into this process)
+    int n_peers = 0;
+    void* y_peers[MAX_PEERS] = {};
 };
 
 cudaError_t launch_matmul_cc(const MatmulArgs& a, cudaStream_t s);
@@ -217,6 +222,9 @@ cudaError_t launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t s);
 size_t matmul_tc_workspace(const MatmulArgs& a);
 bool matmul_tc_supported(const MatmulArgs& a);
 cudaError_t launch_matmul_tc(const MatmulArgs& a, void* ws, size_t ws_bytes, cudaStream_t s);
+// a.n_peers > 0: the tile kernel with the 16-bit TMA-store epilogue is the only path that stores to peers
+bool matmul_tc_peers_ok(const MatmulArgs& a);
+cudaError_t launch_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch, cudaStream_t s);
 // skinny products (smaller side <= 32 rows, gemv_tc.cu); launch_matmul_tc
 // routes eligible shapes there
 bool matmul_gemv_eligible(const MatmulArgs& a);

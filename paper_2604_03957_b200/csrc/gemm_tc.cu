@@ -134,8 +134,14 @@ struct TcParams {
     uint32_t* ph_nz[3];
     int64_t ph_ld[3];
     float ph_tp[3], ph_tn[3];
+    int n_peers;     // fused all-gather: the fast epilogue also stores every tile through PeerMaps::m[0 .. n_peers)
     float dot_bias;  // W1A1: K - K_processed (both operands binary; the generic epilogue adds it)
     int dbg;  // BWTA_TRACE builds only (tools/trace_gemm.py): 1 skip unpack math, 2 skip MMAs, 4 skip TMA, 8 skip A unpack, 16 skip B unpack, 32/64 wait flavour, 128 skip the B-code proxy fence
+};
+
+// output tensor maps of the peers' Y buffers (bwta_gemm_peers): the geometry of tmY at another base
+struct PeerMaps {
+    CUtensorMap m[MAX_PEERS];
 };
 
 __host__ __device__ constexpr int nplanes_of(int kind) { return kind == B_TERNARY ? 2 : 1; }
@@ -309,7 +315,8 @@ __device__ __forceinline__ void epi_tile_generic(const TcParams& p, const CUtens
 // column scales (c * 2^-12, 64 per chunk) when column-scaled; cr = the
 // thread's four row scales (rows 16b + 8i + lane/4) when row-scaled.
 template <int BN, bool BF16>
-__device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorMap& tmY, uint32_t tacc, uint8_t* stg0,
+__device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorMap& tmY, const PeerMaps& pm,
+                                              uint32_t tacc, uint8_t* stg0,
                                               const float* cs, bool col_scaled, const float (&cr)[4], int q, int h,
                                               int lane, int64_t mrow0, int nt, int eb, int eh, int tix, int& nstore) {
     constexpr int CW = 64;
@@ -376,8 +383,10 @@ __device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorM
         __syncwarp();
         TRACE(12, tix * 4 + i, tr);
         if (lane == 0) {
-            if (!p.out_trans) tma_store_4d(&tmY, stg, int(n0), int(mrow0 + q * 32), eh, eb);
-            else tma_store_4d(&tmY, stg, int(mrow0 + q * 32), int(n0), eh, eb);
+            const int c0s = p.out_trans ? int(mrow0 + q * 32) : int(n0), c1s = p.out_trans ? int(n0) : int(mrow0 + q * 32);
+            tma_store_4d(&tmY, stg, c0s, c1s, eh, eb);
+            // fused all-gather: the same staged chunk to every peer's Y (NVLink writes), one bulk group
+            for (int pi = 0; pi < p.n_peers; ++pi) tma_store_4d(&pm.m[pi], stg, c0s, c1s, eh, eb);
             bulk_commit();
         }
     }
@@ -549,7 +558,8 @@ __device__ __forceinline__ void epi_tile_pack(const TcParams& p, uint32_t tacc, 
 // variants are not compiled in, which shrinks the instruction footprint); EO = 2: only the fused
 // next-layer pack; EO = 1: the generic epilogue (f32 / i32 outputs, layouts TMA cannot store).
 template <int BN, int ES, int CG, int EO>
-__device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& tmY, uint32_t tmem_base, uint8_t* sOut,
+__device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& tmY, const PeerMaps& pm,
+                                         uint32_t tmem_base, uint8_t* sOut,
                                          float* sScale, uint64_t* tfull, uint64_t* tempty, int q, int h, int lane,
                                          int64_t tiles_per_entry, int64_t total, int rank, int64_t t0,
                                          int64_t tstep) {
@@ -604,10 +614,10 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
                               int64_t(eb) * p.po_bs + int64_t(eh) * p.po_hs);
         } else if (EO == 0 || (EO == 1 && ok)) {
             if (p.y_dt == DT_BF16)
-                epi_tile_fast<BN, true>(p, tmY, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix,
+                epi_tile_fast<BN, true>(p, tmY, pm, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix,
                                         nstore);
             else
-                epi_tile_fast<BN, false>(p, tmY, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix,
+                epi_tile_fast<BN, false>(p, tmY, pm, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix,
                                          nstore);
         } else if constexpr (EO == 1) {
             epi_tile_generic<BN, ES>(p, tmY, tacc, stg, q, hh, lane, mrow0, nt, eb, eh);
@@ -718,7 +728,7 @@ template <int BN, int CG, int KS, int EO, int KK = 0>
 __global__ void __launch_bounds__(NT, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
-                   const __grid_constant__ CUtensorMap tmY, TcParams p) {
+                   const __grid_constant__ CUtensorMap tmY, const __grid_constant__ PeerMaps pm, TcParams p) {
     using C = Cfg<BN, CG, KS>;
     constexpr int WPS = Stage<KS>::WPS;
     uint8_t* smem =
@@ -754,6 +764,7 @@ __global__ void __launch_bounds__(NT, 1)
         tma_prefetch_desc(&tmB0);
         if (b_planes == 2) tma_prefetch_desc(&tmB1);
         if (p.use_tma_store) tma_prefetch_desc(&tmY);
+        for (int pi = 0; pi < p.n_peers; ++pi) tma_prefetch_desc(&pm.m[pi]);
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&bready[s], 10 * CG);  // 4 A + 6 B unpack warps of every CTA of the pair
@@ -1023,10 +1034,10 @@ __global__ void __launch_bounds__(NT, 1)
         // ------------------------------ epilogue (warps 4-7 and 12-15) ------------------------------
         const int q = warp & 3, h = warp >= 12 ? 1 : 0;
         if (EO != 1 || p.y_dt == DT_F16 || p.y_dt == DT_BF16)
-            epilogue<BN, 2, CG, EO>(p, tmY, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
+            epilogue<BN, 2, CG, EO>(p, tmY, pm, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
                                 rank, t0, tstep);
         else
-            if constexpr (EO == 1) epilogue<BN, 4, CG, EO>(p, tmY, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
+            if constexpr (EO == 1) epilogue<BN, 4, CG, EO>(p, tmY, pm, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
                                 rank, t0, tstep);
     }
     TRACE(7, 0, warp == 4 && lane == 0);
@@ -1148,7 +1159,7 @@ TileChoice choose_tile(int64_t Mk, int64_t Nk, int64_t entries) {
 
 template <int BN, int CG, int KS, int EO, int KK = 0>
 cudaError_t launch_ks(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUtensorMap& mb0, const CUtensorMap& mb1,
-                      const CUtensorMap& my, const TcParams& p, cudaStream_t s) {
+                      const CUtensorMap& my, const PeerMaps& pm, const TcParams& p, cudaStream_t s) {
     using C = Cfg<BN, CG, KS>;
     auto kern = tc_gemm_kernel<BN, CG, KS, EO, KK>;
     static std::atomic<uint64_t> optin{0};  // per device
@@ -1156,13 +1167,15 @@ cudaError_t launch_ks(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUte
     const int64_t tiles = p.entries * int64_t(p.m_tiles) * p.n_tiles;
     const int64_t slots = num_sms() / CG;
     const int grid = int((tiles < slots ? tiles : slots) * CG);
-    return launch_pdl(kern, dim3(grid), dim3(NT), size_t(C::SMEM), s, CG, ma0, ma1, mb0, mb1, my, p);
+    return launch_pdl(kern, dim3(grid), dim3(NT), size_t(C::SMEM), s, CG, ma0, ma1, mb0, mb1, my, pm, p);
 }
 
 template <int BN, int CG>
 cudaError_t launch_cfg(int ks, const CUtensorMap& ma0, const CUtensorMap& ma1, const CUtensorMap& mb0,
-                       const CUtensorMap& mb1, const CUtensorMap& my, const TcParams& p, cudaStream_t s) {
+                       const CUtensorMap& mb1, const CUtensorMap& my, const PeerMaps& pm, const TcParams& p,
+                       cudaStream_t s) {
     const bool fast = !p.pack_out && p.use_tma_store && (p.y_dt == DT_F16 || p.y_dt == DT_BF16) && p.dot_bias == 0.f;
+    if (p.n_peers > 0 && !fast) return cudaErrorNotSupported;  // only the fast epilogue stores to peers
     // the heavy GEMM tiles (BN = 192, 256-K stages) get kinds fixed at compile time for the BWTA
     // linear's combinations: activations (ternary / bool) x binary weights, and the swapped pack
     const int kk = 1 + 3 * p.a_kind + p.b_kind;
@@ -1171,24 +1184,24 @@ cudaError_t launch_cfg(int ks, const CUtensorMap& ma0, const CUtensorMap& ma1, c
                        kk == 1 + 3 * B_BINARY + B_TERNARY);
     if (fast) {
         if constexpr (BN == 192) if (spec) {
-            if (kk == 1 + 3 * B_TERNARY + B_BINARY) return launch_ks<BN, CG, 256, 0, 1 + 3 * B_TERNARY + B_BINARY>(ma0, ma1, mb0, mb1, my, p, s);
-            if (kk == 1 + 3 * B_BOOL + B_BINARY) return launch_ks<BN, CG, 256, 0, 1 + 3 * B_BOOL + B_BINARY>(ma0, ma1, mb0, mb1, my, p, s);
-            return launch_ks<BN, CG, 256, 0, 1 + 3 * B_BINARY + B_TERNARY>(ma0, ma1, mb0, mb1, my, p, s);
+            if (kk == 1 + 3 * B_TERNARY + B_BINARY) return launch_ks<BN, CG, 256, 0, 1 + 3 * B_TERNARY + B_BINARY>(ma0, ma1, mb0, mb1, my, pm, p, s);
+            if (kk == 1 + 3 * B_BOOL + B_BINARY) return launch_ks<BN, CG, 256, 0, 1 + 3 * B_BOOL + B_BINARY>(ma0, ma1, mb0, mb1, my, pm, p, s);
+            return launch_ks<BN, CG, 256, 0, 1 + 3 * B_BINARY + B_TERNARY>(ma0, ma1, mb0, mb1, my, pm, p, s);
         }
-        return ks == 128 ? launch_ks<BN, CG, 128, 0>(ma0, ma1, mb0, mb1, my, p, s)
-                         : launch_ks<BN, CG, 256, 0>(ma0, ma1, mb0, mb1, my, p, s);
+        return ks == 128 ? launch_ks<BN, CG, 128, 0>(ma0, ma1, mb0, mb1, my, pm, p, s)
+                         : launch_ks<BN, CG, 256, 0>(ma0, ma1, mb0, mb1, my, pm, p, s);
     }
     if (p.pack_out) {
         if constexpr (BN == 192) if (spec) {
-            if (kk == 1 + 3 * B_TERNARY + B_BINARY) return launch_ks<BN, CG, 256, 2, 1 + 3 * B_TERNARY + B_BINARY>(ma0, ma1, mb0, mb1, my, p, s);
-            if (kk == 1 + 3 * B_BOOL + B_BINARY) return launch_ks<BN, CG, 256, 2, 1 + 3 * B_BOOL + B_BINARY>(ma0, ma1, mb0, mb1, my, p, s);
-            return launch_ks<BN, CG, 256, 2, 1 + 3 * B_BINARY + B_TERNARY>(ma0, ma1, mb0, mb1, my, p, s);
+            if (kk == 1 + 3 * B_TERNARY + B_BINARY) return launch_ks<BN, CG, 256, 2, 1 + 3 * B_TERNARY + B_BINARY>(ma0, ma1, mb0, mb1, my, pm, p, s);
+            if (kk == 1 + 3 * B_BOOL + B_BINARY) return launch_ks<BN, CG, 256, 2, 1 + 3 * B_BOOL + B_BINARY>(ma0, ma1, mb0, mb1, my, pm, p, s);
+            return launch_ks<BN, CG, 256, 2, 1 + 3 * B_BINARY + B_TERNARY>(ma0, ma1, mb0, mb1, my, pm, p, s);
         }
-        return ks == 128 ? launch_ks<BN, CG, 128, 2>(ma0, ma1, mb0, mb1, my, p, s)
-                         : launch_ks<BN, CG, 256, 2>(ma0, ma1, mb0, mb1, my, p, s);
+        return ks == 128 ? launch_ks<BN, CG, 128, 2>(ma0, ma1, mb0, mb1, my, pm, p, s)
+                         : launch_ks<BN, CG, 256, 2>(ma0, ma1, mb0, mb1, my, pm, p, s);
     }
-    return ks == 128 ? launch_ks<BN, CG, 128, 1>(ma0, ma1, mb0, mb1, my, p, s)
-                     : launch_ks<BN, CG, 256, 1>(ma0, ma1, mb0, mb1, my, p, s);
+    return ks == 128 ? launch_ks<BN, CG, 128, 1>(ma0, ma1, mb0, mb1, my, pm, p, s)
+                     : launch_ks<BN, CG, 256, 1>(ma0, ma1, mb0, mb1, my, pm, p, s);
 }
 
 }  // namespace
@@ -1228,7 +1241,18 @@ bool encode_planes(CUtensorMap* m, const uint32_t* base, int64_t ld, int64_t row
 }
 int kind_of(const uint32_t* sgn, const uint32_t* nz) { return (sgn && nz) ? B_TERNARY : (nz ? B_BOOL : B_BINARY); }
 
+bool matmul_tc_peers_ok(const MatmulArgs& a) {
+    // the 16-bit TMA-store epilogue of the tile kernel (launch_cfg's `fast` class) is the one that
+    // stores to peers; W1A1 (dot_bias) and the fused packs take other epilogues
+    const int es = 2;
+    return a.n_peers >= 0 && a.n_peers <= MAX_PEERS && !matmul_gemv_eligible(a) && matmul_tc_supported(a) &&
+           !a.pack_out && !a.po_heads && (a.y_dt == DT_F16 || a.y_dt == DT_BF16) && (a.a_nz || a.b_nz) &&
+           reinterpret_cast<uintptr_t>(a.y) % 16 == 0 && (uint64_t(a.ldy) * es) % 16 == 0 &&
+           (a.nb == 1 || (uint64_t(a.y_bs) * es) % 16 == 0) && (a.nh == 1 || (uint64_t(a.y_hs) * es) % 16 == 0);
+}
+
 cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s) {
+    if (a.n_peers > 0 && !matmul_tc_peers_ok(a)) return cudaErrorNotSupported;
     if (matmul_gemv_eligible(a)) return launch_matmul_gemv(a, s);
     const int64_t entries = a.nb * a.nh;
     const int64_t kw4 = kw4_of(a.K);
@@ -1254,6 +1278,7 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     // bit-plane tensor maps: plane 0 = sgn (binary/ternary) or nz (bool), plane 1 = nz (ternary)
     const int akind = kind_of(pl.a_sgn, pl.a_nz), bkind = kind_of(pl.b_sgn, pl.b_nz);
     CUtensorMap ma0, ma1, mb0, mb1, my;
+    PeerMaps pm;
     {
         const uint32_t* a0 = akind == B_BOOL ? pl.a_nz : pl.a_sgn;
         const uint32_t* a1 = akind == B_TERNARY ? pl.a_nz : a0;
@@ -1335,15 +1360,30 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     if (const char* dbg = getenv("BWTA_DBG")) p.dbg = atoi(dbg);
 #endif
         if (!ok) my = ma0;  // unused
+        if (a.n_peers > 0 && !ok) return cudaErrorNotSupported;
+        // peers: the same map at each peer buffer's base (the all-gather destinations)
+        p.n_peers = a.n_peers;
+        for (int pi = 0; pi < a.n_peers; ++pi) {
+            if (reinterpret_cast<uintptr_t>(a.y_peers[pi]) % 16 != 0) return cudaErrorInvalidValue;
+            const uint64_t dims[4] = {uint64_t(inner), uint64_t(outer), uint64_t(a.nh), uint64_t(a.nb)};
+            const uint64_t str[3] = {ldb_, hsb, bsb};
+            const uint32_t box_nt[4] = {64, 32, 1, 1};
+            const uint32_t box_t[4] = {32, 64, 1, 1};
+            if (!(p.out_trans ? encode(&pm.m[pi], CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, a.y_peers[pi], dims, str, box_t,
+                                       CU_TENSOR_MAP_SWIZZLE_NONE)
+                              : encode(&pm.m[pi], CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, a.y_peers[pi], dims, str, box_nt,
+                                       CU_TENSOR_MAP_SWIZZLE_128B)))
+                return cudaErrorInvalidValue;
+        }
     }
     if (cg == 2) {
-        if (bn == 192) return launch_cfg<192, 2>(ks, ma0, ma1, mb0, mb1, my, p, s);
-        if (bn == 128) return launch_cfg<128, 2>(ks, ma0, ma1, mb0, mb1, my, p, s);
-        return launch_cfg<64, 2>(ks, ma0, ma1, mb0, mb1, my, p, s);
+        if (bn == 192) return launch_cfg<192, 2>(ks, ma0, ma1, mb0, mb1, my, pm, p, s);
+        if (bn == 128) return launch_cfg<128, 2>(ks, ma0, ma1, mb0, mb1, my, pm, p, s);
+        return launch_cfg<64, 2>(ks, ma0, ma1, mb0, mb1, my, pm, p, s);
     }
-    if (bn == 192) return launch_cfg<192, 1>(ks, ma0, ma1, mb0, mb1, my, p, s);
-    if (bn == 128) return launch_cfg<128, 1>(ks, ma0, ma1, mb0, mb1, my, p, s);
-    return launch_cfg<64, 1>(ks, ma0, ma1, mb0, mb1, my, p, s);
+    if (bn == 192) return launch_cfg<192, 1>(ks, ma0, ma1, mb0, mb1, my, pm, p, s);
+    if (bn == 128) return launch_cfg<128, 1>(ks, ma0, ma1, mb0, mb1, my, pm, p, s);
+    return launch_cfg<64, 1>(ks, ma0, ma1, mb0, mb1, my, pm, p, s);
 }
 
 }  // namespace bwta

@@ -186,3 +186,93 @@ def gemm_nshard_overlap(a, w_local, w_scale_local: Optional[torch.Tensor], a_sca
 def _slice_packed(p, l0: int, l1: int):
     """Rows [l0, l1) of a Packed weight (a view of its planes)."""
     return type(p)(p.sgn[l0:l1], None if p.nz is None else p.nz[l0:l1], p.kind, p.cols)
+
+
+# ----------------------------------------------------------------------------
+# Fused all-gather over NVLink peer memory (SURVEY §8(e), the product path next to the NCCL baseline
+# above): every rank maps every other rank's Y^T buffer into its address space once (CUDA IPC), and
+# its GEMM epilogue stores each output tile of its N-shard block into all of them (bwta_gemm_peers)
+# -- the gather overlaps the math tile by tile with no collective launch; one bwta_peer_barrier
+# per step then makes all ranks' stores visible.  Y^T is double-buffered across steps, so a rank
+# never overwrites a buffer a peer may still be reading: step s writes buffer s % 2, and reaching
+# step s + 2's GEMM requires every peer to have passed step s + 1's barrier, i.e. to have finished
+# everything it enqueued on step s's buffer before that.
+# ----------------------------------------------------------------------------
+class PeerLayout:
+    """Byte layout of one rank's peer buffer: nbuf Y^T buffers [n_pad x M] (16-bit), then the
+    `world` uint32 barrier flags."""
+
+    def __init__(self, plan: NShardPlan, m: int, nbuf: int = 2, elem: int = 2):
+        if plan.chunks != 1:
+            raise ValueError("the fused gather stores each rank's whole block from one GEMM (chunks = 1)")
+        if m % 8:
+            raise ValueError("M must be a multiple of 8 (16-byte Y^T rows for the TMA stores)")
+        self.plan, self.m, self.nbuf, self.elem = plan, m, nbuf, elem
+        self.y_bytes = -(-plan.n_pad * m * elem // 256) * 256
+        self.flags_off = nbuf * self.y_bytes
+        self.total = self.flags_off + 256
+
+    def block_offset(self, step: int) -> int:
+        """Byte offset of this rank's Y^T block in buffer step % nbuf (the same in every rank's buffer)."""
+        r0, _ = self.plan.block(0)
+        return (step % self.nbuf) * self.y_bytes + r0 * self.m * self.elem
+
+
+class PeerAllGather:
+    """Y^T = gather over ranks of the N-sharded BWTA linear, stored by the GEMM epilogue straight
+    into every rank's buffer.  group: the process group the IPC handles are exchanged over (any
+    backend; the data path uses no collective).  One instance per (N, M) shape; close() unmaps."""
+
+    def __init__(self, plan: NShardPlan, m: int, device, out_dtype=torch.float16, group=None, nbuf: int = 2):
+        from . import ipc_handle, ipc_open
+        self.lay = PeerLayout(plan, m, nbuf)
+        self.plan, self.m, self.out_dtype, self.group = plan, m, out_dtype, group
+        self.buf = torch.zeros(self.lay.total, dtype=torch.uint8, device=device)
+        torch.cuda.synchronize(device)  # flags are zero before any peer can signal
+        mine = ipc_handle(self.buf)
+        world = plan.world
+        allh = [None] * world
+        if world > 1 or group is not None:
+            dist.all_gather_object(allh, mine, group=group)
+        else:
+            allh = [mine]
+        self._opened = []
+        self.bases = []
+        for r, (h, off) in enumerate(allh):
+            if r == plan.rank:
+                self.bases.append(self.buf.data_ptr())
+            else:
+                ptr = ipc_open(h, off)
+                self._opened.append((ptr, off))
+                self.bases.append(ptr)
+        self.epoch = 0
+        self.step = 0
+
+    def out(self, step: int) -> torch.Tensor:
+        """Y^T [N x M] of buffer step % nbuf (a view of this rank's buffer)."""
+        b = step % self.lay.nbuf
+        y = self.buf[b * self.lay.y_bytes:b * self.lay.y_bytes + self.plan.n_pad * self.m * 2]
+        return y.view(self.out_dtype).view(self.plan.n_pad, self.m)[:self.plan.n]
+
+    def __call__(self, a, w_local, w_scale_local: Optional[torch.Tensor], a_scale: float, stream=None,
+                 design: str = "auto", tile=None) -> torch.Tensor:
+        """One step: the local GEMM with its peer stores, then the barrier.  w_local: this rank's
+        weight rows (plan.local_rows()).  Returns this step's gathered Y^T [N x M]."""
+        from . import bwta_gemm_peers, bwta_peer_barrier
+        g0, g1 = self.plan.block(0)
+        off = self.lay.block_offset(self.step)
+        if g1 > g0:
+            peers = [b + off for r, b in enumerate(self.bases) if r != self.plan.rank]
+            bwta_gemm_peers(a, w_local, w_scale_local, a_scale, self.bases[self.plan.rank] + off, self.m, peers,
+                            out_dtype=self.out_dtype, y_transposed=True, design=design, stream=stream, tile=tile)
+        self.epoch += 1
+        bwta_peer_barrier([b + self.lay.flags_off for b in self.bases], self.plan.rank, self.epoch, stream=stream)
+        y = self.out(self.step)
+        self.step += 1
+        return y
+
+    def close(self):
+        from . import ipc_close
+        for ptr, off in self._opened:
+            ipc_close(ptr, off)
+        self._opened = []

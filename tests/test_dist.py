@@ -128,3 +128,25 @@ def test_nshard_gemm_and_head_shard_gloo(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     assert all(ok_g and ok_a for _, ok_g, ok_a in res), res
+
+
+def test_peer_layout_blocks_line_up():
+    """The fused gather's byte layout: each rank's block offset in buffer s is its NShardPlan rows
+    (the same offset in every rank's buffer, so peer stores land where the owner's would), 16-byte
+    aligned, buffers disjoint, flags after them."""
+    for n, m, world in ((1000, 256, 2), (11008, 2048, 8), (37, 8, 4), (4096, 2048, 1)):
+        for r in range(world):
+            plan = D.NShardPlan(n, world, r, 1)
+            lay = D.PeerLayout(plan, m, nbuf=2)
+            g0, g1 = plan.block(0)
+            for step in range(4):
+                off = lay.block_offset(step)
+                assert off % 16 == 0
+                assert off == (step % 2) * lay.y_bytes + g0 * m * 2
+                assert off + (g1 - g0) * m * 2 <= (step % 2 + 1) * lay.y_bytes
+            assert lay.y_bytes >= plan.n_pad * m * 2 and lay.flags_off == 2 * lay.y_bytes
+            assert lay.total >= lay.flags_off + 4 * world
+    with pytest.raises(ValueError):
+        D.PeerLayout(D.NShardPlan(100, 2, 0, 2), 64)    # chunked plans are NCCL-only
+    with pytest.raises(ValueError):
+        D.PeerLayout(D.NShardPlan(100, 2, 0, 1), 12)    # 16-byte Y^T rows

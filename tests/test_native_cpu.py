@@ -258,3 +258,44 @@ def test_gemm_x_validation(N):
     assert gx(ld_y=7) == 2
     assert gx(w=40) == 3
     assert gx(m=0) == 0
+
+
+def test_gemm_peers_and_barrier_validation(N):
+    """bwta_gemm_peers / bwta_peer_barrier / IPC: host validation before any device work."""
+    L = N.lib
+
+    def peers_call(n_peers=1, peers=(80,), **kw):
+        a = dict(a_sgn=16, a_nz=32, kind=2, m=64, lda=4, w=48, n=64, ldw=4, k=100, s_a=1.0, y=64, y_dt=0,
+                 ld_y=64, yt=1)
+        a.update(kw)
+        arr = (ctypes.c_void_p * max(1, len(peers)))(*peers)
+        return L.bwta_gemm_peers(a["a_sgn"], a["a_nz"], a["kind"], a["m"], a["lda"], a["w"], a["n"], a["ldw"],
+                                 a["k"], None, ctypes.c_float(a["s_a"]), a["y"], a["y_dt"], a["ld_y"], a["yt"], arr,
+                                 n_peers, None, None)
+    assert peers_call(n_peers=8, peers=(80,) * 8) == 1    # at most 7 peers (8 GPUs)
+    assert peers_call(n_peers=-1) == 1
+    assert peers_call(peers=(0,)) == 1                    # NULL peer
+    assert peers_call(peers=(72,)) == 3                   # peer not 16-byte aligned
+    assert peers_call(y_dt=2) == 4                        # f32 is not a TMA-store epilogue class
+    assert peers_call(y_dt=3) == 4
+    assert peers_call(ld_y=68) == 3                       # 16-byte Y rows
+    assert peers_call(y=72) == 3
+    assert peers_call(a_sgn=None) == 1
+    assert peers_call(k=(1 << 24) + 1) == 2
+    assert peers_call() == 4                              # valid, but no sm_100 device here
+    assert peers_call(n_peers=0, peers=()) == 4
+    bad = N.Opts()
+    bad.design = 1                                        # design (a) has no peer epilogue
+    arr = (ctypes.c_void_p * 1)(80)
+    assert L.bwta_gemm_peers(16, 32, 2, 64, 4, 48, 64, 4, 100, None, ctypes.c_float(1.0), 64, 0, 64, 1, arr, 1,
+                             ctypes.byref(bad), None) == 4
+    flags = (ctypes.c_void_p * 2)(64, 128)
+    assert L.bwta_peer_barrier(flags, 2, 2, 1, None) == 1          # rank out of range
+    assert L.bwta_peer_barrier(flags, 9, 0, 1, None) == 1          # world > 8
+    assert L.bwta_peer_barrier(flags, 2, 0, 0, None) == 1          # epochs start at 1
+    assert L.bwta_peer_barrier((ctypes.c_void_p * 2)(64, 130), 2, 0, 1, None) == 3
+    assert L.bwta_peer_barrier(None, 2, 0, 1, None) == 1
+    assert L.bwta_peer_barrier(flags, 2, 1, 1, None) == 4          # valid, no device
+    assert L.bwta_ipc_handle(None, None, None) == 1
+    assert L.bwta_ipc_open(None, 0, None) == 1
+    assert L.bwta_ipc_close(None, 0) == 1
