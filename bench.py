@@ -119,12 +119,17 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def graph_of(fn, stream):
-    """Capture fn (after one eager warm-up run) into a CUDA graph."""
+def graph_of(fn, stream, pre=None):
+    """Capture fn (after one eager warm-up run) into a CUDA graph; pre() runs on the host before
+    each of the two calls (e.g. to select which output buffer the captured call uses)."""
     with torch.cuda.stream(stream):
+        if pre:
+            pre()
         fn()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
+    if pre:
+        pre()
     with torch.cuda.graph(g, stream=stream):
         fn()
     torch.cuda.synchronize()
@@ -139,7 +144,8 @@ def flush_l2(buf):
 
 
 def time_graph(g, flush, reps, warmup, stream):
-    """Median / list of per-replay device times (ms), L2 flushed before each replay."""
+    """Median / list of per-replay device times (ms), L2 flushed before each replay.  g: a graph, or
+    a runner whose replay() cycles several (the double-buffered fused gather)."""
     ts = []
     with torch.cuda.stream(stream):
         for i in range(warmup + reps):
@@ -386,14 +392,18 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
             "oracle_sample": dict(X=X, Xf=Xf, R=R, P=P, Ws=Ws, s=s, heads=heads, D=D, batch=batch, seq=seq)}
 
 
-def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008), world=1, rank=0, chunks=2, group=None):
+def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008), world=1, rank=0, chunks=2, group=None,
+                  gather="peer"):
     """configs[2]: LLaMA-7B prefill linears, M = 2048 tokens, K = 4096, N = 4096 / 11008.
-    world > 1: each linear N-sharded over the ranks (dist.NShardPlan, `chunks` chunks per rank),
-    Y^T all-gathered chunk by chunk, overlapped with the next chunk's GEMM."""
+    world > 1: each linear N-sharded over the ranks, Y^T gathered on every rank:
+      gather "peer" (default): the GEMM epilogue stores every tile into each peer's Y^T over NVLink
+        (bwta_gemm_peers, dist.PeerAllGather, double-buffered) + one flag barrier per linear;
+      gather "nccl": dist.NShardPlan with `chunks` chunks per rank, NCCL all_gather_into_tensor of
+        each chunk overlapped with the next chunk's GEMM (the baseline)."""
     from paper_2604_03957_b200 import dist as D
     X = gen.activations((M, K), seed).to(dev)
     s_x = gen.act_scale(X)
-    ops, st, outs, ws16 = [], {}, [], {}
+    ops, st, outs, ws16, pgs, alt_outs = [], {}, [], {}, [], []
 
     def op_pack():
         st["xq"] = B.bwta_pack_act(X, s_x)
@@ -414,6 +424,19 @@ def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008), world=1, r
 
             def op_cc(wp=wp, sw=sw, y=y):  # design (a): LOP3 + POPC on CUDA cores
                 B.bwta_gemm(st["xq"], wp, sw, s_x, out=y, design="cuda_core")
+        elif gather == "peer":
+            op_b1 = op_cc = None
+            plan = D.NShardPlan(N, world, rank, 1)
+            rows = plan.local_rows()
+            wp = B.bwta_pack_weight(w[rows].contiguous().to(dev), mu=mu)
+            sw = s_w[rows].contiguous().to(dev)
+            pg = D.PeerAllGather(plan, M, dev, group=group if group is not None else torch.distributed.group.WORLD)
+            pgs.append(pg)
+            y = pg.out(0)
+            alt_outs.append(pg.out(1))
+
+            def op_g(wp=wp, sw=sw, pg=pg):
+                pg(st["xq"], wp, sw, s_x)
         else:
             op_b1 = op_cc = None
             plan = D.NShardPlan(N, world, rank, chunks)
@@ -433,10 +456,19 @@ def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008), world=1, r
     st["w16"] = {N: w.to(dev) for N, w in ws16.items()} if world == 1 and group is None else {}
     op_pack()
     smp = dict(X=X.cpu(), s_x=s_x, Ws=ws16, seed=seed)
-    return {"ops": ops, "inputs": {"X": X}, "outputs": outs, "cfg": CFGS["llama_prefill"](),
-            "oracle_sample": smp, "scaling": "strong",
-            "parallelism": f"N-shard x{world} ({chunks} chunks/rank, in-place all-gather overlapped)"
-            if (world > 1 or group is not None) else "single GPU"}
+    sharded = world > 1 or group is not None
+    W = {"ops": ops, "inputs": {"X": X}, "outputs": outs, "cfg": CFGS["llama_prefill"](),
+         "oracle_sample": smp, "scaling": "strong",
+         "parallelism": ("single GPU" if not sharded else
+                         f"N-shard x{world}, all-gather fused into the GEMM epilogue (peer TMA stores over NVLink "
+                         "+ flag barrier, no collective)" if gather == "peer" else
+                         f"N-shard x{world} ({chunks} chunks/rank, NCCL all-gather in place, overlapped)")}
+    if pgs:   # double-buffered Y^T: the step alternates buffers, so the bench alternates two graphs
+        def set_parity(p):
+            for pg in pgs:
+                pg.step = p
+        W.update(parities=2, set_parity=set_parity, outputs_par=[outs, alt_outs])
+    return W
 
 
 def llama_attn(B, dev, seed=404, heads=32, seq=2048, D=128):
@@ -542,10 +574,11 @@ def decode_attn(B, dev, seed=606, shapes=((1, 32, 2048, 128), (8, 32, 2048, 128)
     return {"ops": ops, "inputs": {}, "outputs": [], "cfg": cfg, "oracle_sample": None}
 
 
-def nshard_gemm(B, dev, seed=707, world=1, rank=0):
+def nshard_gemm(B, dev, seed=707, world=1, rank=0, chunks=2, group=None, gather="peer"):
     """configs[4]: the LLaMA-70B-shaped BWTA linear (K 8192, N 28672, M 2048 tokens) N-sharded across
     the ranks exactly like llama_prefill at N > 1 (strong scaling)."""
-    W = llama_prefill(B, dev, seed, M=2048, K=8192, Ns=(28672,), world=world, rank=rank)
+    W = llama_prefill(B, dev, seed, M=2048, K=8192, Ns=(28672,), world=world, rank=rank, chunks=chunks, group=group,
+                      gather=gather)
     W["cfg"] = CFGS["nshard_gemm"]()
     W["oracle_sample"] = None
     return W
@@ -764,6 +797,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline (oracle) leg")
     ap.add_argument("--ref-row-frac", type=float, default=1.0)
     ap.add_argument("--chunks", type=int, default=2, help="N-shard chunks per rank (N > 1 or --nshard)")
+    ap.add_argument("--gather", default="peer", choices=["peer", "nccl"],
+                    help="N-shard gather: peer = fused into the GEMM epilogue over NVLink, nccl = chunked NCCL "
+                         "all-gathers (baseline)")
     ap.add_argument("--nshard", action="store_true",
                     help="run the N-sharded path with its NCCL all-gathers even at N = 1 (a 1-rank communicator)")
     args = ap.parse_args()
@@ -819,6 +855,8 @@ def main():
             kw["group"] = torch.distributed.group.WORLD
         if "chunks" in inspect.signature(wl_fn).parameters:
             kw["chunks"] = args.chunks
+        if "gather" in inspect.signature(wl_fn).parameters:
+            kw["gather"] = args.gather
     W = wl_fn(B, dev, **kw)
     ops = W["ops"]
     scaling = W.get("scaling", "weak") if world > 1 or W.get("scaling") else "weak"
@@ -837,8 +875,18 @@ def main():
     # the step (incl. the NCCL all-gathers of the sharded path) is captured into a CUDA graph;
     # eager launches only if the capture fails (the host would otherwise bound the sharded step)
     use_graph = True
+    par = {"i": 0, "n": W.get("parities", 1)}
     try:
-        g_step = graph_of(step, stream)
+        if par["n"] == 1:
+            g_step = graph_of(step, stream)
+        else:   # one graph per output buffer, replayed alternately (the fused gather's double buffer)
+            gs = [graph_of(step, stream, pre=lambda p=p: W["set_parity"](p)) for p in range(par["n"])]
+
+            class _Cycle:
+                def replay(self):
+                    par["i"] = (par["i"] + 1) % par["n"]
+                    gs[par["i"]].replay()
+            g_step = _Cycle()
     except Exception as exc:  # pragma: no cover
         print(f"bench: CUDA-graph capture failed ({exc!r}); eager launches", file=sys.stderr)
         torch.cuda.synchronize()
@@ -961,7 +1009,8 @@ def main():
                     if outs:
                         if i >= 2:
                             stream.wait_event(ev_out_free[sl])
-                        for so, o in zip(stage_out[sl], outs):
+                        cur = W["outputs_par"][par["i"]] if (use_graph and "outputs_par" in W) else outs
+                        for so, o in zip(stage_out[sl], cur):
                             so.copy_(o, non_blocking=True)
                         ev_out_ready[sl].record(stream)
                 if outs:

@@ -257,15 +257,17 @@ BWTA_API bwta_status_t bwta_gemm_peers(const uint32_t* a_sgn, const uint32_t* a_
 
 /*
  * Cross-GPU barrier over flag arrays in device memory: flags[r] (host array of `world` device
- * pointers, valid in this process) is rank r's array of `world` uint32 slots, zero-initialised
- * before the first use.  One tiny kernel on `stream`: for every rank t it performs a system-scope
- * release store flags[t][rank] = epoch after a system-scope fence (so every store of the work
- * enqueued before it on this stream -- e.g. bwta_gemm_peers' peer stores -- is visible to rank t),
- * then waits with acquire loads until flags[rank][t] >= epoch for every t.  epoch >= 1 and grows by
- * one per barrier (the same sequence on every rank).  1 <= world <= 8, 0 <= rank < world.  A rank
- * that never arrives traps the kernel after 30 s (sticky CUDA error) instead of hanging.
+ * pointers, valid in this process) is rank r's array of `world` uint32 slots; count is this rank's
+ * own uint32 barrier count (device memory, not shared).  Both zero-initialised before the first
+ * use.  One tiny kernel on `stream`: epoch = *count + 1; for every rank t a system-scope release
+ * store flags[t][rank] = epoch after a system-scope fence (so every store of the work enqueued
+ * before it on this stream -- e.g. bwta_gemm_peers' peer stores -- is visible to rank t), then
+ * acquire loads until flags[rank][t] >= epoch for every t; then *count = epoch.  The epoch lives in
+ * device memory, so a CUDA graph that captured the call advances it on every replay.  Every rank
+ * makes the same sequence of calls.  1 <= world <= 8, 0 <= rank < world.  A rank that never
+ * arrives traps the kernel after 30 s (sticky CUDA error) instead of hanging.
  */
-BWTA_API bwta_status_t bwta_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch,
+BWTA_API bwta_status_t bwta_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t* count,
                                          void* stream);
 
 /* CUDA IPC for the peer mappings: the handle (BWTA_IPC_HANDLE_BYTES bytes, host memory) of the

@@ -260,11 +260,11 @@ def bwta_gemm_peers(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_sca
     _check(st, "bwta_gemm_peers")
 
 
-def bwta_peer_barrier(flag_ptrs, rank: int, epoch: int, stream=None) -> None:
+def bwta_peer_barrier(flag_ptrs, rank: int, count_ptr: int, stream=None) -> None:
     """Cross-GPU barrier (include/bwta.h bwta_peer_barrier): flag_ptrs[r] = device address of rank r's
-    uint32 flag array as mapped in this process."""
+    uint32 flag array as mapped in this process; count_ptr = this rank's uint32 barrier count."""
     arr = (ctypes.c_void_p * len(flag_ptrs))(*[ctypes.c_void_p(int(q)) for q in flag_ptrs])
-    _check(lib.bwta_peer_barrier(arr, len(flag_ptrs), int(rank), ctypes.c_uint32(epoch), _stream(stream)),
+    _check(lib.bwta_peer_barrier(arr, len(flag_ptrs), int(rank), ctypes.c_void_p(int(count_ptr)), _stream(stream)),
            "bwta_peer_barrier")
 
 

@@ -102,7 +102,7 @@ def _declare(L):
     L.bwta_gemm_peers.argtypes = [P, P, i32, i64, i64, P, i64, i64, i64, P, f32, P, i32, i64, i32,
                                   P, i32, OP, P]
     L.bwta_peer_barrier.restype = i32
-    L.bwta_peer_barrier.argtypes = [P, i32, i32, ctypes.c_uint32, P]
+    L.bwta_peer_barrier.argtypes = [P, i32, i32, P, P]
     L.bwta_ipc_handle.restype = i32
     L.bwta_ipc_handle.argtypes = [P, P, ctypes.POINTER(i64)]
     L.bwta_ipc_open.restype = i32

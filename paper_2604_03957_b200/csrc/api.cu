@@ -492,16 +492,17 @@ bwta_status_t bwta_gemm_peers(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_
     return BWTA_OK;
 }
 
-bwta_status_t bwta_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch, void* stream) {
-    if (flags == nullptr || world < 1 || world > MAX_PEERS + 1 || rank < 0 || rank >= world || epoch == 0)
+bwta_status_t bwta_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t* count, void* stream) {
+    if (flags == nullptr || count == nullptr || world < 1 || world > MAX_PEERS + 1 || rank < 0 || rank >= world)
         return BWTA_ERR_INVALID_VALUE;
+    if (reinterpret_cast<uintptr_t>(count) % 4) return BWTA_ERR_ALIGNMENT;
     for (int r = 0; r < world; ++r) {
         if (flags[r] == nullptr) return BWTA_ERR_INVALID_VALUE;
         if (reinterpret_cast<uintptr_t>(flags[r]) % 4) return BWTA_ERR_ALIGNMENT;
     }
     bwta_status_t st = check_device();
     if (st != BWTA_OK) return st;
-    cudaError_t e = launch_peer_barrier(flags, world, rank, epoch, (cudaStream_t)stream);
+    cudaError_t e = launch_peer_barrier(flags, world, rank, count, (cudaStream_t)stream);
     return e == cudaSuccess ? BWTA_OK : cuda_fail(e);
 }
 

@@ -224,7 +224,7 @@ bool matmul_tc_supported(const MatmulArgs& a);
 cudaError_t launch_matmul_tc(const MatmulArgs& a, void* ws, size_t ws_bytes, cudaStream_t s);
 // a.n_peers > 0: the tile kernel with the 16-bit TMA-store epilogue is the only path that stores to peers
 bool matmul_tc_peers_ok(const MatmulArgs& a);
-cudaError_t launch_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t epoch, cudaStream_t s);
+cudaError_t launch_peer_barrier(uint32_t* const* flags, int world, int rank, uint32_t* count, cudaStream_t s);
 // skinny products (smaller side <= 32 rows, gemv_tc.cu); launch_matmul_tc
 // routes eligible shapes there
 bool matmul_gemv_eligible(const MatmulArgs& a);

@@ -200,7 +200,7 @@ def _slice_packed(p, l0: int, l1: int):
 # ----------------------------------------------------------------------------
 class PeerLayout:
     """Byte layout of one rank's peer buffer: nbuf Y^T buffers [n_pad x M] (16-bit), then the
-    `world` uint32 barrier flags."""
+    `world` uint32 barrier flags, then (at count_off, never written by peers) the barrier count."""
 
     def __init__(self, plan: NShardPlan, m: int, nbuf: int = 2, elem: int = 2):
         if plan.chunks != 1:
@@ -210,6 +210,7 @@ class PeerLayout:
         self.plan, self.m, self.nbuf, self.elem = plan, m, nbuf, elem
         self.y_bytes = -(-plan.n_pad * m * elem // 256) * 256
         self.flags_off = nbuf * self.y_bytes
+        self.count_off = self.flags_off + 128
         self.total = self.flags_off + 256
 
     def block_offset(self, step: int) -> int:
@@ -245,7 +246,6 @@ class PeerAllGather:
                 ptr = ipc_open(h, off)
                 self._opened.append((ptr, off))
                 self.bases.append(ptr)
-        self.epoch = 0
         self.step = 0
 
     def out(self, step: int) -> torch.Tensor:
@@ -265,8 +265,8 @@ class PeerAllGather:
             peers = [b + off for r, b in enumerate(self.bases) if r != self.plan.rank]
             bwta_gemm_peers(a, w_local, w_scale_local, a_scale, self.bases[self.plan.rank] + off, self.m, peers,
                             out_dtype=self.out_dtype, y_transposed=True, design=design, stream=stream, tile=tile)
-        self.epoch += 1
-        bwta_peer_barrier([b + self.lay.flags_off for b in self.bases], self.plan.rank, self.epoch, stream=stream)
+        bwta_peer_barrier([b + self.lay.flags_off for b in self.bases], self.plan.rank,
+                          self.bases[self.plan.rank] + self.lay.count_off, stream=stream)
         y = self.out(self.step)
         self.step += 1
         return y

@@ -290,12 +290,13 @@ def test_gemm_peers_and_barrier_validation(N):
     assert L.bwta_gemm_peers(16, 32, 2, 64, 4, 48, 64, 4, 100, None, ctypes.c_float(1.0), 64, 0, 64, 1, arr, 1,
                              ctypes.byref(bad), None) == 4
     flags = (ctypes.c_void_p * 2)(64, 128)
-    assert L.bwta_peer_barrier(flags, 2, 2, 1, None) == 1          # rank out of range
-    assert L.bwta_peer_barrier(flags, 9, 0, 1, None) == 1          # world > 8
-    assert L.bwta_peer_barrier(flags, 2, 0, 0, None) == 1          # epochs start at 1
-    assert L.bwta_peer_barrier((ctypes.c_void_p * 2)(64, 130), 2, 0, 1, None) == 3
-    assert L.bwta_peer_barrier(None, 2, 0, 1, None) == 1
-    assert L.bwta_peer_barrier(flags, 2, 1, 1, None) == 4          # valid, no device
+    assert L.bwta_peer_barrier(flags, 2, 2, 256, None) == 1        # rank out of range
+    assert L.bwta_peer_barrier(flags, 9, 0, 256, None) == 1        # world > 8
+    assert L.bwta_peer_barrier(flags, 2, 0, None, None) == 1       # no count
+    assert L.bwta_peer_barrier(flags, 2, 0, 258, None) == 3
+    assert L.bwta_peer_barrier((ctypes.c_void_p * 2)(64, 130), 2, 0, 256, None) == 3
+    assert L.bwta_peer_barrier(None, 2, 0, 256, None) == 1
+    assert L.bwta_peer_barrier(flags, 2, 1, 256, None) == 4        # valid, no device
     assert L.bwta_ipc_handle(None, None, None) == 1
     assert L.bwta_ipc_open(None, 0, None) == 1
     assert L.bwta_ipc_close(None, 0) == 1

@@ -87,12 +87,23 @@ def test_gemm_peers_unsupported_shapes_enqueue_nothing(B):
     assert not y0.any() and not y1.any()
 
 
-def test_peer_barrier_single_rank(B):
+def test_peer_barrier_single_rank_counts_in_device_memory(B):
+    """The epoch is read from and written back to device memory: eager calls and CUDA-graph replays
+    both advance it."""
     flags = torch.zeros(64, dtype=torch.int32, device="cuda")
-    for e in range(1, 6):
-        B.bwta_peer_barrier([flags.data_ptr()], 0, e)
+    count = flags[32:]
+    for _ in range(5):
+        B.bwta_peer_barrier([flags.data_ptr()], 0, count.data_ptr())
     torch.cuda.synchronize()
-    assert int(flags[0]) == 5
+    assert int(flags[0]) == 5 and int(count[0]) == 5
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        B.bwta_peer_barrier([flags.data_ptr()], 0, count.data_ptr(), stream=s)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert int(flags[0]) == 8 and int(count[0]) == 8
 
 
 def _port():
