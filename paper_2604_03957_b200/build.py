@@ -45,12 +45,15 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False, trace: bool = False) -> str:
-    """trace=True builds libbwta_trace.so with the -DBWTA_TRACE timeline hooks (tools only)."""
-    lib = LIB.replace("libbwta.so", "libbwta_trace.so") if trace else LIB
-    if not force and not trace and not stale():
+def build(force: bool = False, verbose: bool = False, trace: bool = False, variant: str = "",
+          defines: tuple = ()) -> str:
+    """trace=True builds libbwta_trace.so with the -DBWTA_TRACE timeline hooks (tools only);
+    variant="x" + defines builds libbwta_x.so with extra -D flags (A/B experiments, tools only)."""
+    tag = "_".join(t for t in ("trace" if trace else "", variant) if t)
+    lib = LIB.replace("libbwta.so", f"libbwta_{tag}.so") if tag else LIB
+    if not force and not tag and not stale():
         return LIB
-    objdir = os.path.join(PKG, "build_trace" if trace else "build")
+    objdir = os.path.join(PKG, f"build_{tag}" if tag else "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
@@ -59,6 +62,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
         cmd = [NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         if trace:
             cmd.append("-DBWTA_TRACE")
+        cmd += [f"-D{d}" for d in defines]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
@@ -81,4 +85,7 @@ def build(force: bool = False, verbose: bool = False, trace: bool = False) -> st
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv))
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    defs = tuple(a[2:] for a in sys.argv if a.startswith("-D"))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, trace="--trace" in sys.argv, variant=var,
+                defines=defs))

@@ -55,7 +55,13 @@ using namespace sm100;
 
 constexpr int BM = 128;     // MMA M (kernel-A rows per tile), cta_group::1
 constexpr int UMMA_KB = 32; // bytes of K per tcgen05.mma (K = 64 four-bit elements)
-constexpr int NT = 640;     // 20 warps
+constexpr int NT = 640;     // 20 warps (128-K stages)
+// 256-K stages: two kernel-A unpack groups (warps 16-19, 20-23) take alternate stages
+#ifndef BWTA_A_GROUPS
+#define BWTA_A_GROUPS 2
+#endif
+constexpr int A_GROUPS = BWTA_A_GROUPS;
+__host__ __device__ constexpr int nt_of(int ks) { return ks == 256 ? NT + 128 * (A_GROUPS - 1) : NT; }
 constexpr int OUT_BUF = 4096;
 constexpr int OUT_NBUF = 2;  // staging buffers per epilogue warp (fast path: store k overlaps the staging of k + 1)
 
@@ -92,6 +98,9 @@ extern __shared__ __align__(16) uint8_t smem_raw[];  // dynamic shared memory of
 constexpr int TRACE_EV = 16, TRACE_N = 64;
 constexpr int TRACE_BYTES = TRACE_EV * TRACE_N * 8;
 __device__ unsigned long long g_trace[2][TRACE_EV][TRACE_N];
+#define TRACE_EPI(ev, idx, cond) \
+    do {                         \
+    } while (0)  // epilogue-internal hooks 12-15 (slots now used by the MMA issuer)
 #define TRACE(ev, idx, cond)                                                                          \
     do {                                                                                              \
         if ((cond) && (idx) < TRACE_N)                                                                \
@@ -101,6 +110,9 @@ __device__ unsigned long long g_trace[2][TRACE_EV][TRACE_N];
 constexpr int TRACE_BYTES = 0;  // (dynamic smem then starts with the operand ring)
 #define TRACE(ev, idx, cond) \
     do {                     \
+    } while (0)
+#define TRACE_EPI(ev, idx, cond) \
+    do {                         \
     } while (0)
 #endif
 
@@ -136,6 +148,9 @@ struct TcParams {
     float ph_tp[3], ph_tn[3];
     int n_peers;     // fused all-gather: the fast epilogue also stores every tile through PeerMaps::m[0 .. n_peers)
     float dot_bias;  // W1A1: K - K_processed (both operands binary; the generic epilogue adds it)
+    int pf_on;                // L2 prefetch of the operand planes at kernel start
+    const void* pf_ptr[4];    // plane spans (A0, A1, B0, B1; null / 0 bytes: skip), 16-byte aligned
+    uint64_t pf_bytes[4];
     int dbg;  // BWTA_TRACE builds only (tools/trace_gemm.py): 1 skip unpack math, 2 skip MMAs, 4 skip TMA, 8 skip A unpack, 16 skip B unpack, 32/64 wait flavour, 128 skip the B-code proxy fence
 };
 
@@ -359,10 +374,10 @@ __device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorM
                 }
             }
             if (b == 0) {
-                TRACE(13, tix * 4 + i, tr);
+                TRACE_EPI(13, tix * 4 + i, tr);
                 if (lane == 0) bulk_wait_read<OUT_NBUF - 1>();  // the store that last used this buffer has read it
                 __syncwarp();
-                TRACE(14, tix * 4 + i, tr);
+                TRACE_EPI(14, tix * 4 + i, tr);
             }
 #pragma unroll
             for (int gp = 0; gp < 4; ++gp) {
@@ -377,11 +392,11 @@ __device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorM
                                       pk[4 * gp + 3]);
                 }
             }
-            if (b == 0) TRACE(15, tix * 4 + i, tr);
+            if (b == 0) TRACE_EPI(15, tix * 4 + i, tr);
         }
         fence_proxy_async_smem();
         __syncwarp();
-        TRACE(12, tix * 4 + i, tr);
+        TRACE_EPI(12, tix * 4 + i, tr);
         if (lane == 0) {
             const int c0s = p.out_trans ? int(mrow0 + q * 32) : int(n0), c1s = p.out_trans ? int(n0) : int(mrow0 + q * 32);
             tma_store_4d(&tmY, stg, c0s, c1s, eh, eb);
@@ -725,7 +740,7 @@ __device__ __forceinline__ uint64_t smem_desc_stage(uint32_t saddr) {
 // KK = 0: operand kinds read from the parameters; KK = 1 + 3 * a_kind + b_kind: fixed at compile
 // time (the common BWTA combinations), so the other unpack variants are not compiled in
 template <int BN, int CG, int KS, int EO, int KK = 0>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(nt_of(KS), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
                    const __grid_constant__ CUtensorMap tmY, const __grid_constant__ PeerMaps pm, TcParams p) {
@@ -784,7 +799,8 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();               // CTA-local smem order (TMEM address slot, barrier inits)
     if (CG == 2) cluster_sync();   // the pair: relaxed arrive, tcgen05 fences order TMEM
     tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_base_ = *tmem_slot;
+    const uint32_t tmem_base = tmem_base_;
     if (warp >= 4 && warp < 8) {
         // UE8M0 scale factors = 1.0 (0x7F) in columns SF_COL .. SF_COL + 15 of every lane
         uint32_t ones[16];
@@ -797,15 +813,33 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();               // CTA-local smem order (TMEM address slot, barrier inits)
     if (CG == 2) cluster_sync();   // the pair: relaxed arrive, tcgen05 fences order TMEM
     tc_fence_after();
+    const int64_t tiles_per_entry = int64_t(p.m_tiles) * p.n_tiles;
+    const int64_t total = p.entries * tiles_per_entry;
+    const int64_t t0 = blockIdx.x / CG, tstep = gridDim.x / CG;  // persistent over pair-tiles
+    // L2 prefetch of the operand planes, each CTA one contiguous 1/gridDim share of every plane's
+    // span: with cold operands the ring (STAGES slices in flight per CTA) would otherwise wait a
+    // DRAM round trip per few slices; one bulk request per plane and CTA turns that latency chain
+    // into a bandwidth-bound burst without adding per-row TMA work (tensor-box prefetches of the
+    // 32-byte rows measured much slower: the TMA unit's row rate is a co-limit of the mainloop).
+    // Issued before griddepcontrol.wait: a hint only (L2 is the coherence point).
+    if (warp == 0 && lane == 0 && p.pf_on) {
+#pragma unroll 1
+        for (int i = 0; i < 4; ++i) {
+            const uint64_t span = p.pf_bytes[i];
+            if (!p.pf_ptr[i] || span == 0) continue;
+            const uint64_t share = ((span + gridDim.x - 1) / gridDim.x + 15) & ~uint64_t(15);
+            const uint64_t off = share * blockIdx.x;
+            if (off >= span) continue;
+            const uint64_t len = (span - off < share ? ((span - off) & ~uint64_t(15)) : share);
+            if (len) bulk_prefetch_l2(static_cast<const uint8_t*>(p.pf_ptr[i]) + off, uint32_t(len));
+        }
+    }
+
     // prologue done (smem barriers, TMEM, descriptor prefetch): let the next
     // kernel start its own, then wait for our inputs (predecessor grid)
     pdl_launch_dependents();
     pdl_wait();
     TRACE(0, 0, threadIdx.x == 0);
-
-    const int64_t tiles_per_entry = int64_t(p.m_tiles) * p.n_tiles;
-    const int64_t total = p.entries * tiles_per_entry;
-    const int64_t t0 = blockIdx.x / CG, tstep = gridDim.x / CG;  // persistent over pair-tiles
 
     if (warp == 0) {
         // ------------------------------ TMA producer ------------------------------
@@ -859,6 +893,7 @@ __global__ void __launch_bounds__(NT, 1)
         // ------------------------------ MMA issuer (leader CTA) ------------------------------
         if (leader) {
             constexpr uint32_t idesc = idesc_mxf4(BM * CG, BN);
+            const uint32_t tmem_base = __shfl_sync(0xffffffffu, tmem_base_, 0);  // warp-uniform
             const uint32_t sfa = tmem_base + uint32_t(C::SF_COL), sfb = tmem_base + uint32_t(C::SF_COL + 8);
             int stage = 0;
             uint32_t phase = 0;
@@ -872,6 +907,7 @@ __global__ void __launch_bounds__(NT, 1)
                 const uint32_t d = tmem_base + uint32_t(acc * BN);
                 for (int kb = 0; kb < p.num_kb; ++kb) {
 #ifdef BWTA_TRACE
+                    TRACE(12, it, lane == 0);
                     if (!(p.dbg & 256))
 #endif
                     kwait(&bready[stage], phase, p.dbg);
@@ -882,22 +918,24 @@ __global__ void __launch_bounds__(NT, 1)
 #ifdef BWTA_TRACE
                     skip_mma = (p.dbg & 2) != 0;
 #endif
-                    if (lane == 0 && skip_mma) {
-                        if (CG == 1) tc_commit(&empty[stage]);
-                        else tc_commit2_mc(&empty[stage], 0x3);
-                    } else if (lane == 0) {
-                        const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
-                        if (KS == 256 && p.a_tmem) {
-                            const uint32_t a0 = tmem_base + uint32_t(C::A_COL + sa * 32);
+                    const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+                    if (KS == 256 && p.a_tmem) {
+                        // the whole warp issues (elect.sync inside): operands stay in uniform registers
+                        const uint32_t a0 = tmem_base + uint32_t(C::A_COL + sa * 32);
+                        if (!skip_mma) {
 #pragma unroll
                             for (int k = 0; k < Stage<KS>::NMMA; ++k) {
                                 const uint64_t bd = smem_desc_stage<KS>(b0 + k * UMMA_KB);
-                                if (CG == 1) mma_mxf4_ts(d, a0 + 8 * k, bd, idesc, sfa, sfb, (kb | k) != 0);
-                                else mma_mxf4_ts_cg2(d, a0 + 8 * k, bd, idesc, sfa, sfb, (kb | k) != 0);
+                                if (CG == 1) mma_mxf4_ts_w(d, a0 + 8 * k, bd, idesc, sfa, sfb, (kb | k) != 0);
+                                else mma_mxf4_ts_cg2_w(d, a0 + 8 * k, bd, idesc, sfa, sfb, (kb | k) != 0);
                             }
-                            // (the A code stage is released by the same commit as the bit/B stage:
-                            // the A unpack warps wait on empty[] of the stage SA back)
-                        } else {
+                        }
+                        // (the A code stage is released by the same commit as the bit/B stage:
+                        // the A unpack warps wait on empty[] of the stage SA back)
+                        if (CG == 1) tc_commit_w(&empty[stage]);
+                        else tc_commit2_mc_w(&empty[stage], 0x3);
+                    } else {
+                        if (lane == 0 && !skip_mma) {
                             const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
 #pragma unroll
                             for (int k = 0; k < Stage<KS>::NMMA; ++k) {
@@ -907,9 +945,12 @@ __global__ void __launch_bounds__(NT, 1)
                                 else mma_mxf4_cg2(d, ad, bd, idesc, sfa, sfb, (kb | k) != 0);
                             }
                         }
-                        if (CG == 1) tc_commit(&empty[stage]);
-                        else tc_commit2_mc(&empty[stage], 0x3);
+                        if (lane == 0) {
+                            if (CG == 1) tc_commit(&empty[stage]);
+                            else tc_commit2_mc(&empty[stage], 0x3);
+                        }
                     }
+                    TRACE(13, it - 1, lane == 0);
                     __syncwarp();
                     if (++sa == C::SA) sa = 0;
                     if (++stage == C::STAGES) {
@@ -917,76 +958,61 @@ __global__ void __launch_bounds__(NT, 1)
                         phase ^= 1;
                     }
                 }
-                if (lane == 0) {
-                    if (CG == 1) tc_commit(&tfull[acc]);
-                    else tc_commit2_mc(&tfull[acc], 0x3);
-                }
+                if (CG == 1) tc_commit_w(&tfull[acc]);
+                else tc_commit2_mc_w(&tfull[acc], 0x3);
                 __syncwarp();
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
         }
     } else if (warp >= 16 && KS == 256 && p.a_tmem) {
-        // ------------------------------ unpack kernel-A rows into TMEM (warps 16-19) ------------------------------
-        // Software-pipelined: the codes of stage it are computed while the TMEM store of stage it - 1
-        // drains; then stage it - 1 is signalled (wait::st, bready) and stage it stored.  Thread ut owns
-        // kernel-A row ut = TMEM lane ut (warp w: lane quarter w & 3); A code stage it % SA.
-        const int ut = threadIdx.x - 512;
+        // ------------------------------ unpack kernel-A rows into TMEM (warps 16-23) ------------------------------
+        // A_GROUPS groups of 4 warps take alternate stages (group g: it = g mod A_GROUPS): one group's
+        // serial chain per stage (full wait, unpack, A-ring wait, tcgen05.st, wait::st, arrive) was the
+        // mainloop's critical path.  Thread ut owns kernel-A row ut = TMEM lane ut (warp
+        // w: lane quarter w & 3); A code stage it % SA.
+        const int grp = (warp - 16) >> 2;
+        const int ut = (warp & 3) * 32 + lane;
         const int kind = a_kind_;
         const int plane_bytes = BM * WPS * 4;
         const uint32_t bready_addr0 = CG == 2 ? mapa_smem(&bready[0], 0) : 0u;
-        int stage = 0, prev = -1;
-        uint32_t phase = 0;
-        int it = 0;
+        const uint32_t lane_base = tmem_base + (uint32_t(32 * (warp & 3)) << 16);
+        const int64_t n_it = ((total - t0 + tstep - 1) / tstep) * p.num_kb;
         uint32_t v[32];
-        for (int64_t t = t0; t < total; t += tstep) {
-            for (int kb = 0; kb < p.num_kb; ++kb, ++it) {
-                kwait(&full[stage], phase, p.dbg);
-                TRACE(10, it, ut == 0);
-                const uint32_t bits = smem_u32(sABits + stage * C::ABITS);
+        for (int64_t it = grp; it < n_it; it += A_GROUPS) {
+            const int stage = int(it % C::STAGES);
+            kwait(&full[stage], uint32_t((it / C::STAGES) & 1), p.dbg);
+            TRACE(10, it, ut == 0);
+            const uint32_t bits = smem_u32(sABits + stage * C::ABITS);
 #ifdef BWTA_TRACE
-                if (!(p.dbg & 9))
+            if (!(p.dbg & 9))
 #endif
-                unpack_row_regs(kind, bits + ut * 32, bits + plane_bytes + ut * 32, v);
-                if (prev >= 0) {  // stage it - 1 is in TMEM: signal it
-                    tmem_wait_st();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (CG == 1) mbar_arrive(&bready[prev]);
-                        else mbar_arrive_cluster(bready_addr0 + prev * 8);
-                    }
-                }
-                // A code stage sa was last read by the MMAs of stage it - SA, whose commit completes
-                // use (it - SA) / STAGES of empty[(it - SA) % STAGES] (one commit per stage frees both
-                // rings; SA <= STAGES, so that barrier cannot run a phase ahead)
-                const int sa = it % C::SA;
-                if (it >= C::SA
+            unpack_row_regs(kind, bits + ut * 32, bits + plane_bytes + ut * 32, v);
+            TRACE(14, it, ut == 0);
+            // A code stage sa was last read by the MMAs of stage it - SA, whose commit completes
+            // use (it - SA) / STAGES of empty[(it - SA) % STAGES] (one commit per stage frees both
+            // rings; SA <= STAGES, and that barrier cannot complete its next phase before the MMAs
+            // of stage it, which wait for these codes)
+            const int sa = int(it % C::SA);
+            if (it >= C::SA
 #ifdef BWTA_TRACE
-                    && !(p.dbg & 512)
+                && !(p.dbg & 512)
 #endif
-                ) {
-                    const int pit = it - C::SA;
-                    kwait(&empty[pit % C::STAGES], uint32_t((pit / C::STAGES) & 1), p.dbg);
-                }
-                tc_fence_after();
-                tmem_st_32x32b_x32(tmem_base + (uint32_t(32 * (warp & 3)) << 16) + uint32_t(C::A_COL + sa * 32), v);
-                TRACE(11, it, ut == 0);
-                prev = stage;
-                if (++stage == C::STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
+            ) {
+                const int64_t pit = it - C::SA;
+                kwait(&empty[pit % C::STAGES], uint32_t((pit / C::STAGES) & 1), p.dbg);
             }
-        }
-        if (prev >= 0) {
+            TRACE(15, it, ut == 0);
+            tc_fence_after();
+            tmem_st_32x32b_x32(lane_base + uint32_t(C::A_COL + sa * 32), v);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if (CG == 1) mbar_arrive(&bready[prev]);
-                else mbar_arrive_cluster(bready_addr0 + prev * 8);
+                if (CG == 1) mbar_arrive(&bready[stage]);
+                else mbar_arrive_cluster(bready_addr0 + stage * 8);
             }
+            TRACE(11, it, ut == 0);
         }
     } else if (warp >= 16 || (warp >= 8 && warp < 12) || warp == 2 || warp == 3) {
         // ------------------------------ unpack into shared memory ------------------------------
@@ -1167,7 +1193,7 @@ cudaError_t launch_ks(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUte
     const int64_t tiles = p.entries * int64_t(p.m_tiles) * p.n_tiles;
     const int64_t slots = num_sms() / CG;
     const int grid = int((tiles < slots ? tiles : slots) * CG);
-    return launch_pdl(kern, dim3(grid), dim3(NT), size_t(C::SMEM), s, CG, ma0, ma1, mb0, mb1, my, pm, p);
+    return launch_pdl(kern, dim3(grid), dim3(nt_of(KS)), size_t(C::SMEM), s, CG, ma0, ma1, mb0, mb1, my, pm, p);
 }
 
 template <int BN, int CG>
@@ -1356,6 +1382,31 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     // kernel-A codes go to TMEM (no shared-memory round trip for the 128-row operand) for 256-K
     // stages; measured 2-7 % faster than the shared-memory A path (tools/ab_atmem.py)
     p.a_tmem = ks == 256 ? 1 : 0;
+    // L2 prefetch spans of the four plane maps (A0, A1, B0, B1): from the base to the end of the
+    // last entry's last row; skipped when the span is more than twice the bytes the GEMM reads
+    // (strided views into a larger tensor) -- BWTA_L2_PREFETCH=0 turns it off (tools/cold_warm.py)
+    {
+        static const int pf_env = [] {
+            const char* e = getenv("BWTA_L2_PREFETCH");
+            return e ? atoi(e) : 1;
+        }();
+        p.pf_on = pf_env;
+        const uint32_t* bases[4] = {akind == B_BOOL ? pl.a_nz : pl.a_sgn, akind == B_TERNARY ? pl.a_nz : nullptr,
+                                    bkind == B_BOOL ? pl.b_nz : pl.b_sgn, bkind == B_TERNARY ? pl.b_nz : nullptr};
+        const int64_t lds[4] = {pl.lda, pl.lda, pl.ldb, pl.ldb}, rows[4] = {pl.Mk, pl.Mk, pl.Nk, pl.Nk};
+        const int64_t bss[4] = {pl.a_bs, pl.a_bs, pl.b_bs, pl.b_bs}, hss[4] = {pl.a_hs, pl.a_hs, pl.b_hs, pl.b_hs};
+        for (int i = 0; i < 4; ++i) {
+            p.pf_ptr[i] = nullptr;
+            p.pf_bytes[i] = 0;
+            if (!bases[i] || reinterpret_cast<uintptr_t>(bases[i]) % 16 != 0) continue;
+            const int64_t last = (a.nb - 1) * (a.nb > 1 ? bss[i] : 0) + (a.nh - 1) * (a.nh > 1 ? hss[i] : 0);
+            const int64_t span_w = last + rows[i] * lds[i];
+            const int64_t dense_w = a.nb * a.nh * rows[i] * lds[i];
+            if (last < 0 || span_w > 2 * dense_w) continue;
+            p.pf_ptr[i] = bases[i];
+            p.pf_bytes[i] = uint64_t(span_w) * 4;
+        }
+    }
 #ifdef BWTA_TRACE
     if (const char* dbg = getenv("BWTA_DBG")) p.dbg = atoi(dbg);
 #endif

@@ -43,7 +43,7 @@ for it in range(3):
     f(buf.ctypes.data)
 cnt = (buf != 0).sum(-1)
 names = ["start", "tma_issue", "unp_full", "unp_done", "mma_bready", "epi_tfull", "epi_done", "end_work", "exit",
-         "e_ld", "unpA_full", "unpA_done", "e_st", "e_cvt0", "e_wrd0", "e_stm0"]
+         "e_ld", "unpA_full", "unpA_done", "mma_pre", "mma_post", "unpA_math", "unpA_empty"]
 for c in range(2):
     t0 = int(buf[c][0][0])
     print(f"CTA {c}: counts", dict(zip(names, cnt[c][:len(names)].tolist())))
@@ -54,10 +54,11 @@ for c in range(2):
         ev[nm] = v
         if len(v):
             print(f"  {nm:11s}", " ".join(f"{x:6d}" for x in v[:24]))
-    for a_, b_ in (("tma_issue", "unp_full"), ("unp_full", "unp_done"), ("unp_done", "mma_bready")):
+    for a_, b_ in (("tma_issue", "unp_full"), ("unp_full", "unp_done"), ("unp_done", "mma_bready"),
+                   ("tma_issue", "unpA_full"), ("unpA_full", "unpA_done"), ("unpA_done", "mma_bready"), ("mma_pre", "mma_bready"), ("mma_bready", "mma_post"), ("unpA_full", "unpA_math"), ("unpA_math", "unpA_empty"), ("unpA_empty", "unpA_done")):
         if len(ev[a_]) and len(ev[b_]):
             n_ = min(len(ev[a_]), len(ev[b_]))
             print(f"  {a_}->{b_}: median {np.median(ev[b_][:n_] - ev[a_][:n_]):.0f} cycles")
-    for nm in ("tma_issue", "unp_done", "mma_bready"):
+    for nm in ("tma_issue", "unp_done", "unpA_full", "unpA_done", "mma_pre", "mma_bready", "mma_post"):
         if len(ev[nm]) > 2:
             print(f"  {nm} period: median {np.median(np.diff(ev[nm])):.0f} cycles")
