@@ -281,7 +281,9 @@ __global__ void __launch_bounds__(AP_NT, 1)
     } else if (warp == 1) {
         // ------------------------------ MMA issuer ------------------------------
         const uint32_t idesc_qk = idesc_mxf4(AP_BQ, AP_BK), idesc_pv = idesc_mxf4(AP_BQ, p.dhp);
-        const uint32_t sf = tmem + uint32_t(TM_SF);
+        // the whole warp issues (elect.sync inside the asm): operands stay in uniform registers
+        const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+        const uint32_t sf = tmem_u + uint32_t(TM_SF);
         int g = 0, sg = 0, pg = 0, ic = 0;
         // QK^T of K stage st into S buffer sb; the K stage is free again once these MMAs complete
         auto qk = [&](uint32_t qa, int st, int sb) {
@@ -289,10 +291,10 @@ __global__ void __launch_bounds__(AP_NT, 1)
             if (!(p.dbg & 4))
 #pragma unroll
             for (int k = 0; k < 2; ++k)
-                mma_mxf4(tmem + uint32_t(TM_S + sb * AP_BK), smem_desc_sw64(qa + 32 * k), smem_desc_sw64(kc + 32 * k),
-                         idesc_qk, sf, sf + 8, k);
-            tc_commit(&s_full[sb]);
-            tc_commit(&k_empty[st]);
+                mma_mxf4_w(tmem_u + uint32_t(TM_S + sb * AP_BK), smem_desc_sw64(qa + 32 * k), smem_desc_sw64(kc + 32 * k),
+                           idesc_qk, sf, sf + 8, k);
+            tc_commit_w(&s_full[sb]);
+            tc_commit_w(&k_empty[st]);
         };
         for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++ic) {
             const int qb = ic & 1;
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(AP_NT, 1)
                 wait_bar(&k_ready[st], uint32_t((g / AP_S) & 1));
                 wait_bar(&s_free[sb], uint32_t((sg >> 1) & 1) ^ 1u);
                 tc_fence_after();
-                if (lane == 0) qk(qa, st, sb);
+                qk(qa, st, sb);
                 __syncwarp();
             }
             // pass 2: QK^T of block j + 1 is issued before PV of block j (S is double-buffered)
@@ -315,10 +317,8 @@ __global__ void __launch_bounds__(AP_NT, 1)
                     wait_bar(&k_ready[st], uint32_t((gj / AP_S) & 1));
                     wait_bar(&s_free[sb], uint32_t((sgj >> 1) & 1) ^ 1u);
                     tc_fence_after();
-                    if (lane == 0) {
-                        qk(qa, st, sb);
-                        if (j == nblk - 1) tc_commit(&q_empty[qb]);  // the last read of this item's Q codes
-                    }
+                    qk(qa, st, sb);
+                    if (j == nblk - 1) tc_commit_w(&q_empty[qb]);  // the last read of this item's Q codes
                     __syncwarp();
                 }
                 if (j >= 1) {
@@ -327,17 +327,17 @@ __global__ void __launch_bounds__(AP_NT, 1)
                     wait_bar(&v_ready[vs], uint32_t((pg / AP_VS) & 1));
                     if (jj == 0) wait_bar(o_free, uint32_t(ic & 1) ^ 1u);
                     tc_fence_after();
-                    if (lane == 0) {
+                    {
                         const uint32_t pa = smem_u32(sP + pb * P_CODES);
                         const uint32_t vcd = smem_u32(sVc + vs * V_CODES);
                         if (!(p.dbg & 4))
 #pragma unroll
                         for (int k = 0; k < 2; ++k)
-                            mma_mxf4(tmem + uint32_t(TM_O), smem_desc_sw64(pa + 32 * k), smem_desc_sw64(vcd + 32 * k),
-                                     idesc_pv, sf, sf + 8, (jj | k) != 0);
-                        tc_commit(&p_free[pb]);
-                        tc_commit(&v_empty[vs]);
-                        if (jj == nblk - 1) tc_commit(o_full);
+                            mma_mxf4_w(tmem_u + uint32_t(TM_O), smem_desc_sw64(pa + 32 * k), smem_desc_sw64(vcd + 32 * k),
+                                       idesc_pv, sf, sf + 8, (jj | k) != 0);
+                        tc_commit_w(&p_free[pb]);
+                        tc_commit_w(&v_empty[vs]);
+                        if (jj == nblk - 1) tc_commit_w(o_full);
                     }
                     __syncwarp();
                     ++pg;

@@ -61,6 +61,10 @@ constexpr int NT = 640;     // 20 warps (128-K stages)
 #define BWTA_A_GROUPS 2
 #endif
 constexpr int A_GROUPS = BWTA_A_GROUPS;
+#ifndef BWTA_B_PAIR
+#define BWTA_B_PAIR 0
+#endif
+constexpr bool B_PAIR = BWTA_B_PAIR != 0;  // kernel-B unpack warps take two 256-K stages per iteration
 __host__ __device__ constexpr int nt_of(int ks) { return ks == 256 ? NT + 128 * (A_GROUPS - 1) : NT; }
 constexpr int OUT_BUF = 4096;
 constexpr int OUT_NBUF = 2;  // staging buffers per epilogue warp (fast path: store k overlaps the staging of k + 1)
@@ -161,22 +165,28 @@ struct PeerMaps {
 
 __host__ __device__ constexpr int nplanes_of(int kind) { return kind == B_TERNARY ? 2 : 1; }
 
-template <int BN, int CG, int KS = 256>
+#ifndef BWTA_SMEM_BUDGET
+#define BWTA_SMEM_BUDGET (210 * 1024 + 1280)
+#endif
+template <int BN, int CG, int KS = 256, int KK = 0>
 struct Cfg {
     using S = Stage<KS>;
+    // bit planes per operand: 2 unless the operand kinds are fixed at compile time (KK)
+    static constexpr int AP = KK ? nplanes_of((KK - 1) / 3) : 2;
+    static constexpr int BP = KK ? nplanes_of((KK - 1) % 3) : 2;
     static constexpr int BNC = BN / CG;          // kernel-B rows held (and unpacked) per CTA
     // E2M1 codes, 2 per byte; none for 256-K stages (kernel-A codes live in TMEM there), which
     // deepens the bit/B-code ring (the stage chain TMA -> unpack -> MMA -> commit is latency-bound)
     static constexpr int A_BYTES = KS == 256 ? 0 : BM * S::ROWB;
     static constexpr int B_BYTES = BNC * S::ROWB;
-    static constexpr int ABITS = 2 * BM * S::WPS * 4;  // up to 2 planes x WPS words per row
-    static constexpr int BBITS = 2 * BNC * S::WPS * 4;
+    static constexpr int ABITS = AP * BM * S::WPS * 4;  // AP planes x WPS words per row
+    static constexpr int BBITS = BP * BNC * S::WPS * 4;
     static constexpr int STAGE = A_BYTES + B_BYTES + ABITS + BBITS;
     static constexpr int OUT_BYTES = 8 * OUT_NBUF * OUT_BUF;                // OUT_NBUF staging buffers per epilogue warp
     static constexpr int SCALE_COLS = (BN + 127) / 128 * 64;                 // columns per epilogue warp
     static constexpr int SCALE_BYTES = 8 * SCALE_COLS * 4;                  // per-warp column scales
-    static constexpr int STAGES_FIT = (210 * 1024 - OUT_BYTES - SCALE_BYTES - TRACE_BYTES) / STAGE;
-    static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
+    static constexpr int STAGES_FIT = (BWTA_SMEM_BUDGET - 1280 - OUT_BYTES - SCALE_BYTES - TRACE_BYTES) / STAGE;
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr int BAR_BYTES = 256;
     static constexpr int SMEM = 1024 + STAGES * STAGE + OUT_BYTES + SCALE_BYTES + BAR_BYTES + TRACE_BYTES;
     // TMEM: two f32 accumulators of BN columns, then the UE8M0 scale factors
@@ -744,7 +754,7 @@ __global__ void __launch_bounds__(nt_of(KS), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
                    const __grid_constant__ CUtensorMap tmY, const __grid_constant__ PeerMaps pm, TcParams p) {
-    using C = Cfg<BN, CG, KS>;
+    using C = Cfg<BN, CG, KS, KK>;
     constexpr int WPS = Stage<KS>::WPS;
     uint8_t* smem =
         reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw + TRACE_BYTES) + 1023) & ~uintptr_t(1023));
@@ -1024,6 +1034,40 @@ __global__ void __launch_bounds__(nt_of(KS), 1)
         const int rows = is_a ? BM : C::BNC;
         const int plane_bytes = rows * WPS * 4;
         const uint32_t bready_addr0 = CG == 2 ? mapa_smem(&bready[0], 0) : 0u;
+        if (KS == 256 && B_PAIR && !is_a) {
+            // kernel-B, 256-K stages: two stages per iteration (one proxy fence and one pass of the
+            // loop's fixed waits for both), the pair signalled together
+            const int64_t n_it = ((total - t0 + tstep - 1) / tstep) * p.num_kb;
+            for (int64_t it = 0; it < n_it; it += 2) {
+                const bool two = it + 1 < n_it;
+                const int s0 = int(it % C::STAGES), s1 = int((it + 1) % C::STAGES);
+                kwait(&full[s0], uint32_t((it / C::STAGES) & 1), p.dbg);
+                TRACE(2, it, ut == 0);
+#ifdef BWTA_TRACE
+                if (!(p.dbg & 17))
+#endif
+                unpack_quads<KS, C::BNC, 192>(kind, smem_u32(sBBits + s0 * C::BBITS), smem_u32(sB + s0 * C::B_BYTES), ut);
+                if (two) {
+                    kwait(&full[s1], uint32_t(((it + 1) / C::STAGES) & 1), p.dbg);
+#ifdef BWTA_TRACE
+                    if (!(p.dbg & 17))
+#endif
+                    unpack_quads<KS, C::BNC, 192>(kind, smem_u32(sBBits + s1 * C::BBITS), smem_u32(sB + s1 * C::B_BYTES),
+                                                  ut);
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                TRACE(3, it, ut == 0);
+                if (lane == 0) {
+                    if (CG == 1) mbar_arrive(&bready[s0]);
+                    else mbar_arrive_cluster(bready_addr0 + s0 * 8);
+                    if (two) {
+                        if (CG == 1) mbar_arrive(&bready[s1]);
+                        else mbar_arrive_cluster(bready_addr0 + s1 * 8);
+                    }
+                }
+            }
+        } else {
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
@@ -1055,6 +1099,7 @@ __global__ void __launch_bounds__(nt_of(KS), 1)
                     phase ^= 1;
                 }
             }
+        }
         }
     } else if (warp >= 4) {
         // ------------------------------ epilogue (warps 4-7 and 12-15) ------------------------------
@@ -1186,7 +1231,7 @@ TileChoice choose_tile(int64_t Mk, int64_t Nk, int64_t entries) {
 template <int BN, int CG, int KS, int EO, int KK = 0>
 cudaError_t launch_ks(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUtensorMap& mb0, const CUtensorMap& mb1,
                       const CUtensorMap& my, const PeerMaps& pm, const TcParams& p, cudaStream_t s) {
-    using C = Cfg<BN, CG, KS>;
+    using C = Cfg<BN, CG, KS, KK>;
     auto kern = tc_gemm_kernel<BN, CG, KS, EO, KK>;
     static std::atomic<uint64_t> optin{0};  // per device
     if (cudaError_t e = ensure_smem_optin(kern, C::SMEM, optin); e != cudaSuccess) return e;
@@ -1388,7 +1433,7 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     {
         static const int pf_env = [] {
             const char* e = getenv("BWTA_L2_PREFETCH");
-            return e ? atoi(e) : 1;
+            return e ? atoi(e) : 0;  // off by default: measured neutral on C3 (profiles/r02g_l2_prefetch_ab.txt)
         }();
         p.pf_on = pf_env;
         const uint32_t* bases[4] = {akind == B_BOOL ? pl.a_nz : pl.a_sgn, akind == B_TERNARY ? pl.a_nz : nullptr,

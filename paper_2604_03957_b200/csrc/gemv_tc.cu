@@ -219,8 +219,10 @@ __global__ void __launch_bounds__(GV_NT, 1)
         }
     } else if (warp == 1) {
         // ------------------------------ MMA issuer ------------------------------
+        // the whole warp issues (elect.sync inside the asm): operands stay in uniform registers
         constexpr uint32_t idesc = idesc_mxf4(GV_BM, NB);
-        const uint32_t sfa = tmem_base + uint32_t(GV_SFCOL), sfb = tmem_base + uint32_t(GV_SFCOL + 8);
+        const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
+        const uint32_t sfa = tmem_u + uint32_t(GV_SFCOL), sfb = tmem_u + uint32_t(GV_SFCOL + 8);
         int c = 0;
         uint32_t cph = 0;
         int acc = 0;
@@ -228,17 +230,17 @@ __global__ void __launch_bounds__(GV_NT, 1)
         for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
             mbar_wait(&aempty[acc], aph ^ 1);
             tc_fence_after();
-            const uint32_t d = tmem_base + uint32_t(acc * NB);
+            const uint32_t d = tmem_u + uint32_t(acc * NB);
             for (int kb = 0; kb < p.num_kb; ++kb) {
                 mbar_wait(&cfull[c], cph);
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t a0 = tmem_base + uint32_t(GV_ACOL + c * 32);
+                {
+                    const uint32_t a0 = tmem_u + uint32_t(GV_ACOL + c * 32);
                     const uint32_t b0 = smem_u32(sB + c * C::B_BYTES);
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
-                        mma_mxf4_ts(d, a0 + 8 * k, smem_desc_sw128(b0 + 32 * k), idesc, sfa, sfb, (kb | k) != 0);
-                    tc_commit(&cempty[c]);
+                        mma_mxf4_ts_w(d, a0 + 8 * k, smem_desc_sw128(b0 + 32 * k), idesc, sfa, sfb, (kb | k) != 0);
+                    tc_commit_w(&cempty[c]);
                 }
                 __syncwarp();
                 if (++c == GV_CST) {
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(GV_NT, 1)
                     cph ^= 1;
                 }
             }
-            if (lane == 0) tc_commit(&afull[acc]);
+            tc_commit_w(&afull[acc]);
             __syncwarp();
             acc ^= 1;
             if (acc == 0) aph ^= 1;
