@@ -65,7 +65,10 @@ constexpr int A_GROUPS = BWTA_A_GROUPS;
 #define BWTA_B_PAIR 0
 #endif
 constexpr bool B_PAIR = BWTA_B_PAIR != 0;  // kernel-B unpack warps take two 256-K stages per iteration
-__host__ __device__ constexpr int nt_of(int ks) { return ks == 256 ? NT + 128 * (A_GROUPS - 1) : NT; }
+// (the fp16/bf16 TMA-store epilogue class only: the fused-pack and generic epilogues need more than
+// the 80 registers a 768-thread CTA leaves and spill -- BERT FFN1 + pack 17.3 -> 20.4 us)
+__host__ __device__ constexpr int a_groups(int ks, int eo) { return (ks == 256 && eo == 0) ? A_GROUPS : 1; }
+__host__ __device__ constexpr int nt_of(int ks, int eo) { return NT + 128 * (a_groups(ks, eo) - 1); }
 constexpr int OUT_BUF = 4096;
 constexpr int OUT_NBUF = 2;  // staging buffers per epilogue warp (fast path: store k overlaps the staging of k + 1)
 
@@ -750,7 +753,7 @@ __device__ __forceinline__ uint64_t smem_desc_stage(uint32_t saddr) {
 // KK = 0: operand kinds read from the parameters; KK = 1 + 3 * a_kind + b_kind: fixed at compile
 // time (the common BWTA combinations), so the other unpack variants are not compiled in
 template <int BN, int CG, int KS, int EO, int KK = 0>
-__global__ void __launch_bounds__(nt_of(KS), 1)
+__global__ void __launch_bounds__(nt_of(KS, EO), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
                    const __grid_constant__ CUtensorMap tmY, const __grid_constant__ PeerMaps pm, TcParams p) {
@@ -977,7 +980,7 @@ __global__ void __launch_bounds__(nt_of(KS), 1)
         }
     } else if (warp >= 16 && KS == 256 && p.a_tmem) {
         // ------------------------------ unpack kernel-A rows into TMEM (warps 16-23) ------------------------------
-        // A_GROUPS groups of 4 warps take alternate stages (group g: it = g mod A_GROUPS): one group's
+        // AG groups of 4 warps take alternate stages (group g: it = g mod AG): one group's
         // serial chain per stage (full wait, unpack, A-ring wait, tcgen05.st, wait::st, arrive) was the
         // mainloop's critical path.  Thread ut owns kernel-A row ut = TMEM lane ut (warp
         // w: lane quarter w & 3); A code stage it % SA.
@@ -989,7 +992,8 @@ __global__ void __launch_bounds__(nt_of(KS), 1)
         const uint32_t lane_base = tmem_base + (uint32_t(32 * (warp & 3)) << 16);
         const int64_t n_it = ((total - t0 + tstep - 1) / tstep) * p.num_kb;
         uint32_t v[32];
-        for (int64_t it = grp; it < n_it; it += A_GROUPS) {
+        constexpr int AG = a_groups(KS, EO);
+        for (int64_t it = grp; it < n_it; it += AG) {
             const int stage = int(it % C::STAGES);
             kwait(&full[stage], uint32_t((it / C::STAGES) & 1), p.dbg);
             TRACE(10, it, ut == 0);
@@ -1238,7 +1242,7 @@ cudaError_t launch_ks(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUte
     const int64_t tiles = p.entries * int64_t(p.m_tiles) * p.n_tiles;
     const int64_t slots = num_sms() / CG;
     const int grid = int((tiles < slots ? tiles : slots) * CG);
-    return launch_pdl(kern, dim3(grid), dim3(nt_of(KS)), size_t(C::SMEM), s, CG, ma0, ma1, mb0, mb1, my, pm, p);
+    return launch_pdl(kern, dim3(grid), dim3(nt_of(KS, EO)), size_t(C::SMEM), s, CG, ma0, ma1, mb0, mb1, my, pm, p);
 }
 
 template <int BN, int CG>
