@@ -948,7 +948,7 @@ def main():
     # sequence launched eagerly on the bench stream, L2 flushed before every step as in the timed
     # region, CUDA events recorded on that stream between consecutive ops; a device sleep ahead of
     # each step keeps the host's enqueue off the GPU timeline (no idle gaps inside the intervals)
-    in_step = {}
+    in_step, in_graph = {}, {}
     if world == 1 and not W.get("step") and W.get("parities", 1) == 1:
         samples = {op.name: [] for op in ops}
         with torch.cuda.stream(stream):
@@ -965,11 +965,36 @@ def main():
                     for i, op in enumerate(ops):
                         samples[op.name].append(evs[i].elapsed_time(evs[i + 1]))
         in_step = {k: statistics.median(v) for k, v in samples.items()}
+        # the same per-op intervals inside a CUDA graph of the step: external timing events captured
+        # between the ops (each event node also stands between two kernels, so no PDL overlap across
+        # it); replayed with the L2 flushed before every replay, as the timed steps are
+        try:
+            evs = [torch.cuda.Event(enable_timing=True, external=True) for _ in range(len(ops) + 1)]
+
+            def step_ev():
+                evs[0].record(stream)
+                for i, op in enumerate(ops):
+                    op.fn()
+                    evs[i + 1].record(stream)
+            g_ev = graph_of(step_ev, stream)
+            samples = {op.name: [] for op in ops}
+            with torch.cuda.stream(stream):
+                for r in range(max(args.steps, 5) + 2):
+                    flush_l2(flush)
+                    g_ev.replay()
+                    torch.cuda.synchronize()
+                    if r >= 2:
+                        for i, op in enumerate(ops):
+                            samples[op.name].append(evs[i].elapsed_time(evs[i + 1]))
+            in_graph = {k: statistics.median(v) for k, v in samples.items()}
+        except Exception as exc:  # pragma: no cover
+            print(f"bench: in-graph op timing unavailable ({exc!r})", file=sys.stderr)
+            torch.cuda.synchronize()
 
     # -------- roofline of the dominant KERNEL: the single-launch op with the largest time
     cands = [o for o in ops if o.launches == 1]
     dom = max(cands, key=lambda o: per_op[o.name])
-    t_dom = (in_step.get(dom.name) or per_op[dom.name]) / 1e3
+    t_dom = (in_graph.get(dom.name) or in_step.get(dom.name) or per_op[dom.name]) / 1e3
     if dom.kind == "pack" or args.workload.startswith("decode"):  # decode: the bit-plane stream bounds it
         roof = {"bound": "hbm", "achieved": dom.bytes / t_dom / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s"}
     else:
@@ -977,8 +1002,11 @@ def main():
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["kernel"] = dom.name
     roof["duration_us"] = t_dom * 1e6
-    roof["timing"] = ("in-step: CUDA events on the launching stream around the kernel inside the L2-flushed step "
-                      "sequence (median of the timed-step count)" if dom.name in in_step else
+    roof["timing"] = ("in-step, in-graph: CUDA events (external event nodes) on the launching stream around the "
+                      "kernel inside a CUDA graph of the step, L2 flushed before every replay (median of the "
+                      "timed-step count)" if dom.name in in_graph else
+                      "in-step: CUDA events on the launching stream around the kernel inside the L2-flushed step "
+                      "sequence, eager launches (median of the timed-step count)" if dom.name in in_step else
                       "isolated: graph of [L2 flush, kernel] x 20 minus graph of [L2 flush] x 20")
     roof["algorithmic"] = {"ops_per_launch": dom.ops, "bytes_per_launch": dom.bytes}
     roof["peak_source"] = (f"{pk['source']} bf16 {pk['bf16_tflops']} TFLOP/s x 4 (dense fp4/bf16 nominal ratio; "
@@ -1149,6 +1177,7 @@ def main():
             "speedup_vs_cublas_fp16": speed,
             "per_op_us": {k: v * 1e3 for k, v in per_op.items()},
             "in_step_us": {k: v * 1e3 for k, v in in_step.items()},
+            "in_graph_us": {k: v * 1e3 for k, v in in_graph.items()},
             "cublas_fp16_us": {k: v * 1e3 for k, v in cub_ms.items()},
             "other_designs_us": {k: {a: t * 1e3 for a, t in v.items()} for k, v in alt_ms.items()},
             "pack_GBps": pack_gbs, "extras": extras,

@@ -1,5 +1,6 @@
 // Internal declarations shared by the BWTA CUDA sources (not part of the ABI).
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -34,9 +35,15 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
     int n = 0;
-    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[n].val.programmaticStreamSerializationAllowed = 1;
-    ++n;
+    static const bool pdl_off = [] {  // BWTA_NO_PDL=1: plain stream order (A/B measurements only)
+        const char* e = getenv("BWTA_NO_PDL");
+        return e && atoi(e) != 0;
+    }();
+    if (!pdl_off) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
     if (cluster > 1) {
         attr[n].id = cudaLaunchAttributeClusterDimension;
         attr[n].val.clusterDim.x = cluster;

@@ -61,6 +61,14 @@ constexpr int NT = 640;     // 20 warps (128-K stages)
 #define BWTA_A_GROUPS 2
 #endif
 constexpr int A_GROUPS = BWTA_A_GROUPS;
+// L2 policy of the output tile stores (fast epilogue), A/B builds only: 0 default, 1 evict_first,
+// 2 evict_last, 3 evict_normal.  Measured on C3 N = 11008, graph of [L2 flush, GEMM] (the previous
+// output's write-back lands in the next flush, inside the graph): 60.3 / 59.3 / 53.6 / 59.9 us.
+// Not adopted: the configs[2] step did not move (82.1 vs 82.4 us), and evict_last lines can
+// outlive the bench's L2 flush (and, in a deep model, crowd out other tensors).
+#ifndef BWTA_Y_HINT
+#define BWTA_Y_HINT 0
+#endif
 #ifndef BWTA_B_PAIR
 #define BWTA_B_PAIR 0
 #endif
@@ -412,7 +420,15 @@ __device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorM
         TRACE_EPI(12, tix * 4 + i, tr);
         if (lane == 0) {
             const int c0s = p.out_trans ? int(mrow0 + q * 32) : int(n0), c1s = p.out_trans ? int(n0) : int(mrow0 + q * 32);
+#if BWTA_Y_HINT == 1
+            tma_store_4d_hint(&tmY, stg, c0s, c1s, eh, eb, l2_policy_evict_first());
+#elif BWTA_Y_HINT == 2
+            tma_store_4d_hint(&tmY, stg, c0s, c1s, eh, eb, l2_policy_evict_last());
+#elif BWTA_Y_HINT == 3
+            tma_store_4d_hint(&tmY, stg, c0s, c1s, eh, eb, l2_policy_evict_normal());
+#else
             tma_store_4d(&tmY, stg, c0s, c1s, eh, eb);
+#endif
             // fused all-gather: the same staged chunk to every peer's Y (NVLink writes), one bulk group
             for (int pi = 0; pi < p.n_peers; ++pi) tma_store_4d(&pm.m[pi], stg, c0s, c1s, eh, eb);
             bulk_commit();

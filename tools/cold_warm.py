@@ -53,5 +53,16 @@ for (m, k, n) in [(2048, 4096, 4096), (2048, 4096, 11008)]:
     # (e) the bench's per-op condition: graph of 20 x [flush, gemm] minus graph of 20 x [flush]
     fl = lambda: flush.view(torch.int64).max()
     te = (time_graph(lambda: (fl(), fn()), reps=10) - time_graph(fl, reps=10)) * 1e3
+    # (f) in-graph: flush, torch read of the operands, gemm  minus  flush, torch read
+    rd = lambda: [t.view(torch.int32).max() for t in (a.sgn, a.nz, wp.sgn)]
+    tf = (time_graph(lambda: (fl(), rd(), fn()), reps=10) - time_graph(lambda: (fl(), rd()), reps=10)) * 1e3
+    print(f"  in-graph flush+operands-read {tf:.2f}us ({ops/tf/1e6:.0f}T)")
+    # (g) in-graph: flush, zero Y (Y's lines resident and dirty), gemm; (h) write another buffer of Y's size
+    zy = lambda: y.zero_()
+    tg = (time_graph(lambda: (fl(), zy(), fn()), reps=10) - time_graph(lambda: (fl(), zy()), reps=10)) * 1e3
+    y2 = torch.empty_like(y)
+    z2 = lambda: y2.zero_()
+    th = (time_graph(lambda: (z2(), fn()), reps=10) - time_graph(z2, reps=10)) * 1e3
+    print(f"  in-graph flush+zero(Y) {tg:.2f}us   in-graph zero(other {y.numel()*2/1e6:.0f} MB) {th:.2f}us")
     print(f"{m}x{k}x{n} (BWTA_L2_PREFETCH={os.environ.get('BWTA_PF_KB', 'default')}): graph-flushed {te:.2f}us ({ops/te/1e6:.0f}T)  graph-warm {ta:.2f}us ({ops/ta/1e6:.0f}T)  flushed {tb:.2f}us ({ops/tb/1e6:.0f}T)  "
           f"single-warm {tc:.2f}us ({ops/tc/1e6:.0f}T)  flush+operands-read {td:.2f}us ({ops/td/1e6:.0f}T)", flush=True)
