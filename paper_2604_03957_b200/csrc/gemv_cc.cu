@@ -31,7 +31,16 @@ namespace {
 constexpr int GC_NT = 256;    // 8 warps per CTA
 // CTAs per SM: 3 (<= 85 registers) for 1-2 small rows -- more warps in flight and an even
 // spread of the 4-row tasks -- and 2 (<= 128 registers) for 3-4 rows
-__host__ __device__ constexpr int gc_ctas(int ms) { return ms <= 2 ? 3 : 2; }
+#ifndef GC_CTAS_1
+#define GC_CTAS_1 3
+#endif
+__host__ __device__ constexpr int gc_ctas(int ms) { return ms == 1 ? GC_CTAS_1 : ms <= 2 ? 3 : 2; }
+// large rows per warp task: 4 (2 for a ternary large side); GC_RW_BIN for a binary large side and
+// <= 2 small rows (more weight bytes in flight per warp)
+#ifndef GC_RW_BIN
+#define GC_RW_BIN 4
+#endif
+__host__ __device__ constexpr int gc_rw(int ms, bool l_nz) { return l_nz ? 2 : (ms <= 2 ? GC_RW_BIN : 4); }
 
 struct GcParams {
     const uint32_t *l_sgn, *l_nz;  // large side (kernel rows): null plane = absent
@@ -50,6 +59,7 @@ struct GcParams {
     // fused activation pack (the paper's in-kernel bitpack): the small side given as
     // values [S rows x K] (f16 / bf16 / f32, row stride ld_sx elements), quantized by every CTA
     // into shared-memory planes before the main loop (q = +1 iff x >= s_tp, -1 iff x <= s_ntn; R1-R3)
+    FastDiv div_tpe, div_nh;  // tasks per entry, heads (32-bit task indices: host checks total < 2^31)
     const void* sx;
     int sx_dt, s_kind;
     int64_t ld_sx, K;
@@ -63,6 +73,7 @@ __device__ __forceinline__ uint4 ldg_nc4(const uint32_t* p) {
                  : "l"(p));
     return v;
 }
+__device__ __forceinline__ uint32_t fdiv32(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
 __device__ __forceinline__ uint4 ldg4(const uint32_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 __device__ __forceinline__ uint32_t w_of(const uint4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
 
@@ -106,7 +117,7 @@ __global__ void __launch_bounds__(GC_NT, gc_ctas(MS)) cc_gemv_kernel(GcParams p)
     constexpr bool HOIST = !L_NZ;  // m = nz_small: popc(m) summed once per small row
     // rows per task: enough to reuse the small side's L1 loads, few enough for two iterations of
     // large-side loads in registers
-    constexpr int RW = 4 / (L_NZ ? 2 : 1);
+    constexpr int RW = gc_rw(MS, L_NZ);
     constexpr int NV = RW * MS;
     pdl_launch_dependents();
     pdl_wait();
@@ -172,104 +183,132 @@ __global__ void __launch_bounds__(GC_NT, gc_ctas(MS)) cc_gemv_kernel(GcParams p)
         }
         __syncthreads();
     }
-    for (int64_t task = gw; task < total; task += nwarps) {
-        const int64_t e = task / tasks_per_entry;
-        const int64_t r0 = (task % tasks_per_entry) * RW;
-        const int64_t eb = e / p.nh, eh = e % p.nh;
-        const int64_t loff = eb * p.l_bs + eh * p.l_hs, soff = eb * p.s_bs + eh * p.s_hs;
-        int32_t cneg[NV], cpos[HOIST ? MS : NV];  // popc(m & (sgn ^ sgn)), popc(m)
-#pragma unroll
-        for (int i = 0; i < NV; ++i) cneg[i] = 0;
-#pragma unroll
-        for (int i = 0; i < (HOIST ? MS : NV); ++i) cpos[i] = 0;
-        const uint32_t* lsg[RW];
-        const uint32_t* lnz[RW];
+    // The warp's work is a stream of (task, quad iteration) steps; the large-side loads of the next
+    // step -- possibly the next task's first -- are issued before the current step is counted, so
+    // the weight stream never waits on a task's reduction and store (a warp's last task no longer
+    // costs a full DRAM round trip of its own).
+    struct Pos {
+        int64_t r0, eb, eh;
+    };
+    auto pos_of = [&](int64_t task) {  // task -> (first large row, batch, head) without 64-bit divisions
+        const uint32_t t = uint32_t(task);
+        const uint32_t e = fdiv32(t, p.div_tpe);
+        const uint32_t eb = fdiv32(e, p.div_nh);
+        return Pos{int64_t(t - e * p.div_tpe.d) * RW, int64_t(eb), int64_t(e - eb * p.div_nh.d)};
+    };
+    auto large_ptrs = [&](const Pos& ps, const uint32_t* (&lsg)[RW], const uint32_t* (&lnz)[RW]) {
+        const int64_t r0 = ps.r0;
+        const int64_t loff = ps.eb * p.l_bs + ps.eh * p.l_hs;
 #pragma unroll
         for (int r = 0; r < RW; ++r) {
             const int64_t o = loff + (r0 + r < p.L ? r0 + r : r0) * p.ldl;
             lsg[r] = L_SGN ? p.l_sgn + o : nullptr;
             lnz[r] = L_NZ ? p.l_nz + o : nullptr;
         }
-        // large side quads of the RW rows for quad iteration qi (RW x 16 B in flight per plane);
-        // the next iteration's loads are issued before the current one is consumed
-        uint4 ls[RW], ln[RW];
-        auto load_large = [&](int qi, uint4 (&s_)[RW], uint4 (&n_)[RW]) {
-            const int q = qi * 32 + lane;
-            const bool qok = q < p.nq;
+    };
+    auto load_large = [&](const Pos& ps, int qi, uint4 (&s_)[RW], uint4 (&n_)[RW]) {
+        const uint32_t* lsg[RW];
+        const uint32_t* lnz[RW];
+        large_ptrs(ps, lsg, lnz);
+        const int64_t r0 = ps.r0;
+        const int q = qi * 32 + lane;
+        const bool qok = q < p.nq;
 #pragma unroll
-            for (int r = 0; r < RW; ++r) {
-                const bool ok = qok && r0 + r < p.L;
-                s_[r] = L_SGN && ok ? ldg_nc4(lsg[r] + 4 * q) : make_uint4(0, 0, 0, 0);
-                n_[r] = L_NZ && ok ? ldg_nc4(lnz[r] + 4 * q) : make_uint4(0, 0, 0, 0);
+        for (int r = 0; r < RW; ++r) {
+            const bool ok = qok && r0 + r < p.L;
+            s_[r] = L_SGN && ok ? ldg_nc4(lsg[r] + 4 * q) : make_uint4(0, 0, 0, 0);
+            n_[r] = L_NZ && ok ? ldg_nc4(lnz[r] + 4 * q) : make_uint4(0, 0, 0, 0);
+        }
+    };
+    int64_t task = gw;
+    int qi = 0;
+    uint4 ls[RW], ln[RW];
+    Pos cur = pos_of(task < total ? task : 0);
+    if (task < total) load_large(cur, 0, ls, ln);
+    int32_t cneg[NV], cpos[HOIST ? MS : NV];  // popc(m & (sgn ^ sgn)), popc(m)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) cneg[i] = 0;
+#pragma unroll
+    for (int i = 0; i < (HOIST ? MS : NV); ++i) cpos[i] = 0;
+    while (task < total) {
+        // the next step, and its loads in flight
+        const bool last_q = qi + 1 >= nqi;
+        const int64_t ntask = last_q ? task + nwarps : task;
+        const int nqi_ = last_q ? 0 : qi + 1;
+        uint4 lsn[RW], lnn[RW];
+        const Pos nxt = last_q ? pos_of(ntask < total ? ntask : task) : cur;
+        if (ntask < total) load_large(nxt, nqi_, lsn, lnn);
+        const int64_t r0 = cur.r0, eb = cur.eb, eh = cur.eh;
+        const int64_t soff = eb * p.s_bs + eh * p.s_hs;
+        const int q = qi * 32 + lane;
+        const bool qok = q < p.nq;
+        // small side quads (the same for every large row of the task; L1-resident)
+        uint4 ss[MS], sn[MS];
+#pragma unroll
+        for (int m = 0; m < MS; ++m) {
+            const bool ok = qok && m < p.S;
+            if (SQ) {
+                const int64_t o = int64_t(m) * 4 * p.nq + 4 * q;
+                ss[m] = ok ? *reinterpret_cast<const uint4*>(sp_sgn + o) : make_uint4(0, 0, 0, 0);
+                sn[m] = ok ? *reinterpret_cast<const uint4*>(sp_nz + o) : make_uint4(0, 0, 0, 0);
+            } else {
+                const int64_t o = soff + int64_t(m < p.S ? m : 0) * p.lds + 4 * q;
+                ss[m] = S_SGN && ok ? ldg4(p.s_sgn + o) : make_uint4(0, 0, 0, 0);
+                sn[m] = !ok ? make_uint4(0, 0, 0, 0) : S_NZ ? ldg4(p.s_nz + o) : make_uint4(~0u, ~0u, ~0u, ~0u);
             }
-        };
-        load_large(0, ls, ln);
-        for (int qi = 0; qi < nqi; ++qi) {
-            const int q = qi * 32 + lane;
-            const bool qok = q < p.nq;
-            uint4 lsn[RW], lnn[RW];
-            if (qi + 1 < nqi) load_large(qi + 1, lsn, lnn);
-            // small side quads (the same for every large row of the task; L1-resident)
-            uint4 ss[MS], sn[MS];
+        }
+        if (HOIST) {
 #pragma unroll
-            for (int m = 0; m < MS; ++m) {
-                const bool ok = qok && m < p.S;
-                if (SQ) {
-                    const int64_t o = int64_t(m) * 4 * p.nq + 4 * q;
-                    ss[m] = ok ? *reinterpret_cast<const uint4*>(sp_sgn + o) : make_uint4(0, 0, 0, 0);
-                    sn[m] = ok ? *reinterpret_cast<const uint4*>(sp_nz + o) : make_uint4(0, 0, 0, 0);
-                } else {
-                    const int64_t o = soff + int64_t(m < p.S ? m : 0) * p.lds + 4 * q;
-                    ss[m] = S_SGN && ok ? ldg4(p.s_sgn + o) : make_uint4(0, 0, 0, 0);
-                    sn[m] = !ok ? make_uint4(0, 0, 0, 0) : S_NZ ? ldg4(p.s_nz + o) : make_uint4(~0u, ~0u, ~0u, ~0u);
+            for (int m = 0; m < MS; ++m)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) cpos[m] += __popc(w_of(sn[m], i));
+        }
+#pragma unroll
+        for (int r = 0; r < RW; ++r)
+#pragma unroll
+            for (int m = 0; m < MS; ++m)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t mm = HOIST ? w_of(sn[m], i) : (w_of(sn[m], i) & w_of(ln[r], i));
+                    cneg[r * MS + m] += __popc(mm & (w_of(ss[m], i) ^ w_of(ls[r], i)));
+                    if (!HOIST) cpos[r * MS + m] += __popc(mm);
                 }
-            }
-            if (HOIST) {
+        if (last_q) {
+            int32_t v[NV];
 #pragma unroll
-                for (int m = 0; m < MS; ++m)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) cpos[m] += __popc(w_of(sn[m], i));
-            }
-#pragma unroll
-            for (int r = 0; r < RW; ++r)
-#pragma unroll
-                for (int m = 0; m < MS; ++m)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint32_t mm = HOIST ? w_of(sn[m], i) : (w_of(sn[m], i) & w_of(ln[r], i));
-                        cneg[r * MS + m] += __popc(mm & (w_of(ss[m], i) ^ w_of(ls[r], i)));
-                        if (!HOIST) cpos[r * MS + m] += __popc(mm);
+            for (int i = 0; i < NV; ++i) v[i] = (HOIST ? cpos[i % MS] : cpos[i]) - 2 * cneg[i];
+            const int32_t mine = warp_reduce_many<NV>(v, lane);
+            constexpr int SH = 5 - ilog2(NV);
+            if ((lane & ((1 << SH) - 1)) == 0) {
+                const int idx = lane >> SH, r = idx / MS, m = idx % MS;
+                const int64_t row = r0 + r;
+                if (row < p.L && m < p.S) {
+                    const int64_t off = eb * p.y_bs + eh * p.y_hs + row * p.y_rs + int64_t(m) * p.y_cs;
+                    if (p.y_dt == DT_I32) {
+                        reinterpret_cast<int32_t*>(p.y)[off] = mine;
+                    } else {
+                        const float c = p.scale ? __fmul_rn(__ldg(p.scale + (p.scale_on_rows ? row : m)), p.scalar)
+                                                : p.scalar;
+                        const float f = __fmul_rn(float(mine), c);  // exact int -> f32 (|dot| <= 2^24), R5
+                        if (p.y_dt == DT_F16) reinterpret_cast<__half*>(p.y)[off] = __float2half_rn(f);
+                        else if (p.y_dt == DT_BF16) reinterpret_cast<__nv_bfloat16*>(p.y)[off] = __float2bfloat16_rn(f);
+                        else reinterpret_cast<float*>(p.y)[off] = f;
                     }
-            if (qi + 1 < nqi) {
-#pragma unroll
-                for (int r = 0; r < RW; ++r) {
-                    ls[r] = lsn[r];
-                    ln[r] = lnn[r];
                 }
             }
-        }
-        int32_t v[NV];
 #pragma unroll
-        for (int i = 0; i < NV; ++i) v[i] = (HOIST ? cpos[i % MS] : cpos[i]) - 2 * cneg[i];
-        const int32_t mine = warp_reduce_many<NV>(v, lane);
-        constexpr int SH = 5 - ilog2(NV);
-        if ((lane & ((1 << SH) - 1)) == 0) {
-            const int idx = lane >> SH, r = idx / MS, m = idx % MS;
-            const int64_t row = r0 + r;
-            if (row < p.L && m < p.S) {
-                const int64_t off = eb * p.y_bs + eh * p.y_hs + row * p.y_rs + int64_t(m) * p.y_cs;
-                if (p.y_dt == DT_I32) {
-                    reinterpret_cast<int32_t*>(p.y)[off] = mine;
-                } else {
-                    const float c = p.scale ? __fmul_rn(__ldg(p.scale + (p.scale_on_rows ? row : m)), p.scalar)
-                                            : p.scalar;
-                    const float f = __fmul_rn(float(mine), c);  // exact int -> f32 (|dot| <= 2^24), R5
-                    if (p.y_dt == DT_F16) reinterpret_cast<__half*>(p.y)[off] = __float2half_rn(f);
-                    else if (p.y_dt == DT_BF16) reinterpret_cast<__nv_bfloat16*>(p.y)[off] = __float2bfloat16_rn(f);
-                    else reinterpret_cast<float*>(p.y)[off] = f;
-                }
-            }
+            for (int i = 0; i < NV; ++i) cneg[i] = 0;
+#pragma unroll
+            for (int i = 0; i < (HOIST ? MS : NV); ++i) cpos[i] = 0;
         }
+#pragma unroll
+        for (int r = 0; r < RW; ++r) {
+            ls[r] = lsn[r];
+            ln[r] = lnn[r];
+        }
+        task = ntask;
+        qi = nqi_;
+        cur = nxt;
     }
 }
 
@@ -330,7 +369,10 @@ cudaError_t launch_gemv_cc_fused(const void* x, int x_dt, int64_t ld_x, float tp
     p.s_ntn = ntn;
     const int g_sms = device_sms();
     const int ms = p.S == 1 ? 1 : (p.S == 2 ? 2 : 4);
-    int64_t grid = (p.L + 3) / 4 / (GC_NT / 32) + 1;
+    if ((p.L + gc_rw(ms, false) - 1) / gc_rw(ms, false) >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+    p.div_tpe = make_fastdiv(uint32_t((p.L + gc_rw(ms, false) - 1) / gc_rw(ms, false)));
+    p.div_nh = make_fastdiv(1);
+    int64_t grid = (p.L + gc_rw(ms, false) - 1) / gc_rw(ms, false) / (GC_NT / 32) + 1;
     if (grid > int64_t(g_sms) * gc_ctas(ms)) grid = int64_t(g_sms) * gc_ctas(ms);
     if (ms == 1) return launch_sq<1>(p, int(grid), s);
     if (ms == 2) return launch_sq<2>(p, int(grid), s);
@@ -341,6 +383,8 @@ bool matmul_gemv_cc_eligible(const MatmulArgs& a) {
     const int64_t small = a.M < a.N ? a.M : a.N;
     if (small < 1 || small > 4 || a.pack_out) return false;
     if (!a.a_nz && !a.b_nz) return false;  // one side carries the nz plane (activations always do)
+    const int64_t large = a.M < a.N ? a.N : a.M;
+    if (a.nb * a.nh * ((large + 1) / 2) >= (int64_t(1) << 31)) return false;  // 32-bit task indices
     // 16-byte word-quad loads: 16-byte aligned planes, leading dims and strides
     auto al = [](const uint32_t* q) { return q == nullptr || (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
     if (!al(a.a_sgn) || !al(a.a_nz) || !al(a.b_sgn) || !al(a.b_nz)) return false;
@@ -379,9 +423,13 @@ cudaError_t launch_matmul_gemv_cc(const MatmulArgs& a, cudaStream_t s) {
     p.scalar = a.scalar;
     const int lp = (p.l_sgn ? 1 : 0) | (p.l_nz ? 2 : 0), sp = (p.s_sgn ? 1 : 0) | (p.s_nz ? 2 : 0);
     const int g_sms = device_sms();
-    const int64_t warps = p.entries * ((p.L + 3) / 4);
-    int64_t grid = (warps + GC_NT / 32 - 1) / (GC_NT / 32);
     const int ms = p.S == 1 ? 1 : (p.S == 2 ? 2 : 4);
+    const int rw = gc_rw(ms, p.l_nz != nullptr);
+    const int64_t warps = p.entries * ((p.L + rw - 1) / rw);
+    if (warps >= (int64_t(1) << 31) || p.nh >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+    p.div_tpe = make_fastdiv(uint32_t((p.L + rw - 1) / rw));
+    p.div_nh = make_fastdiv(uint32_t(p.nh));
+    int64_t grid = (warps + GC_NT / 32 - 1) / (GC_NT / 32);
     if (grid > int64_t(g_sms) * gc_ctas(ms)) grid = int64_t(g_sms) * gc_ctas(ms);
     if (p.S == 1) return launch_l<1>(lp, sp, p, int(grid), s);
     if (p.S == 2) return launch_l<2>(lp, sp, p, int(grid), s);
