@@ -393,7 +393,7 @@ def bert_layer(B, dev, seed=202, batch=32, seq=128, hidden=768, heads=12, ffn=30
 
 
 def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008), world=1, rank=0, chunks=2, group=None,
-                  gather="peer"):
+                  gather="peer", grouped=True):
     """configs[2]: LLaMA-7B prefill linears, M = 2048 tokens, K = 4096, N = 4096 / 11008.
     world > 1: each linear N-sharded over the ranks, Y^T gathered on every rank:
       gather "peer" (default): the GEMM epilogue stores every tile into each peer's Y^T over NVLink
@@ -408,6 +408,38 @@ def llama_prefill(B, dev, seed=303, M=2048, K=4096, Ns=(4096, 11008), world=1, r
     def op_pack():
         st["xq"] = B.bwta_pack_act(X, s_x)
     ops.append(Op("pack_x", "pack", op_pack, 0, 2 * M * K + M * K / 4))
+    if grouped and world == 1 and group is None:
+        # both linears in ONE launch over the row-concatenated weights [W_4096; W_11008] (per-row mu
+        # keeps each block's own binarization; outputs = the two column blocks of one [M, 15104] Y):
+        # the same products bit for bit (tests/test_parity_gpu_large.py), 632 tiles in 8.5 rounds of
+        # the persistent grid instead of 2.4 + 6.3 rounds in two launches; cuBLAS gets the same
+        # concatenated GEMM as its baseline
+        ws = [gen.weights(N, K, seed + 1 + i) for i, N in enumerate(Ns)]
+        stats = [gen.weight_stats(w) for w in ws]
+        mu_cat = torch.cat([torch.full((N,), float(mu), dtype=torch.float32) for N, (mu, _) in zip(Ns, stats)])
+        wp = B.bwta_pack_weight(torch.cat(ws).to(dev), mu=mu_cat.to(dev))    # offline
+        sw = torch.cat([s for _, s in stats]).to(dev)
+        NT = sum(Ns)
+        y = torch.empty((M, NT), dtype=torch.float16, device=dev)
+
+        def op_g():
+            B.bwta_gemm(st["xq"], wp, sw, s_x, out=y)
+
+        def op_b1():
+            B.bwta_gemm(st["xq"], wp, sw, s_x, out=y, design="mma_b1")
+
+        def op_cc():
+            B.bwta_gemm(st["xq"], wp, sw, s_x, out=y, design="cuda_core")
+        w16 = torch.cat(ws).to(dev).half()
+        name = "gemm_n" + "+".join(str(N) for N in Ns)
+        ops.append(Op(name, "gemm", op_g, 2 * M * NT * K, M * K / 4 + NT * K / 8 + 4 * NT + 2 * M * NT,
+                      lambda: torch.nn.functional.linear(X, w16),
+                      alts={"design_a_cuda_core": op_cc, "prior_art_mma_b1": op_b1}))
+        op_pack()
+        smp = dict(X=X.cpu(), s_x=s_x, Ws={N: w for N, w in zip(Ns, ws)}, seed=seed)
+        return {"ops": ops, "inputs": {"X": X}, "outputs": [y], "cfg": CFGS["llama_prefill"](),
+                "oracle_sample": smp, "scaling": "strong",
+                "parallelism": "single GPU; both linears in one launch over the row-concatenated weights"}
     for i, N in enumerate(Ns):
         w = gen.weights(N, K, seed + 1 + i)
         mu, s_w = gen.weight_stats(w)

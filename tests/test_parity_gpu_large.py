@@ -259,3 +259,31 @@ def test_attention_full_size_sampled(B, cfg):
         ov = oracle.quantize_act(vs[e], "f16", sv, "ternary")
         ref = oracle.attn_pv(op[None], ov[None], beta, "f16", threads=4)[0]
         assert_out_equal(O_h[e][torch.from_numpy(rows)], ref, f"{cfg} pv entry {e}")
+
+
+@gpu
+def test_configs2_grouped_linears_sampled(B):
+    """configs[2] exactly as bench.py times it: both LLaMA-7B prefill linears (N 4096, 11008) in ONE
+    launch over the row-concatenated weights with a per-row mu vector (each block keeps its own
+    binarization); the two column blocks of Y equal the two separate launches bit for bit, and
+    sampled output channels of each block equal the oracle."""
+    M, K, Ns = 2048, 4096, (4096, 11008)
+    x = gen.activations((M, K), 303)
+    s_a = gen.act_scale(x)
+    ws = [gen.weights(n, K, 304 + i) for i, n in enumerate(Ns)]
+    stats = [gen.weight_stats(w) for w in ws]
+    a = B.bwta_pack_act(x.cuda(), s_a, "ternary")
+    mu_cat = torch.cat([torch.full((n,), float(mu), dtype=torch.float32) for n, (mu, _) in zip(Ns, stats)])
+    wcat = B.bwta_pack_weight(torch.cat(ws).cuda(), mu=mu_cat.cuda())
+    ycat = B.bwta_gemm(a, wcat, torch.cat([s for _, s in stats]).cuda(), s_a, out_dtype=torch.float16)
+    qa = oracle.quantize_act(storage(x), "f16", s_a, "ternary")
+    off = 0
+    for n, w, (mu, s_w) in zip(Ns, ws, stats):
+        sep = B.bwta_gemm(a, B.bwta_pack_weight(w.cuda(), mu=mu), s_w.cuda(), s_a, out_dtype=torch.float16)
+        assert torch.equal(ycat[:, off:off + n], sep), f"grouped block N={n} != separate launch"
+        cols = np.concatenate([np.random.default_rng(n).choice(n, 24, replace=False), [0, n - 1]])
+        qw = oracle.binarize_weight(storage(w[torch.from_numpy(cols)]), "f16", mu=mu)
+        d = oracle.dot(qa, qw, threads=oracle.default_threads())          # [M, cols]
+        ref = oracle.epilogue_linear(d, s_w.numpy()[cols], s_a, "f16")
+        assert_out_equal(ycat[:, torch.from_numpy(off + cols).cuda()], ref, f"grouped N={n} vs oracle")
+        off += n
