@@ -288,11 +288,13 @@ __global__ void __launch_bounds__(AP_NT, 1)
         // QK^T of K stage st into S buffer sb; the K stage is free again once these MMAs complete
         auto qk = [&](uint32_t qa, int st, int sb) {
             const uint32_t kc = smem_u32(sStage + st * STAGE_B);
+            // K = head_dim in MMAs of 64 (the second is all zero codes when head_dim <= 64: skipped)
             if (!(p.dbg & 4))
 #pragma unroll
             for (int k = 0; k < 2; ++k)
-                mma_mxf4_w(tmem_u + uint32_t(TM_S + sb * AP_BK), smem_desc_sw64(qa + 32 * k), smem_desc_sw64(kc + 32 * k),
-                           idesc_qk, sf, sf + 8, k);
+                if (k == 0 || p.dh > 64)
+                    mma_mxf4_w(tmem_u + uint32_t(TM_S + sb * AP_BK), smem_desc_sw64(qa + 32 * k),
+                               smem_desc_sw64(kc + 32 * k), idesc_qk, sf, sf + 8, k);
             tc_commit_w(&s_full[sb]);
             tc_commit_w(&k_empty[st]);
         };
