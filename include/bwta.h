@@ -229,6 +229,24 @@ BWTA_API bwta_status_t bwta_gemm(const uint32_t* a_sgn, const uint32_t* a_nz, bw
                         void* workspace, size_t workspace_bytes,
                         const bwta_opts_t* opts, void* stream);
 
+/*
+ * bwta_gemm with the activation rows' nonzero counts (SURVEY §8(b)'s a_row_nnz): a_row_nnz[i] =
+ * popc of A row i's nz plane, as bwta_pack_act(row_nnz) writes it for the same planes (int32 [m],
+ * device, 4-byte aligned; NULL = bwta_gemm).  The paper hoists this count out of the Case-1 inner
+ * loop (dot = popc(nz_a) - 2 popc(nz_a & (sgn_a ^ w))); design (a)'s tile
+ * kernel reads it instead of counting popc(nz_a) per word when A is TERNARY or BOOL; the other
+ * kernels ignore it (the tensor-core kernels form the dot directly; the <= 4-row GEMV counts the
+ * small side once per L1-resident quad -- a run-time switch there measured 15 % slower).  The counts are
+ * trusted: counts that do not match the planes give wrong results.  Errors as bwta_gemm.
+ */
+BWTA_API bwta_status_t bwta_gemm_nnz(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t a_kind,
+                            int64_t m, int64_t lda_words, const int32_t* a_row_nnz,
+                            const uint32_t* w_sgn, int64_t n, int64_t ldw_words, int64_t k,
+                            const float* w_scale, float a_scale,
+                            void* y, bwta_dtype_t y_dt, int64_t ld_y, int y_transposed,
+                            void* workspace, size_t workspace_bytes,
+                            const bwta_opts_t* opts, void* stream);
+
 /* ---- N-sharded BWTA linear with the all-gather fused into the epilogue ---- */
 /*
  * The north star's multi-GPU linear: rank r of `world` GPUs holds the weight rows of its N-shard

@@ -216,7 +216,9 @@ def bwta_gemm(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: fl
               design: str = "auto", stream=None, tile=None) -> torch.Tensor:
     """Y = s_W s_A (sign(W - mu) (x) quant(A^T, s_A)).
 
-    a: Packed activations [M, lda] (ternary or bool); w: Packed weights [N, ldw].
+    a: Packed activations [M, lda] (ternary or bool); w: Packed weights [N, ldw].  When `a` carries
+    the pack's row_nnz (bwta_pack_act(row_nnz=True)) it is passed on (bwta_gemm_nnz: design (a)'s tile
+    kernel uses it instead of counting popc(nz_a)).
     Returns Y [M, N] (or Y^T [N, M] if y_transposed)."""
     if a.kind not in ("ternary", "bool", "binary") or w.kind != "binary" or a.cols != w.cols:
         raise ValueError("bwta_gemm expects ternary/bool/binary activations and binary weights of equal K")
@@ -230,9 +232,10 @@ def bwta_gemm(a: Packed, w: Packed, w_scale: Optional[torch.Tensor], a_scale: fl
     o = _opts(design, tile)
     ws, wsb = _workspace(lib.bwta_gemm_workspace_size(m, n, k, o), dev)
     ws_scale = None if w_scale is None else w_scale.to(device=dev, dtype=torch.float32).contiguous()
-    st = lib.bwta_gemm(_ptr(a.sgn), _ptr(a.nz), _KIND[a.kind], m, ar.stride(-2), _ptr(w.sgn), n,
-                       w.sgn.stride(-2), k, _ptr(ws_scale), ctypes.c_float(a_scale), _ptr(out),
-                       _DT[out.dtype], out.stride(0), int(y_transposed), _ptr(ws), wsb, o, _stream(stream))
+    rn = a.row_nnz if (a.row_nnz is not None and a.row_nnz.dim() == 1 and a.row_nnz.numel() == m) else None
+    st = lib.bwta_gemm_nnz(_ptr(a.sgn), _ptr(a.nz), _KIND[a.kind], m, ar.stride(-2), _ptr(rn), _ptr(w.sgn), n,
+                           w.sgn.stride(-2), k, _ptr(ws_scale), ctypes.c_float(a_scale), _ptr(out),
+                           _DT[out.dtype], out.stride(0), int(y_transposed), _ptr(ws), wsb, o, _stream(stream))
     _check(st, "bwta_gemm")
     return out
 

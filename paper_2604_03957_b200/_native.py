@@ -19,7 +19,7 @@ DESIGN_AUTO, DESIGN_CUDA_CORE, DESIGN_TCGEN05, DESIGN_MMA_B1 = 0, 1, 2, 3
 EXPORTS = ("bwta_ld_words", "bwta_status_string", "bwta_last_cuda_error", "bwta_last_design",
            "bwta_version", "bwta_kernel_launches", "bwta_pack_act", "bwta_pack_act_batch", "bwta_pack_weight",
            "bwta_gemm_workspace_size", "bwta_gemm_pack",
-           "bwta_gemm", "bwta_attn_qk_workspace_size", "bwta_attn_qk",
+           "bwta_gemm", "bwta_gemm_nnz", "bwta_attn_qk_workspace_size", "bwta_attn_qk",
            "bwta_attn_pv_workspace_size", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "bwta_gemm_x",
            "bwta_attn_prefill", "bwta_attn_prefill_pack", "bwta_gemm_pack_qkv", "bwta_gemm_peers",
            "bwta_peer_barrier", "bwta_ipc_handle", "bwta_ipc_open", "bwta_ipc_close")
@@ -74,6 +74,9 @@ def _declare(L):
     L.bwta_gemm.restype = i32
     L.bwta_gemm.argtypes = [P, P, i32, i64, i64, P, i64, i64, i64, P, f32, P, i32, i64, i32,
                             P, sz, OP, P]
+    L.bwta_gemm_nnz.restype = i32
+    L.bwta_gemm_nnz.argtypes = [P, P, i32, i64, i64, P, P, i64, i64, i64, P, f32, P, i32, i64, i32,
+                                P, sz, OP, P]
     L.bwta_attn_qk_workspace_size.restype = sz
     L.bwta_attn_qk_workspace_size.argtypes = [i64, i64, i64, i64, OP]
     L.bwta_attn_qk.restype = i32

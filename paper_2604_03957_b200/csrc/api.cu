@@ -394,6 +394,15 @@ bwta_status_t bwta_gemm(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t
                         const uint32_t* w_sgn, int64_t n, int64_t ldw_words, int64_t k, const float* w_scale,
                         float a_scale, void* y, bwta_dtype_t y_dt, int64_t ld_y, int y_transposed, void* workspace,
                         size_t workspace_bytes, const bwta_opts_t* opts, void* stream) {
+    return bwta_gemm_nnz(a_sgn, a_nz, a_kind, m, lda_words, nullptr, w_sgn, n, ldw_words, k, w_scale, a_scale, y, y_dt,
+                         ld_y, y_transposed, workspace, workspace_bytes, opts, stream);
+}
+
+bwta_status_t bwta_gemm_nnz(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t a_kind, int64_t m,
+                            int64_t lda_words, const int32_t* a_row_nnz, const uint32_t* w_sgn, int64_t n,
+                            int64_t ldw_words, int64_t k, const float* w_scale, float a_scale, void* y,
+                            bwta_dtype_t y_dt, int64_t ld_y, int y_transposed, void* workspace, size_t workspace_bytes,
+                            const bwta_opts_t* opts, void* stream) {
     if (a_kind != BWTA_TERNARY && a_kind != BWTA_BOOL && a_kind != BWTA_BINARY) return BWTA_ERR_UNSUPPORTED;
     if (!valid_out_dt(y_dt)) return BWTA_ERR_UNSUPPORTED;
     if (m < 0 || n < 0 || k < 0 || k > KMAX) return BWTA_ERR_SHAPE;
@@ -429,6 +438,10 @@ bwta_status_t bwta_gemm(const uint32_t* a_sgn, const uint32_t* a_nz, bwta_kind_t
     a.y_trans = y_transposed;
     a.col_scale = w_scale;
     a.scalar = a_scale;
+    if (a_row_nnz) {
+        if (reinterpret_cast<uintptr_t>(a_row_nnz) % 4) return BWTA_ERR_ALIGNMENT;
+        if (a_kind != BWTA_BINARY) a.a_row_nnz = a_row_nnz;  // binary A has no nz plane to count
+    }
     return run_matmul(a, workspace, workspace_bytes, opts, (cudaStream_t)stream);
 }
 

@@ -148,6 +148,9 @@ struct MatmulArgs {
     const float* col_scale;   // [N] or null
     float scalar;
     int tile_n = 0, cta_group = 0;  // design (b) tile overrides (0 = auto)
+    // popc of each A row's nz plane (bwta_pack_act's row_nnz): the CUDA-core kernels use
+    // it instead of counting popc(nz_a) themselves when the other operand is binary (Case 1); null = count
+    const int32_t* a_row_nnz = nullptr;
     // Both operands binary (W1A1, no nz plane on either side): every kernel multiplies its own K
     // padding (zero sign bits = +1 x +1) and subtracts that count from the dot in its epilogue
     // (dot_bias = K - K_processed, exact integer arithmetic).

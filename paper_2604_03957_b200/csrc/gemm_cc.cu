@@ -39,7 +39,8 @@ __device__ __forceinline__ void store_out(void* y, int dt, int64_t idx, int32_t 
 
 // A_NZ = false: binary A (W1A1 activations, sgn plane only): its nz words are all-ones over the
 // kw4 words the kernel reads, and the epilogue removes the (+1)(+1) products of the padding
-template <bool A_SGN, bool B_NZ, bool A_NZ = true>
+// RN: the A rows' popc(nz) come from p.a_row_nnz (binary B only) instead of being counted per word
+template <bool A_SGN, bool B_NZ, bool A_NZ = true, bool RN = false>
 __global__ void __launch_bounds__(NT) matmul_cc_kernel(MatmulArgs p) {
     __shared__ __align__(16) uint32_t sAs[2][KW][BM + PAD];
     __shared__ __align__(16) uint32_t sAn[2][KW][BM + PAD];
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(NT) matmul_cc_kernel(MatmulArgs p) {
             if (!B_NZ) {
 #pragma unroll
                 for (int i = 0; i < TM; ++i) {
-                    base[i] += __popc(an[i]);
+                    if (!RN) base[i] += __popc(an[i]);
 #pragma unroll
                     for (int j = 0; j < TN; ++j) acc[i][j] += __popc(an[i] & (as[i] ^ bs[j]));
                 }
@@ -171,7 +172,8 @@ __global__ void __launch_bounds__(NT) matmul_cc_kernel(MatmulArgs p) {
         for (int i = 0; i < TM; ++i) {
             const int64_t gi = i0 + ty * TM + i;
             if (gi >= p.M) continue;
-            int32_t d = B_NZ ? acc2[i][j] - 2 * acc[i][j] : base[i] - 2 * acc[i][j];
+            const int32_t bi = RN ? __ldg(p.a_row_nnz + gi) : base[i];
+            int32_t d = B_NZ ? acc2[i][j] - 2 * acc[i][j] : bi - 2 * acc[i][j];
             if (!A_NZ && !B_NZ) d -= int32_t(32 * kw4 - p.K);  // W1A1: the K padding counted as +1
             const int64_t idx = ybase + (p.y_trans ? gj * p.ldy + gi : gi * p.ldy + gj);
             store_out(Y, p.y_dt, idx, d, c);
@@ -188,6 +190,10 @@ cudaError_t launch_matmul_cc(const MatmulArgs& a, cudaStream_t s) {
     if (!a.a_nz) {  // binary A (W1A1)
         if (bnz) return launch_pdl(matmul_cc_kernel<true, true, false>, grid, NT, 0, s, 1, a);
         return launch_pdl(matmul_cc_kernel<true, false, false>, grid, NT, 0, s, 1, a);
+    }
+    if (a.a_row_nnz && !bnz && a.nb * a.nh == 1) {  // Case 1 with the pack's row popcounts
+        if (asg) return launch_pdl(matmul_cc_kernel<true, false, true, true>, grid, NT, 0, s, 1, a);
+        return launch_pdl(matmul_cc_kernel<false, false, true, true>, grid, NT, 0, s, 1, a);
     }
     if (asg && bnz) return launch_pdl(matmul_cc_kernel<true, true>, grid, NT, 0, s, 1, a);
     if (asg) return launch_pdl(matmul_cc_kernel<true, false>, grid, NT, 0, s, 1, a);

@@ -658,3 +658,26 @@ def test_gemm_pack_qkv_equals_gemm_then_head_packs(B, kind, y_dt):
             vj = np.ascontiguousarray(yo[:, j * h * d:(j + 1) * h * d].reshape(bsz, t, h, d).transpose(0, 2, 1, 3))
             sg, nz, _ = oracle.pack_act(vj.reshape(bsz * h, t, d), name, sc[j], kind, transpose=(j == 2))
             assert np.array_equal(words(got[j].nz).reshape(nz.shape), nz), (i, j, "oracle")
+
+
+@pytest.mark.parametrize("kind", ["ternary", "bool"])
+@pytest.mark.parametrize("m,k,n", [(200, 300, 130), (3, 4096, 1000), (1, 1000, 4099), (130, 2048, 77)])
+def test_gemm_row_nnz_cuda_core(B, kind, m, k, n):
+    """bwta_gemm_nnz (SURVEY §8(b) a_row_nnz): design (a)'s tile kernel takes popc(nz_a) from the
+    pack's row_nnz instead of counting it (the other kernels ignore it); equal to the plain call and
+    to the oracle element by element, through design (a) and AUTO (GEMV / tcgen05)."""
+    x = gen.activations((m, k), 31)
+    if kind == "bool":
+        x = torch.relu(x)
+    w = gen.weights(n, k, 32)
+    mu, s_w = gen.weight_stats(w)
+    a = B.bwta_pack_act(x.cuda(), 1.6, kind, row_nnz=True)
+    a0 = B.bwta_pack_act(x.cuda(), 1.6, kind)
+    wp = B.bwta_pack_weight(w.cuda(), mu=mu)
+    for design in ("cuda_core", "auto"):
+        y = B.bwta_gemm(a, wp, s_w.cuda(), 1.6, out_dtype=torch.int32, design=design)
+        y0 = B.bwta_gemm(a0, wp, s_w.cuda(), 1.6, out_dtype=torch.int32, design=design)
+        assert torch.equal(y, y0), design
+    qa = oracle.quantize_act(storage(x), "f16", 1.6, kind)
+    qw = oracle.binarize_weight(storage(w), "f16", mu=mu)
+    assert np.array_equal(y.cpu().numpy(), oracle.dot(qa, qw, threads=oracle.default_threads()))
