@@ -163,6 +163,9 @@ struct TcParams {
     float ph_tp[3], ph_tn[3];
     int n_peers;     // fused all-gather: the fast epilogue also stores every tile through PeerMaps::m[0 .. n_peers)
     float dot_bias;  // W1A1: K - K_processed (both operands binary; the generic epilogue adds it)
+    FastDiv fd_tpe, fd_mt, fd_nh;  // tile -> (entry, m tile, n tile), entry -> (batch, head): 32-bit
+                                   // multiply-shift (the int64 divisions were subroutine calls, ~1k
+                                   // cycles per tile in the producer; total tiles < 2^31, host-checked)
     int pf_on;                // L2 prefetch of the operand planes at kernel start
     const void* pf_ptr[4];    // plane spans (A0, A1, B0, B1; null / 0 bytes: skip), 16-byte aligned
     uint64_t pf_bytes[4];
@@ -218,6 +221,19 @@ struct Cfg {
                       ABITS % 128 == 0 && BBITS % 128 == 0,
                   "smem region alignment");
 };
+
+__device__ __forceinline__ uint32_t fdiv_u32(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
+struct TileCoord {
+    int mt, nt, eb, eh;
+};
+__device__ __forceinline__ TileCoord tile_coord(const TcParams& p, int64_t t) {
+    const uint32_t tu = uint32_t(t);
+    const uint32_t e = fdiv_u32(tu, p.fd_tpe);
+    const uint32_t r = tu - e * p.fd_tpe.d;
+    const uint32_t nt = fdiv_u32(r, p.fd_mt);
+    const uint32_t eb = fdiv_u32(e, p.fd_nh);
+    return TileCoord{int(r - nt * p.fd_mt.d), int(nt), int(eb), int(e - eb * p.fd_nh.d)};
+}
 
 // f32 accumulator (the exact integer dot) -> dot / scaled output (R5)
 __device__ __forceinline__ int32_t dot_of(uint32_t acc) { return __float2int_rn(__uint_as_float(acc)); }
@@ -616,10 +632,8 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
     uint32_t acc_phase = 0;
     int tix = 0;
     for (int64_t t = t0; t < total; t += tstep, ++tix) {
-        const int64_t e = t / tiles_per_entry;
-        const int64_t r = t % tiles_per_entry;
-        const int mt = int(r % p.m_tiles), nt = int(r / p.m_tiles);
-        const int eb = int(e / p.nh), eh = int(e % p.nh);
+        const TileCoord tc = tile_coord(p, t);
+        const int mt = tc.mt, nt = tc.nt, eb = tc.eb, eh = tc.eh;
         const int64_t mrow0 = int64_t(mt) * BM * CG + rank * BM;  // first kernel row of this CTA
         // with an odd number of 64-column chunks the two warps of a lane
         // quarter alternate which of them takes the extra chunk
@@ -877,10 +891,8 @@ __global__ void __launch_bounds__(nt_of(KS, EO), 1)
         uint32_t phase = 0;
         int it = 0;
         for (int64_t t = t0; t < total; t += tstep) {
-            const int64_t e = t / tiles_per_entry;
-            const int64_t r = t % tiles_per_entry;
-            const int mt = int(r % p.m_tiles), nt = int(r / p.m_tiles);
-            const int eb = int(e / p.nh), eh = int(e % p.nh);
+            const TileCoord tc = tile_coord(p, t);
+            const int mt = tc.mt, nt = tc.nt, eb = tc.eb, eh = tc.eh;
             const int arow = mt * BM * CG + rank * BM;
             const int brow = nt * BN + rank * C::BNC;
             for (int kb = 0; kb < p.num_kb; ++kb) {
@@ -1392,6 +1404,10 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     p.nh = a.nh;
     p.m_tiles = int((pl.Mk + BM * cg - 1) / (BM * cg));
     p.n_tiles = int((pl.Nk + bn - 1) / bn);
+    if (entries * int64_t(p.m_tiles) * p.n_tiles >= (int64_t(1) << 31)) return cudaErrorNotSupported;
+    p.fd_tpe = make_fastdiv(uint32_t(int64_t(p.m_tiles) * p.n_tiles));
+    p.fd_mt = make_fastdiv(uint32_t(p.m_tiles));
+    p.fd_nh = make_fastdiv(uint32_t(a.nh));
     p.a_kind = akind;
     p.b_kind = bkind;
     p.y = a.y;
