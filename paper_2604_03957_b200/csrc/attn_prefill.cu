@@ -74,8 +74,10 @@ constexpr int SMEM_AP = 1024 + 2 * Q_CODES + AP_S * STAGE_B + AP_VS * V_CODES + 
                         2 * Q_BITS + 4 * 1024 /*tables*/ + 2 * AP_NH * AP_BQ * 4 * 2 /*merge*/ + 512 /*barriers*/;
 static_assert(SMEM_AP <= 227 * 1024, "shared memory");
 constexpr int TM_S = 0, TM_O = 256, TM_SF = 384;  // TMEM columns: S[0], S[1], O, scale factors
+__device__ __forceinline__ uint32_t ap_fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
 
 struct ApParams {
+    FastDiv fd_qt, fd_nh;  // item -> (entry, q tile), entry -> (batch, head): 32-bit multiply-shift
     int64_t nh, tq, tk;
     int dh, dhp;           // head_dim, rounded up to 16 (PV MMA N, V^T box rows)
     int q_tiles, nblk;
@@ -245,9 +247,10 @@ __global__ void __launch_bounds__(AP_NT, 1)
             const uint32_t vbytes = uint32_t(2 * p.dhp * VCH_W * 4);
             int g = 0, ic = 0, vc = 0;
             for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++ic) {
-                const int64_t e = t / p.q_tiles;
-                const int q0 = int(t % p.q_tiles) * AP_BQ;
-                const int eb = int(e / p.nh), eh = int(e % p.nh);
+                const uint32_t e = ap_fdiv(uint32_t(t), p.fd_qt);
+                const int q0 = int(uint32_t(t) - e * p.fd_qt.d) * AP_BQ;
+                const uint32_t eb_ = ap_fdiv(e, p.fd_nh);
+                const int eb = int(eb_), eh = int(e - eb_ * p.fd_nh.d);
                 const int qb = ic & 1;
                 wait_bar(&q_empty[qb], uint32_t((ic >> 1) & 1) ^ 1u);
                 mbar_arrive_expect_tx(&q_full[qb], uint32_t(2 * AP_BQ * 16));
@@ -356,7 +359,8 @@ __global__ void __launch_bounds__(AP_NT, 1)
             const int qb = ic & 1;
             wait_bar(&q_full[qb], uint32_t((ic >> 1) & 1));
             const uint32_t qbits = smem_u32(sQb + qb * Q_BITS);
-            const bool negq = p.alpha_h ? (__ldg(p.alpha_h + (t / p.q_tiles) % p.nh) < 0.f) : p.neg != 0;
+            const uint32_t e_ = ap_fdiv(uint32_t(t), p.fd_qt);
+            const bool negq = p.alpha_h ? (__ldg(p.alpha_h + (e_ - ap_fdiv(e_, p.fd_nh) * p.fd_nh.d)) < 0.f) : p.neg != 0;
             unpack_q_row(qbits + ut * 16, qbits + AP_BQ * 16 + ut * 16, smem_u32(sQ + qb * Q_CODES) + ut * CODE_ROW, ut,
                          negq);
             fence_proxy_async_smem();
@@ -401,9 +405,10 @@ __global__ void __launch_bounds__(AP_NT, 1)
         const float MAGIC = 12582912.f;                    // 1.5 * 2^23: float_as_int(x + MAGIC) = 0x4B400000 + x
         int sg = 0, pg = 0, ic = 0;
         for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++ic) {
-            const int64_t e = t / p.q_tiles;
-            const int64_t qrow = int64_t(t % p.q_tiles) * AP_BQ + r;
-            const int eb = int(e / p.nh), eh = int(e % p.nh);
+            const uint32_t e = ap_fdiv(uint32_t(t), p.fd_qt);
+            const int64_t qrow = int64_t(uint32_t(t) - e * p.fd_qt.d) * AP_BQ + r;
+            const uint32_t eb_ = ap_fdiv(e, p.fd_nh);
+            const int eb = int(eb_), eh = int(e - eb_ * p.fd_nh.d);
             float alpha = p.alpha, beta = p.beta;
             uint32_t tbl_s = smem_u32(tbl);
             if (p.alpha_h) {  // this head's |alpha|: its own exp table (double-buffered by item parity)
@@ -626,6 +631,9 @@ cudaError_t launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t s) {
     p.q_tiles = int((a.tq + AP_BQ - 1) / AP_BQ);
     p.nblk = int((a.tk + AP_BK - 1) / AP_BK);
     p.items = entries * p.q_tiles;
+    if (p.items >= (int64_t(1) << 31) || a.nh >= (int64_t(1) << 31)) return cudaErrorNotSupported;
+    p.fd_qt = make_fastdiv(uint32_t(p.q_tiles));
+    p.fd_nh = make_fastdiv(uint32_t(a.nh));
     p.k_kind = a.k_nz ? B_TERNARY : B_BINARY;
     p.neg = a.alpha < 0.f ? 1 : 0;
     p.alpha = fabsf(a.alpha);
