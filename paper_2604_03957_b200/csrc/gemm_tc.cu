@@ -157,6 +157,8 @@ struct TcParams {
     // head-split Q / K / V^T pack (MatmulArgs::po_heads); kernel rows = tokens (never swapped)
     int po_heads;
     int64_t ph_T, ph_H, ph_D;
+    FastDiv fd_hd, fd_d, fd_t;  // / (H*D), / D, / T as 32-bit multiply-shift (the int64 divisions
+                                // were subroutine calls, several per 32-column chunk)
     uint32_t* ph_sgn[3];
     uint32_t* ph_nz[3];
     int64_t ph_ld[3];
@@ -508,9 +510,9 @@ __device__ __forceinline__ void epi_tile_pack(const TcParams& p, uint32_t tacc, 
         }
         if (p.po_heads) {
             // chunk of Q / K / V (warp-uniform: H*D and D are multiples of 32); thread = token row
-            const int64_t HD = p.ph_H * p.ph_D;
-            const int reg = int(n0 / HD);
-            const int64_t nl = n0 - reg * HD, hh = nl / p.ph_D, dcol = nl - hh * p.ph_D;
+            const int reg = int(fdiv_u32(uint32_t(n0), p.fd_hd));
+            const uint32_t nl = uint32_t(n0) - uint32_t(reg) * p.fd_hd.d;
+            const int64_t hh = fdiv_u32(nl, p.fd_d), dcol = nl - uint32_t(hh) * p.fd_d.d;
             const float tp = p.ph_tp[reg], tn = p.ph_tn[reg];
             uint32_t* psg = p.ph_sgn[reg];
             uint32_t* pnz = p.ph_nz[reg];
@@ -524,7 +526,7 @@ __device__ __forceinline__ void epi_tile_pack(const TcParams& p, uint32_t tacc, 
                     neg |= uint32_t(y <= -tn) << j;
                 }
                 if (rok) {
-                    const int64_t b = row / p.ph_T, t = row - b * p.ph_T;
+                    const int64_t b = fdiv_u32(uint32_t(row), p.fd_t), t = row - b * p.ph_T;
                     const int64_t off = ((b * p.ph_H + hh) * p.ph_T + t) * p.ph_ld[reg] + dcol / 32;
                     pnz[off] = ternary ? (pos | neg) : pos;
                     if (ternary) psg[off] = neg;
@@ -549,7 +551,7 @@ __device__ __forceinline__ void epi_tile_pack(const TcParams& p, uint32_t tacc, 
                 __syncwarp();
                 const int64_t m0 = mrow0 + q * 32;
                 if (m0 < p.M) {
-                    const int64_t b = m0 / p.ph_T, t0 = m0 - b * p.ph_T;
+                    const int64_t b = fdiv_u32(uint32_t(m0), p.fd_t), t0 = m0 - b * p.ph_T;
                     const int64_t off = ((b * p.ph_H + hh) * p.ph_D + dcol + lane) * p.ph_ld[2] + t0 / 32;
                     pnz[off] = ternary ? (my_pos | my_neg) : my_pos;
                     if (ternary) psg[off] = my_neg;
@@ -1432,6 +1434,13 @@ cudaError_t launch_matmul_tc(const MatmulArgs& a, void*, size_t, cudaStream_t s)
     p.ph_T = a.ph_T;
     p.ph_H = a.ph_H;
     p.ph_D = a.ph_D;
+    if (a.po_heads) {
+        if (a.ph_H * a.ph_D >= (int64_t(1) << 31) || a.ph_T >= (int64_t(1) << 31) || pl.Mk >= (int64_t(1) << 31))
+            return cudaErrorNotSupported;
+        p.fd_hd = make_fastdiv(uint32_t(a.ph_H * a.ph_D));
+        p.fd_d = make_fastdiv(uint32_t(a.ph_D));
+        p.fd_t = make_fastdiv(uint32_t(a.ph_T));
+    }
     for (int r = 0; r < 3; ++r) {
         p.ph_sgn[r] = a.ph_sgn[r];
         p.ph_nz[r] = a.ph_nz[r];

@@ -62,12 +62,14 @@ constexpr int GV_SFCOL = GV_ACOL + GV_CST * 32;
 constexpr int GV_TMEM_COLS = 512;
 constexpr int GV_SMEM_MAX = 200 * 1024;
 
+__device__ __forceinline__ uint32_t gv_fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
 struct GvParams {
     float dot_bias;  // W1A1 (both operands binary): K - K_processed, added to every dot
     int64_t M, N;  // kernel-A rows / kernel-B rows (N <= NB) per entry
     int num_kb;
     int64_t nh, entries;
     int tiles_per_entry;
+    FastDiv fd_tpe, fd_nh, fd_nsup;  // 32-bit multiply-shift decode of the tile index (host: total < 2^31)
     int a_kind, b_kind;
     int ring;                        // bit-ring depth
     int a_bits, b_bits;              // bytes per bit stage (all planes, 128 B per row per plane)
@@ -194,10 +196,11 @@ __global__ void __launch_bounds__(GV_NT, 1)
             int s = 0;
             uint32_t ph = 0;
             for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-                const int64_t e = t / p.tiles_per_entry;
-                const int row = int(t % p.tiles_per_entry) * GV_BM;
-                const int eb = int(e / p.nh), eh = int(e % p.nh);
-                const int nsup = (p.num_kb + GV_UPS - 1) / GV_UPS, rot = int(t % nsup);
+                const uint32_t e = gv_fdiv(uint32_t(t), p.fd_tpe);
+                const int row = int(uint32_t(t) - e * p.fd_tpe.d) * GV_BM;
+                const uint32_t eb_ = gv_fdiv(e, p.fd_nh);
+                const int eb = int(eb_), eh = int(e - eb_ * p.fd_nh.d);
+                const int nsup = (p.num_kb + GV_UPS - 1) / GV_UPS, rot = int(uint32_t(t) - gv_fdiv(uint32_t(t), p.fd_nsup) * uint32_t(nsup));
                 for (int j = 0; j < p.num_kb; j += GV_UPS) {
                     mbar_wait(&bempty[s], ph ^ 1);
                     mbar_arrive_expect_tx(&bfull[s], tx);
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(GV_NT, 1)
         uint32_t ph = 0, cph = 0;
         int u = 0;  // unit counter (group grp takes u % 2 == grp), padded to whole bit stages
         for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-            const int nsup = (p.num_kb + GV_UPS - 1) / GV_UPS, rot = int(t % nsup);
+            const int nsup = (p.num_kb + GV_UPS - 1) / GV_UPS, rot = int(uint32_t(t) - gv_fdiv(uint32_t(t), p.fd_nsup) * uint32_t(nsup));
             for (int kb0 = 0; kb0 < p.num_kb; kb0 += GV_UPS) {
                 const int js = kb0 / GV_UPS + rot;
                 const int kb = (js < nsup ? js : js - nsup) * GV_UPS;  // first unit of this bit stage
@@ -328,9 +331,10 @@ __global__ void __launch_bounds__(GV_NT, 1)
         int acc = 0;
         uint32_t aph = 0;
         for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-            const int64_t e = t / p.tiles_per_entry;
-            const int64_t r = int64_t(t % p.tiles_per_entry) * GV_BM + 32 * q + lane;
-            const int64_t eoff = (e / p.nh) * p.y_bs + (e % p.nh) * p.y_hs;
+            const uint32_t e = gv_fdiv(uint32_t(t), p.fd_tpe);
+            const int64_t r = int64_t(uint32_t(t) - e * p.fd_tpe.d) * GV_BM + 32 * q + lane;
+            const uint32_t eb_ = gv_fdiv(e, p.fd_nh);
+            const int64_t eoff = int64_t(eb_) * p.y_bs + int64_t(e - eb_ * p.fd_nh.d) * p.y_hs;
             mbar_wait(&afull[acc], aph);
             tc_fence_after();
             uint32_t v[NB];
@@ -424,10 +428,14 @@ cudaError_t launch_matmul_gemv(const MatmulArgs& a, cudaStream_t s) {
     p.M = Mk;
     p.N = Nk;
     p.num_kb = int((kw4_of(a.K) + GV_WPS - 1) / GV_WPS);
+    p.fd_nsup = make_fastdiv(uint32_t((p.num_kb + GV_UPS - 1) / GV_UPS));
     if (!ka_nz && !kb_nz) p.dot_bias = float(a.K - int64_t(p.num_kb) * GV_WPS * 32);  // W1A1 padding
     p.nh = a.nh;
     p.entries = a.nb * a.nh;
     p.tiles_per_entry = int((Mk + GV_BM - 1) / GV_BM);
+    if (int64_t(p.tiles_per_entry) * a.nb * a.nh >= (int64_t(1) << 31)) return cudaErrorNotSupported;
+    p.fd_tpe = make_fastdiv(uint32_t(p.tiles_per_entry));
+    p.fd_nh = make_fastdiv(uint32_t(a.nh));
     p.a_kind = akind;
     p.b_kind = bkind;
     p.y = a.y;
