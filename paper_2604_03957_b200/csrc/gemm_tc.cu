@@ -61,18 +61,6 @@ constexpr int NT = 640;     // 20 warps (128-K stages)
 #define BWTA_A_GROUPS 2
 #endif
 constexpr int A_GROUPS = BWTA_A_GROUPS;
-// L2 policy of the output tile stores (fast epilogue), A/B builds only: 0 default, 1 evict_first,
-// 2 evict_last, 3 evict_normal.  Measured on C3 N = 11008, graph of [L2 flush, GEMM] (the previous
-// output's write-back lands in the next flush, inside the graph): 60.3 / 59.3 / 53.6 / 59.9 us.
-// Not adopted: the configs[2] step did not move (82.1 vs 82.4 us), and evict_last lines can
-// outlive the bench's L2 flush (and, in a deep model, crowd out other tensors).
-#ifndef BWTA_Y_HINT
-#define BWTA_Y_HINT 0
-#endif
-#ifndef BWTA_B_PAIR
-#define BWTA_B_PAIR 0
-#endif
-constexpr bool B_PAIR = BWTA_B_PAIR != 0;  // kernel-B unpack warps take two 256-K stages per iteration
 // (the fp16/bf16 TMA-store epilogue class only: the fused-pack and generic epilogues need more than
 // the 80 registers a 768-thread CTA leaves and spill -- BERT FFN1 + pack 17.3 -> 20.4 us)
 __host__ __device__ constexpr int a_groups(int ks, int eo) { return (ks == 256 && eo == 0) ? A_GROUPS : 1; }
@@ -438,15 +426,7 @@ __device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorM
         TRACE_EPI(12, tix * 4 + i, tr);
         if (lane == 0) {
             const int c0s = p.out_trans ? int(mrow0 + q * 32) : int(n0), c1s = p.out_trans ? int(n0) : int(mrow0 + q * 32);
-#if BWTA_Y_HINT == 1
-            tma_store_4d_hint(&tmY, stg, c0s, c1s, eh, eb, l2_policy_evict_first());
-#elif BWTA_Y_HINT == 2
-            tma_store_4d_hint(&tmY, stg, c0s, c1s, eh, eb, l2_policy_evict_last());
-#elif BWTA_Y_HINT == 3
-            tma_store_4d_hint(&tmY, stg, c0s, c1s, eh, eb, l2_policy_evict_normal());
-#else
             tma_store_4d(&tmY, stg, c0s, c1s, eh, eb);
-#endif
             // fused all-gather: the same staged chunk to every peer's Y (NVLink writes), one bulk group
             for (int pi = 0; pi < p.n_peers; ++pi) tma_store_4d(&pm.m[pi], stg, c0s, c1s, eh, eb);
             bulk_commit();
@@ -1068,40 +1048,6 @@ __global__ void __launch_bounds__(nt_of(KS, EO), 1)
         const int rows = is_a ? BM : C::BNC;
         const int plane_bytes = rows * WPS * 4;
         const uint32_t bready_addr0 = CG == 2 ? mapa_smem(&bready[0], 0) : 0u;
-        if (KS == 256 && B_PAIR && !is_a) {
-            // kernel-B, 256-K stages: two stages per iteration (one proxy fence and one pass of the
-            // loop's fixed waits for both), the pair signalled together
-            const int64_t n_it = ((total - t0 + tstep - 1) / tstep) * p.num_kb;
-            for (int64_t it = 0; it < n_it; it += 2) {
-                const bool two = it + 1 < n_it;
-                const int s0 = int(it % C::STAGES), s1 = int((it + 1) % C::STAGES);
-                kwait(&full[s0], uint32_t((it / C::STAGES) & 1), p.dbg);
-                TRACE(2, it, ut == 0);
-#ifdef BWTA_TRACE
-                if (!(p.dbg & 17))
-#endif
-                unpack_quads<KS, C::BNC, 192>(kind, smem_u32(sBBits + s0 * C::BBITS), smem_u32(sB + s0 * C::B_BYTES), ut);
-                if (two) {
-                    kwait(&full[s1], uint32_t(((it + 1) / C::STAGES) & 1), p.dbg);
-#ifdef BWTA_TRACE
-                    if (!(p.dbg & 17))
-#endif
-                    unpack_quads<KS, C::BNC, 192>(kind, smem_u32(sBBits + s1 * C::BBITS), smem_u32(sB + s1 * C::B_BYTES),
-                                                  ut);
-                }
-                fence_proxy_async_smem();
-                __syncwarp();
-                TRACE(3, it, ut == 0);
-                if (lane == 0) {
-                    if (CG == 1) mbar_arrive(&bready[s0]);
-                    else mbar_arrive_cluster(bready_addr0 + s0 * 8);
-                    if (two) {
-                        if (CG == 1) mbar_arrive(&bready[s1]);
-                        else mbar_arrive_cluster(bready_addr0 + s1 * 8);
-                    }
-                }
-            }
-        } else {
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
@@ -1133,7 +1079,6 @@ __global__ void __launch_bounds__(nt_of(KS, EO), 1)
                     phase ^= 1;
                 }
             }
-        }
         }
     } else if (warp >= 4) {
         // ------------------------------ epilogue (warps 4-7 and 12-15) ------------------------------
