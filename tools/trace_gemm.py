@@ -15,7 +15,13 @@ import torch
 import bwta_inputs as gen
 import paper_2604_03957_b200 as B
 
-if sys.argv[1] == "qk":   # attention QK^T: qk BH T D
+if sys.argv[1] == "qkvpack":   # BERT QKV projection emitting the per-head Q/K/V^T planes
+    x = gen.activations((4096, 768), 1).cuda()
+    w = gen.weights(2304, 768, 2).cuda()
+    a = B.bwta_pack_act(x, 1.6)
+    wp = B.bwta_pack_weight(w)
+    run = lambda: B.bwta_gemm_pack_qkv(a, wp, None, 0.01, 32, 128, 12, 64, (0.5, 0.5, 0.5))
+elif sys.argv[1] == "qk":   # attention QK^T: qk BH T D
     bh, t, d = (int(v) for v in sys.argv[2:5])
     qp = B.bwta_pack_act(torch.randn(bh, t, d, device="cuda", dtype=torch.float16), 1.6)
     kp = B.bwta_pack_act(torch.randn(bh, t, d, device="cuda", dtype=torch.float16), 1.6)
