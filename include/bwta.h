@@ -455,6 +455,26 @@ BWTA_API bwta_status_t bwta_attn_prefill(const uint32_t* q_sgn, const uint32_t* 
                            uint32_t* p_out, int64_t ldp_words, void* stream);
 
 /*
+ * bwta_attn_prefill with an optional causal mask (SURVEY §8(f) N3's causal tile skipping):
+ * causal = 1: query row i attends to keys j <= i + (tk - tq) only (the decoder / LLaMA prefill
+ * mask; requires tk >= tq, else BWTA_ERR_SHAPE); masked keys are not keys -- out of the row max,
+ * the softmax normaliser, P and PV -- and key blocks past a query tile's last row are never loaded
+ * or multiplied.  causal = 0 is bwta_attn_prefill.  Other arguments and errors as
+ * bwta_attn_prefill.
+ */
+BWTA_API bwta_status_t bwta_attn_prefill_ex(const uint32_t* q_sgn, const uint32_t* q_nz,
+                           const uint32_t* k_sgn, const uint32_t* k_nz,
+                           const uint32_t* vt_sgn, const uint32_t* vt_nz,
+                           int64_t batch, int64_t heads, int64_t tq, int64_t tk, int64_t dh,
+                           int64_t ldq_words, int64_t q_bstride, int64_t q_hstride,
+                           int64_t ldk_words, int64_t k_bstride, int64_t k_hstride,
+                           int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
+                           float alpha, float s_att, bwta_dtype_t p_dt, float beta,
+                           const float* alpha_heads, const float* beta_heads,
+                           void* o, bwta_dtype_t o_dt, int64_t ld_o, int64_t o_bstride, int64_t o_hstride,
+                           uint32_t* p_out, int64_t ldp_words, int causal, void* stream);
+
+/*
  * bwta_attn_prefill with the next layer's activation pack fused into its epilogue (SURVEY
  * §8(f) N2): instead of O, the planes of the [batch*tq, heads*dh] attention context
  * (round_{o_dt}(O), o_dt F16 | BF16) quantized with out_scale / out_kind (TERNARY | BOOL),

@@ -287,17 +287,21 @@ def attn_pv(qp: np.ndarray, qv: np.ndarray, beta: float, out_dt: str, threads: i
 
 
 def attn_decode(qq: np.ndarray, qk: np.ndarray, qv: np.ndarray, alpha: float, s_att: float, p_dt: str,
-                beta: float, out_dt: str, threads: int = 1):
+                beta: float, out_dt: str, threads: int = 1, nkeys=None):
     """Fused decode attention, the composition of the paper's steps in order:
     S = alpha * (q . k_j) (R5 order, f32); P = softmax(S) over j in float64 (the paper
     keeps the softmax in high precision, P:882-891) then rounded to p_dt via f32 (O8 narrowing);
     bool quantization with s_att (R1-R2); O = beta * (P_bool . v) (R5).
 
     qq: int8 [BH, Dh], qk: int8 [BH, Tk, Dh], qv: int8 [BH, Tk, Dh].
+    nkeys: optional int [BH]: entry b sees keys j < nkeys[b] only (a causal decoder's mask: a
+    masked key is not a key -- it is out of the softmax, P = 0 and it adds nothing to PV).
     Returns (O storage [BH, Dh], P_bool int8 [BH, Tk], p float64 [BH, Tk])."""
     bh = qq.shape[0]
     s = np.stack([epilogue_scalar(dot(qq[b][None, :], qk[b], threads), alpha, "f32")[0] for b in range(bh)])
     s64 = s.astype(np.float64)
+    if nkeys is not None:
+        s64[np.arange(s64.shape[1])[None, :] >= np.asarray(nkeys)[:, None]] = -np.inf
     e = np.exp(s64 - s64.max(axis=1, keepdims=True))
     p = e / e.sum(axis=1, keepdims=True)
     if p_dt == "f32":

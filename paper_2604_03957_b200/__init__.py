@@ -467,14 +467,16 @@ def bwta_attn_decode(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: floa
 
 def bwta_attn_prefill(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: float, beta: float,
                       out_dtype=torch.float16, p_dtype=torch.float16, return_p: bool = False,
-                      out: Optional[torch.Tensor] = None, stream=None, alpha_heads=None, beta_heads=None):
+                      out: Optional[torch.Tensor] = None, stream=None, alpha_heads=None, beta_heads=None,
+                      causal: bool = False):
     """Fused prefill attention, one launch:
     O = beta * bool(round(softmax(alpha * ternary(Q) (x) K^T), p_dtype) >= s_att / 2) (x) ternary(V).
 
     q: Packed ternary [B, H, Tq, ld] (or [B, Tq, ld] / [Tq, ld]); k: Packed ternary or binary
     [.., Tk, ld] over the same head_dim (<= 128); vt: Packed ternary [.., Dh, ld(Tk)]
-    (bwta_pack_act(V, transpose=True)).  Returns O [.., Tq, Dh] (and the P planes
-    [entries, Tq, ld(Tk)] with return_p)."""
+    (bwta_pack_act(V, transpose=True)).  causal: row i sees keys j <= i + Tk - Tq only
+    (bwta_attn_prefill_ex).  Returns O [.., Tq, Dh] (and the P planes [entries, Tq, ld(Tk)] with
+    return_p)."""
     qr, kr, vr = q.ref, k.ref, vt.ref
     if q.kind != "ternary" or vt.kind != "ternary" or k.cols != q.cols or vt.cols != kr.shape[-2]:
         raise ValueError("expects ternary Q and V^T, K over the same head_dim, V^T over Tk")
@@ -494,11 +496,11 @@ def bwta_attn_prefill(q: Packed, k: Packed, vt: Packed, alpha: float, s_att: flo
     pout = torch.empty((b * h, tq, ldp), dtype=torch.int32, device=qr.device) if return_p else None
     k_nz = k.nz if k.kind == "ternary" else None
     ah, bh_ = _heads_vec(alpha_heads, h, qr.device), _heads_vec(beta_heads, h, qr.device)
-    st = lib.bwta_attn_prefill(_ptr(q.sgn), _ptr(q.nz), _ptr(k.sgn), _ptr(k_nz), _ptr(vt.sgn), _ptr(vt.nz), b, h,
-                               tq, tk, dh, qr.stride(-2), qbs, qhs, kr.stride(-2), kbs, khs, vr.stride(-2), vbs, vhs,
-                               ctypes.c_float(alpha), ctypes.c_float(s_att), _DT[p_dtype], ctypes.c_float(beta),
-                               _ptr(ah), _ptr(bh_), _ptr(out), _DT[out.dtype], out.stride(-2), obs, ohs, _ptr(pout),
-                               ldp if return_p else 0, _stream(stream))
+    st = lib.bwta_attn_prefill_ex(_ptr(q.sgn), _ptr(q.nz), _ptr(k.sgn), _ptr(k_nz), _ptr(vt.sgn), _ptr(vt.nz), b, h,
+                                  tq, tk, dh, qr.stride(-2), qbs, qhs, kr.stride(-2), kbs, khs, vr.stride(-2), vbs, vhs,
+                                  ctypes.c_float(alpha), ctypes.c_float(s_att), _DT[p_dtype], ctypes.c_float(beta),
+                                  _ptr(ah), _ptr(bh_), _ptr(out), _DT[out.dtype], out.stride(-2), obs, ohs, _ptr(pout),
+                                  ldp if return_p else 0, int(bool(causal)), _stream(stream))
     _check(st, "bwta_attn_prefill")
     return (out, pout) if return_p else out
 

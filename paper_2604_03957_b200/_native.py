@@ -21,7 +21,7 @@ EXPORTS = ("bwta_ld_words", "bwta_status_string", "bwta_last_cuda_error", "bwta_
            "bwta_gemm_workspace_size", "bwta_gemm_pack",
            "bwta_gemm", "bwta_gemm_nnz", "bwta_attn_qk_workspace_size", "bwta_attn_qk",
            "bwta_attn_pv_workspace_size", "bwta_attn_pv", "bwta_attn_pv_pack", "bwta_attn_decode", "bwta_gemm_x",
-           "bwta_attn_prefill", "bwta_attn_prefill_pack", "bwta_gemm_pack_qkv", "bwta_gemm_peers",
+           "bwta_attn_prefill", "bwta_attn_prefill_ex", "bwta_attn_prefill_pack", "bwta_gemm_pack_qkv", "bwta_gemm_peers",
            "bwta_peer_barrier", "bwta_ipc_handle", "bwta_ipc_open", "bwta_ipc_close")
 IPC_HANDLE_BYTES = 64
 
@@ -92,6 +92,9 @@ def _declare(L):
     L.bwta_attn_prefill.restype = i32
     L.bwta_attn_prefill.argtypes = [P, P, P, P, P, P] + [i64] * 14 + [f32, f32, i32, f32, P, P, P, i32, i64, i64, i64,
                                                                       P, i64, P]
+    L.bwta_attn_prefill_ex.restype = i32
+    L.bwta_attn_prefill_ex.argtypes = [P, P, P, P, P, P] + [i64] * 14 + [f32, f32, i32, f32, P, P, P, i32, i64, i64,
+                                                                         i64, P, i64, i32, P]
     L.bwta_gemm_pack_qkv.restype = i32
     L.bwta_gemm_pack_qkv.argtypes = [P, P, i32, i64, i64, P, i64, i64, i64, P, f32, i32, i64, i64, i64, i64, P, i32,
                                      P, P, i64, P, P, i64, P, P, i64, OP, P]

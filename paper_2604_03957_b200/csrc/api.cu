@@ -923,7 +923,10 @@ bwta_status_t attn_prefill_impl(const uint32_t* q_sgn, const uint32_t* q_nz, con
                                 const float* beta_heads, void* o, bwta_dtype_t o_dt,
                                 int64_t ld_o, int64_t o_bstride, int64_t o_hstride, uint32_t* p_out,
                                 int64_t ldp_words, int pack, float out_scale, bwta_kind_t out_kind,
-                                uint32_t* out_sgn, uint32_t* out_nz, int64_t out_ld_words, void* stream) {
+                                uint32_t* out_sgn, uint32_t* out_nz, int64_t out_ld_words, void* stream,
+                                int causal = 0) {
+    if (causal != 0 && causal != 1) return BWTA_ERR_INVALID_VALUE;
+    if (causal && tk < tq) return BWTA_ERR_SHAPE;  // every query row needs at least one key
     if (pack) {
         if (o_dt != BWTA_F16 && o_dt != BWTA_BF16) return BWTA_ERR_UNSUPPORTED;  // the rounding being packed
         if (out_kind != BWTA_TERNARY && out_kind != BWTA_BOOL) return BWTA_ERR_UNSUPPORTED;
@@ -958,6 +961,7 @@ bwta_status_t attn_prefill_impl(const uint32_t* q_sgn, const uint32_t* q_nz, con
     st = check_device();
     if (st != BWTA_OK) return st;
     AttnPrefillArgs a{};
+    a.causal = causal;
     a.q_sgn = q_sgn;
     a.q_nz = q_nz;
     a.k_sgn = k_sgn;
@@ -1046,6 +1050,21 @@ bwta_status_t bwta_attn_prefill(const uint32_t* q_sgn, const uint32_t* q_nz, con
                              q_hstride, ldk_words, k_bstride, k_hstride, ldv_words, v_bstride, v_hstride, alpha, s_att,
                              p_dt, beta, alpha_heads, beta_heads, o, o_dt, ld_o, o_bstride, o_hstride, p_out,
                              ldp_words, 0, 0.f, BWTA_TERNARY, nullptr, nullptr, 0, stream);
+}
+
+bwta_status_t bwta_attn_prefill_ex(const uint32_t* q_sgn, const uint32_t* q_nz, const uint32_t* k_sgn,
+                                   const uint32_t* k_nz, const uint32_t* vt_sgn, const uint32_t* vt_nz, int64_t batch,
+                                   int64_t heads, int64_t tq, int64_t tk, int64_t dh, int64_t ldq_words,
+                                   int64_t q_bstride, int64_t q_hstride, int64_t ldk_words, int64_t k_bstride,
+                                   int64_t k_hstride, int64_t ldv_words, int64_t v_bstride, int64_t v_hstride,
+                                   float alpha, float s_att, bwta_dtype_t p_dt, float beta, const float* alpha_heads,
+                                   const float* beta_heads, void* o, bwta_dtype_t o_dt, int64_t ld_o,
+                                   int64_t o_bstride, int64_t o_hstride, uint32_t* p_out, int64_t ldp_words,
+                                   int causal, void* stream) {
+    return attn_prefill_impl(q_sgn, q_nz, k_sgn, k_nz, vt_sgn, vt_nz, batch, heads, tq, tk, dh, ldq_words, q_bstride,
+                             q_hstride, ldk_words, k_bstride, k_hstride, ldv_words, v_bstride, v_hstride, alpha, s_att,
+                             p_dt, beta, alpha_heads, beta_heads, o, o_dt, ld_o, o_bstride, o_hstride, p_out,
+                             ldp_words, 0, 0.f, BWTA_TERNARY, nullptr, nullptr, 0, stream, causal);
 }
 
 bwta_status_t bwta_attn_prefill_pack(const uint32_t* q_sgn, const uint32_t* q_nz, const uint32_t* k_sgn,

@@ -75,9 +75,21 @@ constexpr int SMEM_AP = 1024 + 2 * Q_CODES + AP_S * STAGE_B + AP_VS * V_CODES + 
 static_assert(SMEM_AP <= 227 * 1024, "shared memory");
 constexpr int TM_S = 0, TM_O = 256, TM_SF = 384;  // TMEM columns: S[0], S[1], O, scale factors
 __device__ __forceinline__ uint32_t ap_fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
+// key blocks an item reads: all of them, or (causal) those holding a key <= the tile's last row + coff
+template <typename P>
+__device__ __forceinline__ int item_blocks(const P& p, int64_t t) {
+    if (!p.causal) return p.nblk;
+    const int64_t q0 = int64_t(uint32_t(t) - ap_fdiv(uint32_t(t), p.fd_qt) * p.fd_qt.d) * 128;
+    int64_t last = q0 + 127;
+    if (last > p.tq - 1) last = p.tq - 1;
+    const int64_t nb = (last + p.coff) / 128 + 1;
+    return int(nb < p.nblk ? nb : p.nblk);
+}
 
 struct ApParams {
     FastDiv fd_qt, fd_nh;  // item -> (entry, q tile), entry -> (batch, head): 32-bit multiply-shift
+    int causal;            // row i sees keys j <= i + coff only; key blocks past the tile's last row skipped
+    int64_t coff;          // tk - tq
     int64_t nh, tq, tk;
     int dh, dhp;           // head_dim, rounded up to 16 (PV MMA N, V^T box rows)
     int q_tiles, nblk;
@@ -239,7 +251,6 @@ __global__ void __launch_bounds__(AP_NT, 1)
     pdl_launch_dependents();
     pdl_wait();
 
-    const int nblk = p.nblk;
     if (warp == 0) {
         // ------------------------------ TMA producer ------------------------------
         if (lane == 0) {
@@ -259,8 +270,9 @@ __global__ void __launch_bounds__(AP_NT, 1)
                 uint8_t* qbits = sQb + qb * Q_BITS;
                 tma_load_4d(qbits, &tmQs, &q_full[qb], 0, qr, eh, eb);
                 tma_load_4d(qbits + AP_BQ * 16, &tmQn, &q_full[qb], 0, qr, eh, eb);
+                const int nbi = item_blocks(p, t);
                 for (int pass = 0; pass < 2; ++pass) {
-                    for (int j = 0; j < nblk; ++j, ++g) {
+                    for (int j = 0; j < nbi; ++j, ++g) {
                         if (pass && j % VCH_BLK == 0) {  // the next 1024 keys of V^T (both planes)
                             const int cb = vc & 1;
                             wait_bar(&vc_empty[cb], uint32_t((vc >> 1) & 1) ^ 1u);
@@ -302,12 +314,13 @@ __global__ void __launch_bounds__(AP_NT, 1)
             tc_commit_w(&k_empty[st]);
         };
         for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++ic) {
+            const int nbi = item_blocks(p, t);
             const int qb = ic & 1;
             const uint32_t qa = smem_u32(sQ + qb * Q_CODES);
             wait_bar(&q_ready[qb], uint32_t((ic >> 1) & 1));
             tc_fence_after();
             // pass 1: S blocks for the row statistics
-            for (int j = 0; j < nblk; ++j, ++g, ++sg) {
+            for (int j = 0; j < nbi; ++j, ++g, ++sg) {
                 const int st = g % AP_S, sb = sg & 1;
                 wait_bar(&k_ready[st], uint32_t((g / AP_S) & 1));
                 wait_bar(&s_free[sb], uint32_t((sg >> 1) & 1) ^ 1u);
@@ -316,14 +329,14 @@ __global__ void __launch_bounds__(AP_NT, 1)
                 __syncwarp();
             }
             // pass 2: QK^T of block j + 1 is issued before PV of block j (S is double-buffered)
-            for (int j = 0; j <= nblk; ++j) {
-                if (j < nblk) {
+            for (int j = 0; j <= nbi; ++j) {
+                if (j < nbi) {
                     const int gj = g + j, sgj = sg + j, st = gj % AP_S, sb = sgj & 1;
                     wait_bar(&k_ready[st], uint32_t((gj / AP_S) & 1));
                     wait_bar(&s_free[sb], uint32_t((sgj >> 1) & 1) ^ 1u);
                     tc_fence_after();
                     qk(qa, st, sb);
-                    if (j == nblk - 1) tc_commit_w(&q_empty[qb]);  // the last read of this item's Q codes
+                    if (j == nbi - 1) tc_commit_w(&q_empty[qb]);  // the last read of this item's Q codes
                     __syncwarp();
                 }
                 if (j >= 1) {
@@ -342,20 +355,21 @@ __global__ void __launch_bounds__(AP_NT, 1)
                                        idesc_pv, sf, sf + 8, (jj | k) != 0);
                         tc_commit_w(&p_free[pb]);
                         tc_commit_w(&v_empty[vs]);
-                        if (jj == nblk - 1) tc_commit_w(o_full);
+                        if (jj == nbi - 1) tc_commit_w(o_full);
                     }
                     __syncwarp();
                     ++pg;
                 }
             }
-            g += nblk;
-            sg += nblk;
+            g += nbi;
+            sg += nbi;
         }
     } else if (warp >= 4 && warp < 8) {
         // ------------------------------ unpack (Q, K, V^T planes -> codes) ------------------------------
         const int ut = threadIdx.x - 128;
         int g = 0, ic = 0, vc = 0, pg = 0;
         for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++ic) {
+            const int nbi = item_blocks(p, t);
             const int qb = ic & 1;
             wait_bar(&q_full[qb], uint32_t((ic >> 1) & 1));
             const uint32_t qbits = smem_u32(sQb + qb * Q_BITS);
@@ -367,7 +381,7 @@ __global__ void __launch_bounds__(AP_NT, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&q_ready[qb]);
             for (int pass = 0; pass < 2; ++pass) {
-                for (int j = 0; j < nblk; ++j, ++g) {
+                for (int j = 0; j < nbi; ++j, ++g) {
                     const int st = g % AP_S;
                     wait_bar(&k_full[st], uint32_t((g / AP_S) & 1));
                     const uint32_t kc = smem_u32(sStage + st * STAGE_B);
@@ -389,9 +403,9 @@ __global__ void __launch_bounds__(AP_NT, 1)
                         __syncwarp();
                         if (lane == 0) {
                             mbar_arrive(&v_ready[vs]);
-                            if (j % VCH_BLK == VCH_BLK - 1 || j == nblk - 1) mbar_arrive(&vc_empty[cb]);
+                            if (j % VCH_BLK == VCH_BLK - 1 || j == nbi - 1) mbar_arrive(&vc_empty[cb]);
                         }
-                        if (j % VCH_BLK == VCH_BLK - 1 || j == nblk - 1) ++vc;
+                        if (j % VCH_BLK == VCH_BLK - 1 || j == nbi - 1) ++vc;
                         ++pg;
                     }
                 }
@@ -405,10 +419,14 @@ __global__ void __launch_bounds__(AP_NT, 1)
         const float MAGIC = 12582912.f;                    // 1.5 * 2^23: float_as_int(x + MAGIC) = 0x4B400000 + x
         int sg = 0, pg = 0, ic = 0;
         for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++ic) {
+            const int nbi = item_blocks(p, t);
             const uint32_t e = ap_fdiv(uint32_t(t), p.fd_qt);
             const int64_t qrow = int64_t(uint32_t(t) - e * p.fd_qt.d) * AP_BQ + r;
             const uint32_t eb_ = ap_fdiv(e, p.fd_nh);
             const int eb = int(eb_), eh = int(e - eb_ * p.fd_nh.d);
+            // keys this row may see: all tk, or (causal) those <= qrow + coff (masked keys are not keys:
+            // out of the max, the normaliser and P, exactly as keys past tk)
+            const int64_t klim = p.causal ? (qrow + p.coff + 1 < p.tk ? qrow + p.coff + 1 : p.tk) : p.tk;
             float alpha = p.alpha, beta = p.beta;
             uint32_t tbl_s = smem_u32(tbl);
             if (p.alpha_h) {  // this head's |alpha|: its own exp table (double-buffered by item parity)
@@ -422,13 +440,13 @@ __global__ void __launch_bounds__(AP_NT, 1)
             if (p.beta_h) beta = __ldg(p.beta_h + eh);
             // ---- pass 1: R = running max of the integer dots (|alpha|-signed), z = sum exp(|alpha| (d - R))
             float R = -INFINITY, z = 0.f;
-            for (int j = 0; j < nblk; ++j, ++sg) {
+            for (int j = 0; j < nbi; ++j, ++sg) {
                 const int sb = sg & 1;
                 if (p.dbg & 16) wait_spin(&s_full[sb], uint32_t((sg >> 1) & 1));
                 else wait_bar(&s_full[sb], uint32_t((sg >> 1) & 1));
                 tc_fence_after();
                 const int64_t k0 = int64_t(j) * AP_BK + AP_KW * h;
-                const int valid = p.tk - k0 >= AP_KW ? AP_KW : int(p.tk - k0 > 0 ? p.tk - k0 : 0);
+                const int valid = klim - k0 >= AP_KW ? AP_KW : int(klim - k0 > 0 ? klim - k0 : 0);
 #pragma unroll 1
                 for (int gg = 0; gg < AP_NG; ++gg) {  // 32 keys at a time (register budget)
                     uint32_t v[32];
@@ -495,13 +513,13 @@ __global__ void __launch_bounds__(AP_NT, 1)
             }
             const float dthr = float(lo);
             // ---- pass 2: P codes of each block, then O += P . V^T on the tensor core
-            for (int j = 0; j < nblk; ++j, ++sg, ++pg) {
+            for (int j = 0; j < nbi; ++j, ++sg, ++pg) {
                 const int sb = sg & 1, pb = pg & 1;
                 if (p.dbg & 16) wait_spin(&s_full[sb], uint32_t((sg >> 1) & 1));
                 else wait_bar(&s_full[sb], uint32_t((sg >> 1) & 1));
                 tc_fence_after();
                 const int64_t k0 = int64_t(j) * AP_BK + AP_KW * h;
-                const int valid = p.tk - k0 >= AP_KW ? AP_KW : int(p.tk - k0 > 0 ? p.tk - k0 : 0);
+                const int valid = klim - k0 >= AP_KW ? AP_KW : int(klim - k0 > 0 ? klim - k0 : 0);
                 uint32_t code[AP_NG][4], bits[AP_NG];
 #pragma unroll
                 for (int gg = 0; gg < AP_NG; ++gg) {
@@ -631,6 +649,9 @@ cudaError_t launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t s) {
     p.q_tiles = int((a.tq + AP_BQ - 1) / AP_BQ);
     p.nblk = int((a.tk + AP_BK - 1) / AP_BK);
     p.items = entries * p.q_tiles;
+    p.causal = a.causal;
+    p.coff = a.tk - a.tq;
+    if (a.causal && a.tk < a.tq) return cudaErrorInvalidValue;  // every row needs at least one key
     if (p.items >= (int64_t(1) << 31) || a.nh >= (int64_t(1) << 31)) return cudaErrorNotSupported;
     p.fd_qt = make_fastdiv(uint32_t(p.q_tiles));
     p.fd_nh = make_fastdiv(uint32_t(a.nh));

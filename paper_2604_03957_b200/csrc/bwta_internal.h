@@ -223,6 +223,7 @@ struct AttnPrefillArgs {
     uint32_t *po_sgn = nullptr, *po_nz = nullptr;
     int64_t po_ld = 0;
     float po_tp = 0.f, po_tn = 0.f;
+    int causal = 0;  // query row i attends to keys j <= i + (tk - tq) only (tk >= tq)
 };
 bool attn_prefill_supported(const AttnPrefillArgs& a);
 cudaError_t launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t s);

@@ -26,13 +26,16 @@ CASES = [  # b, h, tq, tk, dh, binary K, p dtype, alpha sign
 ]
 
 
-def _oracle_rows(oq, ok, ov, alpha, s_att, pname, beta, out):
-    """oracle.attn_decode over every query row (K and V^T repeated per row)."""
+def _oracle_rows(oq, ok, ov, alpha, s_att, pname, beta, out, causal=False):
+    """oracle.attn_decode over every query row (K and V^T repeated per row); causal: row i sees
+    keys j <= i + Tk - Tq (the oracle's nkeys mask)."""
     bh, tq, dh = oq.shape
+    tk = ok.shape[1]
     qq = oq.reshape(bh * tq, dh)
     kk = np.repeat(ok, tq, axis=0)
     vv = np.repeat(ov, tq, axis=0)
-    return oracle.attn_decode(qq, kk, vv, alpha, s_att, pname, beta, out, threads=oracle.default_threads())
+    nk = np.tile(np.arange(tq) + (tk - tq) + 1, bh) if causal else None
+    return oracle.attn_decode(qq, kk, vv, alpha, s_att, pname, beta, out, threads=oracle.default_threads(), nkeys=nk)
 
 
 @pytest.mark.gpu
@@ -209,3 +212,73 @@ def test_attn_per_head_scales(B):
     got = B.bwta_attn_prefill_pack(qp, kp, vt, 1.0, s_att, 1.0, s_ctx, alpha_heads=ah, beta_heads=bh)
     ref = B.bwta_pack_act(ctx, s_ctx)
     assert torch.equal(got.nz, ref.nz) and torch.equal(got.sgn, ref.sgn)
+
+
+CAUSAL_CASES = [  # b, h, tq, tk, dh, binary K, p dtype
+    (1, 2, 128, 128, 128, False, torch.float16),
+    (2, 2, 300, 300, 64, False, torch.bfloat16),
+    (1, 1, 130, 400, 128, True, torch.float16),
+    (1, 2, 257, 1100, 96, False, torch.float32),
+    (1, 1, 5, 2100, 128, False, torch.float16),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", range(len(CAUSAL_CASES)))
+def test_attn_prefill_causal_parity(B, case):
+    """causal = 1 (bwta_attn_prefill_ex): row i sees keys j <= i + Tk - Tq; against the oracle's
+    masked composition under R13's counted tolerance, masked P bits exactly zero, O equal where P
+    agrees, and the unfused PV of the kernel's own P bits equal to its O."""
+    b, h, tq, tk, dh, kbin, p_dt = CAUSAL_CASES[case]
+    seed = 9700 + 10 * case
+    q = gen.activations((b, h, tq, dh), seed)
+    k = gen.activations((b, h, tk, dh), seed + 1)
+    v = gen.activations((b, h, tk, dh), seed + 2)
+    sq, sk, sv = gen.act_scale(q), gen.act_scale(k), gen.act_scale(v)
+    alpha = float(np.float32(sq * sk / np.sqrt(dh)))
+    s_att = float(np.float32(2.0 / tk))
+    beta = float(np.float32(s_att * sv))
+    qp = B.bwta_pack_act(q.cuda(), sq, "ternary")
+    if kbin:
+        kb = B.bwta_pack_weight(k.reshape(-1, dh).cuda())
+        kp = type(qp)(kb.sgn.reshape(b, h, tk, -1), None, "binary", dh)
+    else:
+        kp = B.bwta_pack_act(k.cuda(), sk, "ternary")
+    vt = B.bwta_pack_act(v.cuda(), sv, "ternary", transpose=True)
+    pname = DT[p_dt]
+    o16, pbits = B.bwta_attn_prefill(qp, kp, vt, alpha, s_att, beta, torch.float16, p_dt, return_p=True, causal=True)
+    oi = B.bwta_attn_prefill(qp, kp, vt, alpha, s_att, beta, torch.int32, p_dt, causal=True)
+    oq = oracle.quantize_act(storage(q).reshape(b * h, tq, dh), "f16", sq, "ternary")
+    if kbin:
+        ok = oracle.binarize_weight(storage(k).reshape(-1, dh), "f16").reshape(b * h, tk, dh)
+    else:
+        ok = oracle.quantize_act(storage(k).reshape(b * h, tk, dh), "f16", sk, "ternary")
+    ov = oracle.quantize_act(storage(v).reshape(b * h, tk, dh), "f16", sv, "ternary")
+    ref_i, pb, p64 = _oracle_rows(oq, ok, ov, alpha, s_att, pname, beta, "i32", causal=True)
+    ref_16, _, _ = _oracle_rows(oq, ok, ov, alpha, s_att, pname, beta, "f16", causal=True)
+    got_bits = oracle.unpack(None, words(pbits).reshape(b * h * tq, -1), "bool", tk).astype(np.int8)
+    rows = np.tile(np.arange(tq), b * h)
+    masked = np.arange(tk)[None, :] > (rows + tk - tq)[:, None]
+    assert got_bits[masked].sum() == 0, "a masked key got a P bit"
+    diff = got_bits != pb
+    t = s_att / 2
+    assert np.all(np.abs(p64[diff] / t - 1.0) < 2.0 ** -8), "P differs away from the threshold"
+    flips = diff.sum(axis=1)
+    gi = oi.cpu().numpy().reshape(b * h * tq, dh)
+    assert np.all(np.abs(gi - ref_i) <= flips[:, None])
+    g16 = out_storage(o16).reshape(b * h * tq, dh)
+    same = flips == 0
+    assert np.array_equal(g16[same], ref_16[same])
+    assert pb.sum() > 0 and flips.sum() <= max(2, pb.size // 10000)
+    pp = type(qp)(None, pbits.reshape(b, h, tq, -1), "bool", tk)
+    o_unf = B.bwta_attn_pv(pp, vt, beta, out_dtype=torch.int32)
+    assert torch.equal(o_unf.reshape(-1, dh).cpu(), oi.reshape(-1, dh).cpu())
+
+
+@pytest.mark.gpu
+def test_attn_prefill_causal_rejects_tk_below_tq(B):
+    q = B.bwta_pack_act(gen.activations((1, 1, 64, 64), 1).cuda(), 1.0)
+    k = B.bwta_pack_act(gen.activations((1, 1, 32, 64), 2).cuda(), 1.0)
+    vt = B.bwta_pack_act(gen.activations((1, 1, 32, 64), 3).cuda(), 1.0, transpose=True)
+    with pytest.raises(B.BwtaError):
+        B.bwta_attn_prefill(q, k, vt, 0.1, 0.05, 0.1, causal=True)

@@ -437,3 +437,42 @@ def test_attn_decode_key_permutation_invariance():
     o2, pb2, _ = oracle.attn_decode(qq, qk[:, perm], qv[:, perm], 0.09, 2.0 / tk, "f16", 0.01, "f16")
     assert np.array_equal(pb1[:, perm], pb2) and np.array_equal(o1, o2)
     assert 0 < pb1.sum() < pb1.size
+
+
+def test_attn_causal_mask_uniform_scores_give_prefix_sums():
+    """Causal mask (nkeys): alpha = 0 makes every visible score 0, so row b's softmax is uniform
+    1 / n_b over its first n_b keys and 0 beyond; with s_att = 1 / n_max every visible p clears
+    the threshold 1 / (2 n_max) and O = beta * (sum of the first n_b value rows) -- a closed form,
+    independent of the unmasked path."""
+    rng = np.random.default_rng(14)
+    bh, tk, dh = 4, 40, 64
+    nk = np.array([1, 7, 33, 40])
+    qq = rng.integers(-1, 2, (bh, dh)).astype(np.int8)
+    qk = rng.integers(-1, 2, (bh, tk, dh)).astype(np.int8)
+    qv = rng.integers(-1, 2, (bh, tk, dh)).astype(np.int8)
+    o, pb, p = oracle.attn_decode(qq, qk, qv, 0.0, 1.0 / tk, "f16", 0.25, "f32", nkeys=nk)
+    for b in range(bh):
+        assert np.allclose(p[b, :nk[b]], 1.0 / nk[b]) and np.all(p[b, nk[b]:] == 0)
+        assert pb[b, :nk[b]].all() and pb[b, nk[b]:].sum() == 0
+        ref = (qv[b, :nk[b]].sum(axis=0).astype(np.float32) * np.float32(0.25)).astype(np.float32)
+        assert np.array_equal(o[b], ref)
+
+
+def test_attn_causal_mask_is_truncation():
+    """A row that sees its first n keys gives the same P (on those keys) and O as the unmasked
+    composition on K[:n], V[:n] (masked keys are not keys); all keys visible == unmasked."""
+    rng = np.random.default_rng(15)
+    bh, tk, dh = 3, 200, 128
+    qq = rng.integers(-1, 2, (bh, dh)).astype(np.int8)
+    qk = rng.integers(-1, 2, (bh, tk, dh)).astype(np.int8)
+    qv = rng.integers(-1, 2, (bh, tk, dh)).astype(np.int8)
+    nk = np.array([5, 120, tk])
+    o, pb, _ = oracle.attn_decode(qq, qk, qv, 0.09, 2.0 / 64, "f16", 0.01, "f16", nkeys=nk)
+    for b in range(bh):
+        n = nk[b]
+        o1, pb1, _ = oracle.attn_decode(qq[b:b + 1], qk[b:b + 1, :n], qv[b:b + 1, :n], 0.09, 2.0 / 64, "f16", 0.01,
+                                        "f16")
+        assert np.array_equal(pb[b, :n], pb1[0]) and pb[b, n:].sum() == 0
+        assert np.array_equal(o[b], o1[0])
+    ou, pbu, _ = oracle.attn_decode(qq, qk, qv, 0.09, 2.0 / 64, "f16", 0.01, "f16")
+    assert np.array_equal(o[2], ou[2]) and np.array_equal(pb[2], pbu[2])
