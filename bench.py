@@ -531,7 +531,16 @@ def llama_attn(B, dev, seed=404, heads=32, seq=2048, D=128):
 
     def op_fused():   # QK^T -> fp32 softmax -> bool P -> PV in one launch (N3); S and P stay on chip
         B.bwta_attn_prefill(st["qp"], st["kp"], st["vt"], alpha, s_att, beta, out=O2)
+
+    def op_causal():  # the decoder's causal mask: key blocks above the diagonal skipped
+        B.bwta_attn_prefill(st["qp"], st["kp"], st["vt"], alpha, s_att, beta, out=O3, causal=True)
     O2 = torch.empty((1, heads, seq, D), dtype=torch.float16, device=q.device)
+    O3 = torch.empty((1, heads, seq, D), dtype=torch.float16, device=q.device)
+    cmask = torch.ones((seq, seq), dtype=torch.bool, device=q.device).triu(1)
+
+    def torch_causal():
+        s_ = torch.matmul(q, k.transpose(-1, -2)).float() * alpha
+        return torch.matmul(torch.softmax(s_.masked_fill(cmask, float("-inf")), -1).half(), v)
     op_pack_qkv(); op_pack_p()  # noqa: E702
     n = heads * seq * D
     ops = [Op("pack_qkv", "pack", op_pack_qkv, 0, 3 * (2 * n + n / 4)),
@@ -542,7 +551,10 @@ def llama_attn(B, dev, seed=404, heads=32, seq=2048, D=128):
               lambda: torch.matmul(P, v)),
            # the fused op does both products (4 T^2 D ops); baseline: torch fp16 QK^T, fp32 softmax, PV
            Op("attn_prefill_fused", "attn", op_fused, 4 * heads * seq * seq * D, 2 * n / 4 + n / 4 + 2 * n,
-              lambda: torch.matmul(torch.softmax(torch.matmul(q, k.transpose(-1, -2)).float() * alpha, -1).half(), v))]
+              lambda: torch.matmul(torch.softmax(torch.matmul(q, k.transpose(-1, -2)).float() * alpha, -1).half(), v)),
+           # causal: the products over the visible keys only (4 D per (query, visible key) pair)
+           Op("attn_prefill_causal", "attn", op_causal, 4 * heads * (seq * (seq + 1) // 2) * D,
+              2 * n / 4 + n / 4 + 2 * n, torch_causal)]
     cfg = {"workload": "llama_attn (configs[3]): ternary attention, 32 heads, head_dim 128, seq 2048 (step: Q/K/V^T "
                        "packs + the fused prefill attention; the unfused ops are timed alongside)",
            "heads": heads, "seq_len": seq, "head_dim": D}

@@ -75,6 +75,20 @@ constexpr int SMEM_AP = 1024 + 2 * Q_CODES + AP_S * STAGE_B + AP_VS * V_CODES + 
 static_assert(SMEM_AP <= 227 * 1024, "shared memory");
 constexpr int TM_S = 0, TM_O = 256, TM_SF = 384;  // TMEM columns: S[0], S[1], O, scale factors
 __device__ __forceinline__ uint32_t ap_fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
+// The item of loop slot tr (= round k * gridDim + CTA b).  Causal items differ in length (q tile
+// i reads i + 1 key blocks when tq == tk), so they go heaviest first (q tiles descending, entries
+// fastest) and alternate rounds assign them in reverse CTA order (a zigzag, which pairs a CTA's
+// heavy item with a light one): every CTA ends up with about the same number of key blocks.
+template <typename P>
+__device__ __forceinline__ int64_t item_at(const P& p, int64_t tr) {
+    if (!p.causal) return tr;
+    const uint32_t g = gridDim.x, k = uint32_t(tr) / g, b = uint32_t(tr) - k * g;
+    const uint32_t i = k * g + ((k & 1) ? g - 1 - b : b);
+    if (i >= uint32_t(p.items)) return p.items;
+    const uint32_t r = ap_fdiv(i, p.fd_ent);          // heaviness rank: q tile = Q - 1 - r
+    const uint32_t e = i - r * p.fd_ent.d;
+    return int64_t(e) * p.fd_qt.d + (p.fd_qt.d - 1 - r);
+}
 // key blocks an item reads: all of them, or (causal) those holding a key <= the tile's last row + coff
 template <typename P>
 __device__ __forceinline__ int item_blocks(const P& p, int64_t t) {
@@ -89,6 +103,7 @@ __device__ __forceinline__ int item_blocks(const P& p, int64_t t) {
 struct ApParams {
     FastDiv fd_qt, fd_nh;  // item -> (entry, q tile), entry -> (batch, head): 32-bit multiply-shift
     int causal;            // row i sees keys j <= i + coff only; key blocks past the tile's last row skipped
+    FastDiv fd_ent;        // entries (causal schedule)
     int64_t coff;          // tk - tq
     int64_t nh, tq, tk;
     int dh, dhp;           // head_dim, rounded up to 16 (PV MMA N, V^T box rows)
@@ -257,7 +272,9 @@ __global__ void __launch_bounds__(AP_NT, 1)
             const uint32_t kbytes = uint32_t((p.k_kind == B_TERNARY ? 2 : 1) * AP_BK * 16);
             const uint32_t vbytes = uint32_t(2 * p.dhp * VCH_W * 4);
             int g = 0, ic = 0, vc = 0;
-            for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++ic) {
+            for (int64_t tr = blockIdx.x; tr - blockIdx.x < p.items; tr += gridDim.x, ++ic) {
+            const int64_t t = item_at(p, tr);
+            if (t >= p.items) continue;  // (only in the last round)
                 const uint32_t e = ap_fdiv(uint32_t(t), p.fd_qt);
                 const int q0 = int(uint32_t(t) - e * p.fd_qt.d) * AP_BQ;
                 const uint32_t eb_ = ap_fdiv(e, p.fd_nh);
@@ -313,7 +330,9 @@ __global__ void __launch_bounds__(AP_NT, 1)
             tc_commit_w(&s_full[sb]);
             tc_commit_w(&k_empty[st]);
         };
-        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++ic) {
+        for (int64_t tr = blockIdx.x; tr - blockIdx.x < p.items; tr += gridDim.x, ++ic) {
+            const int64_t t = item_at(p, tr);
+            if (t >= p.items) continue;  // (only in the last round)
             const int nbi = item_blocks(p, t);
             const int qb = ic & 1;
             const uint32_t qa = smem_u32(sQ + qb * Q_CODES);
@@ -368,7 +387,9 @@ __global__ void __launch_bounds__(AP_NT, 1)
         // ------------------------------ unpack (Q, K, V^T planes -> codes) ------------------------------
         const int ut = threadIdx.x - 128;
         int g = 0, ic = 0, vc = 0, pg = 0;
-        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++ic) {
+        for (int64_t tr = blockIdx.x; tr - blockIdx.x < p.items; tr += gridDim.x, ++ic) {
+            const int64_t t = item_at(p, tr);
+            if (t >= p.items) continue;  // (only in the last round)
             const int nbi = item_blocks(p, t);
             const int qb = ic & 1;
             wait_bar(&q_full[qb], uint32_t((ic >> 1) & 1));
@@ -418,7 +439,9 @@ __global__ void __launch_bounds__(AP_NT, 1)
         const uint32_t lane_base = tmem + (uint32_t(32 * q) << 16);
         const float MAGIC = 12582912.f;                    // 1.5 * 2^23: float_as_int(x + MAGIC) = 0x4B400000 + x
         int sg = 0, pg = 0, ic = 0;
-        for (int64_t t = blockIdx.x; t < p.items; t += gridDim.x, ++ic) {
+        for (int64_t tr = blockIdx.x; tr - blockIdx.x < p.items; tr += gridDim.x, ++ic) {
+            const int64_t t = item_at(p, tr);
+            if (t >= p.items) continue;  // (only in the last round)
             const int nbi = item_blocks(p, t);
             const uint32_t e = ap_fdiv(uint32_t(t), p.fd_qt);
             const int64_t qrow = int64_t(uint32_t(t) - e * p.fd_qt.d) * AP_BQ + r;
@@ -651,6 +674,7 @@ cudaError_t launch_attn_prefill(const AttnPrefillArgs& a, cudaStream_t s) {
     p.items = entries * p.q_tiles;
     p.causal = a.causal;
     p.coff = a.tk - a.tq;
+    p.fd_ent = make_fastdiv(uint32_t(entries));
     if (a.causal && a.tk < a.tq) return cudaErrorInvalidValue;  // every row needs at least one key
     if (p.items >= (int64_t(1) << 31) || a.nh >= (int64_t(1) << 31)) return cudaErrorNotSupported;
     p.fd_qt = make_fastdiv(uint32_t(p.q_tiles));
