@@ -74,6 +74,9 @@ constexpr int SMEM_AP = 1024 + 2 * Q_CODES + AP_S * STAGE_B + AP_VS * V_CODES + 
                         2 * Q_BITS + 4 * 1024 /*tables*/ + 2 * AP_NH * AP_BQ * 4 * 2 /*merge*/ + 512 /*barriers*/;
 static_assert(SMEM_AP <= 227 * 1024, "shared memory");
 constexpr int TM_S = 0, TM_O = 256, TM_SF = 384;  // TMEM columns: S[0], S[1], O, scale factors
+#ifndef AP_REUSE
+#define AP_REUSE 1  // items with one key block: pass 2 reuses pass 1's S (no second K load / unpack / QK^T)
+#endif
 __device__ __forceinline__ uint32_t ap_fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
 // The item of loop slot tr (= round k * gridDim + CTA b).  Causal items differ in length (q tile
 // i reads i + 1 key blocks when tq == tk), so they go heaviest first (q tiles descending, entries
@@ -288,8 +291,9 @@ __global__ void __launch_bounds__(AP_NT, 1)
                 tma_load_4d(qbits, &tmQs, &q_full[qb], 0, qr, eh, eb);
                 tma_load_4d(qbits + AP_BQ * 16, &tmQn, &q_full[qb], 0, qr, eh, eb);
                 const int nbi = item_blocks(p, t);
+                const bool reuse = AP_REUSE && nbi == 1;  // one key block: pass 2 reuses pass 1's S
                 for (int pass = 0; pass < 2; ++pass) {
-                    for (int j = 0; j < nbi; ++j, ++g) {
+                    for (int j = 0; j < nbi; ++j) {
                         if (pass && j % VCH_BLK == 0) {  // the next 1024 keys of V^T (both planes)
                             const int cb = vc & 1;
                             wait_bar(&vc_empty[cb], uint32_t((vc >> 1) & 1) ^ 1u);
@@ -299,8 +303,10 @@ __global__ void __launch_bounds__(AP_NT, 1)
                             tma_load_4d(vb + p.dhp * VCH_W * 4, &tmVn, &vc_full[cb], VCH_W * (j / VCH_BLK), 0, eh, eb);
                             ++vc;
                         }
+                        if (pass && reuse) continue;  // no second K load
                         const int st = g % AP_S;
-                        wait_bar(&k_empty[st], uint32_t((g / AP_S) & 1) ^ 1u);
+                        ++g;
+                        wait_bar(&k_empty[st], uint32_t(((g - 1) / AP_S) & 1) ^ 1u);
                         uint8_t* kb = sStage + st * STAGE_B + K_CODES;
                         const int kr = p.k_wide ? j * (AP_BK / 16) : j * AP_BK;
                         mbar_arrive_expect_tx(&k_full[st], kbytes);
@@ -347,9 +353,12 @@ __global__ void __launch_bounds__(AP_NT, 1)
                 qk(qa, st, sb);
                 __syncwarp();
             }
-            // pass 2: QK^T of block j + 1 is issued before PV of block j (S is double-buffered)
+            // pass 2: QK^T of block j + 1 is issued before PV of block j (S is double-buffered); with
+            // one key block pass 1's S is still in its buffer (the softmax warps hold it): no second QK^T
+            const bool reuse = AP_REUSE && nbi == 1;
+            if (reuse) tc_commit_w(&q_empty[qb]);  // the Q codes' last reader was pass 1's QK^T
             for (int j = 0; j <= nbi; ++j) {
-                if (j < nbi) {
+                if (j < nbi && !reuse) {
                     const int gj = g + j, sgj = sg + j, st = gj % AP_S, sb = sgj & 1;
                     wait_bar(&k_ready[st], uint32_t((gj / AP_S) & 1));
                     wait_bar(&s_free[sb], uint32_t((sgj >> 1) & 1) ^ 1u);
@@ -380,8 +389,10 @@ __global__ void __launch_bounds__(AP_NT, 1)
                     ++pg;
                 }
             }
-            g += nbi;
-            sg += nbi;
+            if (!reuse) {
+                g += nbi;
+                sg += nbi;
+            }
         }
     } else if (warp >= 4 && warp < 8) {
         // ------------------------------ unpack (Q, K, V^T planes -> codes) ------------------------------
@@ -401,15 +412,19 @@ __global__ void __launch_bounds__(AP_NT, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&q_ready[qb]);
+            const bool reuse = AP_REUSE && nbi == 1;
             for (int pass = 0; pass < 2; ++pass) {
-                for (int j = 0; j < nbi; ++j, ++g) {
-                    const int st = g % AP_S;
-                    wait_bar(&k_full[st], uint32_t((g / AP_S) & 1));
-                    const uint32_t kc = smem_u32(sStage + st * STAGE_B);
-                    if (!(p.dbg & 8)) unpack_rows<128>(p.k_kind, kc + K_CODES, AP_BK * 16, kc, ut, AP_BK, 128);
-                    fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&k_ready[st]);
+                for (int j = 0; j < nbi; ++j) {
+                    if (!(pass && reuse)) {  // (one key block: no second K unpack)
+                        const int st = g % AP_S;
+                        wait_bar(&k_full[st], uint32_t((g / AP_S) & 1));
+                        ++g;
+                        const uint32_t kc = smem_u32(sStage + st * STAGE_B);
+                        if (!(p.dbg & 8)) unpack_rows<128>(p.k_kind, kc + K_CODES, AP_BK * 16, kc, ut, AP_BK, 128);
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&k_ready[st]);
+                    }
                     if (pass) {
                         const int cb = vc & 1, vs = pg % AP_VS;
                         if (j % VCH_BLK == 0) wait_bar(&vc_full[cb], uint32_t((vc >> 1) & 1));
@@ -462,6 +477,8 @@ __global__ void __launch_bounds__(AP_NT, 1)
             }
             if (p.beta_h) beta = __ldg(p.beta_h + eh);
             // ---- pass 1: R = running max of the integer dots (|alpha|-signed), z = sum exp(|alpha| (d - R))
+            // (one key block: its S buffer is kept for pass 2 -- released after pass 2 reads it)
+            const bool reuse = AP_REUSE && nbi == 1;
             float R = -INFINITY, z = 0.f;
             for (int j = 0; j < nbi; ++j, ++sg) {
                 const int sb = sg & 1;
@@ -475,7 +492,7 @@ __global__ void __launch_bounds__(AP_NT, 1)
                     uint32_t v[32];
                     tmem_ld_32x32b_x32(lane_base + uint32_t(TM_S + sb * AP_BK + AP_KW * h + 32 * gg), v);
                     tmem_wait_ld();
-                    if (gg == AP_NG - 1) {
+                    if (gg == AP_NG - 1 && !reuse) {
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&s_free[sb]);
@@ -536,6 +553,7 @@ __global__ void __launch_bounds__(AP_NT, 1)
             }
             const float dthr = float(lo);
             // ---- pass 2: P codes of each block, then O += P . V^T on the tensor core
+            if (reuse) --sg;  // the same S buffer and phase as pass 1
             for (int j = 0; j < nbi; ++j, ++sg, ++pg) {
                 const int sb = sg & 1, pb = pg & 1;
                 if (p.dbg & 16) wait_spin(&s_full[sb], uint32_t((sg >> 1) & 1));
