@@ -64,7 +64,15 @@ constexpr int A_GROUPS = BWTA_A_GROUPS;
 // (the fp16/bf16 TMA-store epilogue class only: the fused-pack and generic epilogues need more than
 // the 80 registers a 768-thread CTA leaves and spill -- BERT FFN1 + pack 17.3 -> 20.4 us)
 __host__ __device__ constexpr int a_groups(int ks, int eo) { return (ks == 256 && eo == 0) ? A_GROUPS : 1; }
-__host__ __device__ constexpr int nt_of(int ks, int eo) { return NT + 128 * (a_groups(ks, eo) - 1); }
+// Epilogue warps per TMEM lane quarter: 2, or 1 (E1) for the fp16/bf16 TMA-store class when a tile's
+// mainloop is long (K >= 2048): the epilogue's TMEM / shared-memory / issue bursts then slow the next
+// tile's mainloop less (a timeline showed stage periods of 1.1-1.5 k instead of ~0.82 k cycles while
+// the 8 epilogue warps drained a tile); the A groups then take warps 12-19 and the CTA has 20 warps.
+// Short-K tiles (BERT, K = 768) are epilogue-bound and keep 2 (1 warp: 11.3 -> 13.3 us).
+__host__ __device__ constexpr int epi_warps(int ks, int eo, bool e1) { return (e1 && ks == 256 && eo == 0) ? 1 : 2; }
+__host__ __device__ constexpr int nt_of(int ks, int eo, bool e1) {
+    return NT + 128 * (a_groups(ks, eo) - 1) - 128 * (2 - epi_warps(ks, eo, e1));
+}
 constexpr int OUT_BUF = 4096;
 constexpr int OUT_NBUF = 2;  // staging buffers per epilogue warp (fast path: store k overlaps the staging of k + 1)
 
@@ -187,7 +195,7 @@ struct Cfg {
     static constexpr int BBITS = BP * BNC * S::WPS * 4;
     static constexpr int STAGE = A_BYTES + B_BYTES + ABITS + BBITS;
     static constexpr int OUT_BYTES = 8 * OUT_NBUF * OUT_BUF;                // OUT_NBUF staging buffers per epilogue warp
-    static constexpr int SCALE_COLS = (BN + 127) / 128 * 64;                 // columns per epilogue warp
+    static constexpr int SCALE_COLS = BN;  // columns per epilogue warp (one warp per lane quarter: all BN)
     static constexpr int SCALE_BYTES = 8 * SCALE_COLS * 4;                  // per-warp column scales
     static constexpr int STAGES_FIT = (BWTA_SMEM_BUDGET - 1280 - OUT_BYTES - SCALE_BYTES - TRACE_BYTES) / STAGE;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
@@ -356,7 +364,7 @@ __device__ __forceinline__ void epi_tile_generic(const TcParams& p, const CUtens
 // fast tile: fp16/bf16 output through TMA (see above).  cs = this warp's
 // column scales (c * 2^-12, 64 per chunk) when column-scaled; cr = the
 // thread's four row scales (rows 16b + 8i + lane/4) when row-scaled.
-template <int BN, bool BF16>
+template <int BN, bool BF16, int EPW = 2>
 __device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorMap& tmY, const PeerMaps& pm,
                                               uint32_t tacc, uint8_t* stg0,
                                               const float* cs, bool col_scaled, const float (&cr)[4], int q, int h,
@@ -369,7 +377,7 @@ __device__ __forceinline__ void epi_tile_fast(const TcParams& p, const CUtensorM
     // stmatrix addresses: matrix mi = lane/8 (column group offset mi/2, row half mi%2), line li = lane%8
     const int mi = lane >> 3, li = lane & 7;
 #pragma unroll 1
-    for (int i = 0, c0 = h * CW; c0 < BN; ++i, c0 += 2 * CW) {
+    for (int i = 0, c0 = h * CW; c0 < BN; ++i, c0 += EPW * CW) {
         const int64_t n0 = int64_t(nt) * BN + c0;
         if (n0 >= p.N) break;
         uint8_t* stg = stg0 + (nstore % OUT_NBUF) * OUT_BUF;
@@ -599,7 +607,7 @@ __device__ __forceinline__ void epi_tile_pack(const TcParams& p, uint32_t tacc, 
 // EO = 0: the kernel only ever runs the fp16/bf16 TMA-store epilogue (the common case; the other
 // variants are not compiled in, which shrinks the instruction footprint); EO = 2: only the fused
 // next-layer pack; EO = 1: the generic epilogue (f32 / i32 outputs, layouts TMA cannot store).
-template <int BN, int ES, int CG, int EO>
+template <int BN, int ES, int CG, int EO, int EPW = 2>
 __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& tmY, const PeerMaps& pm,
                                          uint32_t tmem_base, uint8_t* sOut,
                                          float* sScale, uint64_t* tfull, uint64_t* tempty, int q, int h, int lane,
@@ -619,14 +627,14 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
         const int64_t mrow0 = int64_t(mt) * BM * CG + rank * BM;  // first kernel row of this CTA
         // with an odd number of 64-column chunks the two warps of a lane
         // quarter alternate which of them takes the extra chunk
-        const int hh = ((BN / 64) & 1) ? (h ^ (tix & 1)) : h;
+        const int hh = (EPW == 2 && ((BN / 64) & 1)) ? (h ^ (tix & 1)) : h;
         // scales of this tile (loaded before the accumulator is ready)
         const bool ok = fast_ok;
         float cr[4] = {0.f, 0.f, 0.f, 0.f};
         if (fast_ok) {
             if (col_scaled) {
                 // this warp's chunks: columns nt*BN + (2i + h)*64 + [0, 64)
-                for (int i = 0, c0 = hh * 64; c0 < BN; ++i, c0 += 128) {
+                for (int i = 0, c0 = hh * 64; c0 < BN; ++i, c0 += 64 * EPW) {
                     const int64_t n = int64_t(nt) * BN + c0 + 2 * lane;
                     const float a = __fmul_rn(__ldg(p.scale + (n < p.N ? n : 0)), p.scalar);
                     const float b = __fmul_rn(__ldg(p.scale + (n + 1 < p.N ? n + 1 : 0)), p.scalar);
@@ -654,11 +662,11 @@ __device__ __forceinline__ void epilogue(const TcParams& p, const CUtensorMap& t
                               int64_t(eb) * p.po_bs + int64_t(eh) * p.po_hs);
         } else if (EO == 0 || (EO == 1 && ok)) {
             if (p.y_dt == DT_BF16)
-                epi_tile_fast<BN, true>(p, tmY, pm, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix,
-                                        nstore);
+                epi_tile_fast<BN, true, EPW>(p, tmY, pm, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh,
+                                             tix, nstore);
             else
-                epi_tile_fast<BN, false>(p, tmY, pm, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb, eh, tix,
-                                         nstore);
+                epi_tile_fast<BN, false, EPW>(p, tmY, pm, tacc, stg, cs, col_scaled, cr, q, hh, lane, mrow0, nt, eb,
+                                              eh, tix, nstore);
         } else if constexpr (EO == 1) {
             epi_tile_generic<BN, ES>(p, tmY, tacc, stg, q, hh, lane, mrow0, nt, eb, eh);
         }
@@ -764,8 +772,8 @@ __device__ __forceinline__ uint64_t smem_desc_stage(uint32_t saddr) {
 
 // KK = 0: operand kinds read from the parameters; KK = 1 + 3 * a_kind + b_kind: fixed at compile
 // time (the common BWTA combinations), so the other unpack variants are not compiled in
-template <int BN, int CG, int KS, int EO, int KK = 0>
-__global__ void __launch_bounds__(nt_of(KS, EO), 1)
+template <int BN, int CG, int KS, int EO, int KK = 0, bool E1 = false>
+__global__ void __launch_bounds__(nt_of(KS, EO, E1), 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1,
                    const __grid_constant__ CUtensorMap tmY, const __grid_constant__ PeerMaps pm, TcParams p) {
@@ -812,7 +820,7 @@ __global__ void __launch_bounds__(nt_of(KS, EO), 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 8 * CG);  // epilogue warps of every CTA of the pair
+            mbar_init(&tempty[a], 4 * epi_warps(KS, EO, E1) * CG);  // epilogue warps of every CTA of the pair
         }
         fence_barrier_init();
     }
@@ -988,13 +996,13 @@ __global__ void __launch_bounds__(nt_of(KS, EO), 1)
                 if (acc == 0) acc_phase ^= 1;
             }
         }
-    } else if (warp >= 16 && KS == 256 && p.a_tmem) {
+    } else if (warp >= (epi_warps(KS, EO, E1) == 1 ? 12 : 16) && KS == 256 && p.a_tmem) {
         // ------------------------------ unpack kernel-A rows into TMEM (warps 16-23) ------------------------------
         // AG groups of 4 warps take alternate stages (group g: it = g mod AG): one group's
         // serial chain per stage (full wait, unpack, A-ring wait, tcgen05.st, wait::st, arrive) was the
         // mainloop's critical path.  Thread ut owns kernel-A row ut = TMEM lane ut (warp
         // w: lane quarter w & 3); A code stage it % SA.
-        const int grp = (warp - 16) >> 2;
+        const int grp = (warp - (epi_warps(KS, EO, E1) == 1 ? 12 : 16)) >> 2;
         const int ut = (warp & 3) * 32 + lane;
         const int kind = a_kind_;
         const int plane_bytes = BM * WPS * 4;
@@ -1084,7 +1092,7 @@ __global__ void __launch_bounds__(nt_of(KS, EO), 1)
         // ------------------------------ epilogue (warps 4-7 and 12-15) ------------------------------
         const int q = warp & 3, h = warp >= 12 ? 1 : 0;
         if (EO != 1 || p.y_dt == DT_F16 || p.y_dt == DT_BF16)
-            epilogue<BN, 2, CG, EO>(p, tmY, pm, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
+            epilogue<BN, 2, CG, EO, epi_warps(KS, EO, E1)>(p, tmY, pm, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
                                 rank, t0, tstep);
         else
             if constexpr (EO == 1) epilogue<BN, 4, CG, EO>(p, tmY, pm, tmem_base, sOut, sScale, tfull, tempty, q, h, lane, tiles_per_entry, total,
@@ -1207,17 +1215,17 @@ TileChoice choose_tile(int64_t Mk, int64_t Nk, int64_t entries) {
     return best;
 }
 
-template <int BN, int CG, int KS, int EO, int KK = 0>
+template <int BN, int CG, int KS, int EO, int KK = 0, bool E1 = false>
 cudaError_t launch_ks(const CUtensorMap& ma0, const CUtensorMap& ma1, const CUtensorMap& mb0, const CUtensorMap& mb1,
                       const CUtensorMap& my, const PeerMaps& pm, const TcParams& p, cudaStream_t s) {
     using C = Cfg<BN, CG, KS, KK>;
-    auto kern = tc_gemm_kernel<BN, CG, KS, EO, KK>;
+    auto kern = tc_gemm_kernel<BN, CG, KS, EO, KK, E1>;
     static std::atomic<uint64_t> optin{0};  // per device
     if (cudaError_t e = ensure_smem_optin(kern, C::SMEM, optin); e != cudaSuccess) return e;
     const int64_t tiles = p.entries * int64_t(p.m_tiles) * p.n_tiles;
     const int64_t slots = num_sms() / CG;
     const int grid = int((tiles < slots ? tiles : slots) * CG);
-    return launch_pdl(kern, dim3(grid), dim3(nt_of(KS, EO)), size_t(C::SMEM), s, CG, ma0, ma1, mb0, mb1, my, pm, p);
+    return launch_pdl(kern, dim3(grid), dim3(nt_of(KS, EO, E1)), size_t(C::SMEM), s, CG, ma0, ma1, mb0, mb1, my, pm, p);
 }
 
 template <int BN, int CG>
@@ -1234,6 +1242,11 @@ cudaError_t launch_cfg(int ks, const CUtensorMap& ma0, const CUtensorMap& ma1, c
                        kk == 1 + 3 * B_BINARY + B_TERNARY);
     if (fast) {
         if constexpr (BN == 192) if (spec) {
+            if (p.num_kb >= 8) {  // K >= 2048: one epilogue warp per lane quarter (E1)
+                if (kk == 1 + 3 * B_TERNARY + B_BINARY) return launch_ks<BN, CG, 256, 0, 1 + 3 * B_TERNARY + B_BINARY, true>(ma0, ma1, mb0, mb1, my, pm, p, s);
+                if (kk == 1 + 3 * B_BOOL + B_BINARY) return launch_ks<BN, CG, 256, 0, 1 + 3 * B_BOOL + B_BINARY, true>(ma0, ma1, mb0, mb1, my, pm, p, s);
+                return launch_ks<BN, CG, 256, 0, 1 + 3 * B_BINARY + B_TERNARY, true>(ma0, ma1, mb0, mb1, my, pm, p, s);
+            }
             if (kk == 1 + 3 * B_TERNARY + B_BINARY) return launch_ks<BN, CG, 256, 0, 1 + 3 * B_TERNARY + B_BINARY>(ma0, ma1, mb0, mb1, my, pm, p, s);
             if (kk == 1 + 3 * B_BOOL + B_BINARY) return launch_ks<BN, CG, 256, 0, 1 + 3 * B_BOOL + B_BINARY>(ma0, ma1, mb0, mb1, my, pm, p, s);
             return launch_ks<BN, CG, 256, 0, 1 + 3 * B_BINARY + B_TERNARY>(ma0, ma1, mb0, mb1, my, pm, p, s);

@@ -10,7 +10,7 @@ import bwta_inputs as gen
 import paper_2604_03957_b200 as B
 from quick_bench_util import time_graph
 
-TILES = [None, (64, 2), (128, 1), (128, 2), (192, 2)]
+TILES = [None, (128, 2), (192, 1), (192, 2)]
 for (m, k, n) in [(2048, 4096, 4096), (2048, 4096, 11008), (2048, 8192, 28672), (4096, 768, 3072)]:
     x = gen.activations((m, k), 1).cuda()
     w = gen.weights(n, k, 2).cuda()
