@@ -136,6 +136,16 @@ def graph_of(fn, stream, pre=None):
     return g
 
 
+def _trimmed_mean(v):
+    """Mean of the middle 80 % of the samples: CUDA event timestamps inside a graph step in ~1 us
+    quanta, so a median of a few tens of samples is quantized; the trimmed mean resolves below
+    the quantum and still drops outliers."""
+    v = sorted(v)
+    k = len(v) // 10
+    v = v[k:len(v) - k] if len(v) > 2 * k else v
+    return sum(v) / len(v)
+
+
 def flush_l2(buf):
     """Evict L2 by READING a buffer 2x its size.  A memset flush would leave the
     L2 full of dirty lines whose write-back then lands inside the next timed
@@ -1008,7 +1018,7 @@ def main():
                 if r >= 2:
                     for i, op in enumerate(ops):
                         samples[op.name].append(evs[i].elapsed_time(evs[i + 1]))
-        in_step = {k: statistics.median(v) for k, v in samples.items()}
+        in_step = {k: _trimmed_mean(v) for k, v in samples.items()}
         # the same per-op intervals inside a CUDA graph of the step: external timing events captured
         # between the ops (each event node also stands between two kernels, so no PDL overlap across
         # it); replayed with the L2 flushed before every replay, as the timed steps are
@@ -1030,7 +1040,7 @@ def main():
                     if r >= 2:
                         for i, op in enumerate(ops):
                             samples[op.name].append(evs[i].elapsed_time(evs[i + 1]))
-            in_graph = {k: statistics.median(v) for k, v in samples.items()}
+            in_graph = {k: _trimmed_mean(v) for k, v in samples.items()}
         except Exception as exc:  # pragma: no cover
             print(f"bench: in-graph op timing unavailable ({exc!r})", file=sys.stderr)
             torch.cuda.synchronize()
@@ -1047,10 +1057,10 @@ def main():
     roof["kernel"] = dom.name
     roof["duration_us"] = t_dom * 1e6
     roof["timing"] = ("in-step, in-graph: CUDA events (external event nodes) on the launching stream around the "
-                      "kernel inside a CUDA graph of the step, L2 flushed before every replay (median of the "
-                      "timed-step count)" if dom.name in in_graph else
+                      "kernel inside a CUDA graph of the step, L2 flushed before every replay (trimmed mean "
+                      "over the timed-step count)" if dom.name in in_graph else
                       "in-step: CUDA events on the launching stream around the kernel inside the L2-flushed step "
-                      "sequence, eager launches (median of the timed-step count)" if dom.name in in_step else
+                      "sequence, eager launches (trimmed mean over the timed-step count)" if dom.name in in_step else
                       "isolated: graph of [L2 flush, kernel] x 20 minus graph of [L2 flush] x 20")
     roof["algorithmic"] = {"ops_per_launch": dom.ops, "bytes_per_launch": dom.bytes}
     roof["peak_source"] = (f"{pk['source']} bf16 {pk['bf16_tflops']} TFLOP/s x 4 (dense fp4/bf16 nominal ratio; "
