@@ -1242,7 +1242,11 @@ cudaError_t launch_cfg(int ks, const CUtensorMap& ma0, const CUtensorMap& ma1, c
                        kk == 1 + 3 * B_BINARY + B_TERNARY);
     if (fast) {
         if constexpr (BN == 192) if (spec) {
-            if (p.num_kb >= 8) {  // K >= 2048: one epilogue warp per lane quarter (E1)
+            // K >= 2048 and at least two rounds of tiles per CTA pair (a tile's epilogue then overlaps
+            // the next tile's mainloop): one epilogue warp per lane quarter (E1).  A single round
+            // (BERT FFN2: 64 tiles) leaves the epilogue exposed and keeps two (11.2 vs 11.8 us).
+            const int64_t tiles_ = p.entries * int64_t(p.m_tiles) * p.n_tiles;
+            if (p.num_kb >= 8 && tiles_ >= 2 * int64_t(num_sms() / CG)) {
                 if (kk == 1 + 3 * B_TERNARY + B_BINARY) return launch_ks<BN, CG, 256, 0, 1 + 3 * B_TERNARY + B_BINARY, true>(ma0, ma1, mb0, mb1, my, pm, p, s);
                 if (kk == 1 + 3 * B_BOOL + B_BINARY) return launch_ks<BN, CG, 256, 0, 1 + 3 * B_BOOL + B_BINARY, true>(ma0, ma1, mb0, mb1, my, pm, p, s);
                 return launch_ks<BN, CG, 256, 0, 1 + 3 * B_BINARY + B_TERNARY, true>(ma0, ma1, mb0, mb1, my, pm, p, s);
