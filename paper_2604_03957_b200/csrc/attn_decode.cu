@@ -74,12 +74,16 @@ __global__ void __launch_bounds__(AD_WARPS * 32) attn_decode_kernel(DecodeArgs p
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cs = p.cs;                 // CTAs per entry (cluster size)
     const int rank = cs > 1 ? int(sm100::cluster_ctarank()) : 0;
-    const int64_t e = blockIdx.x / cs;
+    // (32-bit index arithmetic: the int64 divisions were subroutine calls; the host keeps
+    // entries * cs, tk and nh below 2^31)
+    const int e32 = int(blockIdx.x) / cs;
+    const int64_t e = e32;
     // this CTA's keys: whole words [w_lo, w_hi) of the P row
-    const int64_t nw = (p.tk + 31) / 32;
-    const int64_t w_lo = nw * rank / cs, w_hi = nw * (rank + 1) / cs;
+    const int nw = int((p.tk + 31) / 32);
+    const int64_t w_lo = int(int64_t(nw) * rank / cs), w_hi = int(int64_t(nw) * (rank + 1) / cs);
     const int64_t j_lo = 32 * w_lo, j_hi = 32 * w_hi < p.tk ? 32 * w_hi : p.tk;
-    const int64_t eb = e / p.nh, eh = e % p.nh;
+    const int nh32 = int(p.nh);
+    const int64_t eb = e32 / nh32, eh = e32 - (e32 / nh32) * nh32;
     const float alpha = p.alpha_h ? __ldg(p.alpha_h + eh) : p.alpha;  // per-head alpha (nullable)
     const int qw = int((p.dh + 31) / 32);
     uint32_t qs[AD_QW], qn[AD_QW];
