@@ -33,7 +33,8 @@ def _ref_yt(x, w, s_a, mu, s_w, dt="f16"):
 
 @pytest.mark.parametrize("M,N,K,tile", [(256, 384, 1000, None), (304, 517, 777, None), (2048, 640, 4096, None),
                                         (512, 1000, 2048, (128, 1)), (200, 3000, 1500, None),
-                                        (1000, 96, 2500, (64, 2))])
+                                        (1000, 96, 2500, (64, 2)),
+                                        (2048, 4096, 2048, None)])  # >= 2 tile rounds: the 1-warp epilogue (E1)
 def test_gemm_peers_stores_every_tile_to_every_peer(B, M, N, K, tile):
     seed = 9300 + M + N
     x = gen.activations((M, K), seed)
