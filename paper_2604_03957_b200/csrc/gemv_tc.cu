@@ -54,13 +54,16 @@ constexpr int GV_BM = 128;      // kernel-A rows per tile (MMA M)
 constexpr int GV_WPS = 8;       // packed words per row per plane per unit (256 K)
 constexpr int GV_UPS = 4;       // units per bit stage: TMA boxes of 32 words = one 128-byte line per row
 constexpr int GV_ROWB = 128;    // E2M1 code bytes per row per unit
-constexpr int GV_CST = 12;      // code stages (A in TMEM, B in smem)
+// CTAs per SM: 1, or 2 when the problem has more tiles than SMs (each CTA then gets half the TMEM,
+// shared memory and code stages; the per-unit chain is latency-bound, so two CTAs overlap two
+// chains: M = 16 x K 8192 x N 28672 27.0 -> 22.1 us; with <= 1 tile per SM the halved rings are slower)
+__host__ __device__ constexpr int gv_cst(int cps) { return cps == 2 ? 5 : 12; }  // code stages (A in TMEM, B in smem)
 constexpr int GV_MAXRING = 40;  // bit-ring stages
 constexpr int GV_NT = 512;      // 16 warps
 constexpr int GV_ACOL = 64;     // first TMEM column of the A code stages
-constexpr int GV_SFCOL = GV_ACOL + GV_CST * 32;
-constexpr int GV_TMEM_COLS = 512;
-constexpr int GV_SMEM_MAX = 200 * 1024;
+__host__ __device__ constexpr int gv_sfcol(int cps) { return GV_ACOL + gv_cst(cps) * 32; }
+__host__ __device__ constexpr int gv_tmem_cols(int cps) { return cps == 2 ? 256 : 512; }
+__host__ __device__ constexpr int gv_smem_max(int cps) { return cps == 2 ? 110 * 1024 : 200 * 1024; }
 
 __device__ __forceinline__ uint32_t gv_fdiv(uint32_t n, const FastDiv& f) { return (__umulhi(n, f.mul) + n) >> f.shift; }
 struct GvParams {
@@ -129,21 +132,22 @@ __device__ __forceinline__ void store_out(const GvParams& p, int64_t off, float 
     else reinterpret_cast<int32_t*>(p.y)[off] = __float2int_rn(__uint_as_float(acc));
 }
 
-template <int NB>
-__global__ void __launch_bounds__(GV_NT, 1)
+template <int NB, int CPS>
+__global__ void __launch_bounds__(GV_NT, CPS)
     tc_gemv_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmA1,
                    const __grid_constant__ CUtensorMap tmB0, const __grid_constant__ CUtensorMap tmB1, GvParams p) {
     using C = GvCfg<NB>;
+    constexpr int GV_CST_ = gv_cst(CPS), GV_SFCOL_ = gv_sfcol(CPS), GV_TMEM_COLS_ = gv_tmem_cols(CPS);
     extern __shared__ __align__(1024) uint8_t gv_smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gv_smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sB = smem;                                   // [GV_CST][NB rows][128 B] SW128 codes
-    uint8_t* sBits = sB + GV_CST * C::B_BYTES;            // [ring][A planes | B planes]
+    uint8_t* sB = smem;                                   // [GV_CST_][NB rows][128 B] SW128 codes
+    uint8_t* sBits = sB + GV_CST_ * C::B_BYTES;            // [ring][A planes | B planes]
     const int stage_bytes = p.a_bits + p.b_bits;
     uint64_t* bfull = reinterpret_cast<uint64_t*>(sBits + p.ring * stage_bytes);
     uint64_t* bempty = bfull + GV_MAXRING;
     uint64_t* cfull = bempty + GV_MAXRING;
-    uint64_t* cempty = cfull + GV_CST;
-    uint64_t* afull = cempty + GV_CST;
+    uint64_t* cempty = cfull + GV_CST_;
+    uint64_t* afull = cempty + GV_CST_;
     uint64_t* aempty = afull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
 
@@ -160,7 +164,7 @@ __global__ void __launch_bounds__(GV_NT, 1)
             mbar_init(&bfull[s], 1);
             mbar_init(&bempty[s], 4 * GV_UPS);  // 4 warps per unit
         }
-        for (int c = 0; c < GV_CST; ++c) {
+        for (int c = 0; c < GV_CST_; ++c) {
             mbar_init(&cfull[c], 4);
             mbar_init(&cempty[c], 1);  // MMA commit
         }
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(GV_NT, 1)
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, GV_TMEM_COLS);
+    if (warp == 2) tmem_alloc(tmem_slot, GV_TMEM_COLS_);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(GV_NT, 1)
         uint32_t ones[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) ones[i] = 0x7F7F7F7Fu;  // UE8M0 1.0
-        tmem_st_32x32b_x16(tmem_base + (uint32_t((warp & 3) * 32) << 16) + uint32_t(GV_SFCOL), ones);
+        tmem_st_32x32b_x16(tmem_base + (uint32_t((warp & 3) * 32) << 16) + uint32_t(GV_SFCOL_), ones);
         tmem_wait_st();
     }
     tc_fence_before();
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(GV_NT, 1)
         // the whole warp issues (elect.sync inside the asm): operands stay in uniform registers
         constexpr uint32_t idesc = idesc_mxf4(GV_BM, NB);
         const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
-        const uint32_t sfa = tmem_u + uint32_t(GV_SFCOL), sfb = tmem_u + uint32_t(GV_SFCOL + 8);
+        const uint32_t sfa = tmem_u + uint32_t(GV_SFCOL_), sfb = tmem_u + uint32_t(GV_SFCOL_ + 8);
         int c = 0;
         uint32_t cph = 0;
         int acc = 0;
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(GV_NT, 1)
                     tc_commit_w(&cempty[c]);
                 }
                 __syncwarp();
-                if (++c == GV_CST) {
+                if (++c == GV_CST_) {
                     c = 0;
                     cph ^= 1;
                 }
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(GV_NT, 1)
                             if (real) mbar_arrive(&cfull[c]);
                         }
                     }
-                    if (real && ++c == GV_CST) {
+                    if (real && ++c == GV_CST_) {
                         c = 0;
                         cph ^= 1;
                     }
@@ -364,30 +368,38 @@ __global__ void __launch_bounds__(GV_NT, 1)
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, GV_TMEM_COLS);
+        tmem_dealloc(tmem_base, GV_TMEM_COLS_);
     }
 }
 
-template <int NB>
-cudaError_t launch_gemv(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1,
+template <int NB, int CPS>
+cudaError_t launch_gemv_cps(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1,
                         GvParams& p, cudaStream_t s) {
     using C = GvCfg<NB>;
     const int a_planes = p.a_kind == B_TERNARY ? 2 : 1, b_planes = p.b_kind == B_TERNARY ? 2 : 1;
     p.a_bits = a_planes * GV_BM * 128;
     p.b_bits = b_planes * NB * 128;
     const int stage = p.a_bits + p.b_bits;
-    const int bar_bytes = (2 * GV_MAXRING + 2 * GV_CST + 4) * 8 + 16;
-    const int fixed = 1024 + GV_CST * C::B_BYTES + bar_bytes;
-    int ring = (GV_SMEM_MAX - fixed) / stage;
+    const int bar_bytes = (2 * GV_MAXRING + 2 * gv_cst(CPS) + 4) * 8 + 16;
+    const int fixed = 1024 + gv_cst(CPS) * C::B_BYTES + bar_bytes;
+    int ring = (gv_smem_max(CPS) - fixed) / stage;
     if (ring > GV_MAXRING) ring = GV_MAXRING;
     p.ring = ring;
     const int smem = fixed + ring * stage;
-    auto kern = tc_gemv_kernel<NB>;
+    auto kern = tc_gemv_kernel<NB, CPS>;
     static std::atomic<uint64_t> optin{0};  // per device
-    if (cudaError_t e = ensure_smem_optin(kern, GV_SMEM_MAX, optin); e != cudaSuccess) return e;
+    if (cudaError_t e = ensure_smem_optin(kern, gv_smem_max(CPS), optin); e != cudaSuccess) return e;
     const int64_t total = p.entries * p.tiles_per_entry;
-    const int grid = int(total < num_sms() ? total : num_sms());
+    const int64_t slots = int64_t(num_sms()) * CPS;
+    const int grid = int(total < slots ? total : slots);
     return launch_pdl(kern, dim3(grid), dim3(GV_NT), size_t(smem), s, 1, a0, a1, b0, b1, p);
+}
+template <int NB>
+cudaError_t launch_gemv(const CUtensorMap& a0, const CUtensorMap& a1, const CUtensorMap& b0, const CUtensorMap& b1,
+                        GvParams& p, cudaStream_t s) {
+    const int64_t total = p.entries * p.tiles_per_entry;
+    if (total > num_sms()) return launch_gemv_cps<NB, 2>(a0, a1, b0, b1, p, s);
+    return launch_gemv_cps<NB, 1>(a0, a1, b0, b1, p, s);
 }
 
 }  // namespace

@@ -14,7 +14,10 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 fl = lambda: flush.view(torch.int64).max()
 hbm = 6553.6e9
 t_fl = time_graph(fl, reps=10)
-for (m, k, n) in [(1, 8192, 28672), (2, 8192, 28672), (1, 4096, 11008), (4, 8192, 28672), (16, 8192, 28672)]:
+SHAPES = [(1, 8192, 28672), (2, 8192, 28672), (1, 4096, 11008), (4, 8192, 28672), (16, 8192, 28672)]
+if os.environ.get("DECODE_AB_SKINNY"):
+    SHAPES = [(m, k, n) for m in (8, 16, 32) for (k, n) in ((4096, 4096), (4096, 11008), (11008, 4096), (8192, 28672))]
+for (m, k, n) in SHAPES:
     w = gen.weights(n, k, 2).cuda()
     mu, s_w = gen.weight_stats(w)
     s_w = s_w.cuda()
